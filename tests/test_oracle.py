@@ -1,0 +1,235 @@
+"""Pins for the CPU oracle (tests/ -m "not gpu").
+
+The oracle is checked against things other than itself (task rule 3):
+  * the paper's printed worked examples (tests/golden/paper_examples.json);
+  * library routines: numpy int64 matmul, torch conv2d in float64, Python's
+    floor division, numpy.unpackbits;
+  * brute force over every input of tiny problems;
+  * closed forms (in-frame tap counts for all-(+1) convolutions, the int32
+    overflow boundary).
+Every oracle function (gemm, gemm_bitplane, conv2d, epilogue, pack) has at
+least one such pin, chosen so a dropped term, wrong sign/index or transposed
+operand fails.
+"""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2106_12169_b200 import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")
+
+LEGAL = [(a, w, e) for a in range(1, 9) for w in range(1, 9) for e in range(4)
+         if e == 0 or (e == 1 and a == 1 and w == 1) or (e == 2 and w == 1) or (e == 3 and a == 1)]
+
+
+def decode(codes, pm1):
+    c = codes.astype(np.int64)
+    return 2 * c - 1 if pm1 else c
+
+
+def pm1_flags(enc):
+    return {0: (False, False), 1: (True, True), 2: (False, True), 3: (True, False)}[enc]
+
+
+def test_legal_combo_count():
+    # 64 Case I + 1 Case II + 8 Case III + 8 reversed Case III
+    assert len(LEGAL) == 81
+
+
+@pytest.mark.parametrize("method", ["definition", "bitplane"])
+def test_paper_worked_examples(method):
+    g = json.load(open(GOLD))
+    for ex in g["examples"]:
+        Y = oracle.gemm(np.array(ex["A"]), np.array(ex["W"]), ex["a_bits"], ex["w_bits"], ex["enc"],
+                        method=method)
+        assert Y.tolist() == ex["Y"], ex["id"]
+
+
+@pytest.mark.parametrize("method", ["definition", "bitplane"])
+def test_scalar_template_1bit_weight_2bit_feature(method):
+    # wx for a 1-bit w and a 2-bit x, for both weight encodings.
+    for w_pm1, enc in ((False, 0), (True, 2)):
+        for wc in (0, 1):
+            for x in range(4):
+                Y = oracle.gemm(np.array([[x]]), np.array([[wc]]), 2, 1, enc, method=method)
+                wv = (2 * wc - 1) if w_pm1 else wc
+                assert Y[0, 0] == wv * x
+
+
+@pytest.mark.parametrize("enc", [0, 1, 2, 3])
+def test_bruteforce_tiny(enc):
+    # every code assignment for M = N = 1, K <= 3, bits <= 2 (<= 4096 cases)
+    bit_choices = [(1, 1)] if enc == 1 else [(a, w) for a in (1, 2) for w in (1, 2)
+                                              if (enc != 2 or w == 1) and (enc != 3 or a == 1)]
+    a_pm1, w_pm1 = pm1_flags(enc)
+    for a_bits, w_bits in bit_choices:
+        for K in (1, 2, 3):
+            for av in itertools.product(range(1 << a_bits), repeat=K):
+                for wv in itertools.product(range(1 << w_bits), repeat=K):
+                    want = sum(((2 * x - 1) if a_pm1 else x) * ((2 * y - 1) if w_pm1 else y)
+                               for x, y in zip(av, wv))
+                    A = np.array([av]); W = np.array([wv])
+                    assert oracle.gemm(A, W, a_bits, w_bits, enc)[0, 0] == want
+                    assert oracle.gemm(A, W, a_bits, w_bits, enc, method="bitplane")[0, 0] == want
+
+
+@pytest.mark.parametrize("a_bits,w_bits,enc", LEGAL)
+def test_gemm_vs_numpy_matmul_all_81_combos(a_bits, w_bits, enc):
+    # numpy int64 matmul over decoded values; ragged K crosses 64-bit word edges
+    a_pm1, w_pm1 = pm1_flags(enc)
+    for (M, N, K) in ((5, 7, 1), (3, 4, 63), (6, 5, 65), (9, 3, 200)):
+        A, W = synth.gemm_inputs(M, N, K, a_bits, w_bits, tag="pin")
+        want = decode(A, a_pm1) @ decode(W, w_pm1).T
+        for method in ("definition", "bitplane"):
+            got = oracle.gemm(A, W, a_bits, w_bits, enc, method=method)
+            np.testing.assert_array_equal(got, want)
+
+
+def test_case2_uses_logical_k():
+    # Case II with K = 5 stored in a 64-bit word: n must be 5 not 64
+    A = np.array([[1, 0, 1, 1, 0]]); W = np.array([[1, 1, 0, 1, 0]])
+    for method in ("definition", "bitplane"):
+        assert oracle.gemm(A, W, 1, 1, 1, method=method)[0, 0] == 1
+
+
+def test_hand_worked_case3_2bit():
+    # Hand computation from the definition: values of W = 2*code-1.
+    A = np.array([[0, 1, 2, 3], [3, 3, 0, 1]])
+    W = np.array([[1, 0, 1, 1], [0, 0, 1, 0]])
+    # row0: 0-1+2+3 = 4, 0-1+2-3 = -2; row1: 3-3+0+1 = 1, -3-3+0-1 = -7
+    for method in ("definition", "bitplane"):
+        assert oracle.gemm(A, W, 2, 1, 2, method=method).tolist() == [[4, -2], [1, -7]]
+
+
+def test_overflow_boundary():
+    # 255*255*K fits int32 iff K <= 33025 (2^31-1 = 2147483647; 33025*65025 = 2147450625)
+    K = 33025
+    A = np.full((1, K), 255); W = np.full((1, K), 255)
+    assert oracle.gemm(A, W, 8, 8, 0)[0, 0] == 33025 * 65025
+    A = np.full((1, K + 1), 255); W = np.full((1, K + 1), 255)
+    with pytest.raises(oracle.OracleError):
+        oracle.gemm(A, W, 8, 8, 0)
+
+
+def test_rejects_illegal_encoding_and_codes():
+    A = np.array([[2]]); W = np.array([[1]])
+    with pytest.raises(oracle.OracleError):
+        oracle.gemm(A, W, 2, 1, 1)  # +-1 needs 1-bit operands
+    with pytest.raises(oracle.OracleError):
+        oracle.gemm(A, W, 1, 1, 0)  # code 2 does not fit in 1 bit
+
+
+# ------------------------------------------------------------------ conv
+
+def _torch_conv(X, Wt, stride, pad, a_pm1, w_pm1):
+    import torch
+    x = torch.from_numpy(decode(X, a_pm1).astype(np.float64)).permute(0, 3, 1, 2)
+    w = torch.from_numpy(decode(Wt, w_pm1).astype(np.float64)).permute(0, 3, 1, 2)
+    y = torch.nn.functional.conv2d(x, w, stride=stride, padding=pad)  # zero padding = value 0
+    return y.permute(0, 2, 3, 1).round().to(torch.int64).numpy()
+
+
+@pytest.mark.parametrize("enc,a_bits,w_bits", [(0, 2, 2), (1, 1, 1), (2, 2, 1), (3, 1, 3), (0, 8, 8)])
+@pytest.mark.parametrize("shape", [(2, 5, 6, 3, 4, 3, 3, 1, 1), (1, 7, 7, 5, 3, 3, 3, 2, 1),
+                                   (2, 4, 4, 8, 6, 1, 1, 1, 0), (1, 6, 5, 4, 2, 3, 3, 2, 0)])
+def test_conv_vs_torch_conv2d(enc, a_bits, w_bits, shape):
+    B, H, Wd, C, Co, R, S, st, pad = shape
+    X, Wt = synth.conv_inputs(B, H, Wd, C, Co, R, S, a_bits, w_bits, tag="pin")
+    a_pm1, w_pm1 = pm1_flags(enc)
+    got = oracle.conv2d(X, Wt, st, pad, a_bits, w_bits, enc)
+    np.testing.assert_array_equal(got, _torch_conv(X, Wt, st, pad, a_pm1, w_pm1))
+
+
+def test_conv_pm1_padding_closed_form():
+    # all features +1 and all weights +1 on a 3x3 map with a 3x3 kernel, pad 1:
+    # each output = number of in-frame taps (value-domain zero padding, reading R16)
+    X = np.ones((1, 3, 3, 1), dtype=np.uint8); Wt = np.ones((1, 3, 3, 1), dtype=np.uint8)
+    cnt = [[4, 6, 4], [6, 9, 6], [4, 6, 4]]
+    assert oracle.conv2d(X, Wt, 1, 1, 1, 1, 1)[0, :, :, 0].tolist() == cnt
+    # all features -1 (code 0): padding must not decode stored 0 bits as -1
+    X0 = np.zeros_like(X)
+    assert oracle.conv2d(X0, Wt, 1, 1, 1, 1, 1)[0, :, :, 0].tolist() == [[-v for v in r] for r in cnt]
+
+
+def test_conv_1x1_equals_gemm():
+    X, Wt = synth.conv_inputs(2, 3, 4, 70, 9, 1, 1, 3, 1, tag="pin1x1")
+    Y = oracle.conv2d(X, Wt, 1, 0, 3, 1, 2)
+    G = oracle.gemm(X.reshape(-1, 70), Wt.reshape(9, 70), 3, 1, 2)
+    np.testing.assert_array_equal(Y.reshape(-1, 9), G)
+
+
+# -------------------------------------------------------------- epilogue
+
+def test_epilogue_spec_example():
+    g = json.load(open(GOLD))["spec_epilogue"]
+    q = oracle.epilogue(np.array([[g["Y"]]]), [g["alpha"]], [g["beta"]], g["S"], g["out_bits"])
+    assert q[0, 0] == g["q"]
+    P = oracle.pack(q, g["out_bits"])
+    assert [int(P[0, t, 0]) for t in range(g["out_bits"])] == g["planes"]
+
+
+def test_epilogue_vs_python_floor_division():
+    g = synth.rng("epi-pin")
+    Y = g.integers(-2**31, 2**31, size=(37, 29), dtype=np.int64).astype(np.int32)
+    Y[0, :5] = [-7, 7, 0, -1, 1]
+    alpha = g.integers(-5, 6, size=29).astype(np.int32)
+    beta = g.integers(-2**31, 2**31, size=29, dtype=np.int64).astype(np.int32)
+    for S in (1, 2, 3, 1000, 2**31 - 1):
+        for b in (1, 2, 5, 8):
+            q = oracle.epilogue(Y, alpha, beta, S, b)
+            for m in range(37):
+                for n in range(29):
+                    v = int(alpha[n]) * int(Y[m, n]) + int(beta[n])
+                    assert q[m, n] == min(max(v // S, 0), (1 << b) - 1)
+    # floor toward -inf: floor(-7/2) = -4 (C truncation would give -3); identity alpha/beta
+    q = oracle.epilogue(np.array([[-7, 7, 6, 5]]), None, None, 2, 8)
+    assert q.tolist() == [[0, 3, 3, 2]]
+    q = oracle.epilogue(np.array([[-7]]), [1], [8], 2, 8)   # (-7+8)/2 = 0.5 -> 0
+    assert q[0, 0] == 0
+
+
+# --------------------------------------------------------------- packing
+
+@pytest.mark.parametrize("rows,K,bits", [(3, 1, 1), (4, 127, 2), (2, 128, 8), (5, 129, 3), (1, 300, 4)])
+def test_pack_roundtrip_numpy_unpackbits(rows, K, bits):
+    c = synth.codes((rows, K), bits, "packpin")
+    P = oracle.pack(c, bits)
+    Kp = (K + 127) // 128 * 128
+    assert P.shape == (rows, bits, Kp // 32)
+    assert oracle.packed_words(rows, K, bits) == P.size
+    bitsarr = np.unpackbits(P.view(np.uint8).reshape(rows, bits, -1), axis=-1, bitorder="little")
+    assert bitsarr.shape[-1] == Kp
+    rec = sum(bitsarr[:, t, :K].astype(np.int64) << t for t in range(bits))
+    np.testing.assert_array_equal(rec, c)
+    assert not bitsarr[:, :, K:].any()  # padding bits are zero
+
+
+def test_pack_hand_words():
+    # LSB-first: element k -> bit k of word k/32 (reading R1)
+    A = np.array([[0, 1, 2, 3], [3, 3, 0, 1]])
+    P = oracle.pack(A, 2)
+    assert [[int(P[r, t, 0]) for t in range(2)] for r in range(2)] == [[0xA, 0xC], [0xB, 0x3]]
+    assert not P[:, :, 1:].any()
+
+
+def test_oracle_independent_of_product():
+    # the oracle and the CUDA path share no code: no imports either way
+    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for f in os.listdir(os.path.join(here, "oracle")):
+        if f.endswith((".py", ".c", ".h")):
+            src = open(os.path.join(here, "oracle", f)).read()
+            assert "import paper_2106_12169_b200" not in src, f
+            assert "from paper_2106_12169_b200" not in src, f
+            assert '#include "apnn.h"' not in src and "#include <apnn.h>" not in src, f
+    pkg = os.path.join(here, "paper_2106_12169_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp", ".c")):
+                src = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
+                assert "apnn_oracle" not in src, f
