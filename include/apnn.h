@@ -1,0 +1,188 @@
+/*
+ * apnn.h -- C ABI of the B200-native APNN-TC hot path (arXiv 2106.12169).
+ *
+ * One shared library, libapnn.so (paper_2106_12169_b200/libapnn.so), built for
+ * sm_100a.  Every compute call runs hand-written CUDA kernels; there is no CPU
+ * fallback: a call with no usable CUDA device returns APNN_ERR_CUDA.
+ *
+ * The operation (PAPER.md citations are /root/reference/PAPER.md lines):
+ *   arbitrary-precision integer GEMM  Y = A . W^T, where A holds a_bits-bit
+ *   activation codes and W holds w_bits-bit weight codes (1..8 bits each).
+ *   The paper defines it through p.q one-bit plane products combined with
+ *   weights 2^(s+t) (AP-Bit Operation Template; APMM
+ *   PAPER.md:1489-1494); the result is the exact integer product, and this
+ *   library computes exactly that.
+ *   Convolution is the same operation as an implicit GEMM (APConv,
+ *   PAPER.md:1612-1662).  Outputs are int32 or, through the
+ *   fused element-wise routine, requantised and re-packed codes for the next
+ *   layer.
+ *
+ * Conventions shared by every call
+ *   - Pointers marked "device" are CUDA device pointers owned by the caller
+ *     (allocated by PyTorch in this repo).  The library never allocates,
+ *     frees or retains device memory and keeps no state between calls; it is
+ *     thread-safe.
+ *   - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream) and never synchronise the host.  Arguments are
+ *     validated on the host first; on any error nothing is launched.
+ *   - A launch failure (cudaGetLastError after the launch) returns
+ *     APNN_ERR_CUDA.
+ *   - Device pointers must be 16-byte aligned (APNN_ERR_ALIGNMENT).
+ *
+ * Packed bit-plane format (the layout contract)
+ *   A tensor of `rows` rows of K codes with `bits` bits is stored as uint32
+ *       P[r][t][w],  r < rows, t < bits, w < Kw = roundup(K,128)/32,
+ *   bit (k % 32) of P[r][t][k / 32] = (code[r][k] >> t) & 1        (LSB-first)
+ *   i.e. each row holds its `bits` 1-bit planes back to back, every plane run
+ *   padded with zero bits to a multiple of 128 (Eq. bitDecomposition
+ *   PAPER.md:1419-1421; the 128-bit run is the bmma k = 128 tile PAPER.md:1524
+ *   and "128c channels" PAPER.md:1645).  Padding bits MUST be zero.
+ *     GEMM A:   rows = M,                K = K
+ *     GEMM W:   rows = N,                K = K
+ *     conv X:   rows = B*H*W (NHWC),     K = C_in        (channel-major)
+ *     conv W:   rows = C_out*R*S (OHWI), K = C_in
+ *     packed outputs: rows = M (or B*Ho*Wo), K = N (or C_out), bits = out_bits
+ *
+ * Encodings (data-adaptive operator selection).  A +-1
+ * operand stores -1 as bit 0 and +1 as bit 1 and must be
+ * 1-bit; 0/1 operands are unsigned codes 0 .. 2^bits-1.
+ *
+ * Errors are returned as apnn_status; nothing is printed.
+ */
+#ifndef APNN_H_
+#define APNN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same object as cudaStream_t / CUstream. */
+typedef struct CUstream_st *apnn_stream_t;
+
+typedef enum {
+    APNN_OK = 0,
+    APNN_ERR_INVALID_ARG = 1, /* NULL pointer, negative size, bad epilogue fields */
+    APNN_ERR_BITS = 2,        /* a_bits / w_bits / bits / out_bits outside 1..8 */
+    APNN_ERR_ENCODING = 3,    /* +-1 operand with bits > 1, unknown encoding */
+    APNN_ERR_SHAPE = 4,       /* inconsistent shapes (e.g. conv output < 1) */
+    APNN_ERR_ALIGNMENT = 5,   /* device pointer not 16-byte aligned */
+    APNN_ERR_OVERFLOW = 6,    /* worst-case |Y| may exceed int32 */
+    APNN_ERR_UNSUPPORTED = 7, /* combination not implemented by the requested variant */
+    APNN_ERR_CUDA = 8         /* no device, wrong architecture, or launch failure */
+} apnn_status;
+
+typedef enum {
+    APNN_ENC_01_01 = 0,      /* Case I:   A 0/1, W 0/1 -> AND + popc */
+    APNN_ENC_PM1_PM1 = 1,    /* Case II:  A +-1, W +-1 (1 bit each) -> XOR PAPER.md:1455-1460 */
+    APNN_ENC_W_PM1_A_01 = 2, /* Case III: W +-1 (1 bit), A 0/1 */
+    APNN_ENC_W_01_A_PM1 = 3  /* Case III with roles swapped: A +-1 (1 bit), W 0/1 */
+} apnn_encoding;
+
+/* Kernel family that executes the contraction (north star: "choose by
+ * measurement").  All variants return bit-identical results. */
+typedef enum {
+    APNN_VARIANT_AUTO = 0,  /* library picks (apnn_select_variant) */
+    APNN_VARIANT_TC_I8 = 1, /* planes -> int8 recombination, tcgen05.mma kind::i8, TMEM accumulators */
+    APNN_VARIANT_POPC = 2,  /* CUDA-core AND/XOR + POPC bit-plane products, shift-add combination */
+    APNN_VARIANT_B1MMA = 3  /* legacy mma.sync m16n8k256 b1 .and/.xor.popc (the paper's bmma) */
+} apnn_variant;
+
+/* Element-wise routine fused after the contraction:
+ *   v = alpha[n] * y + beta[n]                  (int64; BN / zero point folded
+ *                                                on the host into integers)
+ *   q = clamp(floor(v / divisor), 0, 2^out_bits - 1)   (floor toward -inf;
+ *                                                the lower clamp is the ReLU)
+ * and q is bit-decomposed and packed along N into the packed format with
+ * bits = out_bits. */
+typedef struct {
+    int32_t out_bits;      /* 1..8 */
+    const int32_t *alpha;  /* device [N] or NULL (= 1) */
+    const int32_t *beta;   /* device [N] or NULL (= 0) */
+    int32_t divisor;       /* S > 0 */
+    int32_t pool;          /* must be 0 (2x2 pooling is a later row) */
+} apnn_epilogue;
+
+/* NHWC convolution geometry.  Ho = (H + 2 pad - R)/stride + 1, Wo likewise. */
+typedef struct {
+    int32_t B, H, W, C_in, C_out, R, S, stride, pad;
+} apnn_conv_shape;
+
+/* Bytes of the packed format: rows * bits * roundup(K,128) / 8.  Returns 0
+ * for invalid arguments. */
+size_t apnn_packed_bytes(int rows, int K, int bits);
+
+/* Bit decomposition + packing (Eq. bitDecomposition).
+ *   codes: device uint8 [rows][K] row-major, each < 2^bits (higher bits are
+ *          ignored: the code is masked to its low `bits` bits).
+ *   dst:   device, apnn_packed_bytes(rows, K, bits) bytes, fully written
+ *          (padding bits are written as zero).
+ * A +-1 tensor is packed as codes 0/1.  HBM-bound streaming kernel. */
+apnn_status apnn_pack_bits(const uint8_t *codes, int rows, int K, int bits, uint32_t *dst,
+                           apnn_stream_t stream);
+
+/* APMM with 32-bit output:
+ *   Y[m][n] = sum_{k<K} dec_A(a[m][k]) * dec_W(w[n][k])
+ *   A: device packed [M][a_bits][Kw];  W: device packed [N][w_bits][Kw];
+ *   Y: device int32 [M][N] row-major.
+ * Returns APNN_ERR_OVERFLOW when K * max|a| * max|w| >= 2^31. */
+apnn_status apnn_gemm(const uint32_t *A, const uint32_t *W, int M, int N, int K, int a_bits,
+                      int w_bits, apnn_encoding enc, int32_t *Y, apnn_stream_t stream);
+
+/* APMM with the fused element-wise routine: Y_packed = pack(requant(A . W^T)).
+ *   Y_packed: device, apnn_packed_bytes(M, N, epi->out_bits) bytes, packed
+ *             [M][out_bits][roundup(N,128)/32]; padding bits written as zero.
+ *   epi: host pointer, read during the call only. */
+apnn_status apnn_gemm_fused(const uint32_t *A, const uint32_t *W, int M, int N, int K,
+                            int a_bits, int w_bits, apnn_encoding enc,
+                            const apnn_epilogue *epi, uint32_t *Y_packed, apnn_stream_t stream);
+
+/* Either of the two above with an explicit kernel variant.
+ *   epi == NULL -> Y is int32 [M][N];  epi != NULL -> Y is the packed output. */
+apnn_status apnn_gemm_ex(const uint32_t *A, const uint32_t *W, int M, int N, int K, int a_bits,
+                         int w_bits, apnn_encoding enc, const apnn_epilogue *epi, void *Y,
+                         apnn_variant variant, apnn_stream_t stream);
+
+/* APConv as implicit GEMM:
+ *   Y[b][ho][wo][co] = sum_{r,s,c} dec_A(X[b][ho*st+r-pad][wo*st+s-pad][c]) * dec_W(W[co][r][s][c])
+ *   with out-of-frame taps contributing the VALUE 0 for every encoding (the
+ *   input-aware padding of PAPER.md:1652-1662).
+ *   X: device packed [B*H*W][a_bits][roundup(C_in,128)/32]   (NHW[P][C])
+ *   W: device packed [C_out*R*S][w_bits][roundup(C_in,128)/32]
+ *   epi == NULL -> Y: device int32 NHWC [B][Ho][Wo][C_out]
+ *   epi != NULL -> Y: packed [B*Ho*Wo][out_bits][roundup(C_out,128)/32]
+ *   shape: host pointer. */
+apnn_status apnn_conv2d(const uint32_t *X, const uint32_t *W, const apnn_conv_shape *shape,
+                        int a_bits, int w_bits, apnn_encoding enc, const apnn_epilogue *epi,
+                        void *Y, apnn_stream_t stream);
+
+apnn_status apnn_conv2d_ex(const uint32_t *X, const uint32_t *W, const apnn_conv_shape *shape,
+                           int a_bits, int w_bits, apnn_encoding enc, const apnn_epilogue *epi,
+                           void *Y, apnn_variant variant, apnn_stream_t stream);
+
+/* Stand-alone element-wise routine (the unfused path): requantise an int32
+ * [M][N] matrix and pack it exactly as apnn_gemm_fused would.
+ *   Y: device int32 [M][N]; out: device packed [M][out_bits][roundup(N,128)/32]. */
+apnn_status apnn_quant_pack_out(const int32_t *Y, int M, int N, const apnn_epilogue *epi,
+                                uint32_t *out, apnn_stream_t stream);
+
+/* Which variant APNN_VARIANT_AUTO resolves to for this problem (no launch). */
+apnn_variant apnn_select_variant(int M, int N, int K, int a_bits, int w_bits, apnn_encoding enc);
+
+const char *apnn_status_string(apnn_status status);
+const char *apnn_variant_name(apnn_variant variant);
+
+/* Number of kernels this library has launched in this process (monotonic;
+ * used by bench.py to report gpu_launches). */
+uint64_t apnn_launch_count(void);
+
+/* ABI version: major * 10000 + minor * 100 + patch. */
+int apnn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* APNN_H_ */

@@ -1,0 +1,250 @@
+"""B200-native APNN-TC hot path (arXiv 2106.12169): Python binding of libapnn.so.
+
+Argument marshalling only.  Every computation runs in the sm_100a kernels of
+``libapnn.so`` behind the C ABI declared in ``include/apnn.h``; PyTorch is
+used for device memory and the current CUDA stream.  There is no CPU fallback:
+if the library is missing or the call fails, an exception is raised.
+
+    planes = pack_bits(codes_u8_cuda, bits)              # apnn_pack_bits
+    Y      = gemm(A_planes, W_planes, M, N, K, a_bits, w_bits, enc)          # int32
+    Yp     = gemm(..., epi=Epilogue(out_bits, alpha, beta, divisor))        # fused requant+pack
+    Y      = conv2d(X_planes, W_planes, ConvShape(...), a_bits, w_bits, enc)
+    Yp     = quant_pack_out(Y_int32, epi)
+
+Packed tensors are torch.int32 of shape [rows, bits, roundup(K,128)/32]
+holding the uint32 words of the packed bit-plane format (include/apnn.h).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libapnn.so")
+
+# apnn_encoding
+ENC_01_01, ENC_PM1_PM1, ENC_W_PM1_A_01, ENC_W_01_A_PM1 = 0, 1, 2, 3
+ENCODINGS = {"01_01": 0, "pm1_pm1": 1, "w_pm1_a_01": 2, "w_01_a_pm1": 3}
+# apnn_variant
+VARIANT_AUTO, VARIANT_TC_I8, VARIANT_POPC, VARIANT_B1MMA = 0, 1, 2, 3
+VARIANTS = {"auto": 0, "tc_i8": 1, "popc": 2, "b1mma": 3}
+# apnn_status
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "BITS", 3: "ENCODING", 4: "SHAPE", 5: "ALIGNMENT",
+          6: "OVERFLOW", 7: "UNSUPPORTED", 8: "CUDA"}
+
+
+class ApnnError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: APNN_ERR_{STATUS.get(status, status)} ({status_string(status)})")
+        self.status = status
+
+
+class _Epi(ctypes.Structure):
+    _fields_ = [("out_bits", ctypes.c_int32), ("alpha", ctypes.c_void_p), ("beta", ctypes.c_void_p),
+                ("divisor", ctypes.c_int32), ("pool", ctypes.c_int32)]
+
+
+class _Conv(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("B", "H", "W", "C_in", "C_out", "R", "S", "stride", "pad")]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libapnn.so (build it first with __graft_entry__.build())."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+            L = ctypes.CDLL(LIB_PATH)
+            vp, ci, st = ctypes.c_void_p, ctypes.c_int, ctypes.c_int
+            L.apnn_packed_bytes.argtypes = [ci, ci, ci]
+            L.apnn_packed_bytes.restype = ctypes.c_size_t
+            L.apnn_pack_bits.argtypes = [vp, ci, ci, ci, vp, vp]
+            L.apnn_pack_bits.restype = st
+            L.apnn_gemm.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, vp, vp]
+            L.apnn_gemm.restype = st
+            L.apnn_gemm_fused.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp, vp]
+            L.apnn_gemm_fused.restype = st
+            L.apnn_gemm_ex.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp, ci, vp]
+            L.apnn_gemm_ex.restype = st
+            L.apnn_conv2d.argtypes = [vp, vp, ctypes.POINTER(_Conv), ci, ci, ci, ctypes.POINTER(_Epi), vp, vp]
+            L.apnn_conv2d.restype = st
+            L.apnn_conv2d_ex.argtypes = [vp, vp, ctypes.POINTER(_Conv), ci, ci, ci, ctypes.POINTER(_Epi),
+                                         vp, ci, vp]
+            L.apnn_conv2d_ex.restype = st
+            L.apnn_quant_pack_out.argtypes = [vp, ci, ci, ctypes.POINTER(_Epi), vp, vp]
+            L.apnn_quant_pack_out.restype = st
+            L.apnn_select_variant.argtypes = [ci, ci, ci, ci, ci, ci]
+            L.apnn_select_variant.restype = ci
+            L.apnn_status_string.argtypes = [ci]
+            L.apnn_status_string.restype = ctypes.c_char_p
+            L.apnn_variant_name.argtypes = [ci]
+            L.apnn_variant_name.restype = ctypes.c_char_p
+            L.apnn_launch_count.argtypes = []
+            L.apnn_launch_count.restype = ctypes.c_uint64
+            L.apnn_version.argtypes = []
+            L.apnn_version.restype = ci
+            _lib = L
+    return _lib
+
+
+ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
+               "apnn_conv2d", "apnn_conv2d_ex", "apnn_quant_pack_out", "apnn_select_variant",
+               "apnn_status_string", "apnn_variant_name", "apnn_launch_count", "apnn_version")
+
+
+def status_string(s: int) -> str:
+    return lib().apnn_status_string(s).decode()
+
+
+def variant_name(v: int) -> str:
+    return lib().apnn_variant_name(v).decode()
+
+
+def launch_count() -> int:
+    return int(lib().apnn_launch_count())
+
+
+def _check(st: int, what: str):
+    if st != 0:
+        raise ApnnError(st, what)
+
+
+def _stream(t: torch.Tensor):
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _cuda(t: torch.Tensor, name: str, dtype=None):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def kw(K: int) -> int:
+    """uint32 words per plane run: roundup(K,128)/32."""
+    return (K + 127) // 128 * 4
+
+
+def packed_shape(rows: int, K: int, bits: int):
+    return (rows, bits, kw(K))
+
+
+@dataclass
+class Epilogue:
+    """Fused element-wise routine: q = clamp(floor((alpha*y+beta)/divisor), 0, 2^out_bits-1)."""
+    out_bits: int
+    alpha: Optional[torch.Tensor] = None  # int32 [N] on the device, or None (= 1)
+    beta: Optional[torch.Tensor] = None   # int32 [N] on the device, or None (= 0)
+    divisor: int = 1
+
+    def _c(self):
+        for name in ("alpha", "beta"):
+            t = getattr(self, name)
+            if t is not None:
+                _cuda(t, name, torch.int32)
+        return _Epi(self.out_bits, None if self.alpha is None else self.alpha.data_ptr(),
+                    None if self.beta is None else self.beta.data_ptr(), self.divisor, 0)
+
+
+@dataclass
+class ConvShape:
+    B: int
+    H: int
+    W: int
+    C_in: int
+    C_out: int
+    R: int = 3
+    S: int = 3
+    stride: int = 1
+    pad: int = 1
+
+    @property
+    def Ho(self):
+        return (self.H + 2 * self.pad - self.R) // self.stride + 1
+
+    @property
+    def Wo(self):
+        return (self.W + 2 * self.pad - self.S) // self.stride + 1
+
+    def _c(self):
+        return _Conv(self.B, self.H, self.W, self.C_in, self.C_out, self.R, self.S, self.stride, self.pad)
+
+
+def pack_bits(codes: torch.Tensor, bits: int, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """uint8 codes [rows, K] (CUDA) -> packed planes int32 [rows, bits, Kw]  (apnn_pack_bits)."""
+    _cuda(codes, "codes", torch.uint8)
+    rows, K = codes.shape
+    if out is None:
+        out = torch.empty(packed_shape(rows, K, bits), dtype=torch.int32, device=codes.device)
+    _cuda(out, "out", torch.int32)
+    _check(lib().apnn_pack_bits(_ptr(codes), rows, K, bits, _ptr(out), _stream(codes)), "apnn_pack_bits")
+    return out
+
+
+def gemm(A: torch.Tensor, W: torch.Tensor, M: int, N: int, K: int, a_bits: int, w_bits: int, enc: int,
+         epi: Optional[Epilogue] = None, variant: int = VARIANT_AUTO,
+         out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """APMM: int32 Y [M, N] (epi None) or packed [M, out_bits, Kw(N)]  (apnn_gemm_ex)."""
+    _cuda(A, "A", torch.int32)
+    _cuda(W, "W", torch.int32)
+    if out is None:
+        shape = (M, N) if epi is None else packed_shape(M, N, epi.out_bits)
+        out = torch.empty(shape, dtype=torch.int32, device=A.device)
+    _cuda(out, "out", torch.int32)
+    ce = None if epi is None else ctypes.byref(epi._c())
+    _check(lib().apnn_gemm_ex(_ptr(A), _ptr(W), M, N, K, a_bits, w_bits, enc, ce, _ptr(out), variant,
+                              _stream(A)), "apnn_gemm_ex")
+    return out
+
+
+def conv2d(X: torch.Tensor, W: torch.Tensor, shape: ConvShape, a_bits: int, w_bits: int, enc: int,
+           epi: Optional[Epilogue] = None, variant: int = VARIANT_AUTO,
+           out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """APConv (implicit GEMM): int32 NHWC [B, Ho, Wo, C_out] or packed [B*Ho*Wo, out_bits, Kw(C_out)]."""
+    _cuda(X, "X", torch.int32)
+    _cuda(W, "W", torch.int32)
+    if out is None:
+        if epi is None:
+            oshape = (shape.B, shape.Ho, shape.Wo, shape.C_out)
+        else:
+            oshape = packed_shape(shape.B * shape.Ho * shape.Wo, shape.C_out, epi.out_bits)
+        out = torch.empty(oshape, dtype=torch.int32, device=X.device)
+    _cuda(out, "out", torch.int32)
+    ce = None if epi is None else ctypes.byref(epi._c())
+    cs = shape._c()
+    _check(lib().apnn_conv2d_ex(_ptr(X), _ptr(W), ctypes.byref(cs), a_bits, w_bits, enc, ce, _ptr(out),
+                                variant, _stream(X)), "apnn_conv2d_ex")
+    return out
+
+
+def quant_pack_out(Y: torch.Tensor, epi: Epilogue, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Stand-alone requantise + pack of int32 [M, N]  (apnn_quant_pack_out)."""
+    _cuda(Y, "Y", torch.int32)
+    M, N = Y.shape
+    if out is None:
+        out = torch.empty(packed_shape(M, N, epi.out_bits), dtype=torch.int32, device=Y.device)
+    _cuda(out, "out", torch.int32)
+    _check(lib().apnn_quant_pack_out(_ptr(Y), M, N, ctypes.byref(epi._c()), _ptr(out), _stream(Y)),
+           "apnn_quant_pack_out")
+    return out
+
+
+def select_variant(M, N, K, a_bits, w_bits, enc) -> int:
+    return int(lib().apnn_select_variant(M, N, K, a_bits, w_bits, enc))

@@ -1,0 +1,284 @@
+// apnn.cu -- the C ABI (include/apnn.h): host-side validation and dispatch.
+//
+// Nothing here computes results: every call validates its arguments, builds
+// the kernel parameters and launches one of the sm_100a kernels on the caller's
+// stream.  There is no CPU path; a missing/unsupported device is an error.
+#include <atomic>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace apnn {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+cudaError_t launch_pack_bits(const uint8_t* codes, int rows, int K, int bits, uint32_t* dst, int sms,
+                             cudaStream_t s);
+cudaError_t launch_quant_pack(const int32_t* Y, int M, int N, const Epi& e, uint32_t* out, int sms,
+                              cudaStream_t s);
+cudaError_t launch_popc(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
+                        cudaStream_t s);
+cudaError_t launch_b1mma(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
+                         cudaStream_t s);
+cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
+                         int sms, cudaStream_t s);
+bool tc_i8_supports(const Geom& g);
+bool b1mma_supports(const Geom& g);
+
+// ---- device properties (cached per device ordinal)
+struct DevInfo {
+    bool ok;
+    int sms;
+};
+static std::mutex g_dev_mu;
+static DevInfo g_dev[64];
+static bool g_dev_init[64];
+
+static apnn_status device_info(DevInfo* out) {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        cudaGetLastError();
+        return APNN_ERR_CUDA;
+    }
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (!g_dev_init[dev]) {
+        cudaDeviceProp p;
+        DevInfo d{false, 0};
+        if (cudaGetDeviceProperties(&p, dev) == cudaSuccess) {
+            d.ok = (p.major == 10 && p.minor == 0);  // sm_100 (B200); the cubin is sm_100a only
+            d.sms = p.multiProcessorCount;
+        } else {
+            cudaGetLastError();
+        }
+        g_dev[dev] = d;
+        g_dev_init[dev] = true;
+    }
+    *out = g_dev[dev];
+    return out->ok ? APNN_OK : APNN_ERR_CUDA;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static apnn_status check_bits_enc(int a_bits, int w_bits, int enc) {
+    if (a_bits < 1 || a_bits > 8 || w_bits < 1 || w_bits > 8) return APNN_ERR_BITS;
+    switch (enc) {
+    case APNN_ENC_01_01: return APNN_OK;
+    case APNN_ENC_PM1_PM1: return (a_bits == 1 && w_bits == 1) ? APNN_OK : APNN_ERR_ENCODING;
+    case APNN_ENC_W_PM1_A_01: return (w_bits == 1) ? APNN_OK : APNN_ERR_ENCODING;
+    case APNN_ENC_W_01_A_PM1: return (a_bits == 1) ? APNN_OK : APNN_ERR_ENCODING;
+    default: return APNN_ERR_ENCODING;
+    }
+}
+
+// worst case |y| = K * max|a| * max|w| must stay below 2^31
+static apnn_status check_overflow(long long K, int a_bits, int w_bits, int enc) {
+    long long ma = (enc == APNN_ENC_PM1_PM1 || enc == APNN_ENC_W_01_A_PM1) ? 1 : ((1LL << a_bits) - 1);
+    long long mw = (enc == APNN_ENC_PM1_PM1 || enc == APNN_ENC_W_PM1_A_01) ? 1 : ((1LL << w_bits) - 1);
+    return (K * ma * mw > 2147483647LL) ? APNN_ERR_OVERFLOW : APNN_OK;
+}
+
+static apnn_status make_epi(const apnn_epilogue* epi, Epi* e) {
+    std::memset(e, 0, sizeof(*e));
+    if (!epi) return APNN_OK;
+    if (epi->out_bits < 1 || epi->out_bits > 8) return APNN_ERR_BITS;
+    if (epi->divisor <= 0 || epi->pool != 0) return APNN_ERR_INVALID_ARG;
+    if ((epi->alpha && !aligned16(epi->alpha)) || (epi->beta && !aligned16(epi->beta)))
+        return APNN_ERR_ALIGNMENT;
+    e->alpha = epi->alpha;
+    e->beta = epi->beta;
+    e->S = epi->divisor;
+    e->out_bits = epi->out_bits;
+    e->qmax = (1 << epi->out_bits) - 1;
+    e->invS = 1.0f / (float)epi->divisor;
+    return APNN_OK;
+}
+
+static apnn_variant resolve(apnn_variant v, const Geom& g) {
+    if (v != APNN_VARIANT_AUTO) return v;
+    if (tc_i8_supports(g)) return APNN_VARIANT_TC_I8;
+    return APNN_VARIANT_POPC;
+}
+
+static apnn_status run(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
+                       apnn_variant variant, cudaStream_t s) {
+    DevInfo d;
+    apnn_status st = device_info(&d);
+    if (st != APNN_OK) return st;
+    if (g.M == 0 || g.N == 0) return APNN_OK;
+    cudaError_t err;
+    switch (resolve(variant, g)) {
+    case APNN_VARIANT_TC_I8:
+        if (!tc_i8_supports(g)) return APNN_ERR_UNSUPPORTED;
+        err = launch_tc_i8(A, W, g, e, Y, d.sms, s);
+        break;
+    case APNN_VARIANT_POPC: err = launch_popc(A, W, g, e, Y, s); break;
+    case APNN_VARIANT_B1MMA:
+        if (!b1mma_supports(g)) return APNN_ERR_UNSUPPORTED;
+        err = launch_b1mma(A, W, g, e, Y, s);
+        break;
+    default: return APNN_ERR_INVALID_ARG;
+    }
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+static void gemm_geom(Geom* g, int M, int N, int K, int a_bits, int w_bits, int enc) {
+    std::memset(g, 0, sizeof(*g));
+    g->M = M; g->N = N; g->K = K;
+    g->a_bits = a_bits; g->w_bits = w_bits; g->enc = enc;
+    g->Cw = (K + 127) / 128 * 4;
+    g->CB = g->Cw / 4;
+    g->C = K;
+    g->RS = 1;
+    g->nchunks = g->CB;
+    g->S = 1; g->stride = 1;
+}
+
+}  // namespace apnn
+
+using namespace apnn;
+
+extern "C" {
+
+size_t apnn_packed_bytes(int rows, int K, int bits) {
+    if (rows < 0 || K < 0 || bits < 1 || bits > 8) return 0;
+    return (size_t)rows * (size_t)bits * (((size_t)K + 127) / 128 * 16);
+}
+
+apnn_status apnn_pack_bits(const uint8_t* codes, int rows, int K, int bits, uint32_t* dst,
+                           apnn_stream_t stream) {
+    if (rows < 0 || K < 0) return APNN_ERR_SHAPE;
+    if (bits < 1 || bits > 8) return APNN_ERR_BITS;
+    if ((rows > 0 && K > 0 && !codes) || (rows > 0 && !dst)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(dst)) return APNN_ERR_ALIGNMENT;
+    DevInfo d;
+    apnn_status st = device_info(&d);
+    if (st != APNN_OK) return st;
+    cudaError_t err = launch_pack_bits(codes, rows, K, bits, dst, d.sms, (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_status apnn_gemm_ex(const uint32_t* A, const uint32_t* W, int M, int N, int K, int a_bits,
+                         int w_bits, apnn_encoding enc, const apnn_epilogue* epi, void* Y,
+                         apnn_variant variant, apnn_stream_t stream) {
+    if (M < 0 || N < 0 || K < 0) return APNN_ERR_SHAPE;
+    apnn_status st = check_bits_enc(a_bits, w_bits, enc);
+    if (st != APNN_OK) return st;
+    if ((M > 0 && K > 0 && !A) || (N > 0 && K > 0 && !W) || (M > 0 && N > 0 && !Y))
+        return APNN_ERR_INVALID_ARG;
+    if (!aligned16(A) || !aligned16(W) || !aligned16(Y)) return APNN_ERR_ALIGNMENT;
+    if ((st = check_overflow(K, a_bits, w_bits, enc)) != APNN_OK) return st;
+    Epi e;
+    if ((st = make_epi(epi, &e)) != APNN_OK) return st;
+    if ((unsigned)variant > (unsigned)APNN_VARIANT_B1MMA) return APNN_ERR_INVALID_ARG;
+    Geom g;
+    gemm_geom(&g, M, N, K, a_bits, w_bits, enc);
+    return run(A, W, g, e, Y, variant, (cudaStream_t)stream);
+}
+
+apnn_status apnn_gemm(const uint32_t* A, const uint32_t* W, int M, int N, int K, int a_bits,
+                      int w_bits, apnn_encoding enc, int32_t* Y, apnn_stream_t stream) {
+    return apnn_gemm_ex(A, W, M, N, K, a_bits, w_bits, enc, nullptr, Y, APNN_VARIANT_AUTO, stream);
+}
+
+apnn_status apnn_gemm_fused(const uint32_t* A, const uint32_t* W, int M, int N, int K, int a_bits,
+                            int w_bits, apnn_encoding enc, const apnn_epilogue* epi,
+                            uint32_t* Y_packed, apnn_stream_t stream) {
+    if (!epi) return APNN_ERR_INVALID_ARG;
+    return apnn_gemm_ex(A, W, M, N, K, a_bits, w_bits, enc, epi, Y_packed, APNN_VARIANT_AUTO, stream);
+}
+
+apnn_status apnn_conv2d_ex(const uint32_t* X, const uint32_t* W, const apnn_conv_shape* shp,
+                           int a_bits, int w_bits, apnn_encoding enc, const apnn_epilogue* epi,
+                           void* Y, apnn_variant variant, apnn_stream_t stream) {
+    if (!shp) return APNN_ERR_INVALID_ARG;
+    const apnn_conv_shape c = *shp;
+    if (c.B < 0 || c.H < 1 || c.W < 1 || c.C_in < 1 || c.C_out < 1 || c.R < 1 || c.S < 1 ||
+        c.stride < 1 || c.pad < 0)
+        return APNN_ERR_SHAPE;
+    const int Ho = (c.H + 2 * c.pad - c.R) / c.stride + 1;
+    const int Wo = (c.W + 2 * c.pad - c.S) / c.stride + 1;
+    if (c.H + 2 * c.pad < c.R || c.W + 2 * c.pad < c.S || Ho < 1 || Wo < 1) return APNN_ERR_SHAPE;
+    apnn_status st = check_bits_enc(a_bits, w_bits, enc);
+    if (st != APNN_OK) return st;
+    const long long Mll = (long long)c.B * Ho * Wo;
+    const long long Kll = (long long)c.R * c.S * c.C_in;
+    if (Mll > 2147483647LL || Kll > 2147483647LL) return APNN_ERR_SHAPE;
+    if ((Mll > 0 && (!X || !W || !Y))) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(X) || !aligned16(W) || !aligned16(Y)) return APNN_ERR_ALIGNMENT;
+    if ((st = check_overflow(Kll, a_bits, w_bits, enc)) != APNN_OK) return st;
+    Epi e;
+    if ((st = make_epi(epi, &e)) != APNN_OK) return st;
+    if ((unsigned)variant > (unsigned)APNN_VARIANT_B1MMA) return APNN_ERR_INVALID_ARG;
+    Geom g;
+    std::memset(&g, 0, sizeof(g));
+    g.M = (int)Mll; g.N = c.C_out; g.K = (int)Kll;
+    g.a_bits = a_bits; g.w_bits = w_bits; g.enc = enc;
+    g.Cw = (c.C_in + 127) / 128 * 4;
+    g.CB = g.Cw / 4;
+    g.C = c.C_in;
+    g.RS = c.R * c.S;
+    g.nchunks = g.RS * g.CB;
+    g.conv = 1;
+    g.H = c.H; g.W = c.W; g.Ho = Ho; g.Wo = Wo; g.S = c.S; g.stride = c.stride; g.pad = c.pad;
+    return run(X, W, g, e, Y, variant, (cudaStream_t)stream);
+}
+
+apnn_status apnn_conv2d(const uint32_t* X, const uint32_t* W, const apnn_conv_shape* shp, int a_bits,
+                        int w_bits, apnn_encoding enc, const apnn_epilogue* epi, void* Y,
+                        apnn_stream_t stream) {
+    return apnn_conv2d_ex(X, W, shp, a_bits, w_bits, enc, epi, Y, APNN_VARIANT_AUTO, stream);
+}
+
+apnn_status apnn_quant_pack_out(const int32_t* Y, int M, int N, const apnn_epilogue* epi,
+                                uint32_t* out, apnn_stream_t stream) {
+    if (M < 0 || N < 0) return APNN_ERR_SHAPE;
+    if (!epi) return APNN_ERR_INVALID_ARG;
+    if ((M > 0 && N > 0 && !Y) || (M > 0 && !out)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(Y) || !aligned16(out)) return APNN_ERR_ALIGNMENT;
+    Epi e;
+    apnn_status st = make_epi(epi, &e);
+    if (st != APNN_OK) return st;
+    DevInfo d;
+    if ((st = device_info(&d)) != APNN_OK) return st;
+    cudaError_t err = launch_quant_pack(Y, M, N, e, out, d.sms, (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_variant apnn_select_variant(int M, int N, int K, int a_bits, int w_bits, apnn_encoding enc) {
+    Geom g;
+    gemm_geom(&g, M, N, K, a_bits, w_bits, enc);
+    return resolve(APNN_VARIANT_AUTO, g);
+}
+
+const char* apnn_status_string(apnn_status s) {
+    switch (s) {
+    case APNN_OK: return "ok";
+    case APNN_ERR_INVALID_ARG: return "invalid argument";
+    case APNN_ERR_BITS: return "bit width outside 1..8";
+    case APNN_ERR_ENCODING: return "illegal encoding for these bit widths";
+    case APNN_ERR_SHAPE: return "bad shape";
+    case APNN_ERR_ALIGNMENT: return "device pointer not 16-byte aligned";
+    case APNN_ERR_OVERFLOW: return "worst-case result exceeds int32";
+    case APNN_ERR_UNSUPPORTED: return "unsupported by the requested kernel variant";
+    case APNN_ERR_CUDA: return "CUDA error (no sm_100 device or launch failure)";
+    }
+    return "unknown status";
+}
+
+const char* apnn_variant_name(apnn_variant v) {
+    switch (v) {
+    case APNN_VARIANT_AUTO: return "auto";
+    case APNN_VARIANT_TC_I8: return "tc_i8";
+    case APNN_VARIANT_POPC: return "popc";
+    case APNN_VARIANT_B1MMA: return "b1mma";
+    }
+    return "unknown";
+}
+
+uint64_t apnn_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int apnn_version(void) { return 100; }
+
+}  // extern "C"

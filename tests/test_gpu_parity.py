@@ -1,0 +1,225 @@
+"""GPU parity: every kernel variant vs the CPU oracle, bit-exact (integer work,
+zero tolerance).  All calls go through the C ABI (paper_2106_12169_b200 is a
+ctypes binding of libapnn.so).  Inputs are the seeded synthetic codes of
+paper_2106_12169_b200.synth; expected values come only from oracle/."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2106_12169_b200 as ap
+from paper_2106_12169_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+LEGAL = [(a, w, e) for a in range(1, 9) for w in range(1, 9) for e in range(4)
+         if e == 0 or (e == 1 and a == 1 and w == 1) or (e == 2 and w == 1) or (e == 3 and a == 1)]
+VARIANTS = [ap.VARIANT_POPC, ap.VARIANT_B1MMA, ap.VARIANT_TC_I8]
+
+
+def cuda(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def supported(variant, M, N, K, a, w, enc, conv=False):
+    if variant == ap.VARIANT_B1MMA and conv and enc in (1, 3):
+        return False
+    if variant == ap.VARIANT_TC_I8:
+        return ap.select_variant(max(M, 1), max(N, 1), max(K, 1), a, w, enc) == ap.VARIANT_TC_I8
+    return True
+
+
+def run_gemm(A, W, a, w, enc, variant, epi=None):
+    M, K = A.shape
+    N = W.shape[0]
+    Ap = ap.pack_bits(cuda(A), a)
+    Wp = ap.pack_bits(cuda(W), w)
+    Y = ap.gemm(Ap, Wp, M, N, K, a, w, enc, epi=epi, variant=variant)
+    torch.cuda.synchronize()
+    return Y
+
+
+# ------------------------------------------------------------------ pack
+
+@pytest.mark.parametrize("rows,K", [(1, 1), (3, 31), (5, 127), (7, 128), (9, 129), (33, 1000), (64, 4096)])
+def test_pack_bits_matches_oracle(rows, K):
+    for bits in range(1, 9):
+        c = synth.codes((rows, K), bits, f"pack{rows}x{K}")
+        got = u32(ap.pack_bits(cuda(c), bits))
+        np.testing.assert_array_equal(got, oracle.pack(c, bits))
+
+
+def test_pack_masks_high_bits():
+    c = synth.codes((4, 100), 8, "packmask")
+    got = u32(ap.pack_bits(cuda(c), 3))
+    np.testing.assert_array_equal(got, oracle.pack(c & 7, 3))
+
+
+# ------------------------------------------------------------------ gemm
+
+@pytest.mark.parametrize("a_bits,w_bits,enc", LEGAL)
+def test_gemm_all_81_combos(a_bits, w_bits, enc):
+    M, N, K = 150, 270, 300  # several tiles in every variant plus ragged tails
+    A, W = synth.gemm_inputs(M, N, K, a_bits, w_bits, tag="par81")
+    want = oracle.gemm(A, W, a_bits, w_bits, enc)
+    for v in VARIANTS:
+        if not supported(v, M, N, K, a_bits, w_bits, enc):
+            continue
+        got = run_gemm(A, W, a_bits, w_bits, enc, v).cpu().numpy()
+        np.testing.assert_array_equal(got, want, err_msg=f"variant {ap.variant_name(v)}")
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 8, 31), (64, 64, 128), (127, 129, 127), (129, 257, 129),
+                                   (300, 64, 1000), (257, 520, 2048), (5, 1000, 4096)])
+@pytest.mark.parametrize("a_bits,w_bits,enc", [(2, 1, 2), (1, 1, 1), (2, 2, 0), (4, 4, 0), (8, 8, 0), (1, 3, 3)])
+def test_gemm_ragged_shapes(M, N, K, a_bits, w_bits, enc):
+    A, W = synth.gemm_inputs(M, N, K, a_bits, w_bits, tag="ragged")
+    want = oracle.gemm(A, W, a_bits, w_bits, enc)
+    for v in VARIANTS:
+        if supported(v, M, N, K, a_bits, w_bits, enc):
+            np.testing.assert_array_equal(run_gemm(A, W, a_bits, w_bits, enc, v).cpu().numpy(), want,
+                                          err_msg=f"variant {ap.variant_name(v)}")
+
+
+def test_gemm_extreme_codes_pm1_padding():
+    # all-ones / all-zero codes with K not a multiple of 128: padding must decode to value 0
+    for K in (1, 5, 127, 129):
+        for fill in (0, 1):
+            A = np.full((3, K), fill, np.uint8); W = np.full((2, K), 1 - fill, np.uint8)
+            want = oracle.gemm(A, W, 1, 1, 1)
+            for v in VARIANTS:
+                if supported(v, 3, 2, K, 1, 1, 1):
+                    np.testing.assert_array_equal(run_gemm(A, W, 1, 1, 1, v).cpu().numpy(), want)
+    A = np.full((130, 33025), 255, np.uint8)
+    W = np.full((3, 33025), 255, np.uint8)
+    for v in VARIANTS:
+        if supported(v, 130, 3, 33025, 8, 8, 0):
+            Y = run_gemm(A, W, 8, 8, 0, v).cpu().numpy()
+            assert (Y == 33025 * 65025).all()
+
+
+def test_gemm_k_zero_and_empty():
+    Ap = torch.zeros((4, 2, 0), dtype=torch.int32, device="cuda")
+    Wp = torch.zeros((3, 1, 0), dtype=torch.int32, device="cuda")
+    for v in VARIANTS[:2]:
+        Y = ap.gemm(Ap, Wp, 4, 3, 0, 2, 1, 2, variant=v)
+        torch.cuda.synchronize()
+        assert (Y.cpu() == 0).all()
+    Y = ap.gemm(torch.zeros((0, 1, 4), dtype=torch.int32, device="cuda"),
+                torch.zeros((3, 1, 4), dtype=torch.int32, device="cuda"), 0, 3, 10, 1, 1, 1)
+    assert Y.shape == (0, 3)
+
+
+# ---------------------------------------------------------------- epilogue
+
+def epi_case(N, out_bits, tag):
+    alpha, beta = synth.epilogue_params(N, tag=tag)
+    return alpha, beta, 37
+
+
+@pytest.mark.parametrize("a_bits,w_bits,enc,out_bits", [(2, 1, 2, 2), (1, 1, 1, 1), (4, 4, 0, 4), (8, 8, 0, 8),
+                                                        (2, 2, 0, 3), (1, 2, 3, 2)])
+@pytest.mark.parametrize("M,N,K", [(150, 270, 300), (7, 33, 129), (257, 128, 512)])
+def test_fused_epilogue(a_bits, w_bits, enc, out_bits, M, N, K):
+    A, W = synth.gemm_inputs(M, N, K, a_bits, w_bits, tag="fused")
+    alpha, beta, S = epi_case(N, out_bits, "fused")
+    Y = oracle.gemm(A, W, a_bits, w_bits, enc)
+    want = oracle.pack(oracle.epilogue(Y, alpha, beta, S, out_bits), out_bits)
+    epi = ap.Epilogue(out_bits, cuda(alpha), cuda(beta), S)
+    for v in VARIANTS:
+        if supported(v, M, N, K, a_bits, w_bits, enc):
+            got = u32(run_gemm(A, W, a_bits, w_bits, enc, v, epi=epi))
+            np.testing.assert_array_equal(got, want, err_msg=f"variant {ap.variant_name(v)}")
+    # the unfused element-wise routine gives the same bytes (fusion equivalence, SPEC 217)
+    Yd = run_gemm(A, W, a_bits, w_bits, enc, ap.VARIANT_POPC)
+    got = u32(ap.quant_pack_out(Yd, epi))
+    np.testing.assert_array_equal(got, want)
+
+
+def test_epilogue_identity_and_defaults():
+    M, N, K = 65, 40, 200
+    A, W = synth.gemm_inputs(M, N, K, 2, 2, tag="epidef")
+    Y = oracle.gemm(A, W, 2, 2, 0)
+    want = oracle.pack(oracle.epilogue(Y, None, None, 5, 2), 2)
+    epi = ap.Epilogue(2, None, None, 5)
+    for v in VARIANTS:
+        if supported(v, M, N, K, 2, 2, 0):
+            np.testing.assert_array_equal(u32(run_gemm(A, W, 2, 2, 0, v, epi=epi)), want)
+
+
+def test_quant_pack_out_extremes():
+    g = synth.rng("qpo")
+    Y = g.integers(-2**31, 2**31, size=(33, 77), dtype=np.int64).astype(np.int32)
+    alpha = g.integers(-3, 4, size=77).astype(np.int32)
+    beta = g.integers(-2**31, 2**31, size=77, dtype=np.int64).astype(np.int32)
+    for S in (1, 7, 2**31 - 1):
+        for b in (1, 2, 8):
+            want = oracle.pack(oracle.epilogue(Y, alpha, beta, S, b), b)
+            got = u32(ap.quant_pack_out(cuda(Y), ap.Epilogue(b, cuda(alpha), cuda(beta), S)))
+            np.testing.assert_array_equal(got, want)
+
+
+# -------------------------------------------------------------------- conv
+
+CONV_SHAPES = [  # B, H, W, C, Co, R, S, stride, pad
+    (2, 6, 7, 3, 5, 3, 3, 1, 1),
+    (1, 9, 9, 64, 64, 3, 3, 1, 1),
+    (2, 8, 8, 128, 130, 3, 3, 2, 1),
+    (1, 5, 6, 192, 40, 1, 1, 1, 0),
+    (1, 7, 7, 70, 300, 3, 3, 2, 0),
+    (3, 4, 4, 200, 16, 3, 3, 1, 1),
+]
+
+
+@pytest.mark.parametrize("shape", CONV_SHAPES)
+@pytest.mark.parametrize("a_bits,w_bits,enc", [(2, 1, 2), (1, 1, 1), (2, 2, 0), (1, 2, 3), (8, 8, 0)])
+def test_conv2d(shape, a_bits, w_bits, enc):
+    B, H, Wd, C, Co, R, S, st, pad = shape
+    X, Wt = synth.conv_inputs(B, H, Wd, C, Co, R, S, a_bits, w_bits, tag="convpar")
+    want = oracle.conv2d(X, Wt, st, pad, a_bits, w_bits, enc)
+    Xp = ap.pack_bits(cuda(X.reshape(-1, C)), a_bits)
+    Wp = ap.pack_bits(cuda(Wt.reshape(-1, C)), w_bits)
+    cs = ap.ConvShape(B, H, Wd, C, Co, R, S, st, pad)
+    for v in VARIANTS:
+        if not supported(v, B * cs.Ho * cs.Wo, Co, R * S * C, a_bits, w_bits, enc, conv=True):
+            continue
+        got = ap.conv2d(Xp, Wp, cs, a_bits, w_bits, enc, variant=v)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(got.cpu().numpy(), want, err_msg=f"variant {ap.variant_name(v)}")
+    # fused requant + pack on the conv path
+    alpha, beta, Sd = epi_case(Co, 2, "convepi")
+    wantp = oracle.pack(oracle.epilogue(want.reshape(-1, Co), alpha, beta, Sd, 2), 2)
+    for v in VARIANTS:
+        if not supported(v, B * cs.Ho * cs.Wo, Co, R * S * C, a_bits, w_bits, enc, conv=True):
+            continue
+        got = ap.conv2d(Xp, Wp, cs, a_bits, w_bits, enc, epi=ap.Epilogue(2, cuda(alpha), cuda(beta), Sd),
+                        variant=v)
+        np.testing.assert_array_equal(u32(got), wantp, err_msg=f"fused variant {ap.variant_name(v)}")
+
+
+def test_conv_pm1_padding_closed_form_gpu():
+    X = np.ones((1, 3, 3, 1), np.uint8); Wt = np.ones((1, 3, 3, 1), np.uint8)
+    Xp = ap.pack_bits(cuda(X.reshape(-1, 1)), 1)
+    Wp = ap.pack_bits(cuda(Wt.reshape(-1, 1)), 1)
+    for v in (ap.VARIANT_POPC, ap.VARIANT_TC_I8):
+        if not supported(v, 9, 1, 9, 1, 1, 1, conv=True):
+            continue
+        got = ap.conv2d(Xp, Wp, ap.ConvShape(1, 3, 3, 1, 1, 3, 3, 1, 1), 1, 1, 1, variant=v).cpu()
+        assert got[0, :, :, 0].tolist() == [[4, 6, 4], [6, 9, 6], [4, 6, 4]]
+
+
+# ----------------------------------------------------------------- variants agree
+
+def test_variants_agree_random_bits():
+    g = synth.rng("agree")
+    for _ in range(10):
+        a, w, e = LEGAL[int(g.integers(len(LEGAL)))]
+        M, N, K = (int(x) for x in g.integers(1, 400, size=3))
+        A, W = synth.gemm_inputs(M, N, K, a, w, tag="agree")
+        outs = [run_gemm(A, W, a, w, e, v).cpu().numpy() for v in VARIANTS if supported(v, M, N, K, a, w, e)]
+        for o in outs[1:]:
+            np.testing.assert_array_equal(o, outs[0])
