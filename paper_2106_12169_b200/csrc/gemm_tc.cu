@@ -5,114 +5,248 @@
 // mma.sync is emulated on the int8 pipe).  The paper's bit combination
 //     Y = sum_s sum_t 2^(s+t) W^(s) X^(t)
 // is bilinear, so it equals (sum_t 2^t X^(t)) . (sum_s 2^s W^(s))^T: the
-// combination can be applied to the OPERANDS (O((a+w)(M+N)K) shift-ors on the
-// CUDA cores) instead of the p.q partial products (O(pq MN) adds), after which
-// a single int8 tensor-core contraction per tile yields Y exactly.  +-1 planes
-// decode to s8 -1/+1 (Cases II/III: the J terms disappear
-// once the value is materialised); 0/1 codes are u8.
+// combination is applied to the OPERANDS (O((a+w)(M+N)K) shift-ors on the CUDA
+// cores, per tile) instead of to the p.q partial products, after which one
+// int8 tensor-core contraction per tile yields Y exactly.  +-1 planes decode to
+// s8 -1/+1 (Cases II/III: the J terms vanish once the value
+// is materialised); 0/1 codes decode to u8.
 //
-// Per CTA: a 128 x BN output tile, K in blocks of 128 (the paper's b_k = 128,
-// PAPER.md:1742), S-stage pipeline:
-//   warp 0      TMA producer: one 3-D box per operand per k-block brings ALL
-//               planes of the tile ("virtual batching", PAPER.md:1528-1533:
-//               the plane index is a box dimension) into shared memory.
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (4 MMAs of
-//               128 x BN x 32 per k-block), int32 accumulator in TMEM
-//               ("fragment caching", now TMEM).
-//   warps 2-9   recombination: planes -> int8.  A goes straight into TMEM with
-//               tcgen05.st (the MMA's A operand is TMEM-resident), B goes into
-//               the UMMA K-major no-swizzle layout in shared memory.  Then the
-//               same warps run the epilogue: tcgen05.ld -> int32 store, or the
-//               fused element-wise routine -> requantise -> bit-decompose ->
-//               pack along N in registers.
-// K ordering inside a 32-element group is permuted identically for A and B
-// (word j of a group holds elements j, j+8, j+16, j+24) so that one shift +
-// one masked OR per plane builds four int8 lanes.
+// Two kernels:
+//   tc2_kernel (main)  persistent, CTA pair (cta_group::2): a 256 x 256 output
+//                      tile per pair, M split across the two CTAs (A in each
+//                      CTA's TMEM), N split across the two CTAs (B halves in
+//                      each CTA's shared memory).  Warp roles per CTA:
+//                        warp 0     TMA producer: one 3-D box per operand and
+//                                   k-block brings ALL planes of the tile
+//                                   ("virtual batching")
+//                        warp 1     TMEM allocator; in CTA 0 the single-thread
+//                                   tcgen05.mma issuer (4 x 256x256x32 per
+//                                   k-block), int32 accumulator in TMEM
+//                                   ("fragment caching")
+//                        warps 2-9  recombination planes -> int8: A rows into
+//                                   TMEM (tcgen05.st), B rows into the UMMA
+//                                   K-major layout in smem; they run ahead into
+//                                   the next tile while the epilogue drains
+//                        warps 10-13 epilogue: tcgen05.ld -> int32, or the fused
+//                                   element-wise routine
+//   tc1_kernel         one CTA, 128 x BN tile (BN = 64/128/256), for small or
+//                      skinny problems.
+// K runs in blocks of 128 (the paper's b_k = 128).
 #include <cuda.h>
 
 #include <mutex>
 
-#include "common.cuh"
-#include "sm100.cuh"
+#include "tc_common.cuh"
 
 namespace apnn {
-
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int NUM_RECOMB_WARPS = 8;
-constexpr int NT = 32 * (2 + NUM_RECOMB_WARPS);
-constexpr int MAX_STAGES = 6;
+constexpr int MAX_STAGES = 8;
 
 struct Params {
     Geom g;
     Epi e;
     void* Y;
     int stages;
-    int nkb;            // k-blocks
-    uint32_t a_bytes;   // planes bytes of A per stage
-    uint32_t b_bytes;   // planes bytes of B per stage
+    int nkb;            // k-blocks per tile
+    uint32_t a_bytes;   // A plane bytes per stage (this CTA's rows)
+    uint32_t b_bytes;   // B plane bytes per stage (this CTA's rows)
     uint32_t tmem_cols;
+    int tiles_m, num_tiles;
+    int use_tab;        // fused epilogue through the threshold table
 };
 
-// decode one 32-element group of 0/1 planes into 8 words of u8 lanes:
-// word j, byte i <- element j + 8 i  (one shift + one masked OR per plane)
-template <int NB>
-__device__ __forceinline__ void decode_01(const uint32_t (&pw)[8], uint32_t (&out)[8]) {
-#pragma unroll
-    for (int j = 0; j < 8; j++) {
-        uint32_t o = 0;
-#pragma unroll
-        for (int t = 0; t < NB; t++) {
-            const uint32_t mask = 0x01010101u << t;
-            const uint32_t sh = (j >= t) ? (pw[t] >> (j - t)) : (pw[t] << (t - j));
-            o |= sh & mask;
-        }
-        out[j] = o;
-    }
-}
-__device__ __forceinline__ void decode_01_any(const uint32_t (&pw)[8], int nb, uint32_t (&out)[8]) {
-    switch (nb) {  // warp-uniform
-    case 1: decode_01<1>(pw, out); break;
-    case 2: decode_01<2>(pw, out); break;
-    case 3: decode_01<3>(pw, out); break;
-    case 4: decode_01<4>(pw, out); break;
-    case 5: decode_01<5>(pw, out); break;
-    case 6: decode_01<6>(pw, out); break;
-    case 7: decode_01<7>(pw, out); break;
-    default: decode_01<8>(pw, out); break;
-    }
-}
+// ============================================================== 2-CTA kernel
+constexpr int T2_THREADS = 14 * 32;
+constexpr int T2_BN = 256;   // N per pair; 128 B rows per CTA
 
-// +-1 plane -> s8 lanes: bit 1 -> 0x01, bit 0 -> 0xFF; vm = valid elements
-__device__ __forceinline__ void decode_pm1(uint32_t pw, uint32_t vm, uint32_t (&out)[8]) {
-#pragma unroll
-    for (int j = 0; j < 8; j++) {
-        const uint32_t s = (pw >> j) & 0x01010101u;
-        uint32_t o = s * 0xFFFFFF02u + 0xFFFFFFFFu;  // 0xFF - 0xFE*s per byte, no borrows
-        const uint32_t v = (vm >> j) & 0x01010101u;
-        out[j] = o & (v * 0xFFu);
-    }
-}
-
-template <int BN, bool A_PM1, bool W_PM1>
-__global__ void __launch_bounds__(NT, 1)
-    tc_i8_gemm_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
-                      const Params p) {
+template <bool A_PM1, bool W_PM1>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
+    tc2_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
+               const Params p) {
     using namespace sm100;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = p.stages;
-    // layout: [B operand stages][A planes stages][B planes stages][barriers]
-    uint8_t* sBop = smem;                                    // S x BN x 128 B, 1024-aligned
+    uint8_t* sBop = smem;                                        // S x 128 rows x 128 B
+    uint8_t* sApl = sBop + (size_t)S * 128 * 128;                // S x a_bytes
+    uint8_t* sBpl = sApl + (size_t)S * p.a_bytes;                // S x b_bytes
+    int32_t* sTab = reinterpret_cast<int32_t*>(sBpl + (size_t)S * p.b_bytes);  // 256 x 16 int32
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sTab + T2_BN * kTabStride);
+    uint64_t* plane_full = bars;
+    uint64_t* plane_empty = bars + MAX_STAGES;
+    uint64_t* op_full = bars + 2 * MAX_STAGES;     // used in CTA 0
+    uint64_t* op_empty = bars + 3 * MAX_STAGES;
+    uint64_t* accum_full = bars + 4 * MAX_STAGES;
+    uint64_t* accum_empty = bars + 4 * MAX_STAGES + 1;  // used in CTA 0
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * MAX_STAGES + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_ctarank();
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const Geom& g = p.g;
+    const int nkb = p.nkb;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmapA);
+        tma_prefetch(&tmapB);
+        for (int s = 0; s < S; s++) {
+            mbar_init(&plane_full[s], 1);
+            mbar_init(&plane_empty[s], 8);
+            mbar_init(&op_full[s], 16);   // 8 recombination warps x 2 CTAs
+            mbar_init(&op_empty[s], 1);
+        }
+        mbar_init(accum_full, 1);
+        mbar_init(accum_empty, 8);        // 4 epilogue warps x 2 CTAs
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc2(tmem_holder, p.tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_holder;
+    constexpr uint32_t A_COL = 256;
+
+    if (warp == 0) {
+        // ---------------------------------------------------- TMA producer
+        if (lane == 0) {
+            int it = 0;
+            for (int tile = cid; tile < p.num_tiles; tile += ncl) {
+                const int m0 = (tile % p.tiles_m) * 256 + rank * 128;
+                const int nr0 = (tile / p.tiles_m) * T2_BN + rank * 128;
+                for (int kb = 0; kb < nkb; kb++, it++) {
+                    const int s = it % S;
+                    const uint32_t ph = (it / S) & 1;
+                    mbar_wait(&plane_empty[s], ph ^ 1);
+                    mbar_arrive_expect_tx(&plane_full[s], p.a_bytes + p.b_bytes);
+                    tma_load_3d(sApl + (size_t)s * p.a_bytes, &tmapA, &plane_full[s], kb * 4, m0, 0);
+                    tma_load_3d(sBpl + (size_t)s * p.b_bytes, &tmapB, &plane_full[s], kb * 4, nr0, 0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------- MMA issuer (CTA 0)
+        if (rank == 0 && lane == 0) {
+            const uint32_t idesc = idesc_i8(256, T2_BN, A_PM1, W_PM1);
+            int it = 0, tc = 0;
+            for (int tile = cid; tile < p.num_tiles; tile += ncl, tc++) {
+                mbar_wait_cluster(accum_empty, (tc & 1) ^ 1);
+                tc_fence_after();
+                for (int kb = 0; kb < nkb; kb++, it++) {
+                    const int s = it % S;
+                    const uint32_t ph = (it / S) & 1;
+                    mbar_wait_cluster(&op_full[s], ph);
+                    tc_fence_after();
+                    const uint32_t bbase = smem_u32(sBop + (size_t)s * 128 * 128);
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++) {
+                        const uint64_t bdesc = umma_desc_noswizzle(bbase + kk * 256, 128, 1024);
+                        mma2_i8_ts(tmem, tmem + A_COL + s * 32 + kk * 8, bdesc, idesc, (kb | kk) != 0);
+                    }
+                    mma2_commit_mc(&op_empty[s], 0x3);
+                }
+                mma2_commit_mc(accum_full, 0x3);
+            }
+        }
+    } else if (warp < 10) {
+        // ---------------------------------------------------- recombination
+        const int q = warp & 3;
+        const int grp = (warp - 2) >> 2;
+        const int t = q * 32 + lane;
+        const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
+        const uint32_t op_full0 = mapa(smem_u32(op_full), 0);
+        int it = 0;
+        for (int tile = cid; tile < p.num_tiles; tile += ncl) {
+            for (int kb = 0; kb < nkb; kb++, it++) {
+                const int s = it % S;
+                const uint32_t ph = (it / S) & 1;
+                int kvalid = 128;
+                if (A_PM1 && W_PM1) {
+                    const int rem = g.K - kb * 128;
+                    kvalid = rem < 128 ? rem : 128;
+                }
+                mbar_wait(&plane_full[s], ph);
+                mbar_wait(&op_empty[s], ph ^ 1);
+                if ((it & 1) == grp) {
+                    a_job_any<A_PM1>(g.a_bits, sApl + (size_t)s * p.a_bytes, 128, t,
+                                     tmem_lane + A_COL + s * 32, kvalid);
+                    tmem_wait_st();
+                } else {
+                    b_job_any<W_PM1>(g.w_bits, sBpl + (size_t)s * p.b_bytes, 128, t,
+                                     sBop + (size_t)s * 128 * 128, 128);
+                    fence_proxy_async_smem();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&plane_empty[s]);
+                    mbar_arrive_cluster(op_full0 + s * 8);
+                }
+            }
+        }
+    } else {
+        // ---------------------------------------------------- epilogue
+        const int q = warp & 3;
+        const int t = q * 32 + lane;               // row in this CTA's 128
+        const int et = threadIdx.x - 10 * 32;      // 0..127
+        const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
+        const uint32_t accum_empty0 = mapa(smem_u32(accum_empty), 0);
+        int tc = 0;
+        for (int tile = cid; tile < p.num_tiles; tile += ncl, tc++) {
+            const int m = (tile % p.tiles_m) * 256 + rank * 128 + t;
+            const int n0 = (tile / p.tiles_m) * T2_BN;
+            if (p.use_tab) {
+                named_bar_sync(1, 128);  // previous tile's readers are done
+                build_threshold_row(sTab + et * kTabStride, n0 + et, g.N, p.e);
+                build_threshold_row(sTab + (et + 128) * kTabStride, n0 + et + 128, g.N, p.e);
+                named_bar_sync(1, 128);
+            }
+            mbar_wait(accum_full, tc & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < T2_BN; c += 32) {
+                uint32_t acc[32];
+                tmem_ld32(tmem_lane + c, acc);
+                tmem_wait_ld();
+                epilogue_chunk(acc, m, n0 + c, c, g, p.e, p.Y, p.use_tab ? sTab : nullptr);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(accum_empty0);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc2(tmem, p.tmem_cols);
+    }
+}
+
+// ============================================================== 1-CTA kernel
+constexpr int T1_THREADS = 10 * 32;
+
+template <int BN, bool A_PM1, bool W_PM1>
+__global__ void __launch_bounds__(T1_THREADS, 1)
+    tc1_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
+               const Params p) {
+    using namespace sm100;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int S = p.stages;
+    uint8_t* sBop = smem;                                    // S x BN x 128 B
     uint8_t* sApl = sBop + (size_t)S * BN * 128;             // S x a_bytes
     uint8_t* sBpl = sApl + (size_t)S * p.a_bytes;            // S x b_bytes
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sBpl + (size_t)S * p.b_bytes);
+    int32_t* sTab = reinterpret_cast<int32_t*>(sBpl + (size_t)S * p.b_bytes);  // BN x 16 int32
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sTab + BN * kTabStride);
     uint64_t* plane_full = bars;
     uint64_t* plane_empty = bars + MAX_STAGES;
     uint64_t* op_full = bars + 2 * MAX_STAGES;
     uint64_t* op_empty = bars + 3 * MAX_STAGES;
     uint64_t* accum_full = bars + 4 * MAX_STAGES;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * MAX_STAGES + 1);
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * MAX_STAGES + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
@@ -124,8 +258,8 @@ __global__ void __launch_bounds__(NT, 1)
         tma_prefetch(&tmapB);
         for (int s = 0; s < S; s++) {
             mbar_init(&plane_full[s], 1);
-            mbar_init(&plane_empty[s], NUM_RECOMB_WARPS);
-            mbar_init(&op_full[s], NUM_RECOMB_WARPS);
+            mbar_init(&plane_empty[s], 8);
+            mbar_init(&op_full[s], 8);
             mbar_init(&op_empty[s], 1);
         }
         mbar_init(accum_full, 1);
@@ -136,10 +270,9 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_holder;
-    const uint32_t A_COL = BN;  // A stages live after the accumulator columns
+    constexpr uint32_t A_COL = BN;
 
     if (warp == 0) {
-        // ------------------------------------------------ TMA producer
         if (lane == 0) {
             for (int kb = 0; kb < nkb; kb++) {
                 const int s = kb % S;
@@ -151,7 +284,6 @@ __global__ void __launch_bounds__(NT, 1)
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer
         if (lane == 0) {
             const uint32_t idesc = idesc_i8(BM, BN, A_PM1, W_PM1);
             for (int kb = 0; kb < nkb; kb++) {
@@ -170,143 +302,50 @@ __global__ void __launch_bounds__(NT, 1)
             mma_commit(accum_full);
         }
     } else {
-        // ------------------------------------------------ recombination warps
-        const int q = warp & 3;             // TMEM lane quarter this warp may access
-        const int grp = (warp - 2) >> 2;    // 0: warps 2-5, 1: warps 6-9
-        const int t = q * 32 + lane;        // row slot 0..127
+        const int q = warp & 3;
+        const int grp = (warp - 2) >> 2;
+        const int t = q * 32 + lane;
+        const int et = threadIdx.x - 64;  // 0..255
         const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
-        const int ab = g.a_bits, wb = g.w_bits;
-
+        if (p.use_tab && et < BN) build_threshold_row(sTab + et * kTabStride, n0 + et, g.N, p.e);
         for (int kb = 0; kb < nkb; kb++) {
             const int s = kb % S;
             const uint32_t ph = (kb / S) & 1;
-            const bool doA = ((kb & 1) == grp);
-            mbar_wait(&plane_full[s], ph);
-            // planes of this thread's rows (smem layout [plane][row][16 B])
-            uint4 pa[8];
-            uint4 pb[2][8];
-            if (doA) {
-                const uint4* src = reinterpret_cast<const uint4*>(sApl + (size_t)s * p.a_bytes);
-#pragma unroll
-                for (int pl = 0; pl < 8; pl++)
-                    if (pl < ab) pa[pl] = src[pl * BM + t];
-            } else {
-                const uint4* src = reinterpret_cast<const uint4*>(sBpl + (size_t)s * p.b_bytes);
-#pragma unroll
-                for (int r = 0; r < 2; r++) {
-                    const int row = t + r * 128;
-                    if (row < BN) {
-#pragma unroll
-                        for (int pl = 0; pl < 8; pl++)
-                            if (pl < wb) pb[r][pl] = src[pl * BN + row];
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&plane_empty[s]);
-
-            mbar_wait(&op_empty[s], ph ^ 1);
-            // valid-element mask for +-1 x +-1 (Case II): padded K must decode to 0
             int kvalid = 128;
             if (A_PM1 && W_PM1) {
                 const int rem = g.K - kb * 128;
                 kvalid = rem < 128 ? rem : 128;
             }
-            if (doA) {
-#pragma unroll
-                for (int gi = 0; gi < 4; gi++) {
-                    uint32_t pw[8];
-#pragma unroll
-                    for (int pl = 0; pl < 8; pl++) {
-                        const uint4 v = pa[pl < ab ? pl : 0];
-                        pw[pl] = gi == 0 ? v.x : gi == 1 ? v.y : gi == 2 ? v.z : v.w;
-                    }
-                    uint32_t o[8];
-                    if (A_PM1) {
-                        const int nv = kvalid - gi * 32;
-                        const uint32_t vm = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
-                        decode_pm1(pw[0], vm, o);
-                    } else {
-                        decode_01_any(pw, ab, o);
-                    }
-                    tmem_st8(tmem_lane + A_COL + s * 32 + gi * 8, o);
-                }
+            mbar_wait(&plane_full[s], ph);
+            mbar_wait(&op_empty[s], ph ^ 1);
+            if ((kb & 1) == grp) {
+                a_job_any<A_PM1>(g.a_bits, sApl + (size_t)s * p.a_bytes, BM, t, tmem_lane + A_COL + s * 32, kvalid);
                 tmem_wait_st();
             } else {
-                uint8_t* dst = sBop + (size_t)s * BN * 128;
-#pragma unroll
-                for (int r = 0; r < 2; r++) {
-                    const int row = t + r * 128;
-                    if (row >= BN) continue;
-                    uint8_t* rbase = dst + (row >> 3) * 1024 + (row & 7) * 16;
-#pragma unroll
-                    for (int gi = 0; gi < 4; gi++) {
-                        uint32_t pw[8];
-#pragma unroll
-                        for (int pl = 0; pl < 8; pl++) {
-                            const uint4 v = pb[r][pl < wb ? pl : 0];
-                            pw[pl] = gi == 0 ? v.x : gi == 1 ? v.y : gi == 2 ? v.z : v.w;
-                        }
-                        uint32_t o[8];
-                        if (W_PM1) decode_pm1(pw[0], 0xFFFFFFFFu, o);
-                        else decode_01_any(pw, wb, o);
-                        *reinterpret_cast<uint4*>(rbase + (2 * gi) * 128) = make_uint4(o[0], o[1], o[2], o[3]);
-                        *reinterpret_cast<uint4*>(rbase + (2 * gi + 1) * 128) = make_uint4(o[4], o[5], o[6], o[7]);
-                    }
-                }
+                uint8_t* bop = sBop + (size_t)s * BN * 128;
+                const uint8_t* bpl = sBpl + (size_t)s * p.b_bytes;
+                if (t < BN) b_job_any<W_PM1>(g.w_bits, bpl, BN, t, bop, 128);
+                if (t + 128 < BN) b_job_any<W_PM1>(g.w_bits, bpl, BN, t + 128, bop, 128);
                 fence_proxy_async_smem();
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&op_full[s]);
+            if (lane == 0) {
+                mbar_arrive(&plane_empty[s]);
+                mbar_arrive(&op_full[s]);
+            }
         }
-
-        // ------------------------------------------------ epilogue
+        named_bar_sync(1, 256);  // threshold table complete (built before the mainloop)
         mbar_wait(accum_full, 0);
         tc_fence_after();
         const int m = m0 + t;
-        const Epi& e = p.e;
-        const int ncol_half = BN / 2;
-        for (int c = grp * ncol_half; c < (grp + 1) * ncol_half; c += 32) {
+        constexpr int half = BN / 2;
+#pragma unroll 1
+        for (int c = grp * half; c < (grp + 1) * half; c += 32) {
             uint32_t acc[32];
             tmem_ld32(tmem_lane + c, acc);
             tmem_wait_ld();
-            const int nb = n0 + c;
-            if (m >= g.M) continue;
-            if (e.out_bits == 0) {
-                int32_t* Y = reinterpret_cast<int32_t*>(p.Y) + (long long)m * g.N;
-                if (nb + 32 <= g.N && (g.N & 3) == 0) {
-#pragma unroll
-                    for (int i = 0; i < 32; i += 4)
-                        *reinterpret_cast<int4*>(Y + nb + i) =
-                            make_int4((int)acc[i], (int)acc[i + 1], (int)acc[i + 2], (int)acc[i + 3]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 32; i++)
-                        if (nb + i < g.N) Y[nb + i] = (int)acc[i];
-                }
-            } else {
-                const int Nw = (g.N + 127) / 128 * 4;
-                const int word = nb / 32;
-                if (word >= Nw) continue;
-                uint32_t qb[8];
-#pragma unroll
-                for (int i = 0; i < 8; i++) qb[i] = 0;
-#pragma unroll
-                for (int i = 0; i < 32; i++) {
-                    const int n = nb + i;
-                    uint32_t qv = 0;
-                    if (n < g.N) qv = requant(e, (int32_t)acc[i], epi_alpha(e, n), epi_beta(e, n));
-                    qb[i >> 2] |= qv << (8 * (i & 3));
-                }
-                uint32_t* o = reinterpret_cast<uint32_t*>(p.Y) + (long long)m * e.out_bits * Nw + word;
-                for (int tb = 0; tb < e.out_bits; tb++) {
-                    uint32_t wv = 0;
-#pragma unroll
-                    for (int qq = 0; qq < 8; qq++) wv |= byte_bits_to_nibble(qb[qq], tb) << (4 * qq);
-                    o[(long long)tb * Nw] = wv;
-                }
-            }
+            epilogue_chunk(acc, m, n0 + c, c, g, p.e, p.Y, p.use_tab ? sTab : nullptr);
         }
     }
 
@@ -340,8 +379,8 @@ static PFN_encodeTiled get_encode() {
 }
 
 // Packed operand [rows][bits][Cw] viewed as a 3-D uint32 tensor {Cw, rows, bits}
-// (dims listed innermost first); box {4 words = 128 elements, box_rows, bits}
-// lands in shared memory as [plane][row][16 B].
+// (innermost first); box {4 words = 128 elements, box_rows, bits} lands in shared
+// memory as [plane][row][16 B] (conflict-free row-per-thread reads).
 static bool make_plane_map(CUtensorMap* m, const uint32_t* base, int rows, int bits, int Cw, int box_rows) {
     PFN_encodeTiled enc = get_encode();
     if (!enc) return false;
@@ -355,6 +394,45 @@ static bool make_plane_map(CUtensorMap* m, const uint32_t* base, int rows, int b
     return r == CUDA_SUCCESS;
 }
 
+static int stage_count(size_t per_stage, size_t fixed) {
+    const size_t budget = 227 * 1024 - fixed;
+    int S = (int)(budget / per_stage);
+    return S > MAX_STAGES ? MAX_STAGES : S;
+}
+
+template <typename K>
+static cudaError_t set_smem(K kfn) {
+    return cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
+
+template <bool AP, bool WP>
+static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid, size_t smem,
+                           cudaStream_t s) {
+    auto kfn = tc2_kernel<AP, WP>;
+    cudaError_t e = set_smem(kfn);
+    if (e != cudaSuccess) return e;
+    kfn<<<grid, T2_THREADS, smem, s>>>(ta, tb, p);
+    return cudaGetLastError();
+}
+
+template <int BN, bool AP, bool WP>
+static cudaError_t launch1(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, dim3 grid, size_t smem,
+                           cudaStream_t s) {
+    auto kfn = tc1_kernel<BN, AP, WP>;
+    cudaError_t e = set_smem(kfn);
+    if (e != cudaSuccess) return e;
+    kfn<<<grid, T1_THREADS, smem, s>>>(ta, tb, p);
+    return cudaGetLastError();
+}
+
+template <bool AP, bool WP>
+static cudaError_t launch1_bn(int BN, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, dim3 grid,
+                              size_t smem, cudaStream_t s) {
+    if (BN == 256) return launch1<256, AP, WP>(ta, tb, p, grid, smem, s);
+    if (BN == 128) return launch1<128, AP, WP>(ta, tb, p, grid, smem, s);
+    return launch1<64, AP, WP>(ta, tb, p, grid, smem, s);
+}
+
 }  // namespace tc
 
 bool tc_i8_supports(const Geom& g) {
@@ -362,64 +440,75 @@ bool tc_i8_supports(const Geom& g) {
     return !g.conv && g.K > 0 && g.M > 0 && g.N > 0;
 }
 
-template <int BN, bool AP, bool WP>
-static cudaError_t launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& p, dim3 grid,
-                               size_t smem, cudaStream_t s) {
-    auto kfn = tc::tc_i8_gemm_kernel<BN, AP, WP>;
-    static bool attr_set = false;  // per-instantiation; benign race (same value)
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
+// variant knob for experiments: APNN_TC_KERNEL=1 forces the 1-CTA kernel
+static int tc_kernel_override() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("APNN_TC_KERNEL");
+        v = s ? atoi(s) : 0;
     }
-    kfn<<<grid, tc::NT, smem, s>>>(ta, tb, p);
-    return cudaGetLastError();
-}
-
-template <int BN>
-static cudaError_t launch_tc_bn(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& p, dim3 grid,
-                                size_t smem, cudaStream_t s) {
-    switch (p.g.enc) {
-    case APNN_ENC_01_01: return launch_tc_t<BN, false, false>(ta, tb, p, grid, smem, s);
-    case APNN_ENC_PM1_PM1: return launch_tc_t<BN, true, true>(ta, tb, p, grid, smem, s);
-    case APNN_ENC_W_PM1_A_01: return launch_tc_t<BN, false, true>(ta, tb, p, grid, smem, s);
-    default: return launch_tc_t<BN, true, false>(ta, tb, p, grid, smem, s);
-    }
+    return v;
 }
 
 cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y, int sms,
                          cudaStream_t s) {
-    (void)sms;
-    const int BN = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
-    tc::Params p;
+    using namespace tc;
+    Params p;
     p.g = g;
     p.e = e;
     p.Y = Y;
     p.nkb = g.nchunks;
-    p.a_bytes = 16u * tc::BM * g.a_bits;
-    p.b_bytes = 16u * BN * g.w_bits;
-    const size_t per_stage = (size_t)BN * 128 + p.a_bytes + p.b_bytes;
-    const size_t budget = 227 * 1024 - 1024 - 256;
-    int S = (int)(budget / per_stage);
-    if (S > tc::MAX_STAGES) S = tc::MAX_STAGES;
-    if (S < 2) return cudaErrorInvalidConfiguration;
-    p.stages = S;
-    uint32_t cols = BN + 32 * S;
-    uint32_t pow2 = 32;
-    while (pow2 < cols) pow2 <<= 1;
-    p.tmem_cols = pow2;
-    const size_t smem = (size_t)S * per_stage + (4 * tc::MAX_STAGES + 2) * 8 + 64;
-
-    CUtensorMap ta, tb;
-    if (!tc::make_plane_map(&ta, A, g.M, g.a_bits, g.Cw, tc::BM)) return cudaErrorInvalidValue;
-    if (!tc::make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, BN)) return cudaErrorInvalidValue;
-
+    p.use_tab = (e.out_bits > 0 && e.out_bits <= 4) ? 1 : 0;
     const int ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
-    dim3 grid((g.M + tc::BM - 1) / tc::BM, (ncols + BN - 1) / BN);
+    const bool two = (g.N > 128) && (g.M > 128) && tc_kernel_override() != 1;
+    CUtensorMap ta, tb;
     cudaError_t err;
-    if (BN == 256) err = launch_tc_bn<256>(ta, tb, p, grid, smem, s);
-    else if (BN == 128) err = launch_tc_bn<128>(ta, tb, p, grid, smem, s);
-    else err = launch_tc_bn<64>(ta, tb, p, grid, smem, s);
+    if (two) {
+        p.a_bytes = 16u * 128 * g.a_bits;
+        p.b_bytes = 16u * 128 * g.w_bits;
+        const size_t fixed = (size_t)T2_BN * kTabStride * 4 + (4 * MAX_STAGES + 4) * 8 + 1024;
+        const int S = stage_count((size_t)128 * 128 + p.a_bytes + p.b_bytes, fixed);
+        if (S < 2) return cudaErrorInvalidConfiguration;
+        p.stages = S;
+        p.tmem_cols = 512;
+        p.tiles_m = (g.M + 255) / 256;
+        const int tiles_n = (ncols + T2_BN - 1) / T2_BN;
+        p.num_tiles = p.tiles_m * tiles_n;
+        int clusters = sms / 2;
+        if (clusters > p.num_tiles) clusters = p.num_tiles;
+        const size_t smem = (size_t)S * ((size_t)128 * 128 + p.a_bytes + p.b_bytes) + fixed - 1024 + 64;
+        if (!make_plane_map(&ta, A, g.M, g.a_bits, g.Cw, 128)) return cudaErrorInvalidValue;
+        if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, 128)) return cudaErrorInvalidValue;
+        switch (g.enc) {
+        case APNN_ENC_01_01: err = launch2<false, false>(ta, tb, p, clusters * 2, smem, s); break;
+        case APNN_ENC_PM1_PM1: err = launch2<true, true>(ta, tb, p, clusters * 2, smem, s); break;
+        case APNN_ENC_W_PM1_A_01: err = launch2<false, true>(ta, tb, p, clusters * 2, smem, s); break;
+        default: err = launch2<true, false>(ta, tb, p, clusters * 2, smem, s); break;
+        }
+    } else {
+        const int BN = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
+        p.a_bytes = 16u * BM * g.a_bits;
+        p.b_bytes = 16u * BN * g.w_bits;
+        const size_t fixed = (size_t)BN * kTabStride * 4 + (4 * MAX_STAGES + 4) * 8 + 1024;
+        const int S = stage_count((size_t)BN * 128 + p.a_bytes + p.b_bytes, fixed);
+        if (S < 2) return cudaErrorInvalidConfiguration;
+        p.stages = S;
+        uint32_t cols = BN + 32 * S, pow2 = 32;
+        while (pow2 < cols) pow2 <<= 1;
+        p.tmem_cols = pow2;
+        p.tiles_m = 0;
+        p.num_tiles = 0;
+        const size_t smem = (size_t)S * ((size_t)BN * 128 + p.a_bytes + p.b_bytes) + fixed - 1024 + 64;
+        if (!make_plane_map(&ta, A, g.M, g.a_bits, g.Cw, BM)) return cudaErrorInvalidValue;
+        if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, BN)) return cudaErrorInvalidValue;
+        dim3 grid((g.M + BM - 1) / BM, (ncols + BN - 1) / BN);
+        switch (g.enc) {
+        case APNN_ENC_01_01: err = launch1_bn<false, false>(BN, ta, tb, p, grid, smem, s); break;
+        case APNN_ENC_PM1_PM1: err = launch1_bn<true, true>(BN, ta, tb, p, grid, smem, s); break;
+        case APNN_ENC_W_PM1_A_01: err = launch1_bn<false, true>(BN, ta, tb, p, grid, smem, s); break;
+        default: err = launch1_bn<true, false>(BN, ta, tb, p, grid, smem, s); break;
+        }
+    }
     count_launch();
     return err;
 }

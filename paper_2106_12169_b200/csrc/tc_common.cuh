@@ -1,0 +1,239 @@
+// tc_common.cuh -- building blocks of the tcgen05 kind::i8 kernels (gemm_tc.cu):
+//   * plane -> int8 recombination jobs (the operand-side bit combination),
+//   * the epilogue: int32 store, or the fused element-wise routine
+//     (requantise -> bit-decompose -> pack along N).
+#pragma once
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace apnn {
+namespace tc {
+
+// Element order inside a 32-element group (identical for A and B, so the dot
+// product is unchanged): output word j (j = 0..7) holds elements j, j+8, j+16,
+// j+24 in its bytes 0..3.  Word j of group gi sits at K-byte 32*gi + 4*j.
+
+__device__ __forceinline__ uint32_t sel4(const uint4& v, int gi) {
+    return gi == 0 ? v.x : gi == 1 ? v.y : gi == 2 ? v.z : v.w;
+}
+
+// 0/1 codes with NB planes -> u8 lanes: byte = sum_t bit_t << t  (Eq. bitCombination
+// applied to the operand: one shift + one masked OR per plane and word)
+template <int NB>
+__device__ __forceinline__ void decode_01(const uint32_t (&pw)[NB], uint32_t (&out)[8]) {
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        uint32_t o = 0;
+#pragma unroll
+        for (int t = 0; t < NB; t++) {
+            const uint32_t mask = 0x01010101u << t;
+            const uint32_t sh = (j >= t) ? (pw[t] >> (j - t)) : (pw[t] << (t - j));
+            o |= sh & mask;
+        }
+        out[j] = o;
+    }
+}
+
+// +-1 plane -> s8 lanes: bit 1 -> +1 (0x01), bit 0 -> -1 (0xFF);
+// elements outside `vm` decode to 0 (padded K of Case II).
+template <bool kMasked>
+__device__ __forceinline__ void decode_pm1(uint32_t pw, uint32_t vm, uint32_t (&out)[8]) {
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const uint32_t s = (pw >> j) & 0x01010101u;
+        uint32_t o = s * 0xFFFFFF02u + 0xFFFFFFFFu;  // 0xFF - 0xFE*s per byte, no borrows
+        if (kMasked) o &= ((vm >> j) & 0x01010101u) * 0xFFu;
+        out[j] = o;
+    }
+}
+
+__device__ __forceinline__ uint32_t valid_mask(int kvalid, int gi) {
+    const int nv = kvalid - gi * 32;
+    return nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
+}
+
+template <int NB, bool PM1>
+__device__ __forceinline__ void decode_group(const uint4 (&v)[NB], int gi, int kvalid, uint32_t (&o)[8]) {
+    uint32_t pw[NB];
+#pragma unroll
+    for (int pl = 0; pl < NB; pl++) pw[pl] = sel4(v[pl], gi);
+    if (PM1) {
+        if (kvalid >= 128) decode_pm1<false>(pw[0], 0u, o);
+        else decode_pm1<true>(pw[0], valid_mask(kvalid, gi), o);
+    } else {
+        decode_01<NB>(pw, o);
+    }
+}
+
+// A job: one 128-element k-block of one A row -> 32 TMEM columns of the thread's lane.
+// planes: smem [plane][rows][16 B] as written by the TMA box.
+template <int NB, bool PM1>
+__device__ __forceinline__ void a_job(const uint8_t* planes, int rows, int row, uint32_t taddr, int kvalid) {
+    const uint4* src = reinterpret_cast<const uint4*>(planes);
+    uint4 v[NB];
+#pragma unroll
+    for (int pl = 0; pl < NB; pl++) v[pl] = src[pl * rows + row];
+#pragma unroll
+    for (int gi = 0; gi < 4; gi++) {
+        uint32_t o[8];
+        decode_group<NB, PM1>(v, gi, kvalid, o);
+        sm100::tmem_st8(taddr + gi * 8, o);
+    }
+}
+
+// B job: one 128-element k-block of one B row -> UMMA K-major no-swizzle layout:
+// row r, 16-byte chunk c at (r>>3)*1024 + c*128 + (r&7)*16.
+template <int NB, bool PM1>
+__device__ __forceinline__ void b_job(const uint8_t* planes, int rows, int row, uint8_t* bop, int kvalid) {
+    const uint4* src = reinterpret_cast<const uint4*>(planes);
+    uint4 v[NB];
+#pragma unroll
+    for (int pl = 0; pl < NB; pl++) v[pl] = src[pl * rows + row];
+    uint8_t* rbase = bop + (row >> 3) * 1024 + (row & 7) * 16;
+#pragma unroll
+    for (int gi = 0; gi < 4; gi++) {
+        uint32_t o[8];
+        decode_group<NB, PM1>(v, gi, kvalid, o);
+        *reinterpret_cast<uint4*>(rbase + (2 * gi) * 128) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(rbase + (2 * gi + 1) * 128) = make_uint4(o[4], o[5], o[6], o[7]);
+    }
+}
+
+template <bool PM1>
+__device__ __forceinline__ void a_job_any(int nb, const uint8_t* planes, int rows, int row, uint32_t taddr,
+                                          int kvalid) {
+    if (PM1) { a_job<1, true>(planes, rows, row, taddr, kvalid); return; }
+    switch (nb) {  // warp-uniform
+    case 1: a_job<1, false>(planes, rows, row, taddr, kvalid); break;
+    case 2: a_job<2, false>(planes, rows, row, taddr, kvalid); break;
+    case 3: a_job<3, false>(planes, rows, row, taddr, kvalid); break;
+    case 4: a_job<4, false>(planes, rows, row, taddr, kvalid); break;
+    case 5: a_job<5, false>(planes, rows, row, taddr, kvalid); break;
+    case 6: a_job<6, false>(planes, rows, row, taddr, kvalid); break;
+    case 7: a_job<7, false>(planes, rows, row, taddr, kvalid); break;
+    default: a_job<8, false>(planes, rows, row, taddr, kvalid); break;
+    }
+}
+
+template <bool PM1>
+__device__ __forceinline__ void b_job_any(int nb, const uint8_t* planes, int rows, int row, uint8_t* bop,
+                                          int kvalid) {
+    if (PM1) { b_job<1, true>(planes, rows, row, bop, kvalid); return; }
+    switch (nb) {
+    case 1: b_job<1, false>(planes, rows, row, bop, kvalid); break;
+    case 2: b_job<2, false>(planes, rows, row, bop, kvalid); break;
+    case 3: b_job<3, false>(planes, rows, row, bop, kvalid); break;
+    case 4: b_job<4, false>(planes, rows, row, bop, kvalid); break;
+    case 5: b_job<5, false>(planes, rows, row, bop, kvalid); break;
+    case 6: b_job<6, false>(planes, rows, row, bop, kvalid); break;
+    case 7: b_job<7, false>(planes, rows, row, bop, kvalid); break;
+    default: b_job<8, false>(planes, rows, row, bop, kvalid); break;
+    }
+}
+
+// ------------------------------------------------------------------ epilogue
+// Threshold table for out_bits <= 4 (Q = 2^b - 1 <= 15).  For column n:
+//   q = clamp(floor((alpha y + beta)/S), 0, Q) = #{k in 1..Q : y' > U_k},
+//   y' = -y if alpha < 0 else y,
+//   alpha > 0: U_k = ceil((kS - beta)/alpha) - 1
+//   alpha < 0: U_k = -floor((kS - beta)/alpha) - 1
+//   alpha = 0: U_k = INT32_MIN if beta >= kS else INT32_MAX
+// (|y| <= 2^31 - 1 by the host overflow check, so clamping U to int32 is exact.)
+// Row layout: 16 int32 per column: [negate, U_1, ..., U_15].
+constexpr int kTabStride = 16;
+
+__device__ __forceinline__ long long floor_div64(long long a, long long b) {
+    long long q = a / b;
+    if ((a % b != 0) && ((a < 0) != (b < 0))) q -= 1;
+    return q;
+}
+
+__device__ __forceinline__ void build_threshold_row(int32_t* row, int n, int N, const Epi& e) {
+    const int Q = e.qmax;
+    if (n >= N) {  // padding columns: q = 0
+        row[0] = 0;
+        for (int k = 1; k <= 15; k++) row[k] = 0x7FFFFFFF;
+        return;
+    }
+    const long long al = epi_alpha(e, n), be = epi_beta(e, n), S = e.S;
+    row[0] = al < 0 ? 1 : 0;
+    for (int k = 1; k <= 15; k++) {
+        long long U;
+        if (k > Q) {
+            U = 0x7FFFFFFFLL;
+        } else {
+            const long long num = (long long)k * S - be;
+            if (al > 0) U = -floor_div64(-num, al) - 1;  // ceil(num/al) - 1
+            else if (al < 0) U = -floor_div64(num, al) - 1;
+            else U = (be >= (long long)k * S) ? (long long)INT32_MIN : 0x7FFFFFFFLL;
+        }
+        if (U < INT32_MIN) U = INT32_MIN;
+        if (U > 0x7FFFFFFFLL) U = 0x7FFFFFFFLL;
+        row[k] = (int32_t)U;
+    }
+}
+
+__device__ __forceinline__ uint32_t requant_tab(const int32_t* row, int32_t y, int Q) {
+    const int4 h = *reinterpret_cast<const int4*>(row);
+    const int32_t yp = h.x ? -y : y;
+    uint32_t q = (yp > h.y) + (yp > h.z) + (yp > h.w);
+    if (Q > 3) {
+#pragma unroll
+        for (int c = 1; c < 4; c++) {
+            const int4 u = *reinterpret_cast<const int4*>(row + 4 * c);
+            q += (yp > u.x) + (yp > u.y) + (yp > u.z) + (yp > u.w);
+        }
+    }
+    return q;
+}
+
+// 32 accumulators of row m, columns nb..nb+31 (lc = tile-local column of nb).
+// tab: threshold table of the tile (nullptr -> division path / int32 output).
+__device__ __forceinline__ void epilogue_chunk(const uint32_t (&acc)[32], int m, int nb, int lc, const Geom& g,
+                                               const Epi& e, void* Yout, const int32_t* tab) {
+    if (m >= g.M) return;
+    if (e.out_bits == 0) {
+        int32_t* Y = reinterpret_cast<int32_t*>(Yout) + (long long)m * g.N;
+        if (nb + 32 <= g.N && (g.N & 3) == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+                *reinterpret_cast<int4*>(Y + nb + i) =
+                    make_int4((int)acc[i], (int)acc[i + 1], (int)acc[i + 2], (int)acc[i + 3]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; i++)
+                if (nb + i < g.N) Y[nb + i] = (int)acc[i];
+        }
+        return;
+    }
+    const int Nw = (g.N + 127) / 128 * 4;
+    const int word = nb / 32;
+    if (word >= Nw) return;
+    uint32_t qb[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) qb[i] = 0;
+    if (tab) {
+#pragma unroll
+        for (int i = 0; i < 32; i++)
+            qb[i >> 2] |= requant_tab(tab + (lc + i) * kTabStride, (int32_t)acc[i], e.qmax) << (8 * (i & 3));
+    } else {
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            const int n = nb + i;
+            uint32_t qv = 0;
+            if (n < g.N) qv = requant(e, (int32_t)acc[i], epi_alpha(e, n), epi_beta(e, n));
+            qb[i >> 2] |= qv << (8 * (i & 3));
+        }
+    }
+    uint32_t* o = reinterpret_cast<uint32_t*>(Yout) + (long long)m * e.out_bits * Nw + word;
+    for (int tb = 0; tb < e.out_bits; tb++) {
+        uint32_t wv = 0;
+#pragma unroll
+        for (int qq = 0; qq < 8; qq++) wv |= byte_bits_to_nibble(qb[qq], tb) << (4 * qq);
+        o[(long long)tb * Nw] = wv;
+    }
+}
+
+}  // namespace tc
+}  // namespace apnn
