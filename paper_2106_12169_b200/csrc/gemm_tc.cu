@@ -58,7 +58,9 @@ struct Params {
 };
 
 // ============================================================== 2-CTA kernel
-constexpr int T2_THREADS = 14 * 32;
+constexpr int T2_RECOMB_WARPS = 16;  // two teams of 8 warps on alternating k-blocks
+constexpr int T2_EPI_WARP0 = 2 + T2_RECOMB_WARPS;
+constexpr int T2_THREADS = (T2_EPI_WARP0 + 4) * 32;
 constexpr int T2_BN = 256;   // N per pair; 128 B rows per CTA
 
 template <bool A_PM1, bool W_PM1>
@@ -149,16 +151,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 mma2_commit_mc(accum_full, 0x3);
             }
         }
-    } else if (warp < 10) {
+    } else if (warp < T2_EPI_WARP0) {
         // ---------------------------------------------------- recombination
+        // team (0/1) handles k-blocks of its parity, so two k-blocks are in flight
+        // per SM sub-partition; inside a team warps 0-3 decode A rows, 4-7 B rows.
         const int q = warp & 3;
-        const int grp = (warp - 2) >> 2;
+        const int team = (warp - 2) >> 3;
+        const int grp = ((warp - 2) >> 2) & 1;
         const int t = q * 32 + lane;
         const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
         const uint32_t op_full0 = mapa(smem_u32(op_full), 0);
         int it = 0;
         for (int tile = cid; tile < p.num_tiles; tile += ncl) {
             for (int kb = 0; kb < nkb; kb++, it++) {
+                if ((it & 1) != team) continue;
                 const int s = it % S;
                 const uint32_t ph = (it / S) & 1;
                 int kvalid = 128;
@@ -168,7 +174,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 }
                 mbar_wait(&plane_full[s], ph);
                 mbar_wait(&op_empty[s], ph ^ 1);
-                if ((it & 1) == grp) {
+                if (grp == 0) {
                     a_job_any<A_PM1>(g.a_bits, sApl + (size_t)s * p.a_bytes, 128, t,
                                      tmem_lane + A_COL + s * 32, kvalid);
                     tmem_wait_st();
@@ -189,7 +195,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
         // ---------------------------------------------------- epilogue
         const int q = warp & 3;
         const int t = q * 32 + lane;               // row in this CTA's 128
-        const int et = threadIdx.x - 10 * 32;      // 0..127
+        const int et = threadIdx.x - T2_EPI_WARP0 * 32;  // 0..127
         const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
         const uint32_t accum_empty0 = mapa(smem_u32(accum_empty), 0);
         int tc = 0;
