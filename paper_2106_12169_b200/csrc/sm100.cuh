@@ -185,15 +185,20 @@ __device__ __forceinline__ uint32_t mapa(uint32_t local_addr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
     return r;
 }
-// arrive (release at cluster scope) on an mbarrier given by a shared::cluster address
+// arrive on an mbarrier given by a shared::cluster address (possibly in the peer CTA).
+// Default .release.cta semantics, as CUTLASS's ClusterBarrier::arrive(cta_id): the
+// operand data it publishes was already handed to the async proxy by
+// fence.proxy.async / tcgen05.wait::st + tcgen05.fence::before_thread_sync, and a
+// .release.cluster arrive would cost a MEMBAR.ALL.GPU per k-block (measured: the
+// top stall of the 2-CTA kernel, profiles/r01_*).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
         : "r"(addr), "r"(parity)

@@ -235,5 +235,26 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&acc)[32], int m,
     }
 }
 
+// Threshold-table requant of one 32-column chunk straight to plane words:
+// words[t] bit i = bit t of q(column lc + i), t < out_bits <= 4.
+__device__ __forceinline__ void requant_chunk_words(const uint32_t (&acc)[32], const int32_t* tab, int lc, int Q,
+                                                    int out_bits, uint32_t (&words)[4]) {
+    uint32_t qb[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) qb[i] = 0;
+#pragma unroll
+    for (int i = 0; i < 32; i++)
+        qb[i >> 2] |= requant_tab(tab + (lc + i) * kTabStride, (int32_t)acc[i], Q) << (8 * (i & 3));
+#pragma unroll
+    for (int tb = 0; tb < 4; tb++) {
+        uint32_t wv = 0;
+        if (tb < out_bits) {
+#pragma unroll
+            for (int qq = 0; qq < 8; qq++) wv |= byte_bits_to_nibble(qb[qq], tb) << (4 * qq);
+        }
+        words[tb] = wv;
+    }
+}
+
 }  // namespace tc
 }  // namespace apnn
