@@ -210,40 +210,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             }
             mbar_wait(accum_full, tc & 1);
             tc_fence_after();
-            const int Nw = (g.N + 127) / 128 * 4;
-            if (p.use_tab && n0 / 32 + 8 <= Nw) {
-                // packed output: all 8 words of each plane of this row segment in
-                // registers, then two 16-byte stores per plane
-                uint32_t wv[4][8];
-#pragma unroll
-                for (int c = 0; c < 8; c++) {
-                    uint32_t acc[32];
-                    tmem_ld32(tmem_lane + c * 32, acc);
-                    tmem_wait_ld();
-                    uint32_t w4[4];
-                    requant_chunk_words(acc, sTab, c * 32, p.e.qmax, p.e.out_bits, w4);
-#pragma unroll
-                    for (int tb = 0; tb < 4; tb++) wv[tb][c] = w4[tb];
-                }
-                if (m < g.M) {
-                    uint32_t* o = reinterpret_cast<uint32_t*>(p.Y) + (long long)m * p.e.out_bits * Nw + n0 / 32;
-#pragma unroll
-                    for (int tb = 0; tb < 4; tb++) {
-                        if (tb < p.e.out_bits) {
-                            uint4* d = reinterpret_cast<uint4*>(o + (long long)tb * Nw);
-                            d[0] = make_uint4(wv[tb][0], wv[tb][1], wv[tb][2], wv[tb][3]);
-                            d[1] = make_uint4(wv[tb][4], wv[tb][5], wv[tb][6], wv[tb][7]);
-                        }
-                    }
-                }
-            } else {
 #pragma unroll 1
-                for (int c = 0; c < T2_BN; c += 32) {
-                    uint32_t acc[32];
-                    tmem_ld32(tmem_lane + c, acc);
-                    tmem_wait_ld();
-                    epilogue_chunk(acc, m, n0 + c, c, g, p.e, p.Y, p.use_tab ? sTab : nullptr);
-                }
+            for (int c = 0; c < T2_BN; c += 32) {
+                uint32_t acc[32];
+                tmem_ld32(tmem_lane + c, acc);
+                tmem_wait_ld();
+                epilogue_chunk(acc, m, n0 + c, c, g, p.e, p.Y, p.use_tab ? sTab : nullptr);
             }
             tc_fence_before();
             __syncwarp();

@@ -174,11 +174,12 @@ __device__ __forceinline__ void build_threshold_row(int32_t* row, int n, int N, 
     }
 }
 
-__device__ __forceinline__ uint32_t requant_tab(const int32_t* row, int32_t y, int Q) {
+template <bool kSmallQ>  // kSmallQ: Q <= 3 (out_bits <= 2), one 16-byte table read
+__device__ __forceinline__ uint32_t requant_tab(const int32_t* row, int32_t y) {
     const int4 h = *reinterpret_cast<const int4*>(row);
     const int32_t yp = h.x ? -y : y;
     uint32_t q = (yp > h.y) + (yp > h.z) + (yp > h.w);
-    if (Q > 3) {
+    if (!kSmallQ) {
 #pragma unroll
         for (int c = 1; c < 4; c++) {
             const int4 u = *reinterpret_cast<const int4*>(row + 4 * c);
@@ -186,6 +187,28 @@ __device__ __forceinline__ uint32_t requant_tab(const int32_t* row, int32_t y, i
         }
     }
     return q;
+}
+
+// Threshold-table requant of one 32-column chunk straight to plane words:
+// words[t] bit i = bit t of q(column lc + i), t < out_bits <= 4.
+template <bool kSmallQ>
+__device__ __forceinline__ void requant_chunk_words(const uint32_t (&acc)[32], const int32_t* tab, int lc,
+                                                    int out_bits, uint32_t (&words)[4]) {
+    uint32_t qb[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) qb[i] = 0;
+#pragma unroll
+    for (int i = 0; i < 32; i++)
+        qb[i >> 2] |= requant_tab<kSmallQ>(tab + (lc + i) * kTabStride, (int32_t)acc[i]) << (8 * (i & 3));
+#pragma unroll
+    for (int tb = 0; tb < 4; tb++) {
+        uint32_t wv = 0;
+        if (tb < out_bits) {
+#pragma unroll
+            for (int qq = 0; qq < 8; qq++) wv |= byte_bits_to_nibble(qb[qq], tb) << (4 * qq);
+        }
+        words[tb] = wv;
+    }
 }
 
 // 32 accumulators of row m, columns nb..nb+31 (lc = tile-local column of nb).
@@ -210,49 +233,31 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&acc)[32], int m,
     const int Nw = (g.N + 127) / 128 * 4;
     const int word = nb / 32;
     if (word >= Nw) return;
+    uint32_t* o = reinterpret_cast<uint32_t*>(Yout) + (long long)m * e.out_bits * Nw + word;
+    if (tab) {
+        uint32_t w4[4];
+        if (e.out_bits <= 2) requant_chunk_words<true>(acc, tab, lc, e.out_bits, w4);
+        else requant_chunk_words<false>(acc, tab, lc, e.out_bits, w4);
+#pragma unroll
+        for (int tb = 0; tb < 4; tb++)
+            if (tb < e.out_bits) o[(long long)tb * Nw] = w4[tb];
+        return;
+    }
     uint32_t qb[8];
 #pragma unroll
     for (int i = 0; i < 8; i++) qb[i] = 0;
-    if (tab) {
 #pragma unroll
-        for (int i = 0; i < 32; i++)
-            qb[i >> 2] |= requant_tab(tab + (lc + i) * kTabStride, (int32_t)acc[i], e.qmax) << (8 * (i & 3));
-    } else {
-#pragma unroll
-        for (int i = 0; i < 32; i++) {
-            const int n = nb + i;
-            uint32_t qv = 0;
-            if (n < g.N) qv = requant(e, (int32_t)acc[i], epi_alpha(e, n), epi_beta(e, n));
-            qb[i >> 2] |= qv << (8 * (i & 3));
-        }
+    for (int i = 0; i < 32; i++) {
+        const int n = nb + i;
+        uint32_t qv = 0;
+        if (n < g.N) qv = requant(e, (int32_t)acc[i], epi_alpha(e, n), epi_beta(e, n));
+        qb[i >> 2] |= qv << (8 * (i & 3));
     }
-    uint32_t* o = reinterpret_cast<uint32_t*>(Yout) + (long long)m * e.out_bits * Nw + word;
     for (int tb = 0; tb < e.out_bits; tb++) {
         uint32_t wv = 0;
 #pragma unroll
         for (int qq = 0; qq < 8; qq++) wv |= byte_bits_to_nibble(qb[qq], tb) << (4 * qq);
         o[(long long)tb * Nw] = wv;
-    }
-}
-
-// Threshold-table requant of one 32-column chunk straight to plane words:
-// words[t] bit i = bit t of q(column lc + i), t < out_bits <= 4.
-__device__ __forceinline__ void requant_chunk_words(const uint32_t (&acc)[32], const int32_t* tab, int lc, int Q,
-                                                    int out_bits, uint32_t (&words)[4]) {
-    uint32_t qb[8];
-#pragma unroll
-    for (int i = 0; i < 8; i++) qb[i] = 0;
-#pragma unroll
-    for (int i = 0; i < 32; i++)
-        qb[i >> 2] |= requant_tab(tab + (lc + i) * kTabStride, (int32_t)acc[i], Q) << (8 * (i & 3));
-#pragma unroll
-    for (int tb = 0; tb < 4; tb++) {
-        uint32_t wv = 0;
-        if (tb < out_bits) {
-#pragma unroll
-            for (int qq = 0; qq < 8; qq++) wv |= byte_bits_to_nibble(qb[qq], tb) << (4 * qq);
-        }
-        words[tb] = wv;
     }
 }
 
