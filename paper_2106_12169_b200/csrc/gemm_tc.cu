@@ -48,6 +48,7 @@ struct Params {
     Geom g;
     Epi e;
     void* Y;
+    const uint32_t* A;  // raw packed activations (conv gathers rows from here)
     int stages;
     int nkb;            // k-blocks per tile
     uint32_t a_bytes;   // A plane bytes per stage (this CTA's rows)
@@ -93,7 +94,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
         tma_prefetch(&tmapA);
         tma_prefetch(&tmapB);
         for (int s = 0; s < S; s++) {
-            mbar_init(&plane_full[s], 1);
+            mbar_init(&plane_full[s], g.conv ? 1 + 32 : 1);  // conv: + one cp.async arrival per gather lane
             mbar_init(&plane_empty[s], 8);
             mbar_init(&op_full[s], 16);   // 8 recombination warps x 2 CTAs
             mbar_init(&op_empty[s], 1);
@@ -112,18 +113,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
 
     if (warp == 0) {
         // ---------------------------------------------------- TMA producer
-        if (lane == 0) {
+        // (conv: the whole warp also gathers the A rows of each filter tap)
+        const bool conv = g.conv;
+        if (conv || lane == 0) {
+            RowCtx rc[4];
             int it = 0;
             for (int tile = cid; tile < p.num_tiles; tile += ncl) {
                 const int m0 = (tile % p.tiles_m) * 256 + rank * 128;
                 const int nr0 = (tile / p.tiles_m) * T2_BN + rank * 128;
+                if (conv) {
+#pragma unroll
+                    for (int i = 0; i < 4; i++) rc[i] = make_row(g, m0 + lane + 32 * i);
+                }
                 for (int kb = 0; kb < nkb; kb++, it++) {
                     const int s = it % S;
                     const uint32_t ph = (it / S) & 1;
                     mbar_wait(&plane_empty[s], ph ^ 1);
-                    mbar_arrive_expect_tx(&plane_full[s], p.a_bytes + p.b_bytes);
-                    tma_load_3d(sApl + (size_t)s * p.a_bytes, &tmapA, &plane_full[s], kb * 4, m0, 0);
-                    tma_load_3d(sBpl + (size_t)s * p.b_bytes, &tmapB, &plane_full[s], kb * 4, nr0, 0);
+                    if (lane == 0) {
+                        const int rs = conv ? kb / g.CB : 0;
+                        const int cb = conv ? kb - rs * g.CB : kb;
+                        mbar_arrive_expect_tx(&plane_full[s], (conv ? 0u : p.a_bytes) + p.b_bytes);
+                        if (!conv) tma_load_4d(sApl + (size_t)s * p.a_bytes, &tmapA, &plane_full[s], kb * 4, m0, 0, 0);
+                        tma_load_4d(sBpl + (size_t)s * p.b_bytes, &tmapB, &plane_full[s], cb * 4, nr0, 0, rs);
+                    }
+                    if (conv) conv_gather_kb<4>(p.A, g, rc, kb, sApl + (size_t)s * p.a_bytes, 128, lane, &plane_full[s]);
                 }
             }
         }
@@ -163,14 +176,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
         const uint32_t op_full0 = mapa(smem_u32(op_full), 0);
         int it = 0;
         for (int tile = cid; tile < p.num_tiles; tile += ncl) {
+            RowCtx rc;
+            if (A_PM1 && g.conv) rc = make_row(g, (tile % p.tiles_m) * 256 + rank * 128 + t);
             for (int kb = 0; kb < nkb; kb++, it++) {
                 if ((it & 1) != team) continue;
                 const int s = it % S;
                 const uint32_t ph = (it / S) & 1;
-                int kvalid = 128;
-                if (A_PM1 && W_PM1) {
-                    const int rem = g.K - kb * 128;
-                    kvalid = rem < 128 ? rem : 128;
+                int kvalid = 128;  // +-1 activations: elements beyond kvalid decode to 0
+                if (A_PM1) {
+                    if (g.conv) {
+                        kvalid = conv_kvalid(g, rc, kb_tap(g, kb));
+                    } else if (W_PM1) {
+                        const int rem = g.K - kb * 128;
+                        kvalid = rem < 128 ? rem : 128;
+                    }
                 }
                 mbar_wait(&plane_full[s], ph);
                 mbar_wait(&op_empty[s], ph ^ 1);
@@ -263,7 +282,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
         tma_prefetch(&tmapA);
         tma_prefetch(&tmapB);
         for (int s = 0; s < S; s++) {
-            mbar_init(&plane_full[s], 1);
+            mbar_init(&plane_full[s], g.conv ? 1 + 32 : 1);
             mbar_init(&plane_empty[s], 8);
             mbar_init(&op_full[s], 8);
             mbar_init(&op_empty[s], 1);
@@ -279,14 +298,25 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
     constexpr uint32_t A_COL = BN;
 
     if (warp == 0) {
-        if (lane == 0) {
+        const bool conv = g.conv;
+        if (conv || lane == 0) {
+            RowCtx rc[4];
+            if (conv) {
+#pragma unroll
+                for (int i = 0; i < 4; i++) rc[i] = make_row(g, m0 + lane + 32 * i);
+            }
             for (int kb = 0; kb < nkb; kb++) {
                 const int s = kb % S;
                 const uint32_t ph = (kb / S) & 1;
                 mbar_wait(&plane_empty[s], ph ^ 1);
-                mbar_arrive_expect_tx(&plane_full[s], p.a_bytes + p.b_bytes);
-                tma_load_3d(sApl + (size_t)s * p.a_bytes, &tmapA, &plane_full[s], kb * 4, m0, 0);
-                tma_load_3d(sBpl + (size_t)s * p.b_bytes, &tmapB, &plane_full[s], kb * 4, n0, 0);
+                if (lane == 0) {
+                    const int rs = conv ? kb / g.CB : 0;
+                    const int cb = conv ? kb - rs * g.CB : kb;
+                    mbar_arrive_expect_tx(&plane_full[s], (conv ? 0u : p.a_bytes) + p.b_bytes);
+                    if (!conv) tma_load_4d(sApl + (size_t)s * p.a_bytes, &tmapA, &plane_full[s], kb * 4, m0, 0, 0);
+                    tma_load_4d(sBpl + (size_t)s * p.b_bytes, &tmapB, &plane_full[s], cb * 4, n0, 0, rs);
+                }
+                if (conv) conv_gather_kb<4>(p.A, g, rc, kb, sApl + (size_t)s * p.a_bytes, BM, lane, &plane_full[s]);
             }
         }
     } else if (warp == 1) {
@@ -314,13 +344,19 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
         const int et = threadIdx.x - 64;  // 0..255
         const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
         if (p.use_tab && et < BN) build_threshold_row(sTab + et * kTabStride, n0 + et, g.N, p.e);
+        RowCtx rc;
+        if (A_PM1 && g.conv) rc = make_row(g, m0 + t);
         for (int kb = 0; kb < nkb; kb++) {
             const int s = kb % S;
             const uint32_t ph = (kb / S) & 1;
             int kvalid = 128;
-            if (A_PM1 && W_PM1) {
-                const int rem = g.K - kb * 128;
-                kvalid = rem < 128 ? rem : 128;
+            if (A_PM1) {
+                if (g.conv) {
+                    kvalid = conv_kvalid(g, rc, kb_tap(g, kb));
+                } else if (W_PM1) {
+                    const int rem = g.K - kb * 128;
+                    kvalid = rem < 128 ? rem : 128;
+                }
             }
             mbar_wait(&plane_full[s], ph);
             mbar_wait(&op_empty[s], ph ^ 1);
@@ -384,17 +420,19 @@ static PFN_encodeTiled get_encode() {
     return fn;
 }
 
-// Packed operand [rows][bits][Cw] viewed as a 3-D uint32 tensor {Cw, rows, bits}
-// (innermost first); box {4 words = 128 elements, box_rows, bits} lands in shared
-// memory as [plane][row][16 B] (conflict-free row-per-thread reads).
-static bool make_plane_map(CUtensorMap* m, const uint32_t* base, int rows, int bits, int Cw, int box_rows) {
+// Packed operand [rows][RS][bits][Cw] (GEMM: RS = 1; conv weights: RS = R*S taps)
+// viewed as a 4-D uint32 tensor {Cw, rows, bits, RS} (innermost first).  The box
+// {4 words = 128 elements, box_rows, bits, 1} lands in shared memory as
+// [plane][row][16 B] (conflict-free row-per-thread reads); coordinates
+// {cb*4, row0, 0, tap}.
+static bool make_plane_map(CUtensorMap* m, const uint32_t* base, int rows, int bits, int Cw, int RS, int box_rows) {
     PFN_encodeTiled enc = get_encode();
     if (!enc) return false;
-    cuuint64_t dims[3] = {(cuuint64_t)Cw, (cuuint64_t)rows, (cuuint64_t)bits};
-    cuuint64_t strides[2] = {(cuuint64_t)bits * Cw * 4, (cuuint64_t)Cw * 4};
-    cuuint32_t box[3] = {4, (cuuint32_t)box_rows, (cuuint32_t)bits};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(base), dims, strides, box, estr,
+    cuuint64_t dims[4] = {(cuuint64_t)Cw, (cuuint64_t)rows, (cuuint64_t)bits, (cuuint64_t)RS};
+    cuuint64_t strides[3] = {(cuuint64_t)RS * bits * Cw * 4, (cuuint64_t)Cw * 4, (cuuint64_t)bits * Cw * 4};
+    cuuint32_t box[4] = {4, (cuuint32_t)box_rows, (cuuint32_t)bits, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint32_t*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -442,8 +480,8 @@ static cudaError_t launch1_bn(int BN, const CUtensorMap& ta, const CUtensorMap& 
 }  // namespace tc
 
 bool tc_i8_supports(const Geom& g) {
-    // GEMM only for now (conv runs on the popc variant); K = 0 has no MMA to issue
-    return !g.conv && g.K > 0 && g.M > 0 && g.N > 0;
+    // GEMM and implicit-GEMM conv; K = 0 has no MMA to issue (handled by the popc variant)
+    return g.K > 0 && g.M > 0 && g.N > 0;
 }
 
 // variant knob for experiments: APNN_TC_KERNEL=1 forces the 1-CTA kernel
@@ -463,6 +501,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     p.g = g;
     p.e = e;
     p.Y = Y;
+    p.A = A;
     p.nkb = g.nchunks;
     p.use_tab = (e.out_bits > 0 && e.out_bits <= 4) ? 1 : 0;
     const int ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
@@ -483,8 +522,8 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         int clusters = sms / 2;
         if (clusters > p.num_tiles) clusters = p.num_tiles;
         const size_t smem = (size_t)S * ((size_t)128 * 128 + p.a_bytes + p.b_bytes) + fixed - 1024 + 64;
-        if (!make_plane_map(&ta, A, g.M, g.a_bits, g.Cw, 128)) return cudaErrorInvalidValue;
-        if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, 128)) return cudaErrorInvalidValue;
+        if (!make_plane_map(&ta, A, g.conv ? 1 : g.M, g.a_bits, g.Cw, 1, 128)) return cudaErrorInvalidValue;
+        if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, g.RS, 128)) return cudaErrorInvalidValue;
         switch (g.enc) {
         case APNN_ENC_01_01: err = launch2<false, false>(ta, tb, p, clusters * 2, smem, s); break;
         case APNN_ENC_PM1_PM1: err = launch2<true, true>(ta, tb, p, clusters * 2, smem, s); break;
@@ -505,8 +544,8 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         p.tiles_m = 0;
         p.num_tiles = 0;
         const size_t smem = (size_t)S * ((size_t)BN * 128 + p.a_bytes + p.b_bytes) + fixed - 1024 + 64;
-        if (!make_plane_map(&ta, A, g.M, g.a_bits, g.Cw, BM)) return cudaErrorInvalidValue;
-        if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, BN)) return cudaErrorInvalidValue;
+        if (!make_plane_map(&ta, A, g.conv ? 1 : g.M, g.a_bits, g.Cw, 1, BM)) return cudaErrorInvalidValue;
+        if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, g.RS, BN)) return cudaErrorInvalidValue;
         dim3 grid((g.M + BM - 1) / BM, (ncols + BN - 1) / BN);
         switch (g.enc) {
         case APNN_ENC_01_01: err = launch1_bn<false, false>(BN, ta, tb, p, grid, smem, s); break;

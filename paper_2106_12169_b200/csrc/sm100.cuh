@@ -240,6 +240,16 @@ __device__ __forceinline__ void mma2_commit_mc(uint64_t* bar, uint16_t mask) {
         : "memory");
 }
 
+// 16-byte cp.async with zero fill (src_bytes = 0 -> 16 zero bytes, nothing read)
+__device__ __forceinline__ void cp_async16_zfill(uint32_t smem_dst, const void* gsrc, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_dst), "l"(gsrc), "r"(src_bytes)
+                 : "memory");
+}
+// arrive on `bar` once all prior cp.async of this thread have landed (count pre-armed: .noinc)
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

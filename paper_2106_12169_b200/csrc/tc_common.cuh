@@ -132,6 +132,56 @@ __device__ __forceinline__ void b_job_any(int nb, const uint8_t* planes, int row
     }
 }
 
+// ------------------------------------------------------- conv A-row gather
+// Implicit GEMM (APConv as GEMM): k-block kb is filter tap
+// rs = kb / CB and channel block cb = kb % CB; A row m is output pixel
+// (b, ho, wo) and reads input pixel (ho*st + r - pad, wo*st + s - pad).
+struct KbTap {
+    int r, s, cb;
+};
+__device__ __forceinline__ KbTap kb_tap(const Geom& g, int kb) {
+    KbTap t;
+    const int rs = kb / g.CB;
+    t.cb = kb - rs * g.CB;
+    t.r = rs / g.S;
+    t.s = rs - t.r * g.S;
+    return t;
+}
+// plane-0 address of the chunk, or nullptr when the tap is out of frame / row >= M
+__device__ __forceinline__ const uint32_t* conv_a_src(const uint32_t* X, const Geom& g, const RowCtx& c,
+                                                      const KbTap& t) {
+    const int hi = c.hb + t.r, wi = c.wb + t.s;
+    if (!c.valid || hi < 0 || hi >= g.H || wi < 0 || wi >= g.W) return nullptr;
+    return X + ((c.pix + (long long)hi * g.W + wi) * g.a_bits) * g.Cw + t.cb * 4;
+}
+// logical elements of the chunk for +-1 activations: 0 out of frame (value-domain
+// zero padding), else the unpadded channels of block cb
+__device__ __forceinline__ int conv_kvalid(const Geom& g, const RowCtx& c, const KbTap& t) {
+    const int hi = c.hb + t.r, wi = c.wb + t.s;
+    if (!c.valid || hi < 0 || hi >= g.H || wi < 0 || wi >= g.W) return 0;
+    const int rem = g.C - t.cb * 128;
+    return rem < 128 ? rem : 128;
+}
+// one warp gathers `rows` A rows (lane, lane+32, ...) of k-block kb into the
+// plane stage [plane][rows][16 B] with zero-filling cp.async, then arms the
+// stage's mbarrier (one .noinc arrival per lane).
+template <int kRowsPerLane>
+__device__ __forceinline__ void conv_gather_kb(const uint32_t* X, const Geom& g, const RowCtx (&rc)[kRowsPerLane],
+                                               int kb, uint8_t* stage, int rows, int lane, uint64_t* bar) {
+    const KbTap t = kb_tap(g, kb);
+    const uint32_t sbase = sm100::smem_u32(stage);
+#pragma unroll
+    for (int i = 0; i < kRowsPerLane; i++) {
+        const int row = lane + 32 * i;
+        if (row >= rows) break;
+        const uint32_t* src = conv_a_src(X, g, rc[i], t);
+        for (int pl = 0; pl < g.a_bits; pl++)
+            sm100::cp_async16_zfill(sbase + (pl * rows + row) * 16, src ? src + (long long)pl * g.Cw : X,
+                                    src ? 16u : 0u);
+    }
+    sm100::cp_async_mbar_arrive_noinc(bar);
+}
+
 // ------------------------------------------------------------------ epilogue
 // Threshold table for out_bits <= 4 (Q = 2^b - 1 <= 15).  For column n:
 //   q = clamp(floor((alpha y + beta)/S), 0, Q) = #{k in 1..Q : y' > U_k},

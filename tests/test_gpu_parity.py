@@ -29,7 +29,7 @@ def supported(variant, M, N, K, a, w, enc, conv=False):
     if variant == ap.VARIANT_B1MMA and conv and enc in (1, 3):
         return False
     if variant == ap.VARIANT_TC_I8 and conv:
-        return ap.conv_supported_tc() if hasattr(ap, "conv_supported_tc") else False
+        return K > 0
     if variant == ap.VARIANT_TC_I8:
         return ap.select_variant(max(M, 1), max(N, 1), max(K, 1), a, w, enc) == ap.VARIANT_TC_I8
     return True
