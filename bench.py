@@ -143,9 +143,9 @@ def oracle_sample(A, W, args, seconds, out_bits, alpha, beta, S):
         dt = time.perf_counter() - t0
         t_used += dt
         done_rows = rows
-        if t_used >= seconds * 0.3 or rows >= A.shape[0]:
+        if dt >= seconds * 0.5 or rows >= A.shape[0]:
             break
-        rows = min(A.shape[0], max(rows * 2, int(rows * seconds * 0.5 / max(dt, 1e-3))))
+        rows = min(A.shape[0], max(rows * 2, int(rows * seconds / max(dt, 1e-3))))
     ops = 2.0 * done_rows * W.shape[0] * W.shape[1]
     return {"value": ops / dt / 1e12, "unit": "TOPS", "cores": threads, "kind": "oracle",
             "sample": f"{done_rows} of {A.shape[0]} rows of A x full W (N={W.shape[0]}, K={W.shape[1]}): "
@@ -173,8 +173,9 @@ def run_reference(args):
             times.append(r["value"])
             last = r
     value = statistics.mean(times)
+    full_step_ms = 2.0 * args.M * args.N * args.K / (value * 1e12) * 1e3  # extrapolated: work is linear in M
     line = {"metric": "effective_tops_apmm", "value": value, "unit": "TOPS", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": full_step_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8 codes, int64 accumulate", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"apmm_w{args.w}a{args.a}_{args.M}x{args.N}x{args.K}_fused_pack",
@@ -219,7 +220,8 @@ def run_ours(args):
     Y_packed = torch.empty(ap.packed_shape(M, N, out_bits), dtype=torch.int32, device=dev)
     gathered = None
     if args.allgather and dist is not None:
-        gathered = torch.empty((world,) + tuple(Y_packed.shape), dtype=torch.int32, device=dev)
+        from paper_2106_12169_b200.dist import gather_rows
+        gathered = True
     resolved = variant if variant else ap.select_variant(M, N, K, a, w, enc)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
@@ -232,7 +234,7 @@ def run_ours(args):
         if ev_g1 is not None:
             ev_g1.record(stream)
         if gathered is not None:
-            dist.all_gather_into_tensor(gathered, Y_packed)
+            gather_rows(Y_packed, world * M, None)  # NCCL all-gather: every rank ends with all world*M output rows
 
     # correctness spot check on sampled rows against nothing but the oracle happens in tests;
     # here only warm up
