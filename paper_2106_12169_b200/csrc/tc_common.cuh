@@ -190,7 +190,7 @@ __device__ __forceinline__ void conv_gather_kb(const uint32_t* X, const Geom& g,
 //   alpha < 0: U_k = -floor((kS - beta)/alpha) - 1
 //   alpha = 0: U_k = INT32_MIN if beta >= kS else INT32_MAX
 // (|y| <= 2^31 - 1 by the host overflow check, so clamping U to int32 is exact.)
-// Row layout: 16 int32 per column: [negate, U_1, ..., U_15].
+// Row layout: 16 int32 per column: [sign (+1 / -1), U_1, ..., U_15].
 constexpr int kTabStride = 16;
 
 __device__ __forceinline__ long long floor_div64(long long a, long long b) {
@@ -202,12 +202,12 @@ __device__ __forceinline__ long long floor_div64(long long a, long long b) {
 __device__ __forceinline__ void build_threshold_row(int32_t* row, int n, int N, const Epi& e) {
     const int Q = e.qmax;
     if (n >= N) {  // padding columns: q = 0
-        row[0] = 0;
+        row[0] = 1;
         for (int k = 1; k <= 15; k++) row[k] = 0x7FFFFFFF;
         return;
     }
     const long long al = epi_alpha(e, n), be = epi_beta(e, n), S = e.S;
-    row[0] = al < 0 ? 1 : 0;
+    row[0] = al < 0 ? -1 : 1;
     for (int k = 1; k <= 15; k++) {
         long long U;
         if (k > Q) {
@@ -227,7 +227,7 @@ __device__ __forceinline__ void build_threshold_row(int32_t* row, int n, int N, 
 template <bool kSmallQ>  // kSmallQ: Q <= 3 (out_bits <= 2), one 16-byte table read
 __device__ __forceinline__ uint32_t requant_tab(const int32_t* row, int32_t y) {
     const int4 h = *reinterpret_cast<const int4*>(row);
-    const int32_t yp = h.x ? -y : y;
+    const int32_t yp = y * h.x;
     uint32_t q = (yp > h.y) + (yp > h.z) + (yp > h.w);
     if (!kSmallQ) {
 #pragma unroll
@@ -237,6 +237,23 @@ __device__ __forceinline__ uint32_t requant_tab(const int32_t* row, int32_t y) {
         }
     }
     return q;
+}
+
+// out_bits <= 2 (Q <= 3): with c_k = [y' > U_k] monotone (c1 >= c2 >= c3),
+// q = c1 + c2 + c3, so bit 1 of q is c2 and bit 0 is c1 ^ c2 ^ c3.  Plane words
+// are assembled straight from the comparisons (no byte staging).
+__device__ __forceinline__ void requant_chunk_words_q3(const uint32_t (&acc)[32], const int32_t* tab, int lc,
+                                                       uint32_t& w0, uint32_t& w1) {
+    w0 = 0;
+    w1 = 0;
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+        const int4 h = *reinterpret_cast<const int4*>(tab + (lc + i) * kTabStride);
+        const int32_t yp = (int32_t)acc[i] * h.x;
+        const bool c1 = yp > h.y, c2 = yp > h.z, c3 = yp > h.w;
+        if (c1 ^ c2 ^ c3) w0 |= 1u << i;
+        if (c2) w1 |= 1u << i;
+    }
 }
 
 // Threshold-table requant of one 32-column chunk straight to plane words:
@@ -286,8 +303,13 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&acc)[32], int m,
     uint32_t* o = reinterpret_cast<uint32_t*>(Yout) + (long long)m * e.out_bits * Nw + word;
     if (tab) {
         uint32_t w4[4];
-        if (e.out_bits <= 2) requant_chunk_words<true>(acc, tab, lc, e.out_bits, w4);
-        else requant_chunk_words<false>(acc, tab, lc, e.out_bits, w4);
+        if (e.out_bits <= 2) {
+            requant_chunk_words_q3(acc, tab, lc, w4[0], w4[1]);
+            o[0] = w4[0];
+            if (e.out_bits == 2) o[Nw] = w4[1];
+            return;
+        }
+        requant_chunk_words<false>(acc, tab, lc, e.out_bits, w4);
 #pragma unroll
         for (int tb = 0; tb < 4; tb++)
             if (tb < e.out_bits) o[(long long)tb * Nw] = w4[tb];

@@ -225,3 +225,59 @@ def test_variants_agree_random_bits():
         outs = [run_gemm(A, W, a, w, e, v).cpu().numpy() for v in VARIANTS if supported(v, M, N, K, a, w, e)]
         for o in outs[1:]:
             np.testing.assert_array_equal(o, outs[0])
+
+
+# ------------------------------------------------ full size, bench launch configuration
+
+def _sample_rows(M, n, tag):
+    g = synth.rng(tag)
+    rows = sorted(set([0, 1, 2, 3, M - 4, M - 3, M - 2, M - 1] + g.integers(0, M, size=n).tolist()))
+    return np.array(rows)
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_full_size_bench_config_sampled_rows(fused):
+    # BASELINE.json configs[1] at its largest point, exactly as bench.py runs it:
+    # M = N = K = 8192, w1a2, Case III, auto variant (tcgen05 2-CTA kernel); rows
+    # sampled (first/last 4 + random) and checked against the oracle one by one.
+    M = N = K = 8192
+    a, w, enc = 2, 1, 2
+    A, W = synth.gemm_inputs(M, N, K, a, w, tag="bench")
+    alpha, beta = synth.epilogue_params(N, tag="bench")
+    S = 1 << 10
+    epi = ap.Epilogue(a, cuda(alpha), cuda(beta), S) if fused else None
+    Ap = ap.pack_bits(cuda(A), a)
+    Wp = ap.pack_bits(cuda(W), w)
+    assert ap.select_variant(M, N, K, a, w, enc) == ap.VARIANT_TC_I8
+    Y = ap.gemm(Ap, Wp, M, N, K, a, w, enc, epi=epi)
+    torch.cuda.synchronize()
+    rows = _sample_rows(M, 24, "fullsize")
+    want = oracle.gemm(A[rows], W, a, w, enc)
+    if fused:
+        want = oracle.pack(oracle.epilogue(want, alpha, beta, S, a), a)
+        got = u32(Y)[rows]
+    else:
+        got = Y.cpu().numpy()[rows]
+    np.testing.assert_array_equal(got, want)
+
+
+def test_full_size_w8a8_sampled_rows():
+    M, N, K = 4096, 8192, 8192
+    A, W = synth.gemm_inputs(M, N, K, 8, 8, tag="full88")
+    Y = ap.gemm(ap.pack_bits(cuda(A), 8), ap.pack_bits(cuda(W), 8), M, N, K, 8, 8, 0)
+    torch.cuda.synchronize()
+    rows = _sample_rows(M, 8, "full88")
+    np.testing.assert_array_equal(Y.cpu().numpy()[rows], oracle.gemm(A[rows], W, 8, 8, 0))
+
+
+def test_full_size_resnet_l1_conv_sampled_images():
+    # BASELINE.json configs[2] layer L1 (batch 64, 56x56, 64->64, 3x3, pad 1), w1a2 Case III:
+    # whole output computed on the GPU, images 0 and 63 checked against the oracle.
+    B, H, C, Co = 64, 56, 64, 64
+    X, Wt = synth.conv_inputs(B, H, H, C, Co, 3, 3, 2, 1, tag="l1full")
+    cs = ap.ConvShape(B, H, H, C, Co, 3, 3, 1, 1)
+    Y = ap.conv2d(ap.pack_bits(cuda(X.reshape(-1, C)), 2), ap.pack_bits(cuda(Wt.reshape(-1, C)), 1), cs, 2, 1, 2)
+    torch.cuda.synchronize()
+    Yc = Y.cpu().numpy()
+    for b in (0, B - 1):
+        np.testing.assert_array_equal(Yc[b:b + 1], oracle.conv2d(X[b:b + 1], Wt, 1, 1, 2, 1, 2))
