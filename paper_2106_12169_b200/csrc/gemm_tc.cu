@@ -42,14 +42,16 @@ namespace apnn {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int MAX_STAGES = 8;
+constexpr int MAX_STAGES = 8;     // operand stages (A in TMEM: 32 columns each)
+constexpr int MAX_PSTAGES = 16;   // packed-plane stages of the 2-CTA kernel
 
 struct Params {
     Geom g;
     Epi e;
     void* Y;
     const uint32_t* A;  // raw packed activations (conv gathers rows from here)
-    int stages;
+    int stages;         // operand ring depth
+    int pstages;        // plane ring depth (2-CTA kernel)
     int nkb;            // k-blocks per tile
     uint32_t a_bytes;   // A plane bytes per stage (this CTA's rows)
     uint32_t b_bytes;   // B plane bytes per stage (this CTA's rows)
@@ -70,19 +72,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                const Params p) {
     using namespace sm100;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int S = p.stages;
+    const int S = p.stages, SP = p.pstages;
     uint8_t* sBop = smem;                                        // S x 128 rows x 128 B
-    uint8_t* sApl = sBop + (size_t)S * 128 * 128;                // S x a_bytes
-    uint8_t* sBpl = sApl + (size_t)S * p.a_bytes;                // S x b_bytes
-    int32_t* sTab = reinterpret_cast<int32_t*>(sBpl + (size_t)S * p.b_bytes);  // 256 x 16 int32
+    uint8_t* sApl = sBop + (size_t)S * 128 * 128;                // SP x a_bytes
+    uint8_t* sBpl = sApl + (size_t)SP * p.a_bytes;               // SP x b_bytes
+    int32_t* sTab = reinterpret_cast<int32_t*>(sBpl + (size_t)SP * p.b_bytes);  // 256 x 16 int32
     uint64_t* bars = reinterpret_cast<uint64_t*>(sTab + T2_BN * kTabStride);
-    uint64_t* plane_full = bars;
-    uint64_t* plane_empty = bars + MAX_STAGES;
-    uint64_t* op_full = bars + 2 * MAX_STAGES;     // used in CTA 0
-    uint64_t* op_empty = bars + 3 * MAX_STAGES;
-    uint64_t* accum_full = bars + 4 * MAX_STAGES;
-    uint64_t* accum_empty = bars + 4 * MAX_STAGES + 1;  // used in CTA 0
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * MAX_STAGES + 2);
+    uint64_t* plane_full = bars;                                   // [MAX_PSTAGES]
+    uint64_t* plane_empty = bars + MAX_PSTAGES;                    // [MAX_PSTAGES]
+    uint64_t* op_full = bars + 2 * MAX_PSTAGES;                    // [MAX_STAGES], used in CTA 0
+    uint64_t* op_empty = op_full + MAX_STAGES;                     // [MAX_STAGES]
+    uint64_t* accum_full = op_empty + MAX_STAGES;
+    uint64_t* accum_empty = accum_full + 1;                        // used in CTA 0
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accum_empty + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = cluster_ctarank();
@@ -93,9 +95,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmapA);
         tma_prefetch(&tmapB);
-        for (int s = 0; s < S; s++) {
+        for (int s = 0; s < SP; s++) {
             mbar_init(&plane_full[s], g.conv ? 1 + 32 : 1);  // conv: + one cp.async arrival per gather lane
             mbar_init(&plane_empty[s], 8);
+        }
+        for (int s = 0; s < S; s++) {
             mbar_init(&op_full[s], 16);   // 8 recombination warps x 2 CTAs
             mbar_init(&op_empty[s], 1);
         }
@@ -126,8 +130,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                     for (int i = 0; i < 4; i++) rc[i] = make_row(g, m0 + lane + 32 * i);
                 }
                 for (int kb = 0; kb < nkb; kb++, it++) {
-                    const int s = it % S;
-                    const uint32_t ph = (it / S) & 1;
+                    const int s = it % SP;
+                    const uint32_t ph = (it / SP) & 1;
                     mbar_wait(&plane_empty[s], ph ^ 1);
                     if (lane == 0) {
                         const int rs = conv ? kb / g.CB : 0;
@@ -191,23 +195,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                         kvalid = rem < 128 ? rem : 128;
                     }
                 }
-                mbar_wait(&plane_full[s], ph);
-                mbar_wait(&op_empty[s], ph ^ 1);
+                const int ps = it % SP;
+                const uint32_t pph = (it / SP) & 1;
+                mbar_wait(&plane_full[ps], pph);
                 if (grp == 0) {
-                    a_job_any<A_PM1>(g.a_bits, sApl + (size_t)s * p.a_bytes, 128, t,
-                                     tmem_lane + A_COL + s * 32, kvalid);
+                    recomb_step_any<A_PM1, true>(g.a_bits, sApl + (size_t)ps * p.a_bytes, 128, t, &plane_empty[ps],
+                                                 &op_empty[s], ph ^ 1, tmem_lane + A_COL + s * 32, nullptr, kvalid,
+                                                 lane);
                     tmem_wait_st();
                 } else {
-                    b_job_any<W_PM1>(g.w_bits, sBpl + (size_t)s * p.b_bytes, 128, t,
-                                     sBop + (size_t)s * 128 * 128, 128);
+                    recomb_step_any<W_PM1, false>(g.w_bits, sBpl + (size_t)ps * p.b_bytes, 128, t, &plane_empty[ps],
+                                                  &op_empty[s], ph ^ 1, 0, sBop + (size_t)s * 128 * 128, 128, lane);
                     fence_proxy_async_smem();
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&plane_empty[s]);
-                    mbar_arrive_cluster(op_full0 + s * 8);
-                }
+                if (lane == 0) mbar_arrive_cluster(op_full0 + s * 8);
             }
         }
     } else {
@@ -511,17 +514,26 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     if (two) {
         p.a_bytes = 16u * 128 * g.a_bits;
         p.b_bytes = 16u * 128 * g.w_bits;
-        const size_t fixed = (size_t)T2_BN * kTabStride * 4 + (4 * MAX_STAGES + 4) * 8 + 1024;
-        const int S = stage_count((size_t)128 * 128 + p.a_bytes + p.b_bytes, fixed);
+        const size_t fixed = (size_t)T2_BN * kTabStride * 4 + (2 * MAX_PSTAGES + 2 * MAX_STAGES + 4) * 8 + 1024;
+        const size_t budget = 227 * 1024 - fixed;
+        const size_t op_stage = (size_t)128 * 128, pl_stage = p.a_bytes + p.b_bytes;
+        int S = 0, SP = 0;
+        for (int s_try = MAX_STAGES; s_try >= 2; s_try--) {  // deepest operand ring with >= s+2 plane stages
+            if (budget < s_try * op_stage) continue;
+            int sp = (int)((budget - s_try * op_stage) / pl_stage);
+            if (sp > MAX_PSTAGES) sp = MAX_PSTAGES;
+            if (sp >= s_try + 2 || (s_try == 2 && sp >= 2)) { S = s_try; SP = sp; break; }
+        }
         if (S < 2) return cudaErrorInvalidConfiguration;
         p.stages = S;
+        p.pstages = SP;
         p.tmem_cols = 512;
         p.tiles_m = (g.M + 255) / 256;
         const int tiles_n = (ncols + T2_BN - 1) / T2_BN;
         p.num_tiles = p.tiles_m * tiles_n;
         int clusters = sms / 2;
         if (clusters > p.num_tiles) clusters = p.num_tiles;
-        const size_t smem = (size_t)S * ((size_t)128 * 128 + p.a_bytes + p.b_bytes) + fixed - 1024 + 64;
+        const size_t smem = (size_t)S * op_stage + (size_t)SP * pl_stage + fixed - 1024 + 64;
         if (!make_plane_map(&ta, A, g.conv ? 1 : g.M, g.a_bits, g.Cw, 1, 128)) return cudaErrorInvalidValue;
         if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, g.RS, 128)) return cudaErrorInvalidValue;
         switch (g.enc) {
@@ -538,6 +550,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         const int S = stage_count((size_t)BN * 128 + p.a_bytes + p.b_bytes, fixed);
         if (S < 2) return cudaErrorInvalidConfiguration;
         p.stages = S;
+        p.pstages = S;
         uint32_t cols = BN + 32 * S, pow2 = 32;
         while (pow2 < cols) pow2 <<= 1;
         p.tmem_cols = pow2;

@@ -100,6 +100,58 @@ __device__ __forceinline__ void b_job(const uint8_t* planes, int rows, int row, 
     }
 }
 
+// Recombination step with early release of the plane stage: load this thread's
+// planes into registers, release the plane stage (the TMA can refill it), then
+// wait for the operand stage to be free and decode + store.
+template <int NB, bool PM1, bool IS_A>
+__device__ __forceinline__ void recomb_step(const uint8_t* planes, int rows, int row, uint64_t* plane_empty,
+                                            uint64_t* op_empty, uint32_t op_parity, uint32_t taddr, uint8_t* bop,
+                                            int kvalid, int lane) {
+    const uint4* src = reinterpret_cast<const uint4*>(planes);
+    uint4 v[NB];
+#pragma unroll
+    for (int pl = 0; pl < NB; pl++) v[pl] = src[pl * rows + row];
+    __syncwarp();
+    if (lane == 0) sm100::mbar_arrive(plane_empty);
+    sm100::mbar_wait(op_empty, op_parity);
+    if (IS_A) {
+#pragma unroll
+        for (int gi = 0; gi < 4; gi++) {
+            uint32_t o[8];
+            decode_group<NB, PM1>(v, gi, kvalid, o);
+            sm100::tmem_st8(taddr + gi * 8, o);
+        }
+    } else {
+        uint8_t* rbase = bop + (row >> 3) * 1024 + (row & 7) * 16;
+#pragma unroll
+        for (int gi = 0; gi < 4; gi++) {
+            uint32_t o[8];
+            decode_group<NB, PM1>(v, gi, kvalid, o);
+            *reinterpret_cast<uint4*>(rbase + (2 * gi) * 128) = make_uint4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<uint4*>(rbase + (2 * gi + 1) * 128) = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+    }
+}
+
+template <bool PM1, bool IS_A>
+__device__ __forceinline__ void recomb_step_any(int nb, const uint8_t* planes, int rows, int row,
+                                                uint64_t* plane_empty, uint64_t* op_empty, uint32_t op_parity,
+                                                uint32_t taddr, uint8_t* bop, int kvalid, int lane) {
+#define APNN_RS(N_) recomb_step<N_, PM1, IS_A>(planes, rows, row, plane_empty, op_empty, op_parity, taddr, bop, kvalid, lane)
+    if (PM1) { recomb_step<1, true, IS_A>(planes, rows, row, plane_empty, op_empty, op_parity, taddr, bop, kvalid, lane); return; }
+    switch (nb) {  // warp-uniform
+    case 1: APNN_RS(1); break;
+    case 2: APNN_RS(2); break;
+    case 3: APNN_RS(3); break;
+    case 4: APNN_RS(4); break;
+    case 5: APNN_RS(5); break;
+    case 6: APNN_RS(6); break;
+    case 7: APNN_RS(7); break;
+    default: APNN_RS(8); break;
+    }
+#undef APNN_RS
+}
+
 template <bool PM1>
 __device__ __forceinline__ void a_job_any(int nb, const uint8_t* planes, int rows, int row, uint32_t taddr,
                                           int kvalid) {
