@@ -25,7 +25,7 @@ from typing import Optional
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libapnn.so")
+LIB_PATH = os.environ.get("APNN_LIB", os.path.join(_HERE, "libapnn.so"))  # APNN_LIB: A/B experiments only
 
 # apnn_encoding
 ENC_01_01, ENC_PM1_PM1, ENC_W_PM1_A_01, ENC_W_01_A_PM1 = 0, 1, 2, 3

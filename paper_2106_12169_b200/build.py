@@ -41,7 +41,11 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
+def build(force: bool = False, verbose: bool = False, extra=(), so_path: str = None, build_dir: str = None) -> str:
+    """Compile every csrc/*.cu; `extra`/`so_path`/`build_dir` build experiment variants side by side."""
+    global BUILD, SO
+    if so_path or build_dir:
+        BUILD, SO = build_dir or BUILD + "_exp", so_path or SO
     os.makedirs(BUILD, exist_ok=True)
     hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "apnn.h")]
     jobs = []
@@ -71,4 +75,13 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    # python build.py [--force] [--variant NAME -DFOO=1 ...]  (variant -> libapnn_NAME.so)
+    args = sys.argv[1:]
+    if "--variant" in args:
+        i = args.index("--variant")
+        name = args[i + 1]
+        defs = [a for a in args[i + 2:] if a.startswith("-D")]
+        print(build(force=True, verbose=False, extra=defs, so_path=os.path.join(HERE, f"libapnn_{name}.so"),
+                    build_dir=os.path.join(HERE, f"build_{name}")))
+    else:
+        print(build(force="--force" in args, verbose=True))

@@ -160,7 +160,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                     const uint32_t bbase = smem_u32(sBop + (size_t)s * 128 * 128);
 #pragma unroll
                     for (int kk = 0; kk < 4; kk++) {
-                        const uint64_t bdesc = umma_desc_noswizzle(bbase + kk * 256, 128, 1024);
+                        const uint64_t bdesc = b_desc(bbase, kk);
                         mma2_i8_ts(tmem, tmem + A_COL + s * 32 + kk * 8, bdesc, idesc, (kb | kk) != 0);
                     }
                     mma2_commit_mc(&op_empty[s], 0x3);
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
                 const uint32_t bbase = smem_u32(sBop + (size_t)s * BN * 128);
 #pragma unroll
                 for (int kk = 0; kk < 4; kk++) {
-                    const uint64_t bdesc = umma_desc_noswizzle(bbase + kk * 256, 128, 1024);
+                    const uint64_t bdesc = b_desc(bbase, kk);
                     mma_i8_ts(tmem, tmem + A_COL + s * 32 + kk * 8, bdesc, idesc, (kb | kk) != 0);
                 }
                 mma_commit(&op_empty[s]);

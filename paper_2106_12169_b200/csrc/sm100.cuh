@@ -155,6 +155,19 @@ __device__ __forceinline__ uint64_t umma_desc_noswizzle(uint32_t smem_addr, uint
     return d;
 }
 
+// UMMA shared-memory matrix descriptor, K-major, SWIZZLE_128B: 8-row x 128-byte
+// atoms (1024 B, base 1024-aligned), SBO = byte stride between 8-row groups,
+// LBO unused (1).  Advancing K inside the 128-byte atom = adding bytes to the start.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;                         // LBO (ignored for swizzled K-major)
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;                         // version
+    d |= (uint64_t)2 << 61;                         // SWIZZLE_128B
+    return d;
+}
+
 // Instruction descriptor for kind::i8: int32 accumulate, K-major A and B.
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool a_signed, bool b_signed) {
     return (2u << 4)                      // D format: S32

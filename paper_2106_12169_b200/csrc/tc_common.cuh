@@ -82,21 +82,43 @@ __device__ __forceinline__ void a_job(const uint8_t* planes, int rows, int row, 
     }
 }
 
-// B job: one 128-element k-block of one B row -> UMMA K-major no-swizzle layout:
-// row r, 16-byte chunk c at (r>>3)*1024 + c*128 + (r&7)*16.
+// B operand tile layout in shared memory (one 128-byte K row per N row):
+//   APNN_B_SWIZZLE128 (default): UMMA K-major SWIZZLE_128B atoms of 8 rows x 128 B,
+//     row r, 16-byte chunk c at (r>>3)*1024 + (r&7)*128 + ((c ^ (r&7))*16)
+//   otherwise: K-major no-swizzle core matrices, chunk c at (r>>3)*1024 + c*128 + (r&7)*16.
+// Both are conflict-free for the row-per-thread 16-byte stores.
+#ifndef APNN_B_SWIZZLE128
+#define APNN_B_SWIZZLE128 1
+#endif
+__device__ __forceinline__ uint32_t b_chunk_offset(int row, int c) {
+#if APNN_B_SWIZZLE128
+    return (row >> 3) * 1024 + (row & 7) * 128 + ((c ^ (row & 7)) << 4);
+#else
+    return (row >> 3) * 1024 + c * 128 + (row & 7) * 16;
+#endif
+}
+// smem descriptor of k-step kk (32 bytes of K) of a B tile starting at `base` (1024-aligned)
+__device__ __forceinline__ uint64_t b_desc(uint32_t base, int kk) {
+#if APNN_B_SWIZZLE128
+    return sm100::umma_desc_sw128(base + kk * 32, 1024);
+#else
+    return sm100::umma_desc_noswizzle(base + kk * 256, 128, 1024);
+#endif
+}
+
+// B job: one 128-element k-block of one B row -> the B operand tile layout above.
 template <int NB, bool PM1>
 __device__ __forceinline__ void b_job(const uint8_t* planes, int rows, int row, uint8_t* bop, int kvalid) {
     const uint4* src = reinterpret_cast<const uint4*>(planes);
     uint4 v[NB];
 #pragma unroll
     for (int pl = 0; pl < NB; pl++) v[pl] = src[pl * rows + row];
-    uint8_t* rbase = bop + (row >> 3) * 1024 + (row & 7) * 16;
 #pragma unroll
     for (int gi = 0; gi < 4; gi++) {
         uint32_t o[8];
         decode_group<NB, PM1>(v, gi, kvalid, o);
-        *reinterpret_cast<uint4*>(rbase + (2 * gi) * 128) = make_uint4(o[0], o[1], o[2], o[3]);
-        *reinterpret_cast<uint4*>(rbase + (2 * gi + 1) * 128) = make_uint4(o[4], o[5], o[6], o[7]);
+        *reinterpret_cast<uint4*>(bop + b_chunk_offset(row, 2 * gi)) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(bop + b_chunk_offset(row, 2 * gi + 1)) = make_uint4(o[4], o[5], o[6], o[7]);
     }
 }
 
@@ -122,13 +144,12 @@ __device__ __forceinline__ void recomb_step(const uint8_t* planes, int rows, int
             sm100::tmem_st8(taddr + gi * 8, o);
         }
     } else {
-        uint8_t* rbase = bop + (row >> 3) * 1024 + (row & 7) * 16;
 #pragma unroll
         for (int gi = 0; gi < 4; gi++) {
             uint32_t o[8];
             decode_group<NB, PM1>(v, gi, kvalid, o);
-            *reinterpret_cast<uint4*>(rbase + (2 * gi) * 128) = make_uint4(o[0], o[1], o[2], o[3]);
-            *reinterpret_cast<uint4*>(rbase + (2 * gi + 1) * 128) = make_uint4(o[4], o[5], o[6], o[7]);
+            *reinterpret_cast<uint4*>(bop + b_chunk_offset(row, 2 * gi)) = make_uint4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<uint4*>(bop + b_chunk_offset(row, 2 * gi + 1)) = make_uint4(o[4], o[5], o[6], o[7]);
         }
     }
 }
