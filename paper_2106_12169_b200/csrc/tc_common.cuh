@@ -97,6 +97,12 @@ __device__ __forceinline__ uint32_t b_chunk_offset(int row, int c) {
     return (row >> 3) * 1024 + c * 128 + (row & 7) * 16;
 #endif
 }
+// descriptor increment (16-byte units) between consecutive 32-byte K steps
+#if APNN_B_SWIZZLE128
+constexpr uint32_t kBDescKStep = 2;
+#else
+constexpr uint32_t kBDescKStep = 16;
+#endif
 // smem descriptor of k-step kk (32 bytes of K) of a B tile starting at `base` (1024-aligned)
 __device__ __forceinline__ uint64_t b_desc(uint32_t base, int kk) {
 #if APNN_B_SWIZZLE128

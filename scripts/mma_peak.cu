@@ -1,0 +1,117 @@
+// mma_peak.cu -- microbenchmark of tcgen05.mma kind::i8 issue rate on B200 (sm_100a).
+// Measures the int8 tensor-core ceiling for the instruction shapes the APNN kernels use:
+//   mode 0: 1-CTA  M=128 N=256 K=32, A smem  (SS)
+//   mode 1: 1-CTA  M=128 N=256 K=32, A TMEM  (TS)
+//   mode 2: 2-CTA  M=256 N=256 K=32, A smem  (SS, cta_group::2)
+//   mode 3: 2-CTA  M=256 N=256 K=32, A TMEM  (TS, cta_group::2)
+// Operands are zeros (timing is value-independent).  Build:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I ../paper_2106_12169_b200/csrc mma_peak.cu -o mma_peak
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+#include "sm100.cuh"
+
+using namespace apnn::sm100;
+
+template <int MODE>
+__global__ void __launch_bounds__(128, 1) peak_kernel(int iters, unsigned long long* cycles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* sA = smem;            // 128 rows x 128 B (one K=128 block)
+    uint8_t* sB = smem + 16384;    // 256 rows x 128 B (1-CTA) / 128 rows (2-CTA)
+    __shared__ uint64_t bar;
+    __shared__ uint32_t holder;
+    constexpr bool two = MODE >= 2;
+    const int warp = threadIdx.x / 32;
+    for (int i = threadIdx.x; i < 49152 / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+    fence_proxy_async_smem();
+    if (warp == 0) {
+        if (two) tmem_alloc2(&holder, 512); else tmem_alloc_dyn(&holder, 512);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (two) cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = holder;
+    const bool leader = !two || cluster_ctarank() == 0;
+    unsigned long long t0 = clock64();
+    if (warp == 1 && leader && (threadIdx.x % 32) == 0) {
+        const uint32_t idesc = idesc_i8(two ? 256 : 128, 256, false, false);
+        const uint32_t abase = smem_u32(sA), bbase = smem_u32(sB);
+        for (int it = 0; it < iters; it++) {
+#pragma unroll
+            for (int kk = 0; kk < 4; kk++) {
+                const uint64_t bd = umma_desc_sw128(bbase + kk * 32, 1024);
+                if (MODE == 0) mma_i8_ss(tmem, umma_desc_sw128(abase + kk * 32, 1024), bd, idesc, 1);
+                if (MODE == 1) mma_i8_ts(tmem, tmem + 256 + kk * 8, bd, idesc, 1);
+                if (MODE == 2) {
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                                 "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                                 "l"(umma_desc_sw128(abase + kk * 32, 1024)), "l"(bd), "r"(idesc) : "memory");
+                }
+                if (MODE == 3) mma2_i8_ts(tmem, tmem + 256 + kk * 8, bd, idesc, 1);
+            }
+        }
+        if (two) mma2_commit_mc(&bar, 0x3); else mma_commit(&bar);
+    }
+    mbar_wait(&bar, 0);
+    unsigned long long t1 = clock64();
+    if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+    tc_fence_before();
+    __syncthreads();
+    if (two) cluster_sync();
+    if (warp == 0) { tc_fence_after(); if (two) tmem_dealloc2(tmem, 512); else tmem_dealloc(tmem, 512); }
+}
+
+template <int MODE>
+void run(int iters, int sms) {
+    auto k = peak_kernel<MODE>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 49152 + 1024);
+    unsigned long long* d;
+    cudaMalloc(&d, sms * sizeof(unsigned long long));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sms);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = 49152 + 1024;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = MODE >= 2 ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaLaunchKernelEx(&cfg, k, iters / 10, d);  // warm-up
+    cudaDeviceSynchronize();
+    cudaEventRecord(e0);
+    cudaLaunchKernelEx(&cfg, k, iters, d);
+    cudaEventRecord(e1);
+    cudaError_t err = cudaDeviceSynchronize();
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    unsigned long long cyc[512];
+    cudaMemcpy(cyc, d, sms * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    const double M = MODE >= 2 ? 256 : 128;
+    const int units = MODE >= 2 ? sms / 2 : sms;
+    const double ops = 2.0 * M * 256 * 32 * 4.0 * iters * units;
+    const double mac_per_clk_sm = (ops / 2) / (double)cyc[0] / (MODE >= 2 ? 2 : 1) / 1.0 * 1.0 / 1.0;
+    printf("{\"mode\": %d, \"name\": \"%s\", \"err\": \"%s\", \"ms\": %.3f, \"tops\": %.1f, \"cycles_cta0\": %llu, "
+           "\"int8_mac_per_clk_per_sm\": %.0f}\n",
+           MODE, MODE == 0 ? "1cta_SS" : MODE == 1 ? "1cta_TS" : MODE == 2 ? "2cta_SS" : "2cta_TS",
+           cudaGetErrorString(err), ms, ops / (ms * 1e-3) / 1e12, cyc[0],
+           (2.0 * M * 256 * 32 * 4.0 * iters / 2) / (double)cyc[0] / (MODE >= 2 ? 2 : 1));
+    (void)mac_per_clk_sm;
+    cudaFree(d);
+}
+
+int main(int argc, char** argv) {
+    int iters = argc > 1 ? atoi(argv[1]) : 20000;
+    int sms = 148;
+    run<0>(iters, sms);
+    run<1>(iters, sms);
+    run<2>(iters, sms);
+    run<3>(iters, sms);
+    return 0;
+}
