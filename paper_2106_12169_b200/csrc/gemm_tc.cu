@@ -519,11 +519,17 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         const size_t fixed = (size_t)T2_BN * kTabStride * 4 + (2 * MAX_PSTAGES + 2 * MAX_STAGES + 4) * 8 + 1024;
         const size_t budget = 227 * 1024 - fixed;
         const size_t op_stage = (size_t)128 * 128, pl_stage = p.a_bytes + p.b_bytes;
+        // Both ring depths must be EVEN: the two recombination teams take alternating
+        // k-blocks, so with an even depth every stage (and its mbarrier phase sequence)
+        // belongs to exactly one team.  With an odd depth a team can wait on a stage
+        // whose barrier is two phases behind and try_wait.parity passes early (parity
+        // aliasing) -- measured as wrong k-blocks in ~20 tiles per 8192^3 run.
         int S = 0, SP = 0;
-        for (int s_try = MAX_STAGES; s_try >= 2; s_try--) {  // deepest operand ring with >= s+2 plane stages
+        for (int s_try = MAX_STAGES; s_try >= 2; s_try -= 2) {  // deepest operand ring with >= s+2 plane stages
             if (budget < s_try * op_stage) continue;
             int sp = (int)((budget - s_try * op_stage) / pl_stage);
             if (sp > MAX_PSTAGES) sp = MAX_PSTAGES;
+            sp &= ~1;
             if (sp >= s_try + 2 || (s_try == 2 && sp >= 2)) { S = s_try; SP = sp; break; }
         }
         if (S < 2) return cudaErrorInvalidConfiguration;
