@@ -66,7 +66,11 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, uint64_
 
 // generic-proxy smem writes -> visible to the async proxy (tensor core reads)
 __device__ __forceinline__ void fence_proxy_async_smem() {
+#if APNN_CLUSTER_RELEASE
+    asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+#else
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
 }
 
 // ------------------------------------------------------------------- tcgen05
@@ -204,14 +208,25 @@ __device__ __forceinline__ uint32_t mapa(uint32_t local_addr, uint32_t rank) {
 // fence.proxy.async / tcgen05.wait::st + tcgen05.fence::before_thread_sync, and a
 // .release.cluster arrive would cost a MEMBAR.ALL.GPU per k-block (measured: the
 // top stall of the 2-CTA kernel, profiles/r01_*).
+#ifndef APNN_CLUSTER_RELEASE
+#define APNN_CLUSTER_RELEASE 0
+#endif
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+#if APNN_CLUSTER_RELEASE
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#else
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#endif
 }
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
+#if APNN_CLUSTER_RELEASE
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+#else
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+#endif
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
         : "r"(addr), "r"(parity)
