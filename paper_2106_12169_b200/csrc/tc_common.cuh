@@ -129,8 +129,11 @@ __device__ __forceinline__ void b_job(const uint8_t* planes, int rows, int row, 
 }
 
 // Recombination step with early release of the plane stage: load this thread's
-// planes into registers, release the plane stage (the TMA can refill it), then
-// wait for the operand stage to be free and decode + store.
+// planes and decode them into the 32 int8-lane words in registers (this consumes
+// the shared-memory loads, so the release below cannot overtake them -- releasing
+// right after issuing the LDS raced with the TMA refill: whole rows read the next
+// use of the stage), release the plane stage (the TMA can refill it), then wait
+// for the operand stage to be free and store.
 template <int NB, bool PM1, bool IS_A>
 __device__ __forceinline__ void recomb_step(const uint8_t* planes, int rows, int row, uint64_t* plane_empty,
                                             uint64_t* op_empty, uint32_t op_parity, uint32_t taddr, uint8_t* bop,
@@ -139,23 +142,22 @@ __device__ __forceinline__ void recomb_step(const uint8_t* planes, int rows, int
     uint4 v[NB];
 #pragma unroll
     for (int pl = 0; pl < NB; pl++) v[pl] = src[pl * rows + row];
+    uint32_t o[4][8];
+#pragma unroll
+    for (int gi = 0; gi < 4; gi++) decode_group<NB, PM1>(v, gi, kvalid, o[gi]);
     __syncwarp();
     if (lane == 0) sm100::mbar_arrive(plane_empty);
     sm100::mbar_wait(op_empty, op_parity);
     if (IS_A) {
 #pragma unroll
-        for (int gi = 0; gi < 4; gi++) {
-            uint32_t o[8];
-            decode_group<NB, PM1>(v, gi, kvalid, o);
-            sm100::tmem_st8(taddr + gi * 8, o);
-        }
+        for (int gi = 0; gi < 4; gi++) sm100::tmem_st8(taddr + gi * 8, o[gi]);
     } else {
 #pragma unroll
         for (int gi = 0; gi < 4; gi++) {
-            uint32_t o[8];
-            decode_group<NB, PM1>(v, gi, kvalid, o);
-            *reinterpret_cast<uint4*>(bop + b_chunk_offset(row, 2 * gi)) = make_uint4(o[0], o[1], o[2], o[3]);
-            *reinterpret_cast<uint4*>(bop + b_chunk_offset(row, 2 * gi + 1)) = make_uint4(o[4], o[5], o[6], o[7]);
+            *reinterpret_cast<uint4*>(bop + b_chunk_offset(row, 2 * gi)) =
+                make_uint4(o[gi][0], o[gi][1], o[gi][2], o[gi][3]);
+            *reinterpret_cast<uint4*>(bop + b_chunk_offset(row, 2 * gi + 1)) =
+                make_uint4(o[gi][4], o[gi][5], o[gi][6], o[gi][7]);
         }
     }
 }

@@ -31,4 +31,9 @@ for r in range(reps):
                           "row_mod256": sorted(set((rows % 256).tolist()))[:20],
                           "col_mod256_count": len(set((cols % 256).tolist())),
                           "example": [int(Y[idx[0, 0], idx[0, 1]]), int(ref[idx[0, 0], idx[0, 1]])]}), flush=True)
+        if r == 0:
+            sel = idx[:4000].cpu().numpy()
+            np.savez(os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out", "race_bad.npz"),
+                     idx=sel, got=Y[idx[:4000, 0], idx[:4000, 1]].cpu().numpy(),
+                     ref=ref[idx[:4000, 0], idx[:4000, 1]].cpu().numpy())
 print("bad runs", bad_runs, "of", reps)
