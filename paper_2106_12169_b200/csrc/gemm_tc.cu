@@ -89,6 +89,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     uint64_t* accum_full = op_empty + MAX_STAGES;
     uint64_t* accum_empty = accum_full + 1;                        // used in CTA 0
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accum_empty + 1);
+    volatile uint32_t* dep_slots = tmem_holder + 1;                // [T2_RECOMB_WARPS * 32]
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = cluster_ctarank();
@@ -203,11 +204,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 if (grp == 0) {
                     recomb_step_any<A_PM1, true>(g.a_bits, sApl + (size_t)ps * p.a_bytes, 128, t, &plane_empty[ps],
                                                  &op_empty[s], ph ^ 1, tmem_lane + A_COL + s * 32, nullptr, kvalid,
-                                                 lane);
+                                                 lane, dep_slots + threadIdx.x);
                     tmem_wait_st();
                 } else {
                     recomb_step_any<W_PM1, false>(g.w_bits, sBpl + (size_t)ps * p.b_bytes, 128, t, &plane_empty[ps],
-                                                  &op_empty[s], ph ^ 1, 0, sBop + (size_t)s * 128 * 128, 128, lane);
+                                                  &op_empty[s], ph ^ 1, 0, sBop + (size_t)s * 128 * 128, 128, lane,
+                                                  dep_slots + threadIdx.x);
                     fence_proxy_async_smem();
                 }
                 tc_fence_before();
@@ -516,7 +518,8 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     if (two) {
         p.a_bytes = 16u * 128 * g.a_bits;
         p.b_bytes = 16u * 128 * g.w_bits;
-        const size_t fixed = (size_t)T2_BN * kTabStride * 4 + (2 * MAX_PSTAGES + 2 * MAX_STAGES + 4) * 8 + 1024;
+        const size_t fixed = (size_t)T2_BN * kTabStride * 4 + (2 * MAX_PSTAGES + 2 * MAX_STAGES + 4) * 8 +
+                             T2_RECOMB_WARPS * 32 * 4 + 1024;
         const size_t budget = 227 * 1024 - fixed;
         const size_t op_stage = (size_t)128 * 128, pl_stage = p.a_bytes + p.b_bytes;
         // Both ring depths must be EVEN: the two recombination teams take alternating

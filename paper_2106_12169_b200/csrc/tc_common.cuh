@@ -137,7 +137,7 @@ __device__ __forceinline__ void b_job(const uint8_t* planes, int rows, int row, 
 template <int NB, bool PM1, bool IS_A>
 __device__ __forceinline__ void recomb_step(const uint8_t* planes, int rows, int row, uint64_t* plane_empty,
                                             uint64_t* op_empty, uint32_t op_parity, uint32_t taddr, uint8_t* bop,
-                                            int kvalid, int lane) {
+                                            int kvalid, int lane, volatile uint32_t* dep_slot) {
     const uint4* src = reinterpret_cast<const uint4*>(planes);
     uint4 v[NB];
 #pragma unroll
@@ -145,6 +145,18 @@ __device__ __forceinline__ void recomb_step(const uint8_t* planes, int rows, int
     uint32_t o[4][8];
 #pragma unroll
     for (int gi = 0; gi < 4; gi++) decode_group<NB, PM1>(v, gi, kvalid, o[gi]);
+    // The release below must not overtake the plane loads: neither mbarrier.arrive's
+    // release semantics nor program order make the hardware wait for in-flight LDS,
+    // and ptxas may schedule the (register-only) decode after the arrive.  A store of
+    // a value that depends on every decoded word forces the loads to complete first.
+    // (Without it the TMA refill of this plane stage raced the tail of the LDS: the
+    // k-block 12 (= ring depth) later leaked into some rows, ~20 tiles per 8192^3 run.)
+    uint32_t dep = 0;
+#pragma unroll
+    for (int gi = 0; gi < 4; gi++)
+#pragma unroll
+        for (int j = 0; j < 8; j++) dep ^= o[gi][j];
+    *dep_slot = dep;
     __syncwarp();
     if (lane == 0) sm100::mbar_arrive(plane_empty);
     sm100::mbar_wait(op_empty, op_parity);
@@ -165,9 +177,10 @@ __device__ __forceinline__ void recomb_step(const uint8_t* planes, int rows, int
 template <bool PM1, bool IS_A>
 __device__ __forceinline__ void recomb_step_any(int nb, const uint8_t* planes, int rows, int row,
                                                 uint64_t* plane_empty, uint64_t* op_empty, uint32_t op_parity,
-                                                uint32_t taddr, uint8_t* bop, int kvalid, int lane) {
-#define APNN_RS(N_) recomb_step<N_, PM1, IS_A>(planes, rows, row, plane_empty, op_empty, op_parity, taddr, bop, kvalid, lane)
-    if (PM1) { recomb_step<1, true, IS_A>(planes, rows, row, plane_empty, op_empty, op_parity, taddr, bop, kvalid, lane); return; }
+                                                uint32_t taddr, uint8_t* bop, int kvalid, int lane,
+                                                volatile uint32_t* dep_slot) {
+#define APNN_RS(N_) recomb_step<N_, PM1, IS_A>(planes, rows, row, plane_empty, op_empty, op_parity, taddr, bop, kvalid, lane, dep_slot)
+    if (PM1) { recomb_step<1, true, IS_A>(planes, rows, row, plane_empty, op_empty, op_parity, taddr, bop, kvalid, lane, dep_slot); return; }
     switch (nb) {  // warp-uniform
     case 1: APNN_RS(1); break;
     case 2: APNN_RS(2); break;
