@@ -142,21 +142,19 @@ __device__ __forceinline__ void recomb_step(const uint8_t* planes, int rows, int
     uint4 v[NB];
 #pragma unroll
     for (int pl = 0; pl < NB; pl++) v[pl] = src[pl * rows + row];
+    // The release below must not overtake the plane loads: neither mbarrier.arrive's
+    // release semantics nor program order make the hardware wait for in-flight LDS.
+    // A store of a value that depends on one register of every LDS.128 forces all of
+    // them to complete first.  (Without it the TMA refill of this plane stage raced
+    // the tail of the LDS: the k-block one ring depth later leaked into whole rows,
+    // ~20 tiles per 8192^3 run -- scripts/race_check.py.)
+    uint32_t dep = 0;
+#pragma unroll
+    for (int pl = 0; pl < NB; pl++) dep ^= v[pl].x;
+    *dep_slot = dep;
     uint32_t o[4][8];
 #pragma unroll
     for (int gi = 0; gi < 4; gi++) decode_group<NB, PM1>(v, gi, kvalid, o[gi]);
-    // The release below must not overtake the plane loads: neither mbarrier.arrive's
-    // release semantics nor program order make the hardware wait for in-flight LDS,
-    // and ptxas may schedule the (register-only) decode after the arrive.  A store of
-    // a value that depends on every decoded word forces the loads to complete first.
-    // (Without it the TMA refill of this plane stage raced the tail of the LDS: the
-    // k-block 12 (= ring depth) later leaked into some rows, ~20 tiles per 8192^3 run.)
-    uint32_t dep = 0;
-#pragma unroll
-    for (int gi = 0; gi < 4; gi++)
-#pragma unroll
-        for (int j = 0; j < 8; j++) dep ^= o[gi][j];
-    *dep_slot = dep;
     __syncwarp();
     if (lane == 0) sm100::mbar_arrive(plane_empty);
     sm100::mbar_wait(op_empty, op_parity);

@@ -281,3 +281,16 @@ def test_full_size_resnet_l1_conv_sampled_images():
     Yc = Y.cpu().numpy()
     for b in (0, B - 1):
         np.testing.assert_array_equal(Yc[b:b + 1], oracle.conv2d(X[b:b + 1], Wt, 1, 1, 2, 1, 2))
+
+
+def test_tc_repeatable_and_equal_to_b1mma_full_8192():
+    # race stress: the persistent 2-CTA kernel must give identical results on every
+    # run and agree element by element with the independent b1 mma.sync variant.
+    M = N = K = 8192
+    A, W = synth.gemm_inputs(M, N, K, 2, 1, tag="race")
+    Ap, Wp = ap.pack_bits(cuda(A), 2), ap.pack_bits(cuda(W), 1)
+    ref = ap.gemm(Ap, Wp, M, N, K, 2, 1, 2, variant=ap.VARIANT_B1MMA)
+    for _ in range(4):
+        Y = ap.gemm(Ap, Wp, M, N, K, 2, 1, 2, variant=ap.VARIANT_TC_I8)
+        torch.cuda.synchronize()
+        assert torch.equal(Y, ref)
