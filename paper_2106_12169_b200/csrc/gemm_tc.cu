@@ -58,6 +58,7 @@ struct Params {
     uint32_t tmem_cols;
     int tiles_m, num_tiles;
     int use_tab;        // fused epilogue through the threshold table
+    int acc_shift;      // scaled operands: accumulator = Y << acc_shift (2-CTA kernel)
 };
 
 // ============================================================== 2-CTA kernel
@@ -70,7 +71,7 @@ constexpr int T2_MMA_WARP = T2_TMA_WARP + 1;        // warp 21: TMEM allocator +
 constexpr int T2_THREADS = (T2_MMA_WARP + 1) * 32;
 constexpr int T2_BN = 256;   // N per pair; 128 B rows per CTA
 
-template <bool A_PM1, bool W_PM1>
+template <bool A_PM1, bool W_PM1, bool SCALED>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     tc2_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
                const Params p) {
@@ -202,12 +203,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 }
                 mbar_wait(&plane_full[ps], pph);
                 if (grp == 0) {
-                    recomb_step_any<A_PM1, true>(g.a_bits, sApl + (size_t)ps * p.a_bytes, 128, t, &plane_empty[ps],
+                    recomb_step_any<A_PM1, true, SCALED>(g.a_bits, sApl + (size_t)ps * p.a_bytes, 128, t, &plane_empty[ps],
                                                  &op_empty[s], ph ^ 1, tmem_lane + A_COL + s * 32, nullptr, kvalid,
                                                  lane, dep_slots + threadIdx.x);
                     tmem_wait_st();
                 } else {
-                    recomb_step_any<W_PM1, false>(g.w_bits, sBpl + (size_t)ps * p.b_bytes, 128, t, &plane_empty[ps],
+                    recomb_step_any<W_PM1, false, SCALED>(g.w_bits, sBpl + (size_t)ps * p.b_bytes, 128, t, &plane_empty[ps],
                                                   &op_empty[s], ph ^ 1, 0, sBop + (size_t)s * 128 * 128, 128, lane,
                                                   dep_slots + threadIdx.x);
                     fence_proxy_async_smem();
@@ -241,6 +242,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 uint32_t acc[32];
                 tmem_ld32(tmem_lane + c, acc);
                 tmem_wait_ld();
+                if (SCALED) {
+#pragma unroll
+                    for (int i = 0; i < 32; i++) acc[i] = (uint32_t)((int32_t)acc[i] >> p.acc_shift);
+                }
                 epilogue_chunk(acc, m, n0 + c, c, g, p.e, p.Y, p.use_tab ? sTab : nullptr);
             }
             tc_fence_before();
@@ -459,7 +464,7 @@ static cudaError_t set_smem(K kfn) {
 template <bool AP, bool WP>
 static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid, size_t smem,
                            cudaStream_t s) {
-    auto kfn = tc2_kernel<AP, WP>;
+    auto kfn = p.acc_shift > 0 ? tc2_kernel<AP, WP, true> : tc2_kernel<AP, WP, false>;
     cudaError_t e = set_smem(kfn);
     if (e != cudaSuccess) return e;
     kfn<<<grid, T2_THREADS, smem, s>>>(ta, tb, p);
@@ -491,6 +496,16 @@ bool tc_i8_supports(const Geom& g) {
     return g.K > 0 && g.M > 0 && g.N > 0;
 }
 
+// experiment knob: APNN_TC_SCALED=0 disables the scaled operand form
+static bool tc_scaled_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("APNN_TC_SCALED");
+        v = s ? atoi(s) : 1;
+    }
+    return v != 0;
+}
+
 // variant knob for experiments: APNN_TC_KERNEL=1 forces the 1-CTA kernel
 static int tc_kernel_override() {
     static int v = -1;
@@ -511,6 +526,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     p.A = A;
     p.nkb = g.nchunks;
     p.use_tab = (e.out_bits > 0 && e.out_bits <= 4) ? 1 : 0;
+    p.acc_shift = 0;
     const int ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
     const bool two = (g.N > 128) && (g.M > 128) && tc_kernel_override() != 1;
     CUtensorMap ta, tb;
@@ -538,6 +554,15 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         if (S < 2) return cudaErrorInvalidConfiguration;
         p.stages = S;
         p.pstages = SP;
+        {   // scaled operand form when the scaled accumulator cannot overflow int32
+            const bool apm = g.enc == APNN_ENC_PM1_PM1 || g.enc == APNN_ENC_W_01_A_PM1;
+            const bool wpm = g.enc == APNN_ENC_PM1_PM1 || g.enc == APNN_ENC_W_PM1_A_01;
+            const int ka = apm ? 6 : 8 - g.a_bits, kw = wpm ? 6 : 8 - g.w_bits;
+            const long long ma = apm ? 64 : (((1LL << g.a_bits) - 1) << ka);
+            const long long mw = wpm ? 64 : (((1LL << g.w_bits) - 1) << kw);
+            const bool safe = (long long)g.K * ma * mw < 2147483647LL;
+            p.acc_shift = (safe && ka + kw > 0 && tc_scaled_enabled()) ? ka + kw : 0;
+        }
         p.tmem_cols = 512;
         p.tiles_m = (g.M + 255) / 256;
         const int tiles_n = (ncols + T2_BN - 1) / T2_BN;

@@ -53,16 +53,62 @@ __device__ __forceinline__ uint32_t valid_mask(int kvalid, int gi) {
     return nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
 }
 
-template <int NB, bool PM1>
+// ---- scaled decodes (FMA-pipe form).  The operand bytes are the codes times a
+// power of two: 0/1 codes with NB planes are top-aligned (x 2^(8-NB)), +-1 values
+// are +-64.  The int32 result is then Y * 2^(kA+kB), shifted back exactly in the
+// epilogue (the host only picks this form when K*max|a'|*max|w'| < 2^31).  Each
+// plane-word costs one LOP3 mask (ALU) + one IMAD shift-and-add (FMA pipe) instead
+// of SHF + LOP3 on the ALU; the multipliers live in constant memory so ptxas keeps
+// real IMADs instead of strength-reducing them back to ALU shifts.
+__constant__ uint32_t kPow2[16] = {1u, 2u, 4u, 8u, 16u, 32u, 64u, 128u, 256u, 512u, 1024u, 2048u, 4096u,
+                                   8192u, 16384u, 32768u};
+__constant__ uint32_t kPm1Mul[8] = {0xFFFFFF80u, 0xFFFFFFC0u, 0xFFFFFFE0u, 0xFFFFFFF0u,
+                                    0xFFFFFFF8u, 0xFFFFFFFCu, 0xFFFFFFFEu, 0xFFFFFFFFu};  // -(128 >> j)
+
+template <int NB>
+__device__ __forceinline__ void decode_01_scaled(const uint32_t (&pw)[NB], uint32_t (&out)[8]) {
+    constexpr int k = 8 - NB;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        uint32_t o = 0;
+#pragma unroll
+        for (int t = 0; t < NB; t++) {
+            const int sh = k + t - j;
+            const uint32_t x = pw[t] & (0x01010101u << j);
+            if (sh >= 0) o = x * kPow2[sh] + o;   // disjoint bits: add == or
+            else o |= x >> (-sh);
+        }
+        out[j] = o;
+    }
+}
+// +-1 -> +-64: byte = 192 - 128*bit (no borrows); masked elements -> 0
+template <bool kMasked>
+__device__ __forceinline__ void decode_pm1_scaled(uint32_t pw, uint32_t vm, uint32_t (&out)[8]) {
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const uint32_t x = pw & (0x01010101u << j);
+        uint32_t o = x * kPm1Mul[j] + 0xC0C0C0C0u;
+        if (kMasked) o &= ((vm >> j) & 0x01010101u) * 0xFFu;
+        out[j] = o;
+    }
+}
+
+template <int NB, bool PM1, bool SCALED = false>
 __device__ __forceinline__ void decode_group(const uint4 (&v)[NB], int gi, int kvalid, uint32_t (&o)[8]) {
     uint32_t pw[NB];
 #pragma unroll
     for (int pl = 0; pl < NB; pl++) pw[pl] = sel4(v[pl], gi);
     if (PM1) {
-        if (kvalid >= 128) decode_pm1<false>(pw[0], 0u, o);
-        else decode_pm1<true>(pw[0], valid_mask(kvalid, gi), o);
+        if (SCALED) {
+            if (kvalid >= 128) decode_pm1_scaled<false>(pw[0], 0u, o);
+            else decode_pm1_scaled<true>(pw[0], valid_mask(kvalid, gi), o);
+        } else {
+            if (kvalid >= 128) decode_pm1<false>(pw[0], 0u, o);
+            else decode_pm1<true>(pw[0], valid_mask(kvalid, gi), o);
+        }
     } else {
-        decode_01<NB>(pw, o);
+        if (SCALED) decode_01_scaled<NB>(pw, o);
+        else decode_01<NB>(pw, o);
     }
 }
 
@@ -134,7 +180,7 @@ __device__ __forceinline__ void b_job(const uint8_t* planes, int rows, int row, 
 // right after issuing the LDS raced with the TMA refill: whole rows read the next
 // use of the stage), release the plane stage (the TMA can refill it), then wait
 // for the operand stage to be free and store.
-template <int NB, bool PM1, bool IS_A>
+template <int NB, bool PM1, bool IS_A, bool SCALED>
 __device__ __forceinline__ void recomb_step(const uint8_t* planes, int rows, int row, uint64_t* plane_empty,
                                             uint64_t* op_empty, uint32_t op_parity, uint32_t taddr, uint8_t* bop,
                                             int kvalid, int lane, volatile uint32_t* dep_slot) {
@@ -154,7 +200,7 @@ __device__ __forceinline__ void recomb_step(const uint8_t* planes, int rows, int
     *dep_slot = dep;
     uint32_t o[4][8];
 #pragma unroll
-    for (int gi = 0; gi < 4; gi++) decode_group<NB, PM1>(v, gi, kvalid, o[gi]);
+    for (int gi = 0; gi < 4; gi++) decode_group<NB, PM1, SCALED>(v, gi, kvalid, o[gi]);
     __syncwarp();
     if (lane == 0) sm100::mbar_arrive(plane_empty);
     sm100::mbar_wait(op_empty, op_parity);
@@ -172,13 +218,13 @@ __device__ __forceinline__ void recomb_step(const uint8_t* planes, int rows, int
     }
 }
 
-template <bool PM1, bool IS_A>
+template <bool PM1, bool IS_A, bool SCALED>
 __device__ __forceinline__ void recomb_step_any(int nb, const uint8_t* planes, int rows, int row,
                                                 uint64_t* plane_empty, uint64_t* op_empty, uint32_t op_parity,
                                                 uint32_t taddr, uint8_t* bop, int kvalid, int lane,
                                                 volatile uint32_t* dep_slot) {
-#define APNN_RS(N_) recomb_step<N_, PM1, IS_A>(planes, rows, row, plane_empty, op_empty, op_parity, taddr, bop, kvalid, lane, dep_slot)
-    if (PM1) { recomb_step<1, true, IS_A>(planes, rows, row, plane_empty, op_empty, op_parity, taddr, bop, kvalid, lane, dep_slot); return; }
+#define APNN_RS(N_) recomb_step<N_, PM1, IS_A, SCALED>(planes, rows, row, plane_empty, op_empty, op_parity, taddr, bop, kvalid, lane, dep_slot)
+    if (PM1) { recomb_step<1, true, IS_A, SCALED>(planes, rows, row, plane_empty, op_empty, op_parity, taddr, bop, kvalid, lane, dep_slot); return; }
     switch (nb) {  // warp-uniform
     case 1: APNN_RS(1); break;
     case 2: APNN_RS(2); break;
