@@ -69,17 +69,20 @@ constexpr int T2_EPI0 = T2_RECOMB_WARPS;            // warps 16-19: epilogue
 constexpr int T2_TMA_WARP = T2_EPI0 + 4;            // warp 20: TMA producer / conv gather
 constexpr int T2_MMA_WARP = T2_TMA_WARP + 1;        // warp 21: TMEM allocator + MMA issuer (CTA 0)
 constexpr int T2_THREADS = (T2_MMA_WARP + 1) * 32;
-constexpr int T2_BN = 256;   // N per pair; 128 B rows per CTA
 
-template <bool A_PM1, bool W_PM1, bool SCALED>
+// BNP = N of the pair tile (256 / 128 / 64); each CTA holds BNP/2 B rows.
+template <int BNP, bool A_PM1, bool W_PM1, bool SCALED>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     tc2_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
                const Params p) {
     using namespace sm100;
     extern __shared__ __align__(1024) uint8_t smem[];
+    constexpr int BROWS = BNP / 2;                               // B rows per CTA
+    constexpr int T2_BN = BNP;
+    constexpr uint32_t BOP_STAGE = BROWS * 128;                  // bytes of one B operand stage
     const int S = p.stages, SP = p.pstages;
-    uint8_t* sBop = smem;                                        // S x 128 rows x 128 B
-    uint8_t* sApl = sBop + (size_t)S * 128 * 128;                // SP x a_bytes
+    uint8_t* sBop = smem;                                        // S x BROWS rows x 128 B
+    uint8_t* sApl = sBop + (size_t)S * BOP_STAGE;                // SP x a_bytes
     uint8_t* sBpl = sApl + (size_t)SP * p.a_bytes;               // SP x b_bytes
     int32_t* sTab = reinterpret_cast<int32_t*>(sBpl + (size_t)SP * p.b_bytes);  // 256 x 16 int32
     uint64_t* bars = reinterpret_cast<uint64_t*>(sTab + T2_BN * kTabStride);
@@ -131,7 +134,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             uint32_t ph = 0;
             for (int tile = cid; tile < p.num_tiles; tile += ncl) {
                 const int m0 = (tile % p.tiles_m) * 256 + rank * 128;
-                const int nr0 = (tile / p.tiles_m) * T2_BN + rank * 128;
+                const int nr0 = (tile / p.tiles_m) * T2_BN + rank * BROWS;
                 if (conv) {
 #pragma unroll
                     for (int i = 0; i < 4; i++) rc[i] = make_row(g, m0 + lane + 32 * i);
@@ -163,7 +166,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 for (int kb = 0; kb < nkb; kb++) {
                     mbar_wait_cluster(&op_full[s], ph);
                     tc_fence_after();
-                    const uint64_t bd = bdesc0 + (uint64_t)(s * (128 * 128 / 16));
+                    const uint64_t bd = bdesc0 + (uint64_t)(s * (BOP_STAGE / 16));
                     const uint32_t as = a_col0 + s * 32;
 #pragma unroll
                     for (int kk = 0; kk < 4; kk++)
@@ -207,11 +210,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                                                  &op_empty[s], ph ^ 1, tmem_lane + A_COL + s * 32, nullptr, kvalid,
                                                  lane, dep_slots + threadIdx.x);
                     tmem_wait_st();
-                } else {
-                    recomb_step_any<W_PM1, false, SCALED>(g.w_bits, sBpl + (size_t)ps * p.b_bytes, 128, t, &plane_empty[ps],
-                                                  &op_empty[s], ph ^ 1, 0, sBop + (size_t)s * 128 * 128, 128, lane,
-                                                  dep_slots + threadIdx.x);
+                } else if (t < BROWS) {  // warp-uniform: BROWS is a multiple of 32
+                    recomb_step_any<W_PM1, false, SCALED>(g.w_bits, sBpl + (size_t)ps * p.b_bytes, BROWS, t,
+                                                          &plane_empty[ps], &op_empty[s], ph ^ 1, 0,
+                                                          sBop + (size_t)s * BOP_STAGE, 128, lane,
+                                                          dep_slots + threadIdx.x);
                     fence_proxy_async_smem();
+                } else {                 // idle B warp (narrow pair tile): release the plane stage only
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&plane_empty[ps]);
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -231,8 +238,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             const int n0 = (tile / p.tiles_m) * T2_BN;
             if (p.use_tab) {
                 named_bar_sync(1, 128);  // previous tile's readers are done
-                build_threshold_row(sTab + et * kTabStride, n0 + et, g.N, p.e);
-                build_threshold_row(sTab + (et + 128) * kTabStride, n0 + et + 128, g.N, p.e);
+                if (et < T2_BN) build_threshold_row(sTab + et * kTabStride, n0 + et, g.N, p.e);
+                if (et + 128 < T2_BN) build_threshold_row(sTab + (et + 128) * kTabStride, n0 + et + 128, g.N, p.e);
                 named_bar_sync(1, 128);
             }
             mbar_wait(accum_full, tc & 1);
@@ -461,14 +468,22 @@ static cudaError_t set_smem(K kfn) {
     return cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
-template <bool AP, bool WP>
+template <int BNP, bool AP, bool WP>
 static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid, size_t smem,
                            cudaStream_t s) {
-    auto kfn = p.acc_shift > 0 ? tc2_kernel<AP, WP, true> : tc2_kernel<AP, WP, false>;
+    auto kfn = p.acc_shift > 0 ? tc2_kernel<BNP, AP, WP, true> : tc2_kernel<BNP, AP, WP, false>;
     cudaError_t e = set_smem(kfn);
     if (e != cudaSuccess) return e;
     kfn<<<grid, T2_THREADS, smem, s>>>(ta, tb, p);
     return cudaGetLastError();
+}
+
+template <bool AP, bool WP>
+static cudaError_t launch2_bn(int BNP, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid,
+                              size_t smem, cudaStream_t s) {
+    if (BNP == 256) return launch2<256, AP, WP>(ta, tb, p, grid, smem, s);
+    if (BNP == 128) return launch2<128, AP, WP>(ta, tb, p, grid, smem, s);
+    return launch2<64, AP, WP>(ta, tb, p, grid, smem, s);
 }
 
 template <int BN, bool AP, bool WP>
@@ -528,21 +543,23 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     p.use_tab = (e.out_bits > 0 && e.out_bits <= 4) ? 1 : 0;
     p.acc_shift = 0;
     const int ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
-    const bool two = (g.N > 128) && (g.M > 128) && tc_kernel_override() != 1;
+    const bool two = (g.M > 128) && tc_kernel_override() != 1;
     CUtensorMap ta, tb;
     cudaError_t err;
     if (two) {
+        const int BNP = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);   // pair tile width
+        const int brows = BNP / 2;
         p.a_bytes = 16u * 128 * g.a_bits;
-        p.b_bytes = 16u * 128 * g.w_bits;
-        const size_t fixed = (size_t)T2_BN * kTabStride * 4 + (2 * MAX_PSTAGES + 2 * MAX_STAGES + 4) * 8 +
+        p.b_bytes = 16u * brows * g.w_bits;
+        const size_t fixed = (size_t)256 * kTabStride * 4 + (2 * MAX_PSTAGES + 2 * MAX_STAGES + 4) * 8 +
                              T2_RECOMB_WARPS * 32 * 4 + 1024;
         const size_t budget = 227 * 1024 - fixed;
-        const size_t op_stage = (size_t)128 * 128, pl_stage = p.a_bytes + p.b_bytes;
+        const size_t op_stage = (size_t)brows * 128, pl_stage = p.a_bytes + p.b_bytes;
         // Both ring depths must be EVEN: the two recombination teams take alternating
         // k-blocks, so with an even depth every stage (and its mbarrier phase sequence)
         // belongs to exactly one team.  With an odd depth a team can wait on a stage
         // whose barrier is two phases behind and try_wait.parity passes early (parity
-        // aliasing) -- measured as wrong k-blocks in ~20 tiles per 8192^3 run.
+        // aliasing).
         int S = 0, SP = 0;
         for (int s_try = MAX_STAGES; s_try >= 2; s_try -= 2) {  // deepest operand ring with >= s+2 plane stages
             if (budget < s_try * op_stage) continue;
@@ -565,18 +582,18 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         }
         p.tmem_cols = 512;
         p.tiles_m = (g.M + 255) / 256;
-        const int tiles_n = (ncols + T2_BN - 1) / T2_BN;
+        const int tiles_n = (ncols + BNP - 1) / BNP;
         p.num_tiles = p.tiles_m * tiles_n;
         int clusters = sms / 2;
         if (clusters > p.num_tiles) clusters = p.num_tiles;
         const size_t smem = (size_t)S * op_stage + (size_t)SP * pl_stage + fixed - 1024 + 64;
         if (!make_plane_map(&ta, A, g.conv ? 1 : g.M, g.a_bits, g.Cw, 1, 128)) return cudaErrorInvalidValue;
-        if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, g.RS, 128)) return cudaErrorInvalidValue;
+        if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, g.RS, brows)) return cudaErrorInvalidValue;
         switch (g.enc) {
-        case APNN_ENC_01_01: err = launch2<false, false>(ta, tb, p, clusters * 2, smem, s); break;
-        case APNN_ENC_PM1_PM1: err = launch2<true, true>(ta, tb, p, clusters * 2, smem, s); break;
-        case APNN_ENC_W_PM1_A_01: err = launch2<false, true>(ta, tb, p, clusters * 2, smem, s); break;
-        default: err = launch2<true, false>(ta, tb, p, clusters * 2, smem, s); break;
+        case APNN_ENC_01_01: err = launch2_bn<false, false>(BNP, ta, tb, p, clusters * 2, smem, s); break;
+        case APNN_ENC_PM1_PM1: err = launch2_bn<true, true>(BNP, ta, tb, p, clusters * 2, smem, s); break;
+        case APNN_ENC_W_PM1_A_01: err = launch2_bn<false, true>(BNP, ta, tb, p, clusters * 2, smem, s); break;
+        default: err = launch2_bn<true, false>(BNP, ta, tb, p, clusters * 2, smem, s); break;
         }
     } else {
         const int BN = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);

@@ -168,6 +168,10 @@ def test_quant_pack_out_extremes():
 # -------------------------------------------------------------------- conv
 
 CONV_SHAPES = [  # B, H, W, C, Co, R, S, stride, pad
+    (4, 14, 14, 64, 64, 3, 3, 1, 1),    # M = 784: persistent 2-CTA kernel, pair tile N = 64
+    (2, 16, 17, 128, 96, 3, 3, 1, 1),   # M = 544, N = 96 -> pair tile 128
+    (3, 12, 12, 70, 300, 3, 3, 2, 1),   # M = 108 < 128 rows -> 1-CTA kernel; N = 300
+    (2, 20, 20, 192, 260, 3, 3, 2, 1),  # M = 200, N = 260 -> pair tile 256, ragged N
     (2, 6, 7, 3, 5, 3, 3, 1, 1),
     (1, 9, 9, 64, 64, 3, 3, 1, 1),
     (2, 8, 8, 128, 130, 3, 3, 2, 1),
