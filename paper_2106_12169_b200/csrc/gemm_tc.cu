@@ -216,9 +216,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                                                           sBop + (size_t)s * BOP_STAGE, 128, lane,
                                                           dep_slots + threadIdx.x);
                     fence_proxy_async_smem();
-                } else {                 // idle B warp (narrow pair tile): release the plane stage only
+                } else {                 // idle B warp (narrow pair tile): nothing to write, but it
+                    // must keep the barrier phase accounting of a writer: release the plane
+                    // stage, and wait for the previous use of the operand stage to be consumed
+                    // before arriving on op_full (an early arrival would complete the
+                    // previous use's phase before the real writers finish -- measured as a
+                    // rare wrong k-block).
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&plane_empty[ps]);
+                    mbar_wait(&op_empty[s], ph ^ 1);
                 }
                 tc_fence_before();
                 __syncwarp();
