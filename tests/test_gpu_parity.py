@@ -298,3 +298,13 @@ def test_tc_repeatable_and_equal_to_b1mma_full_8192():
         Y = ap.gemm(Ap, Wp, M, N, K, 2, 1, 2, variant=ap.VARIANT_TC_I8)
         torch.cuda.synchronize()
         assert torch.equal(Y, ref)
+
+
+def test_tc_narrow_pair_tiles_repeatable():
+    # race stress for the 64/128-wide pair tiles (idle B warps): repeat, compare with b1mma
+    for (M, N, K, a, w, e) in [(300, 64, 1000, 8, 8, 0), (4096, 64, 2048, 2, 1, 2), (2048, 96, 1024, 4, 4, 0)]:
+        A, W = synth.gemm_inputs(M, N, K, a, w, tag="rn")
+        Ap, Wp = ap.pack_bits(cuda(A), a), ap.pack_bits(cuda(W), w)
+        ref = ap.gemm(Ap, Wp, M, N, K, a, w, e, variant=ap.VARIANT_B1MMA)
+        for _ in range(6):
+            assert torch.equal(ap.gemm(Ap, Wp, M, N, K, a, w, e, variant=ap.VARIANT_TC_I8), ref)
