@@ -63,6 +63,7 @@ struct Params {
     //   conv_k > 0: a CTA tile is conv_k whole output rows (conv_k * Wo <= 128 pixels)
     //   conv_k = 0: a CTA tile is a 128-pixel segment of one output row (Wo > 128)
     int conv_k, conv_bw, conv_segs, conv_nbox;
+    int conv_box_stride;  // bytes between row boxes in a plane stage (16*bw*bits rounded up to 128: TMA dst alignment)
 };
 
 // Rows of CTA tile `ct`: output rows m_base .. m_base + len - 1 (GEMM: 128-row tiles).
@@ -168,7 +169,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                         tma_load_4d(adst, &tmapA, &plane_full[s], kb * 4, m0, 0, 0);
                     } else {
                         const int r = rs / g.S, sx = rs - r * g.S;
-                        const int box_bytes = 16 * p.conv_bw * g.a_bits;
+                        const int box_bytes = p.conv_box_stride;
                         for (int i = 0; i < p.conv_nbox; i++) {
                             int gr, wo0;
                             if (p.conv_k > 0) { gr = ct * p.conv_k + i; wo0 = 0; }
@@ -228,7 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             a_row = tt - a_box * p.conv_bw;
             a_rows = p.conv_bw;
         }
-        const uint32_t a_box_off = (uint32_t)(a_box * 16 * p.conv_bw * g.a_bits);
+        const uint32_t a_box_off = (uint32_t)(a_box * p.conv_box_stride);
         for (int tile = cid; tile < p.num_tiles; tile += ncl) {
             RowCtx rc;
             if (A_PM1 && g.conv) {
@@ -622,8 +623,14 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         const int BNP = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);   // pair tile width
         const int brows = BNP / 2;
         p.b_bytes = 16u * brows * g.w_bits;
-        if (g.conv && g.Wo <= 128) p.a_bytes = 16u * (128 / g.Wo) * g.Wo * g.a_bits;
-        else p.a_bytes = 16u * 128 * g.a_bits;
+        p.conv_box_stride = 0;
+        if (g.conv) {
+            const int bw = g.Wo <= 128 ? g.Wo : 128, nbox = g.Wo <= 128 ? 128 / g.Wo : 1;
+            p.conv_box_stride = (16 * bw * g.a_bits + 127) / 128 * 128;
+            p.a_bytes = (uint32_t)(nbox * p.conv_box_stride);
+        } else {
+            p.a_bytes = 16u * 128 * g.a_bits;
+        }
         const size_t fixed = (size_t)256 * kTabStride * 4 + (2 * MAX_PSTAGES + 2 * MAX_STAGES + 4) * 8 +
                              T2_RECOMB_WARPS * 32 * 4 + 1024;
         const size_t budget = 227 * 1024 - fixed;
