@@ -64,6 +64,7 @@ struct Params {
     //   conv_k = 0: a CTA tile is a 128-pixel segment of one output row (Wo > 128)
     int conv_k, conv_bw, conv_segs, conv_nbox;
     int conv_box_stride;  // bytes between row boxes in a plane stage (16*bw*bits rounded up to 128: TMA dst alignment)
+    uint32_t a_tx_bytes;  // bytes the A loads of one stage actually deliver (expect_tx; excludes slot padding)
 };
 
 // Rows of CTA tile `ct`: output rows m_base .. m_base + len - 1 (GEMM: 128-row tiles).
@@ -163,7 +164,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                     mbar_wait(&plane_empty[s], ph ^ 1);
                     const int rs = conv ? kb / g.CB : 0;
                     const int cb = conv ? kb - rs * g.CB : kb;
-                    mbar_arrive_expect_tx(&plane_full[s], p.a_bytes + p.b_bytes);
+                    mbar_arrive_expect_tx(&plane_full[s], p.a_tx_bytes + p.b_bytes);
                     uint8_t* adst = sApl + (size_t)s * p.a_bytes;
                     if (!conv) {
                         tma_load_4d(adst, &tmapA, &plane_full[s], kb * 4, m0, 0, 0);
@@ -628,8 +629,10 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
             const int bw = g.Wo <= 128 ? g.Wo : 128, nbox = g.Wo <= 128 ? 128 / g.Wo : 1;
             p.conv_box_stride = (16 * bw * g.a_bits + 127) / 128 * 128;
             p.a_bytes = (uint32_t)(nbox * p.conv_box_stride);
+            p.a_tx_bytes = (uint32_t)(nbox * 16 * bw * g.a_bits);
         } else {
             p.a_bytes = 16u * 128 * g.a_bits;
+            p.a_tx_bytes = p.a_bytes;
         }
         const size_t fixed = (size_t)256 * kTabStride * 4 + (2 * MAX_PSTAGES + 2 * MAX_STAGES + 4) * 8 +
                              T2_RECOMB_WARPS * 32 * 4 + 1024;
