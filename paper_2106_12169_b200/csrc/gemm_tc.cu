@@ -34,6 +34,7 @@
 // K runs in blocks of 128 (the paper's b_k = 128).
 #include <cuda.h>
 
+#include <cstdio>
 #include <mutex>
 
 #include "tc_common.cuh"
@@ -65,7 +66,20 @@ struct Params {
     int conv_k, conv_bw, conv_segs, conv_nbox;
     int conv_box_stride;  // bytes between row boxes in a plane stage (16*bw*bits rounded up to 128: TMA dst alignment)
     uint32_t a_tx_bytes;  // bytes the A loads of one stage actually deliver (expect_tx; excludes slot padding)
+    unsigned long long* trace;  // development trace (APNN_TRACE), nullptr normally
 };
+
+// development trace of CTA 0: clock64 stamps per k-block / tile (APNN_TRACE=<file>)
+constexpr int kTraceN = 2048;
+enum { TR_PROD = 0, TR_A_PLANE = 1, TR_A_OP = 2, TR_A_DONE = 3, TR_MMA_OPFULL = 4, TR_MMA_ISSUED = 5,
+       TR_EPI_FULL = 6, TR_EPI_DONE = 7, TR_N = 8 };
+__device__ __forceinline__ void trace_at(const Params& p, int ev, int idx) {
+    if (p.trace && blockIdx.x == 0 && idx < kTraceN) {
+        unsigned long long c;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+        p.trace[ev * kTraceN + idx] = c;
+    }
+}
 
 // Rows of CTA tile `ct`: output rows m_base .. m_base + len - 1 (GEMM: 128-row tiles).
 __device__ __forceinline__ void cta_tile_rows(const Params& p, int ct, int& m_base, int& len) {
@@ -154,7 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
         //  out-of-frame pixels are zero-filled by the TMA unit)
         const bool conv = g.conv;
         if (lane == 0) {
-            int s = 0;
+            int s = 0, tr_it = 0;
             uint32_t ph = 0;
             for (int tile = cid; tile < p.num_tiles; tile += ncl) {
                 const int ct = (tile % p.tiles_m) * 2 + rank;
@@ -162,6 +176,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 const int nr0 = (tile / p.tiles_m) * T2_BN + rank * BROWS;
                 for (int kb = 0; kb < nkb; kb++, s = (s + 1 == SP) ? 0 : s + 1, ph ^= (s == 0)) {
                     mbar_wait(&plane_empty[s], ph ^ 1);
+                    trace_at(p, TR_PROD, tr_it++);
                     const int rs = conv ? kb / g.CB : 0;
                     const int cb = conv ? kb - rs * g.CB : kb;
                     mbar_arrive_expect_tx(&plane_full[s], p.a_tx_bytes + p.b_bytes);
@@ -197,6 +212,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 tc_fence_after();
                 for (int kb = 0; kb < nkb; kb++) {
                     mbar_wait_cluster(&op_full[s], ph);
+                    trace_at(p, TR_MMA_OPFULL, tc * nkb + kb);
                     tc_fence_after();
                     const uint64_t bd = bdesc0 + (uint64_t)(s * (BOP_STAGE / 16));
                     const uint32_t as = a_col0 + s * 32;
@@ -204,6 +220,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                     for (int kk = 0; kk < 4; kk++)
                         mma2_i8_ts(tmem, as + kk * 8, bd + (uint64_t)(kk * kBDescKStep), idesc, (kb | kk) != 0);
                     mma2_commit_mc(&op_empty[s], 0x3);
+                    trace_at(p, TR_MMA_ISSUED, tc * nkb + kb);
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
                 mma2_commit_mc(accum_full, 0x3);
@@ -251,6 +268,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                     }
                 }
                 mbar_wait(&plane_full[ps], pph);
+                if (warp == 0 && lane == 0) trace_at(p, TR_A_PLANE, it >> 1);
                 if (grp == 0) {
                     recomb_step_any<A_PM1, true, SCALED>(g.a_bits, sApl + (size_t)ps * p.a_bytes + a_box_off, a_rows,
                                                          a_row, &plane_empty[ps],
@@ -276,6 +294,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(op_full0 + s * 8);
+                if (warp == 0 && lane == 0) trace_at(p, TR_A_DONE, it >> 1);
             }
         }
     } else {
@@ -298,6 +317,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 named_bar_sync(1, 128);
             }
             mbar_wait(accum_full, tc & 1);
+            if (warp == T2_EPI0 && lane == 0) trace_at(p, TR_EPI_FULL, tc);
             tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < T2_BN; c += 32) {
@@ -313,6 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(accum_empty0);
+            if (warp == T2_EPI0 && lane == 0) trace_at(p, TR_EPI_DONE, tc);
         }
     }
 
@@ -585,6 +606,8 @@ bool tc_i8_supports(const Geom& g) {
     return g.K > 0 && g.M > 0 && g.N > 0;
 }
 
+static int nkb_dbg(const tc::Params& p) { return p.nkb; }
+
 // experiment knob: APNN_TC_SCALED=0 disables the scaled operand form
 static bool tc_scaled_enabled() {
     static int v = -1;
@@ -616,6 +639,12 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     p.nkb = g.nchunks;
     p.use_tab = (e.out_bits > 0 && e.out_bits <= 4) ? 1 : 0;
     p.acc_shift = 0;
+    p.trace = nullptr;
+    const char* trace_path = getenv("APNN_TRACE");
+    if (trace_path) {
+        cudaMalloc(&p.trace, sizeof(unsigned long long) * kTraceN * TR_N);
+        cudaMemset(p.trace, 0, sizeof(unsigned long long) * kTraceN * TR_N);
+    }
     const int ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
     const bool two = (g.M > 128) && tc_kernel_override() != 1;
     CUtensorMap ta, tb;
@@ -697,6 +726,18 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         case APNN_ENC_PM1_PM1: err = launch2_bn<true, true>(BNP, ta, tb, p, clusters * 2, smem, s); break;
         case APNN_ENC_W_PM1_A_01: err = launch2_bn<false, true>(BNP, ta, tb, p, clusters * 2, smem, s); break;
         default: err = launch2_bn<true, false>(BNP, ta, tb, p, clusters * 2, smem, s); break;
+        }
+        if (p.trace) {  // development only: synchronous dump
+            static unsigned long long host[kTraceN * TR_N];
+            cudaStreamSynchronize(s);
+            cudaMemcpy(host, p.trace, sizeof(host), cudaMemcpyDeviceToHost);
+            cudaFree(p.trace);
+            if (FILE* f = fopen(trace_path, "wb")) {
+                int hdr[4] = {kTraceN, TR_N, nkb_dbg(p), S};
+                fwrite(hdr, sizeof(hdr), 1, f);
+                fwrite(host, sizeof(host), 1, f);
+                fclose(f);
+            }
         }
     } else {
         const int BN = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
