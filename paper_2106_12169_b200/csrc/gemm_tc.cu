@@ -668,7 +668,14 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     if (two) {
         const int BNP = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);   // pair tile width
         const int brows = BNP / 2;
-        p.kps = g.conv ? 1 : (g.nchunks >= 4 ? 4 : (g.nchunks >= 2 ? 2 : 1));
+        p.kps = 1;
+        if (!g.conv) {  // k-blocks per plane stage: APNN_TC_KPS (experiments), default 1
+            static int kps_env = -1;
+            if (kps_env < 0) { const char* e = getenv("APNN_TC_KPS"); kps_env = e ? atoi(e) : 1; }
+            p.kps = kps_env;
+            while (p.kps > 1 && p.kps > g.nchunks) p.kps >>= 1;
+            if (p.kps < 1 || p.kps > 16) p.kps = 1;
+        }
         p.b_bytes = 16u * p.kps * brows * g.w_bits;
         p.conv_box_stride = 0;
         if (g.conv) {
