@@ -53,7 +53,6 @@ struct Params {
     const uint32_t* A;  // raw packed activations (conv gathers rows from here)
     int stages;         // operand ring depth
     int pstages;        // plane ring depth (2-CTA kernel)
-    int kps;            // k-blocks per plane stage (2-CTA GEMM: 4 -> 64-byte TMA box rows)
     int nkb;            // k-blocks per tile
     uint32_t a_bytes;   // A plane bytes per stage (this CTA's rows)
     uint32_t b_bytes;   // B plane bytes per stage (this CTA's rows)
@@ -145,7 +144,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
         tma_prefetch(&tmapB);
         for (int s = 0; s < SP; s++) {
             mbar_init(&plane_full[s], 1);
-            mbar_init(&plane_empty[s], T2_RECOMB_WARPS);  // every recombination warp releases every stage once
+            mbar_init(&plane_empty[s], 8);
         }
         for (int s = 0; s < S; s++) {
             mbar_init(&op_full[s], 16);   // 8 recombination warps x 2 CTAs
@@ -175,7 +174,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 const int ct = (tile % p.tiles_m) * 2 + rank;
                 const int m0 = ct * 128;
                 const int nr0 = (tile / p.tiles_m) * T2_BN + rank * BROWS;
-                for (int kb = 0; kb < nkb; kb += p.kps, s = (s + 1 == SP) ? 0 : s + 1, ph ^= (s == 0)) {
+                for (int kb = 0; kb < nkb; kb++, s = (s + 1 == SP) ? 0 : s + 1, ph ^= (s == 0)) {
                     mbar_wait(&plane_empty[s], ph ^ 1);
                     trace_at(p, TR_PROD, tr_it++);
                     const int rs = conv ? kb / g.CB : 0;
@@ -238,7 +237,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
         const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
         const uint32_t op_full0 = mapa(smem_u32(op_full), 0);
         int it = 0, s = 0, ps = 0;
-        uint32_t ph = 0, pph = 0;   // operand ring (per k-block) / plane ring (per kps k-blocks)
+        uint32_t ph = 0, pph = 0;
         // A job source row inside the plane stage: conv stages hold conv_nbox row boxes
         // of conv_bw pixels ([box][plane][pixel][16 B]); unused tile rows read row 0
         int a_box = 0, a_row = t, a_rows = 128;
@@ -256,22 +255,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 cta_tile_rows(p, (tile % p.tiles_m) * 2 + rank, mb, len);
                 rc = make_row(g, t < len ? mb + t : g.M);
             }
-            for (int kb = 0; kb < nkb; kb++, it++, s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
-                const int sub = kb % p.kps;
-                const bool last_in_stage = (sub == p.kps - 1) || (kb + 1 == nkb);
-                const int ps_now = ps;
-                const uint32_t pph_now = pph;
-                if (last_in_stage) { ps = (ps + 1 == SP) ? 0 : ps + 1; pph ^= (ps == 0); }
-                if ((it & 1) != team) {
-                    // the other team decodes this k-block; still release the plane stage once
-                    // (after its data landed, so the arrival cannot count toward an older phase)
-                    if (last_in_stage) {
-                        mbar_wait(&plane_full[ps_now], pph_now);
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&plane_empty[ps_now]);
-                    }
-                    continue;
-                }
+            for (int kb = 0; kb < nkb; kb++, it++, s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0),
+                     ps = (ps + 1 == SP) ? 0 : ps + 1, pph ^= (ps == 0)) {
+                if ((it & 1) != team) continue;
                 int kvalid = 128;  // +-1 activations: elements beyond kvalid decode to 0
                 if (A_PM1) {
                     if (g.conv) {
@@ -281,20 +267,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                         kvalid = rem < 128 ? rem : 128;
                     }
                 }
-                mbar_wait(&plane_full[ps_now], pph_now);
+                mbar_wait(&plane_full[ps], pph);
                 if (warp == 0 && lane == 0) trace_at(p, TR_A_PLANE, it >> 1);
                 if (grp == 0) {
-                    recomb_step_any<A_PM1, true, SCALED>(g.a_bits, sApl + (size_t)ps_now * p.a_bytes + a_box_off,
-                                                         a_rows, a_row, p.kps, sub, last_in_stage,
-                                                         &plane_empty[ps_now], &op_empty[s], ph ^ 1,
-                                                         tmem_lane + A_COL + s * 32, nullptr, kvalid, lane,
-                                                         dep_slots + threadIdx.x);
+                    recomb_step_any<A_PM1, true, SCALED>(g.a_bits, sApl + (size_t)ps * p.a_bytes + a_box_off, a_rows,
+                                                         a_row, &plane_empty[ps],
+                                                 &op_empty[s], ph ^ 1, tmem_lane + A_COL + s * 32, nullptr, kvalid,
+                                                 lane, dep_slots + threadIdx.x);
                     tmem_wait_st();
                 } else if (t < BROWS) {  // warp-uniform: BROWS is a multiple of 32
-                    recomb_step_any<W_PM1, false, SCALED>(g.w_bits, sBpl + (size_t)ps_now * p.b_bytes, BROWS, t,
-                                                          p.kps, sub, last_in_stage, &plane_empty[ps_now],
-                                                          &op_empty[s], ph ^ 1, 0, sBop + (size_t)s * BOP_STAGE,
-                                                          128, lane, dep_slots + threadIdx.x);
+                    recomb_step_any<W_PM1, false, SCALED>(g.w_bits, sBpl + (size_t)ps * p.b_bytes, BROWS, t,
+                                                          &plane_empty[ps], &op_empty[s], ph ^ 1, 0,
+                                                          sBop + (size_t)s * BOP_STAGE, 128, lane,
+                                                          dep_slots + threadIdx.x);
                     fence_proxy_async_smem();
                 } else {                 // idle B warp (narrow pair tile): nothing to write, but it
                     // must keep the barrier phase accounting of a writer: release the plane
@@ -303,7 +288,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                     // previous use's phase before the real writers finish -- measured as a
                     // rare wrong k-block).
                     __syncwarp();
-                    if (last_in_stage && lane == 0) mbar_arrive(&plane_empty[ps_now]);
+                    if (lane == 0) mbar_arrive(&plane_empty[ps]);
                     mbar_wait(&op_empty[s], ph ^ 1);
                 }
                 tc_fence_before();
@@ -535,13 +520,12 @@ static PFN_encodeTiled get_encode() {
 // {4 words = 128 elements, box_rows, bits, 1} lands in shared memory as
 // [plane][row][16 B] (conflict-free row-per-thread reads); coordinates
 // {cb*4, row0, 0, tap}.
-static bool make_plane_map(CUtensorMap* m, const uint32_t* base, int rows, int bits, int Cw, int RS, int box_rows,
-                           int kps = 1) {
+static bool make_plane_map(CUtensorMap* m, const uint32_t* base, int rows, int bits, int Cw, int RS, int box_rows) {
     PFN_encodeTiled enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[4] = {(cuuint64_t)Cw, (cuuint64_t)rows, (cuuint64_t)bits, (cuuint64_t)RS};
     cuuint64_t strides[3] = {(cuuint64_t)RS * bits * Cw * 4, (cuuint64_t)Cw * 4, (cuuint64_t)bits * Cw * 4};
-    cuuint32_t box[4] = {(cuuint32_t)(4 * kps), (cuuint32_t)box_rows, (cuuint32_t)bits, 1};
+    cuuint32_t box[4] = {4, (cuuint32_t)box_rows, (cuuint32_t)bits, 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint32_t*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -668,15 +652,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     if (two) {
         const int BNP = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);   // pair tile width
         const int brows = BNP / 2;
-        p.kps = 1;
-        if (!g.conv) {  // k-blocks per plane stage: APNN_TC_KPS (experiments), default 1
-            static int kps_env = -1;
-            if (kps_env < 0) { const char* e = getenv("APNN_TC_KPS"); kps_env = e ? atoi(e) : 1; }
-            p.kps = kps_env;
-            while (p.kps > 1 && p.kps > g.nchunks) p.kps >>= 1;
-            if (p.kps < 1 || p.kps > 16) p.kps = 1;
-        }
-        p.b_bytes = 16u * p.kps * brows * g.w_bits;
+        p.b_bytes = 16u * brows * g.w_bits;
         p.conv_box_stride = 0;
         if (g.conv) {
             const int bw = g.Wo <= 128 ? g.Wo : 128, nbox = g.Wo <= 128 ? 128 / g.Wo : 1;
@@ -684,7 +660,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
             p.a_bytes = (uint32_t)(nbox * p.conv_box_stride);
             p.a_tx_bytes = (uint32_t)(nbox * 16 * bw * g.a_bits);
         } else {
-            p.a_bytes = 16u * p.kps * 128 * g.a_bits;
+            p.a_bytes = 16u * 128 * g.a_bits;
             p.a_tx_bytes = p.a_bytes;
         }
         const size_t fixed = (size_t)256 * kTabStride * 4 + (2 * MAX_PSTAGES + 2 * MAX_STAGES + 4) * 8 +
@@ -696,13 +672,13 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         // belongs to exactly one team.  With an odd depth a team can wait on a stage
         // whose barrier is two phases behind and try_wait.parity passes early (parity
         // aliasing).
-        // (The plane ring is consumed in order by both teams, so its depth may be odd.)
         int S = 0, SP = 0;
-        for (int s_try = MAX_STAGES; s_try >= 2; s_try -= 2) {  // deepest operand ring with >= s+2 k-blocks of planes
+        for (int s_try = MAX_STAGES; s_try >= 2; s_try -= 2) {  // deepest operand ring with >= s+2 plane stages
             if (budget < s_try * op_stage) continue;
             int sp = (int)((budget - s_try * op_stage) / pl_stage);
             if (sp > MAX_PSTAGES) sp = MAX_PSTAGES;
-            if (sp * p.kps >= s_try + 2 || (s_try == 2 && sp >= 2)) { S = s_try; SP = sp; break; }
+            sp &= ~1;
+            if (sp >= s_try + 2 || (s_try == 2 && sp >= 2)) { S = s_try; SP = sp; break; }
         }
         if (S < 2) return cudaErrorInvalidConfiguration;
         p.stages = S;
@@ -741,10 +717,10 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         const size_t smem = (size_t)S * op_stage + (size_t)SP * pl_stage + fixed - 1024 + 64;
         if (g.conv) {
             if (!make_conv_act_map(&ta, A, g, p.conv_bw)) return cudaErrorInvalidValue;
-        } else if (!make_plane_map(&ta, A, g.M, g.a_bits, g.Cw, 1, 128, p.kps)) {
+        } else if (!make_plane_map(&ta, A, g.M, g.a_bits, g.Cw, 1, 128)) {
             return cudaErrorInvalidValue;
         }
-        if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, g.RS, brows, p.kps)) return cudaErrorInvalidValue;
+        if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, g.RS, brows)) return cudaErrorInvalidValue;
         switch (g.enc) {
         case APNN_ENC_01_01: err = launch2_bn<false, false>(BNP, ta, tb, p, clusters * 2, smem, s); break;
         case APNN_ENC_PM1_PM1: err = launch2_bn<true, true>(BNP, ta, tb, p, clusters * 2, smem, s); break;
@@ -772,7 +748,6 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         if (S < 2) return cudaErrorInvalidConfiguration;
         p.stages = S;
         p.pstages = S;
-        p.kps = 1;
         uint32_t cols = BN + 32 * S, pow2 = 32;
         while (pow2 < cols) pow2 <<= 1;
         p.tmem_cols = pow2;
