@@ -35,6 +35,7 @@
 #include <cuda.h>
 
 #include <cstdio>
+#include <cstring>
 #include <mutex>
 
 #include "tc_common.cuh"
@@ -45,6 +46,8 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int MAX_STAGES = 8;     // operand stages (A in TMEM: 32 columns each)
 constexpr int MAX_PSTAGES = 16;   // packed-plane stages of the 2-CTA kernel
+constexpr int kStgWarpBytes = 8192;  // store staging per epilogue warp (1024-aligned)
+enum { kOutDirect = 0, kOutTma = 1, kOutLsu = 2 };
 
 struct Params {
     Geom g;
@@ -58,7 +61,9 @@ struct Params {
     uint32_t b_bytes;   // B plane bytes per stage (this CTA's rows)
     uint32_t tmem_cols;
     int tiles_m, num_tiles;
-    int use_tab;        // fused epilogue through the threshold table
+    int tab_mode;       // fused epilogue: kTabNone / kTabQ3 / kTabHybrid (tc_common.cuh)
+    int out_mode;       // epilogue stores: kOutDirect / kOutTma (tensor map tmapY) / kOutLsu (coalesced)
+    int nwb;            // packed TMA store box width in words (2-CTA kernel)
     int acc_shift;      // scaled operands: accumulator = Y << acc_shift (2-CTA kernel)
     // conv A-row tiling of the 2-CTA kernel (TMA row boxes):
     //   conv_k > 0: a CTA tile is conv_k whole output rows (conv_k * Wo <= 128 pixels)
@@ -67,6 +72,7 @@ struct Params {
     int conv_box_stride;  // bytes between row boxes in a plane stage (16*bw*bits rounded up to 128: TMA dst alignment)
     uint32_t a_tx_bytes;  // bytes the A loads of one stage actually deliver (expect_tx; excludes slot padding)
     unsigned long long* trace;  // development trace (APNN_TRACE), nullptr normally
+    int exp_nostore;            // experiment knob (APNN_EXP_NOSTORE): skip the epilogue stores
 };
 
 // development trace of CTA 0: clock64 stamps per k-block / tile (APNN_TRACE=<file>)
@@ -78,6 +84,16 @@ __device__ __forceinline__ void trace_at(const Params& p, int ev, int idx) {
         unsigned long long c;
         asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
         p.trace[ev * kTraceN + idx] = c;
+    }
+}
+// per-CTA %globaltimer stamps (ns): 0 entry, 1 after the prologue, 2 work done, 3 exit
+constexpr int kCtaTraceMax = 1024;
+__device__ __forceinline__ void cta_stamp(const Params& p, int k) {
+    const int b = blockIdx.x + blockIdx.y * gridDim.x;
+    if (p.trace && threadIdx.x == 0 && b < kCtaTraceMax) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[kTraceN * TR_N + b * 4 + k] = t;
     }
 }
 
@@ -112,7 +128,7 @@ constexpr int T2_THREADS = (T2_MMA_WARP + 1) * 32;
 template <int BNP, bool A_PM1, bool W_PM1, bool SCALED>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     tc2_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
-               const Params p) {
+               const __grid_constant__ CUtensorMap tmapY, const Params p) {
     using namespace sm100;
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr int BROWS = BNP / 2;                               // B rows per CTA
@@ -120,7 +136,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     constexpr uint32_t BOP_STAGE = BROWS * 128;                  // bytes of one B operand stage
     const int S = p.stages, SP = p.pstages;
     uint8_t* sBop = smem;                                        // S x BROWS rows x 128 B
-    uint8_t* sApl = sBop + (size_t)S * BOP_STAGE;                // SP x a_bytes
+    uint8_t* sStg = sBop + (size_t)S * BOP_STAGE;                // 4 epilogue warps x 8 KB TMA-store staging
+    uint8_t* sApl = sStg + 4 * kStgWarpBytes;                    // SP x a_bytes
     uint8_t* sBpl = sApl + (size_t)SP * p.a_bytes;               // SP x b_bytes
     int32_t* sTab = reinterpret_cast<int32_t*>(sBpl + (size_t)SP * p.b_bytes);  // 256 x 16 int32
     uint64_t* bars = reinterpret_cast<uint64_t*>(sTab + T2_BN * kTabStride);
@@ -133,6 +150,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accum_empty + 1);
     volatile uint32_t* dep_slots = tmem_holder + 1;                // [T2_RECOMB_WARPS * 32]
 
+    cta_stamp(p, 0);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = cluster_ctarank();
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
@@ -142,6 +160,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     if (warp == T2_TMA_WARP && lane == 0) {
         tma_prefetch(&tmapA);
         tma_prefetch(&tmapB);
+        if (p.out_mode == kOutTma) tma_prefetch(&tmapY);
         for (int s = 0; s < SP; s++) {
             mbar_init(&plane_full[s], 1);
             mbar_init(&plane_empty[s], 8);
@@ -161,6 +180,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_holder;
     constexpr uint32_t A_COL = 256;
+    cta_stamp(p, 1);
 
     if (warp == T2_TMA_WARP) {
         // ---------------------------------------------------- TMA producer
@@ -299,22 +319,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
         }
     } else {
         // ---------------------------------------------------- epilogue
+        // Each warp owns 32 rows of the CTA tile (its TMEM lane quarter).  Stores go
+        // through shared-memory staging and TMA (coalesced, clipped at M / N): int32
+        // as 32 x 32 swizzled blocks (double-buffered per warp), packed codes as one
+        // {nwb words, out_bits, 32 rows} box per tile.  Warps whose 32-row slab runs
+        // past a conv tile's rows store directly (the box would overwrite the next
+        // tile's rows).
         const int q = warp & 3;
         const int t = q * 32 + lane;               // row in this CTA's 128
         const int et = threadIdx.x - T2_EPI0 * 32;  // 0..127
         const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
         const uint32_t accum_empty0 = mapa(smem_u32(accum_empty), 0);
+        const int ob = p.e.out_bits;
+        uint8_t* stg = sStg + q * kStgWarpBytes;
+        const uint32_t stg_addr = smem_u32(stg);
         int tc = 0;
+        uint32_t nst = 0;
         for (int tile = cid; tile < p.num_tiles; tile += ncl, tc++) {
             int mb, len;
             cta_tile_rows(p, (tile % p.tiles_m) * 2 + rank, mb, len);
             const int m = t < len ? mb + t : g.M;   // rows beyond the tile are not stored
             const int n0 = (tile / p.tiles_m) * T2_BN;
-            if (p.use_tab) {
+            const bool any = q * 32 < len;
+            const bool use_tma = p.out_mode == kOutTma && any && (!g.conv || q * 32 + 32 <= len) && !p.exp_nostore;
+            const bool use_lsu = p.out_mode == kOutLsu && any && !p.exp_nostore;
+            const int row0 = mb + q * 32, row_end = mb + len;
+            if (p.tab_mode) {
                 named_bar_sync(1, 128);  // previous tile's readers are done
                 if (et < T2_BN) build_threshold_row(sTab + et * kTabStride, n0 + et, g.N, p.e);
                 if (et + 128 < T2_BN) build_threshold_row(sTab + (et + 128) * kTabStride, n0 + et + 128, g.N, p.e);
                 named_bar_sync(1, 128);
+            }
+            if (ob && use_tma) {  // the previous tile's packed box has been read out of staging
+                if (lane == 0) bulk_wait_read<0>();
+                __syncwarp();
             }
             mbar_wait(accum_full, tc & 1);
             if (warp == T2_EPI0 && lane == 0) trace_at(p, TR_EPI_FULL, tc);
@@ -328,22 +366,75 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < 32; i++) acc[i] = (uint32_t)((int32_t)acc[i] >> p.acc_shift);
                 }
-                epilogue_chunk(acc, m, n0 + c, c, g, p.e, p.Y, p.use_tab ? sTab : nullptr);
+                if (!any || p.exp_nostore) continue;
+                if (ob == 0) {
+                    if (use_tma) {
+                        uint8_t* b = stg + (nst & 1) * 4096;
+                        if (lane == 0) bulk_wait_read<1>();  // this buffer's store (two ago) has been read
+                        __syncwarp();
+                        stage_int32_chunk(acc, b, lane);
+                        fence_async_smem_cta();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tmapY, smem_u32(b), n0 + c, mb + q * 32);
+                            bulk_commit();
+                        }
+                        nst++;
+                    } else if (use_lsu) {
+                        stage_int32_chunk(acc, stg, lane);
+                        __syncwarp();
+                        writeback_int32_block(stg, lane, reinterpret_cast<int32_t*>(p.Y), row0, row_end, n0 + c, g.N);
+                        __syncwarp();
+                    } else {
+                        epilogue_chunk(acc, m, n0 + c, c, g, p.e, p.Y, nullptr, kTabNone);
+                    }
+                } else if (use_tma || use_lsu) {
+                    uint32_t w[8];
+                    requant_chunk(acc, n0 + c, c, g, p.e, sTab, p.tab_mode, w);
+                    stage_words(w, ob, p.nwb, c >> 5, reinterpret_cast<uint32_t*>(stg), lane);
+                } else {
+                    epilogue_chunk(acc, m, n0 + c, c, g, p.e, p.Y, sTab, p.tab_mode);
+                }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(accum_empty0);
+            if (ob && any && !p.exp_nostore) {
+                if (use_tma || use_lsu) {
+                    const uint32_t zero8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    for (int wi = T2_BN / 32; wi < p.nwb; wi++)  // box words past the tile: N padding
+                        stage_words(zero8, ob, p.nwb, wi, reinterpret_cast<uint32_t*>(stg), lane);
+                }
+                if (use_tma) {
+                    fence_async_smem_cta();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_3d(&tmapY, stg_addr, n0 / 32, 0, row0);
+                        bulk_commit();
+                    }
+                } else if (use_lsu) {
+                    __syncwarp();
+                    writeback_packed_block(reinterpret_cast<const uint32_t*>(stg), lane, reinterpret_cast<uint32_t*>(p.Y),
+                                           row0, row_end, n0 / 32, (g.N + 127) / 128 * 4, ob, p.nwb);
+                    __syncwarp();
+                } else if (n0 + T2_BN >= g.N) {
+                    zero_pad_words(m, (n0 + T2_BN) / 32, g, p.e, p.Y);
+                }
+            }
             if (warp == T2_EPI0 && lane == 0) trace_at(p, TR_EPI_DONE, tc);
         }
+        if (lane == 0) bulk_wait<0>();
     }
 
     tc_fence_before();
     __syncthreads();
+    cta_stamp(p, 2);
     cluster_sync();
     if (warp == T2_MMA_WARP) {
         tc_fence_after();
         tmem_dealloc2(tmem, p.tmem_cols);
     }
+    cta_stamp(p, 3);
 }
 
 // ============================================================== 1-CTA kernel
@@ -352,7 +443,7 @@ constexpr int T1_THREADS = 10 * 32;
 template <int BN, bool A_PM1, bool W_PM1>
 __global__ void __launch_bounds__(T1_THREADS, 1)
     tc1_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
-               const Params p) {
+               const __grid_constant__ CUtensorMap tmapY, const Params p) {
     using namespace sm100;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = p.stages;
@@ -368,6 +459,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
     uint64_t* accum_full = bars + 4 * MAX_STAGES;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * MAX_STAGES + 2);
 
+    cta_stamp(p, 0);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
     const Geom& g = p.g;
@@ -391,6 +483,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_holder;
     constexpr uint32_t A_COL = BN;
+    cta_stamp(p, 1);
 
     if (warp == 0) {
         const bool conv = g.conv;
@@ -438,7 +531,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
         const int t = q * 32 + lane;
         const int et = threadIdx.x - 64;  // 0..255
         const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
-        if (p.use_tab && et < BN) build_threshold_row(sTab + et * kTabStride, n0 + et, g.N, p.e);
+        if (p.tab_mode && et < BN) build_threshold_row(sTab + et * kTabStride, n0 + et, g.N, p.e);
         RowCtx rc;
         if (A_PM1 && g.conv) rc = make_row(g, m0 + t);
         for (int kb = 0; kb < nkb; kb++) {
@@ -477,21 +570,50 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
         tc_fence_after();
         const int m = m0 + t;
         constexpr int half = BN / 2;
+        // int32 output: TMA stores from per-warp staging that reuses the (now idle)
+        // pipeline buffers; packed output: direct stores (small problems only)
+        const bool use_tma = p.out_mode == kOutTma && p.e.out_bits == 0 && m0 + q * 32 < g.M && !p.exp_nostore;
+        const bool use_lsu = p.out_mode == kOutLsu && p.e.out_bits == 0 && m0 + q * 32 < g.M && !p.exp_nostore;
+        uint8_t* stg = smem + (warp - 2) * kStgWarpBytes;
+        uint32_t nst = 0;
 #pragma unroll 1
         for (int c = grp * half; c < (grp + 1) * half; c += 32) {
             uint32_t acc[32];
             tmem_ld32(tmem_lane + c, acc);
             tmem_wait_ld();
-            epilogue_chunk(acc, m, n0 + c, c, g, p.e, p.Y, p.use_tab ? sTab : nullptr);
+            if (p.exp_nostore) continue;
+            if (use_tma) {
+                uint8_t* b = stg + (nst & 1) * 4096;
+                if (lane == 0) bulk_wait_read<1>();
+                __syncwarp();
+                stage_int32_chunk(acc, b, lane);
+                fence_async_smem_cta();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tmapY, smem_u32(b), n0 + c, m0 + q * 32);
+                    bulk_commit();
+                }
+                nst++;
+            } else if (use_lsu) {
+                stage_int32_chunk(acc, stg, lane);
+                __syncwarp();
+                writeback_int32_block(stg, lane, reinterpret_cast<int32_t*>(p.Y), m0 + q * 32, g.M, n0 + c, g.N);
+                __syncwarp();
+            } else {
+                epilogue_chunk(acc, m, n0 + c, c, g, p.e, p.Y, sTab, p.tab_mode);
+            }
         }
+        if (use_tma && lane == 0) bulk_wait<0>();
     }
 
     tc_fence_before();
     __syncthreads();
+    cta_stamp(p, 2);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, p.tmem_cols);
     }
+    cta_stamp(p, 3);
 }
 
 // ------------------------------------------------------------------ host side
@@ -552,6 +674,32 @@ static bool make_conv_act_map(CUtensorMap* m, const uint32_t* base, const Geom& 
     return r == CUDA_SUCCESS;
 }
 
+// int32 output Y [M][N] as a 2-D tensor {N, M}; box {32 cols, 32 rows}, SWIZZLE_128B
+// (the staging layout of stage_int32_chunk).  Needs N % 4 == 0 (16-byte row stride).
+static bool make_out_map_i32(CUtensorMap* m, void* Y, int M, int N) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+    cuuint64_t strides[1] = {(cuuint64_t)N * 4};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, Y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// packed output [M][bits][Nw] as a 3-D tensor {Nw, bits, M}; box {nwb, bits, 32}
+static bool make_out_map_packed(CUtensorMap* m, void* Y, int M, int Nw, int bits, int nwb) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)Nw, (cuuint64_t)bits, (cuuint64_t)M};
+    cuuint64_t strides[2] = {(cuuint64_t)Nw * 4, (cuuint64_t)bits * Nw * 4};
+    cuuint32_t box[3] = {(cuuint32_t)nwb, (cuuint32_t)bits, 32};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, Y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static int stage_count(size_t per_stage, size_t fixed) {
     const size_t budget = 227 * 1024 - fixed;
     int S = (int)(budget / per_stage);
@@ -564,39 +712,39 @@ static cudaError_t set_smem(K kfn) {
 }
 
 template <int BNP, bool AP, bool WP>
-static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid, size_t smem,
-                           cudaStream_t s) {
+static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, const Params& p,
+                           int grid, size_t smem, cudaStream_t s) {
     auto kfn = p.acc_shift > 0 ? tc2_kernel<BNP, AP, WP, true> : tc2_kernel<BNP, AP, WP, false>;
     cudaError_t e = set_smem(kfn);
     if (e != cudaSuccess) return e;
-    kfn<<<grid, T2_THREADS, smem, s>>>(ta, tb, p);
+    kfn<<<grid, T2_THREADS, smem, s>>>(ta, tb, ty, p);
     return cudaGetLastError();
 }
 
 template <bool AP, bool WP>
-static cudaError_t launch2_bn(int BNP, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid,
-                              size_t smem, cudaStream_t s) {
-    if (BNP == 256) return launch2<256, AP, WP>(ta, tb, p, grid, smem, s);
-    if (BNP == 128) return launch2<128, AP, WP>(ta, tb, p, grid, smem, s);
-    return launch2<64, AP, WP>(ta, tb, p, grid, smem, s);
+static cudaError_t launch2_bn(int BNP, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty,
+                              const Params& p, int grid, size_t smem, cudaStream_t s) {
+    if (BNP == 256) return launch2<256, AP, WP>(ta, tb, ty, p, grid, smem, s);
+    if (BNP == 128) return launch2<128, AP, WP>(ta, tb, ty, p, grid, smem, s);
+    return launch2<64, AP, WP>(ta, tb, ty, p, grid, smem, s);
 }
 
 template <int BN, bool AP, bool WP>
-static cudaError_t launch1(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, dim3 grid, size_t smem,
-                           cudaStream_t s) {
+static cudaError_t launch1(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, const Params& p,
+                           dim3 grid, size_t smem, cudaStream_t s) {
     auto kfn = tc1_kernel<BN, AP, WP>;
     cudaError_t e = set_smem(kfn);
     if (e != cudaSuccess) return e;
-    kfn<<<grid, T1_THREADS, smem, s>>>(ta, tb, p);
+    kfn<<<grid, T1_THREADS, smem, s>>>(ta, tb, ty, p);
     return cudaGetLastError();
 }
 
 template <bool AP, bool WP>
-static cudaError_t launch1_bn(int BN, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, dim3 grid,
-                              size_t smem, cudaStream_t s) {
-    if (BN == 256) return launch1<256, AP, WP>(ta, tb, p, grid, smem, s);
-    if (BN == 128) return launch1<128, AP, WP>(ta, tb, p, grid, smem, s);
-    return launch1<64, AP, WP>(ta, tb, p, grid, smem, s);
+static cudaError_t launch1_bn(int BN, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty,
+                              const Params& p, dim3 grid, size_t smem, cudaStream_t s) {
+    if (BN == 256) return launch1<256, AP, WP>(ta, tb, ty, p, grid, smem, s);
+    if (BN == 128) return launch1<128, AP, WP>(ta, tb, ty, p, grid, smem, s);
+    return launch1<64, AP, WP>(ta, tb, ty, p, grid, smem, s);
 }
 
 }  // namespace tc
@@ -618,6 +766,19 @@ static bool tc_scaled_enabled() {
     return v != 0;
 }
 
+// epilogue store path.  Default (measured, 8192^3 w1a2, scripts/exp_time.py): int32
+// output through TMA stores (441 us vs 481 coalesced-LSU vs 497 direct), packed
+// output through coalesced LSU stores (equal to TMA, fewer constraints).
+// Experiment knob APNN_EPI_STORE: 0 direct, 1 TMA, 2 coalesced LSU.
+static int epi_store_mode(bool packed) {
+    static int v = -2;
+    if (v == -2) {
+        const char* s = getenv("APNN_EPI_STORE");
+        v = s ? atoi(s) : -1;
+    }
+    return v >= 0 ? v : (packed ? tc::kOutLsu : tc::kOutTma);
+}
+
 // variant knob for experiments: APNN_TC_KERNEL=1 forces the 1-CTA kernel
 static int tc_kernel_override() {
     static int v = -1;
@@ -637,17 +798,27 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     p.Y = Y;
     p.A = A;
     p.nkb = g.nchunks;
-    p.use_tab = (e.out_bits > 0 && e.out_bits <= 4) ? 1 : 0;
+    p.tab_mode = kTabNone;
+    if (e.out_bits > 0 && e.out_bits <= 2) {
+        p.tab_mode = kTabQ3;
+    } else if (e.out_bits > 2 && (unsigned long long)e.qmax * (unsigned long long)e.S <= 0xFFFFFFFFull) {
+        p.tab_mode = kTabHybrid;  // 32-bit in-range division is exact (requant_hybrid)
+    }
+    p.out_mode = kOutDirect;
+    p.nwb = 0;
+    const int want_mode = epi_store_mode(e.out_bits > 0);
     p.acc_shift = 0;
     p.trace = nullptr;
+    p.exp_nostore = getenv("APNN_EXP_NOSTORE") ? 1 : 0;
     const char* trace_path = getenv("APNN_TRACE");
     if (trace_path) {
-        cudaMalloc(&p.trace, sizeof(unsigned long long) * kTraceN * TR_N);
-        cudaMemset(p.trace, 0, sizeof(unsigned long long) * kTraceN * TR_N);
+        cudaMalloc(&p.trace, sizeof(unsigned long long) * (kTraceN * TR_N + 4 * kCtaTraceMax));
+        cudaMemset(p.trace, 0, sizeof(unsigned long long) * (kTraceN * TR_N + 4 * kCtaTraceMax));
     }
     const int ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
     const bool two = (g.M > 128) && tc_kernel_override() != 1;
-    CUtensorMap ta, tb;
+    CUtensorMap ta, tb, ty;
+    std::memset(&ty, 0, sizeof(ty));
     cudaError_t err;
     if (two) {
         const int BNP = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);   // pair tile width
@@ -664,7 +835,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
             p.a_tx_bytes = p.a_bytes;
         }
         const size_t fixed = (size_t)256 * kTabStride * 4 + (2 * MAX_PSTAGES + 2 * MAX_STAGES + 4) * 8 +
-                             T2_RECOMB_WARPS * 32 * 4 + 1024;
+                             T2_RECOMB_WARPS * 32 * 4 + 4 * kStgWarpBytes + 1024;
         const size_t budget = 227 * 1024 - fixed;
         const size_t op_stage = (size_t)brows * 128, pl_stage = p.a_bytes + p.b_bytes;
         // Both ring depths must be EVEN: the two recombination teams take alternating
@@ -710,7 +881,8 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
             if (p.conv_bw * g.stride > 256 || g.stride > 8) return cudaErrorInvalidConfiguration;
         }
         p.tiles_m = (cta_tiles + 1) / 2;
-        const int tiles_n = (ncols + BNP - 1) / BNP;
+        // tiles cover [0, N); the packed path also writes the N padding words (zero)
+        const int tiles_n = (g.N + BNP - 1) / BNP;
         p.num_tiles = p.tiles_m * tiles_n;
         int clusters = sms / 2;
         if (clusters > p.num_tiles) clusters = p.num_tiles;
@@ -721,23 +893,22 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
             return cudaErrorInvalidValue;
         }
         if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, g.RS, brows)) return cudaErrorInvalidValue;
-        switch (g.enc) {
-        case APNN_ENC_01_01: err = launch2_bn<false, false>(BNP, ta, tb, p, clusters * 2, smem, s); break;
-        case APNN_ENC_PM1_PM1: err = launch2_bn<true, true>(BNP, ta, tb, p, clusters * 2, smem, s); break;
-        case APNN_ENC_W_PM1_A_01: err = launch2_bn<false, true>(BNP, ta, tb, p, clusters * 2, smem, s); break;
-        default: err = launch2_bn<true, false>(BNP, ta, tb, p, clusters * 2, smem, s); break;
-        }
-        if (p.trace) {  // development only: synchronous dump
-            static unsigned long long host[kTraceN * TR_N];
-            cudaStreamSynchronize(s);
-            cudaMemcpy(host, p.trace, sizeof(host), cudaMemcpyDeviceToHost);
-            cudaFree(p.trace);
-            if (FILE* f = fopen(trace_path, "wb")) {
-                int hdr[4] = {kTraceN, TR_N, nkb_dbg(p), S};
-                fwrite(hdr, sizeof(hdr), 1, f);
-                fwrite(host, sizeof(host), 1, f);
-                fclose(f);
+        p.nwb = BNP / 32 < 4 ? 4 : BNP / 32;
+        if (want_mode == kOutLsu) {
+            p.out_mode = (e.out_bits > 0 || g.N % 4 == 0) ? kOutLsu : kOutDirect;
+        } else if (want_mode == kOutTma) {
+            if (e.out_bits == 0) {
+                p.out_mode = (g.N % 4 == 0 && make_out_map_i32(&ty, Y, g.M, g.N)) ? kOutTma : kOutDirect;
+            } else {
+                const int Nw = (g.N + 127) / 128 * 4;
+                p.out_mode = make_out_map_packed(&ty, Y, g.M, Nw, e.out_bits, p.nwb) ? kOutTma : kOutDirect;
             }
+        }
+        switch (g.enc) {
+        case APNN_ENC_01_01: err = launch2_bn<false, false>(BNP, ta, tb, ty, p, clusters * 2, smem, s); break;
+        case APNN_ENC_PM1_PM1: err = launch2_bn<true, true>(BNP, ta, tb, ty, p, clusters * 2, smem, s); break;
+        case APNN_ENC_W_PM1_A_01: err = launch2_bn<false, true>(BNP, ta, tb, ty, p, clusters * 2, smem, s); break;
+        default: err = launch2_bn<true, false>(BNP, ta, tb, ty, p, clusters * 2, smem, s); break;
         }
     } else {
         const int BN = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
@@ -757,11 +928,29 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         if (!make_plane_map(&ta, A, g.conv ? 1 : g.M, g.a_bits, g.Cw, 1, BM)) return cudaErrorInvalidValue;
         if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, g.RS, BN)) return cudaErrorInvalidValue;
         dim3 grid((g.M + BM - 1) / BM, (ncols + BN - 1) / BN);
+        // int32 output through TMA stores, staged in the idle pipeline buffers (8 warps x 8 KB)
+        if (e.out_bits == 0 && g.N % 4 == 0 && want_mode != kOutDirect &&
+            (size_t)S * ((size_t)BN * 128 + p.a_bytes + p.b_bytes) >= 8 * kStgWarpBytes) {
+            if (want_mode == kOutLsu) p.out_mode = kOutLsu;
+            else p.out_mode = make_out_map_i32(&ty, Y, g.M, g.N) ? kOutTma : kOutDirect;
+        }
         switch (g.enc) {
-        case APNN_ENC_01_01: err = launch1_bn<false, false>(BN, ta, tb, p, grid, smem, s); break;
-        case APNN_ENC_PM1_PM1: err = launch1_bn<true, true>(BN, ta, tb, p, grid, smem, s); break;
-        case APNN_ENC_W_PM1_A_01: err = launch1_bn<false, true>(BN, ta, tb, p, grid, smem, s); break;
-        default: err = launch1_bn<true, false>(BN, ta, tb, p, grid, smem, s); break;
+        case APNN_ENC_01_01: err = launch1_bn<false, false>(BN, ta, tb, ty, p, grid, smem, s); break;
+        case APNN_ENC_PM1_PM1: err = launch1_bn<true, true>(BN, ta, tb, ty, p, grid, smem, s); break;
+        case APNN_ENC_W_PM1_A_01: err = launch1_bn<false, true>(BN, ta, tb, ty, p, grid, smem, s); break;
+        default: err = launch1_bn<true, false>(BN, ta, tb, ty, p, grid, smem, s); break;
+        }
+    }
+    if (p.trace) {  // development only: synchronous dump
+        static unsigned long long host[kTraceN * TR_N + 4 * kCtaTraceMax];
+        cudaStreamSynchronize(s);
+        cudaMemcpy(host, p.trace, sizeof(host), cudaMemcpyDeviceToHost);
+        cudaFree(p.trace);
+        if (FILE* f = fopen(trace_path, "wb")) {
+            int hdr[4] = {kTraceN, TR_N, nkb_dbg(p), p.stages};
+            fwrite(hdr, sizeof(hdr), 1, f);
+            fwrite(host, sizeof(host), 1, f);
+            fclose(f);
         }
     }
     count_launch();

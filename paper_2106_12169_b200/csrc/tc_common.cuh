@@ -321,15 +321,18 @@ __device__ __forceinline__ void conv_gather_kb(const uint32_t* X, const Geom& g,
 }
 
 // ------------------------------------------------------------------ epilogue
-// Threshold table for out_bits <= 4 (Q = 2^b - 1 <= 15).  For column n:
-//   q = clamp(floor((alpha y + beta)/S), 0, Q) = #{k in 1..Q : y' > U_k},
-//   y' = -y if alpha < 0 else y,
-//   alpha > 0: U_k = ceil((kS - beta)/alpha) - 1
-//   alpha < 0: U_k = -floor((kS - beta)/alpha) - 1
-//   alpha = 0: U_k = INT32_MIN if beta >= kS else INT32_MAX
-// (|y| <= 2^31 - 1 by the host overflow check, so clamping U to int32 is exact.)
-// Row layout: 16 int32 per column: [sign (+1 / -1), U_1, ..., U_15].
-constexpr int kTabStride = 16;
+// Per-column requantisation table (built once per output tile in shared memory).
+// For column n, with y' = -y if alpha < 0 else y (|y| <= 2^31 - 1 by the host
+// overflow check, so y' never overflows), q = clamp(floor((alpha y + beta)/S), 0, Q)
+// is a non-decreasing function of y', and
+//   q >= k  <=>  y' > U_k,   U_k = ceil((kS - beta)/alpha) - 1   (alpha > 0)
+//                                = -floor((kS - beta)/alpha) - 1  (alpha < 0)
+//                                = INT32_MIN if beta >= kS else INT32_MAX (alpha = 0)
+// (clamped to int32: exact for int32 y').  Row layout, kTabStride int32:
+//   [0] sign  [1] U_1  [2] U_2  [3] U_3  [4] U_Q  [5] alpha  [6] beta  [7] unused
+// Padding columns (n >= N) get all thresholds INT32_MAX and alpha = beta = 0: q = 0.
+constexpr int kTabStride = 8;
+enum { kTabNone = 0, kTabQ3 = 1, kTabHybrid = 2 };
 
 __device__ __forceinline__ long long floor_div64(long long a, long long b) {
     long long q = a / b;
@@ -337,47 +340,33 @@ __device__ __forceinline__ long long floor_div64(long long a, long long b) {
     return q;
 }
 
+__device__ __forceinline__ int32_t threshold_k(long long al, long long be, long long S, int k) {
+    const long long num = (long long)k * S - be;
+    long long U;
+    if (al > 0) U = -floor_div64(-num, al) - 1;  // ceil(num/al) - 1
+    else if (al < 0) U = -floor_div64(num, al) - 1;
+    else U = (be >= (long long)k * S) ? (long long)INT32_MIN : 0x7FFFFFFFLL;
+    if (U < INT32_MIN) U = INT32_MIN;
+    if (U > 0x7FFFFFFFLL) U = 0x7FFFFFFFLL;
+    return (int32_t)U;
+}
+
 __device__ __forceinline__ void build_threshold_row(int32_t* row, int n, int N, const Epi& e) {
     const int Q = e.qmax;
-    if (n >= N) {  // padding columns: q = 0
-        row[0] = 1;
-        for (int k = 1; k <= 15; k++) row[k] = 0x7FFFFFFF;
+    if (n >= N) {
+        *reinterpret_cast<int4*>(row) = make_int4(1, 0x7FFFFFFF, 0x7FFFFFFF, 0x7FFFFFFF);
+        *reinterpret_cast<int4*>(row + 4) = make_int4(0x7FFFFFFF, 0, 0, 0);
         return;
     }
     const long long al = epi_alpha(e, n), be = epi_beta(e, n), S = e.S;
-    row[0] = al < 0 ? -1 : 1;
-    for (int k = 1; k <= 15; k++) {
-        long long U;
-        if (k > Q) {
-            U = 0x7FFFFFFFLL;
-        } else {
-            const long long num = (long long)k * S - be;
-            if (al > 0) U = -floor_div64(-num, al) - 1;  // ceil(num/al) - 1
-            else if (al < 0) U = -floor_div64(num, al) - 1;
-            else U = (be >= (long long)k * S) ? (long long)INT32_MIN : 0x7FFFFFFFLL;
-        }
-        if (U < INT32_MIN) U = INT32_MIN;
-        if (U > 0x7FFFFFFFLL) U = 0x7FFFFFFFLL;
-        row[k] = (int32_t)U;
-    }
-}
-
-template <bool kSmallQ>  // kSmallQ: Q <= 3 (out_bits <= 2), one 16-byte table read
-__device__ __forceinline__ uint32_t requant_tab(const int32_t* row, int32_t y) {
-    const int4 h = *reinterpret_cast<const int4*>(row);
-    const int32_t yp = y * h.x;
-    uint32_t q = (yp > h.y) + (yp > h.z) + (yp > h.w);
-    if (!kSmallQ) {
+    int32_t u[3];
 #pragma unroll
-        for (int c = 1; c < 4; c++) {
-            const int4 u = *reinterpret_cast<const int4*>(row + 4 * c);
-            q += (yp > u.x) + (yp > u.y) + (yp > u.z) + (yp > u.w);
-        }
-    }
-    return q;
+    for (int k = 1; k <= 3; k++) u[k - 1] = (k <= Q) ? threshold_k(al, be, S, k) : 0x7FFFFFFF;
+    *reinterpret_cast<int4*>(row) = make_int4(al < 0 ? -1 : 1, u[0], u[1], u[2]);
+    *reinterpret_cast<int4*>(row + 4) = make_int4(threshold_k(al, be, S, Q), (int32_t)al, (int32_t)be, 0);
 }
 
-// out_bits <= 2 (Q <= 3): with c_k = [y' > U_k] monotone (c1 >= c2 >= c3),
+// Q <= 3 (out_bits <= 2): with c_k = [y' > U_k] monotone (c1 >= c2 >= c3),
 // q = c1 + c2 + c3, so bit 1 of q is c2 and bit 0 is c1 ^ c2 ^ c3.  Plane words
 // are assembled straight from the comparisons (no byte staging).
 __device__ __forceinline__ void requant_chunk_words_q3(const uint32_t (&acc)[32], const int32_t* tab, int lc,
@@ -394,21 +383,53 @@ __device__ __forceinline__ void requant_chunk_words_q3(const uint32_t (&acc)[32]
     }
 }
 
-// Threshold-table requant of one 32-column chunk straight to plane words:
-// words[t] bit i = bit t of q(column lc + i), t < out_bits <= 4.
-template <bool kSmallQ>
-__device__ __forceinline__ void requant_chunk_words(const uint32_t (&acc)[32], const int32_t* tab, int lc,
-                                                    int out_bits, uint32_t (&words)[4]) {
+// Q >= 7 (out_bits >= 3), host-checked Q*S < 2^32: the two clamps come from the
+// table; in between S <= v < Q*S, so v = alpha*y + beta is exact in 32-bit
+// (wrap-around) arithmetic and q = v / S is a 32-bit division by the layer
+// constant: an fp32 estimate (off by at most one) and one exact correction.
+__device__ __forceinline__ uint32_t requant_hybrid(const int32_t* row, int32_t y, uint32_t S, float invS,
+                                                   uint32_t Q) {
+    const int4 h = *reinterpret_cast<const int4*>(row);
+    const int4 h2 = *reinterpret_cast<const int4*>(row + 4);
+    const int32_t yp = y * h.x;
+    const uint32_t v = (uint32_t)h2.y * (uint32_t)y + (uint32_t)h2.z;
+    uint32_t q = __float2uint_rz(__uint2float_rn(v) * invS);
+    const int32_t r = (int32_t)(v - q * S);
+    q = r < 0 ? q - 1 : (r >= (int32_t)S ? q + 1 : q);
+    q = yp > h2.x ? Q : q;
+    return yp > h.y ? q : 0u;
+}
+
+// 32 accumulators of row m, columns nb..nb+31 (lc = tile-local column of nb) ->
+// plane words: words[t] bit i = bit t of q(column nb + i), t < out_bits.
+__device__ __forceinline__ void requant_chunk(const uint32_t (&acc)[32], int nb, int lc, const Geom& g,
+                                              const Epi& e, const int32_t* tab, int tab_mode,
+                                              uint32_t (&words)[8]) {
+    if (tab_mode == kTabQ3) {
+        requant_chunk_words_q3(acc, tab, lc, words[0], words[1]);
+        return;
+    }
     uint32_t qb[8];
 #pragma unroll
     for (int i = 0; i < 8; i++) qb[i] = 0;
+    if (tab_mode == kTabHybrid) {
+        const uint32_t S = (uint32_t)e.S, Q = (uint32_t)e.qmax;
 #pragma unroll
-    for (int i = 0; i < 32; i++)
-        qb[i >> 2] |= requant_tab<kSmallQ>(tab + (lc + i) * kTabStride, (int32_t)acc[i]) << (8 * (i & 3));
+        for (int i = 0; i < 32; i++)
+            qb[i >> 2] |= requant_hybrid(tab + (lc + i) * kTabStride, (int32_t)acc[i], S, e.invS, Q) << (8 * (i & 3));
+    } else {
 #pragma unroll
-    for (int tb = 0; tb < 4; tb++) {
+        for (int i = 0; i < 32; i++) {
+            const int n = nb + i;
+            uint32_t qv = 0;
+            if (n < g.N) qv = requant(e, (int32_t)acc[i], epi_alpha(e, n), epi_beta(e, n));
+            qb[i >> 2] |= qv << (8 * (i & 3));
+        }
+    }
+#pragma unroll
+    for (int tb = 0; tb < 8; tb++) {
         uint32_t wv = 0;
-        if (tb < out_bits) {
+        if (tb < e.out_bits) {
 #pragma unroll
             for (int qq = 0; qq < 8; qq++) wv |= byte_bits_to_nibble(qb[qq], tb) << (4 * qq);
         }
@@ -416,10 +437,11 @@ __device__ __forceinline__ void requant_chunk_words(const uint32_t (&acc)[32], c
     }
 }
 
-// 32 accumulators of row m, columns nb..nb+31 (lc = tile-local column of nb).
-// tab: threshold table of the tile (nullptr -> division path / int32 output).
+// Direct (per-thread) stores of one 32-column chunk of row m: int32 row segment, or
+// the out_bits plane words.  Used where a TMA store box does not fit (partial conv
+// row slabs, the one-CTA kernel's packed output).
 __device__ __forceinline__ void epilogue_chunk(const uint32_t (&acc)[32], int m, int nb, int lc, const Geom& g,
-                                               const Epi& e, void* Yout, const int32_t* tab) {
+                                               const Epi& e, void* Yout, const int32_t* tab, int tab_mode) {
     if (m >= g.M) return;
     if (e.out_bits == 0) {
         int32_t* Y = reinterpret_cast<int32_t*>(Yout) + (long long)m * g.N;
@@ -439,36 +461,69 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&acc)[32], int m,
     const int word = nb / 32;
     if (word >= Nw) return;
     uint32_t* o = reinterpret_cast<uint32_t*>(Yout) + (long long)m * e.out_bits * Nw + word;
-    if (tab) {
-        uint32_t w4[4];
-        if (e.out_bits <= 2) {
-            requant_chunk_words_q3(acc, tab, lc, w4[0], w4[1]);
-            o[0] = w4[0];
-            if (e.out_bits == 2) o[Nw] = w4[1];
-            return;
-        }
-        requant_chunk_words<false>(acc, tab, lc, e.out_bits, w4);
+    uint32_t w[8];
+    requant_chunk(acc, nb, lc, g, e, tab, tab_mode, w);
 #pragma unroll
-        for (int tb = 0; tb < 4; tb++)
-            if (tb < e.out_bits) o[(long long)tb * Nw] = w4[tb];
-        return;
+    for (int tb = 0; tb < 8; tb++)
+        if (tb < e.out_bits) o[(long long)tb * Nw] = w[tb];
+}
+
+// zero the packed padding words [w_from, Nw) of row m (direct stores)
+__device__ __forceinline__ void zero_pad_words(int m, int w_from, const Geom& g, const Epi& e, void* Yout) {
+    if (m >= g.M) return;
+    const int Nw = (g.N + 127) / 128 * 4;
+    uint32_t* o = reinterpret_cast<uint32_t*>(Yout) + (long long)m * e.out_bits * Nw;
+    for (int tb = 0; tb < e.out_bits; tb++)
+        for (int w = w_from; w < Nw; w++) o[(long long)tb * Nw + w] = 0u;
+}
+
+// ---- TMA-store staging (one warp = 32 output rows; lane = row)
+// int32: a 32 x 32 block in the SWIZZLE_128B layout of a {32 cols, 32 rows} box:
+// 16-byte chunk j of row r at r*128 + ((j ^ (r & 7)) * 16): conflict-free st.shared.v4.
+__device__ __forceinline__ void stage_int32_chunk(const uint32_t (&acc)[32], uint8_t* stg, int lane) {
+    uint8_t* row = stg + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+        *reinterpret_cast<uint4*>(row + ((j ^ (lane & 7)) << 4)) =
+            make_uint4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+}
+// Coalesced write-back of a staged 32 x 32 int32 block (rows row0.., columns col0..):
+// lane l moves 16-byte piece (l & 7) of rows 4i + (l >> 3), so every st.global.v4
+// instruction writes four whole 128-byte row segments.  Rows >= row_end and columns
+// >= N are not written.  Requires N % 4 == 0.
+__device__ __forceinline__ void writeback_int32_block(const uint8_t* stg, int lane, int32_t* Y, int row0,
+                                                      int row_end, int col0, int N) {
+    const int j = lane & 7;
+    const int col = col0 + 4 * j;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        const int r = 4 * i + (lane >> 3);
+        const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 128 + ((j ^ (r & 7)) << 4));
+        if (row0 + r < row_end && col < N)
+            *reinterpret_cast<uint4*>(Y + (long long)(row0 + r) * N + col) = v;
     }
-    uint32_t qb[8];
-#pragma unroll
-    for (int i = 0; i < 8; i++) qb[i] = 0;
-#pragma unroll
-    for (int i = 0; i < 32; i++) {
-        const int n = nb + i;
-        uint32_t qv = 0;
-        if (n < g.N) qv = requant(e, (int32_t)acc[i], epi_alpha(e, n), epi_beta(e, n));
-        qb[i >> 2] |= qv << (8 * (i & 3));
+}
+// Coalesced write-back of a staged packed box [32 rows][bits][nwb words] to
+// out[m][t][w0 .. w0 + nwb) (clipped at Nw and row_end); lane handles 16-byte pieces.
+__device__ __forceinline__ void writeback_packed_block(const uint32_t* stg, int lane, uint32_t* out, int row0,
+                                                       int row_end, int w0, int Nw, int bits, int nwb) {
+    const int per_row = bits * nwb / 4;  // 16-byte pieces per row
+    const int total = 32 * per_row;
+    for (int i = lane; i < total; i += 32) {
+        const int r = i / per_row, pc = i - r * per_row;
+        const int t = (pc * 4) / nwb, w = (pc * 4) - t * nwb;
+        if (row0 + r < row_end && w0 + w < Nw)
+            *reinterpret_cast<uint4*>(out + ((long long)(row0 + r) * bits + t) * Nw + w0 + w) =
+                *reinterpret_cast<const uint4*>(stg + r * bits * nwb + t * nwb + w);
     }
-    for (int tb = 0; tb < e.out_bits; tb++) {
-        uint32_t wv = 0;
+}
+// packed: a {nwb words, bits, 32 rows} box, dense [row][plane][nwb] uint32
+__device__ __forceinline__ void stage_words(const uint32_t (&w)[8], int bits, int nwb, int wi, uint32_t* stg,
+                                            int lane) {
+    uint32_t* row = stg + lane * bits * nwb + wi;
 #pragma unroll
-        for (int qq = 0; qq < 8; qq++) wv |= byte_bits_to_nibble(qb[qq], tb) << (4 * qq);
-        o[(long long)tb * Nw] = wv;
-    }
+    for (int tb = 0; tb < 8; tb++)
+        if (tb < bits) row[tb * nwb] = w[tb];
 }
 
 }  // namespace tc

@@ -14,7 +14,18 @@ os.environ["APNN_TRACE"] = path  # read once per process by the library? no: rea
 ap.gemm(Ap, Wp, M, N, K, a, w, enc, epi=epi); torch.cuda.synchronize()
 raw = open(path, "rb").read()
 n, nev, nkb, S = struct.unpack("4i", raw[:16])
-t = np.frombuffer(raw[16:], dtype=np.uint64).reshape(nev, n).astype(np.int64)
+allv = np.frombuffer(raw[16:], dtype=np.uint64).astype(np.int64)
+t = allv[:nev * n].reshape(nev, n)
+ct = allv[nev * n:].reshape(-1, 4)
+ct = ct[ct[:, 0] > 0]
+if len(ct):
+    g0 = ct[:, 0].min()
+    c = ct - g0
+    print(f"CTAs={len(ct)} entry spread(ns): min {c[:,0].min()} max {c[:,0].max()}; "
+          f"prologue(ns) med {np.median(c[:,1]-c[:,0]):.0f} max {(c[:,1]-c[:,0]).max()}; "
+          f"work(ns) med {np.median(c[:,2]-c[:,1]):.0f} max {(c[:,2]-c[:,1]).max()}; "
+          f"teardown(ns) med {np.median(c[:,3]-c[:,2]):.0f} max {(c[:,3]-c[:,2]).max()}; "
+          f"span(ns) {c[:,3].max()}")
 t0 = t[t > 0].min()
 names = ["prod", "a_plane", "a_op", "a_done", "mma_opfull", "mma_issued", "epi_full", "epi_done"]
 print("nkb", nkb, "S", S)

@@ -142,6 +142,28 @@ def test_fused_epilogue(a_bits, w_bits, enc, out_bits, M, N, K):
     np.testing.assert_array_equal(got, want)
 
 
+@pytest.mark.parametrize("out_bits", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("M", [60, 300])  # 1-CTA and 2-CTA kernels
+def test_fused_requant_modes(out_bits, M):
+    """Every requantisation regime of the fused epilogue: comparison table (b <= 2),
+    the 32-bit in-range division (b >= 3, Q*S < 2^32) and the exact 64-bit path
+    (Q*S >= 2^32), with alpha = 0 / negative columns and extreme beta."""
+    N, K = 200, 384
+    A, W = synth.gemm_inputs(M, N, K, 4, 4, tag="rqm")
+    Y = oracle.gemm(A, W, 4, 4, 0)
+    g = synth.rng(f"rqm:{out_bits}:{M}")
+    alpha = g.integers(-40, 41, size=N).astype(np.int32)
+    alpha[::7] = 0
+    beta = g.integers(-2**31, 2**31, size=N, dtype=np.int64).astype(np.int32)
+    beta[1::3] = g.integers(-20000, 20000, size=len(beta[1::3])).astype(np.int32)
+    lim = (2**32 - 1) // ((1 << out_bits) - 1)  # largest S of the 32-bit in-range division
+    for S in sorted({min(x, 2**31 - 1) for x in (1, 37, 9973, lim, lim + 1, 2**31 - 1)}):
+        want = oracle.pack(oracle.epilogue(Y, alpha, beta, S, out_bits), out_bits)
+        epi = ap.Epilogue(out_bits, cuda(alpha), cuda(beta), S)
+        got = u32(run_gemm(A, W, 4, 4, 0, ap.VARIANT_TC_I8, epi=epi))
+        np.testing.assert_array_equal(got, want, err_msg=f"S={S}")
+
+
 def test_epilogue_identity_and_defaults():
     M, N, K = 65, 40, 200
     A, W = synth.gemm_inputs(M, N, K, 2, 2, tag="epidef")
@@ -196,15 +218,16 @@ def test_conv2d(shape, a_bits, w_bits, enc):
         got = ap.conv2d(Xp, Wp, cs, a_bits, w_bits, enc, variant=v)
         torch.cuda.synchronize()
         np.testing.assert_array_equal(got.cpu().numpy(), want, err_msg=f"variant {ap.variant_name(v)}")
-    # fused requant + pack on the conv path
-    alpha, beta, Sd = epi_case(Co, 2, "convepi")
-    wantp = oracle.pack(oracle.epilogue(want.reshape(-1, Co), alpha, beta, Sd, 2), 2)
-    for v in VARIANTS:
-        if not supported(v, B * cs.Ho * cs.Wo, Co, R * S * C, a_bits, w_bits, enc, conv=True):
-            continue
-        got = ap.conv2d(Xp, Wp, cs, a_bits, w_bits, enc, epi=ap.Epilogue(2, cuda(alpha), cuda(beta), Sd),
-                        variant=v)
-        np.testing.assert_array_equal(u32(got), wantp, err_msg=f"fused variant {ap.variant_name(v)}")
+    # fused requant + pack on the conv path (2-bit and 5-bit outputs)
+    for ob in (2, 5):
+        alpha, beta, Sd = epi_case(Co, ob, "convepi")
+        wantp = oracle.pack(oracle.epilogue(want.reshape(-1, Co), alpha, beta, Sd, ob), ob)
+        for v in VARIANTS:
+            if not supported(v, B * cs.Ho * cs.Wo, Co, R * S * C, a_bits, w_bits, enc, conv=True):
+                continue
+            got = ap.conv2d(Xp, Wp, cs, a_bits, w_bits, enc, epi=ap.Epilogue(ob, cuda(alpha), cuda(beta), Sd),
+                            variant=v)
+            np.testing.assert_array_equal(u32(got), wantp, err_msg=f"fused {ob}-bit variant {ap.variant_name(v)}")
 
 
 def test_conv_pm1_padding_closed_form_gpu():
