@@ -72,6 +72,9 @@ def _load():
             lib.oracle_conv2d.restype = ci
             lib.oracle_epilogue.argtypes = [i32p, ci, ci, i32p, i32p, ctypes.c_int32, ci, u8p]
             lib.oracle_epilogue.restype = ci
+            lib.oracle_pool_epilogue.argtypes = [i32p, ci, ci, ci, ci, i32p, i32p, ctypes.c_int32, ci, ci, ci,
+                                                 ci, u8p]
+            lib.oracle_pool_epilogue.restype = ci
             lib.oracle_pack.argtypes = [u8p, ci, ci, ci, u32p]
             lib.oracle_pack.restype = ci
             lib.oracle_packed_words.argtypes = [ci, ci, ci]
@@ -145,6 +148,24 @@ def epilogue(Y, alpha, beta, S, out_bits):
                                    None if ap is None else _p(ap, ctypes.c_int32),
                                    None if bp is None else _p(bp, ctypes.c_int32),
                                    int(S), out_bits, _p(q, ctypes.c_uint8)))
+    return q
+
+
+def pool_epilogue(Y, alpha, beta, S, out_bits, k, stride=None, avg=False):
+    """BN affine -> k x k max (or average) pooling -> quantisation over NHWC int32 Y
+    [B,H,W,N]; returns codes [B,Hp,Wp,N] (oracle_pool_epilogue, reading R15)."""
+    Y = np.ascontiguousarray(Y, dtype=np.int32)
+    B, H, Wd, N = Y.shape
+    stride = k if stride is None else stride
+    Hp, Wp = (H - k) // stride + 1, (Wd - k) // stride + 1
+    q = np.zeros((B, max(Hp, 0), max(Wp, 0), N), dtype=np.uint8)
+    ap = None if alpha is None else np.ascontiguousarray(alpha, dtype=np.int32)
+    bp = None if beta is None else np.ascontiguousarray(beta, dtype=np.int32)
+    _check(_load().oracle_pool_epilogue(_p(Y, ctypes.c_int32), B, H, Wd, N,
+                                        None if ap is None else _p(ap, ctypes.c_int32),
+                                        None if bp is None else _p(bp, ctypes.c_int32),
+                                        int(S), out_bits, k, stride, 1 if avg else 0,
+                                        _p(q, ctypes.c_uint8)))
     return q
 
 

@@ -37,6 +37,9 @@
  *                           (APConv PAPER.md:1612-1613, input-aware padding 1652-1662)
  *   oracle_epilogue       fused requantisation  q = clamp(floor((alpha*y + beta)/S), 0, 2^b-1)
  *                           (quantisation PAPER.md:1283-1287, fused formula 1303-1306)
+ *   oracle_pool_epilogue  BN affine -> k x k pooling (max or average) -> quantisation
+ *                           (pooling PAPER.md:1293, fused conv+pool+quant 641-647,
+ *                            layer order of the fused formula 1299-1306; reading R15)
  *   oracle_pack           byte-exact packed bit-plane format [rows][bits][Kp/32]
  *                           (decomposition PAPER.md:1419-1421, packing 1255-1256)
  *
@@ -309,6 +312,48 @@ int oracle_epilogue(const int32_t *Y, int M, int N, const int32_t *alpha, const 
             q[(size_t)m * N + n] = (uint8_t)f;
         }
     }
+    return OR_OK;
+}
+
+/* Pooling between the BN affine and the quantisation (reading R15; pooling
+ * PAPER.md:1293 "splits the feature map spatially into k x k grids and generates
+ * 1 scalar output for each grid by computing the average or the maximum value";
+ * fused conv + pooling + quantisation PAPER.md:641-647):
+ *   v[b][h][w][n] = alpha[n] * Y[b][h][w][n] + beta[n]                 (int64)
+ *   P[b][i][j][n] = max over the k x k grid at (i*st, j*st) of v        (avg = 0), or
+ *                 = floor( sum over the grid of v / k^2 )               (avg = 1)
+ *   q = clamp(floor(P / S), 0, 2^out_bits - 1)
+ * Y is NHWC int32 [B][H][W][N]; q is [B][Hp][Wp][N] codes, Hp = (H - k)/st + 1
+ * (grids that do not fit are dropped, "floor" pooling). */
+int oracle_pool_epilogue(const int32_t *Y, int B, int H, int Wd, int N, const int32_t *alpha,
+                         const int32_t *beta, int32_t S, int out_bits, int k, int stride, int avg,
+                         uint8_t *q)
+{
+    if (out_bits < 1 || out_bits > 8) return OR_ERR_BITS;
+    if (S <= 0 || B < 0 || H < 1 || Wd < 1 || N < 0 || k < 1 || stride < 1 || k > H || k > Wd)
+        return OR_ERR_SHAPE;
+    int Hp = (H - k) / stride + 1, Wp = (Wd - k) / stride + 1;
+    int64_t qmax = ((int64_t)1 << out_bits) - 1;
+    for (int b = 0; b < B; b++)
+        for (int i = 0; i < Hp; i++)
+            for (int j = 0; j < Wp; j++)
+                for (int n = 0; n < N; n++) {
+                    int64_t a = alpha ? alpha[n] : 1;
+                    int64_t c = beta ? beta[n] : 0;
+                    int64_t best = 0, sum = 0;
+                    for (int r = 0; r < k; r++)
+                        for (int s = 0; s < k; s++) {
+                            int h = i * stride + r, w = j * stride + s;
+                            int64_t v = a * (int64_t)Y[(((size_t)b * H + h) * Wd + w) * N + n] + c;
+                            if ((r == 0 && s == 0) || v > best) best = v;
+                            sum += v;
+                        }
+                    int64_t P = avg ? floor_div(sum, (int64_t)k * k) : best;
+                    int64_t f = floor_div(P, S);
+                    if (f < 0) f = 0;
+                    if (f > qmax) f = qmax;
+                    q[(((size_t)b * Hp + i) * Wp + j) * N + n] = (uint8_t)f;
+                }
     return OR_OK;
 }
 

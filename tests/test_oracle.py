@@ -193,6 +193,57 @@ def test_epilogue_vs_python_floor_division():
     assert q[0, 0] == 0
 
 
+# ---------------------------------------------------------------- pooling
+
+def _pool_case(tag, B=2, H=7, W=9, N=11):
+    g = synth.rng(f"poolpin:{tag}")
+    Y = g.integers(-5000, 5000, size=(B, H, W, N)).astype(np.int32)
+    alpha = g.integers(-4, 5, size=N).astype(np.int32)
+    alpha[0] = 0
+    beta = g.integers(-3000, 3000, size=N).astype(np.int32)
+    return Y, alpha, beta
+
+
+@pytest.mark.parametrize("k,st", [(2, 2), (3, 2), (2, 1), (3, 3)])
+@pytest.mark.parametrize("avg", [False, True])
+def test_pool_epilogue_vs_torch_pooling(k, st, avg):
+    """Pooling on v = alpha*y + beta (reading R15) against torch's max_pool2d /
+    avg_pool2d in float64 (exact: |v| < 2^53), then the integer floor + clamp."""
+    import torch
+    Y, alpha, beta = _pool_case(f"{k}{st}{avg}")
+    S, b = 97, 3
+    q = oracle.pool_epilogue(Y, alpha, beta, S, b, k, st, avg=avg)
+    v = torch.from_numpy(Y.astype(np.float64) * alpha + beta).permute(0, 3, 1, 2)
+    if avg:
+        P = torch.floor(torch.nn.functional.avg_pool2d(v, k, st, divisor_override=1) / (k * k))
+    else:
+        P = torch.nn.functional.max_pool2d(v, k, st)
+    want = torch.clamp(torch.floor(P / S), 0, (1 << b) - 1).permute(0, 2, 3, 1).numpy().astype(np.uint8)
+    np.testing.assert_array_equal(q, want)
+
+
+def test_pool_max_commutes_with_requant():
+    """q is non-decreasing in v, so max-pooling v then quantising equals max-pooling
+    the quantised codes (any alpha sign): an identity the fused kernel relies on."""
+    Y, alpha, beta = _pool_case("commute", B=3, H=8, W=6, N=13)
+    for S in (1, 50, 2**20):
+        for b in (1, 2, 8):
+            q = oracle.pool_epilogue(Y, alpha, beta, S, b, 2, 2)
+            u = oracle.epilogue(Y.reshape(-1, 13), alpha, beta, S, b).reshape(Y.shape)
+            m = np.maximum(np.maximum(u[:, 0::2, 0::2], u[:, 0::2, 1::2]), np.maximum(u[:, 1::2, 0::2], u[:, 1::2, 1::2]))
+            np.testing.assert_array_equal(q, m)
+
+
+def test_pool_identity_window_and_hand_example():
+    Y, alpha, beta = _pool_case("id")
+    q1 = oracle.pool_epilogue(Y, alpha, beta, 7, 5, 1, 1)
+    np.testing.assert_array_equal(q1.reshape(-1, 11), oracle.epilogue(Y.reshape(-1, 11), alpha, beta, 7, 5))
+    # 2x2 grid of y = [[1, -6], [3, 2]], alpha = -1, beta = 4: v = [[3, 10], [1, 2]]
+    y = np.array([[[[1], [-6]], [[3], [2]]]], dtype=np.int32)
+    assert oracle.pool_epilogue(y, [-1], [4], 3, 8, 2)[0, 0, 0, 0] == 3            # max v = 10 -> 10 // 3
+    assert oracle.pool_epilogue(y, [-1], [4], 3, 8, 2, avg=True)[0, 0, 0, 0] == 1  # floor(16/4)=4 -> 4 // 3
+
+
 # --------------------------------------------------------------- packing
 
 @pytest.mark.parametrize("rows,K,bits", [(3, 1, 1), (4, 127, 2), (2, 128, 8), (5, 129, 3), (1, 300, 4)])
