@@ -93,6 +93,9 @@ typedef enum {
 /* Element-wise routine fused after the contraction:
  *   v = alpha[n] * y + beta[n]                  (int64; BN / zero point folded
  *                                                on the host into integers)
+ *   [conv only, pool > 0: k x k pooling of v over the output feature map,
+ *    stride pool_stride (0 = k), maximum or floor of the average; grids that do
+ *    not fit are dropped: Hp = (Ho - k)/stride + 1]
  *   q = clamp(floor(v / divisor), 0, 2^out_bits - 1)   (floor toward -inf;
  *                                                the lower clamp is the ReLU)
  * and q is bit-decomposed and packed along N into the packed format with
@@ -102,7 +105,10 @@ typedef struct {
     const int32_t *alpha;  /* device [N] or NULL (= 1) */
     const int32_t *beta;   /* device [N] or NULL (= 0) */
     int32_t divisor;       /* S > 0 */
-    int32_t pool;          /* must be 0 (2x2 pooling is a later row) */
+    int32_t pool;          /* 0: none; k >= 1: k x k pooling window (apnn_conv2d and
+                              apnn_pool_quant_pack_out only; APNN_ERR_INVALID_ARG elsewhere) */
+    int32_t pool_stride;   /* 0: = pool */
+    int32_t pool_avg;      /* 0: max pooling, 1: average (floor of the sum / k^2) */
 } apnn_epilogue;
 
 /* NHWC convolution geometry.  Ho = (H + 2 pad - R)/stride + 1, Wo likewise. */
@@ -157,6 +163,11 @@ apnn_status apnn_gemm_ex(const uint32_t *A, const uint32_t *W, int M, int N, int
 apnn_status apnn_conv2d(const uint32_t *X, const uint32_t *W, const apnn_conv_shape *shape,
                         int a_bits, int w_bits, apnn_encoding enc, const apnn_epilogue *epi,
                         void *Y, apnn_stream_t stream);
+/*   Pooling (epi->pool > 0) is fused into the tensor-core epilogue for 2 x 2 /
+ *   stride 2 max pooling when Ho is even, 2 <= Wo <= 64 and B*Ho*Wo > 128; the
+ *   output is then packed [B*Hp*Wp][out_bits][roundup(C_out,128)/32].  Any other
+ *   pooling returns APNN_ERR_UNSUPPORTED without launching: run the conv with
+ *   int32 output and apnn_pool_quant_pack_out (the unfused pair). */
 
 apnn_status apnn_conv2d_ex(const uint32_t *X, const uint32_t *W, const apnn_conv_shape *shape,
                            int a_bits, int w_bits, apnn_encoding enc, const apnn_epilogue *epi,
@@ -167,6 +178,14 @@ apnn_status apnn_conv2d_ex(const uint32_t *X, const uint32_t *W, const apnn_conv
  *   Y: device int32 [M][N]; out: device packed [M][out_bits][roundup(N,128)/32]. */
 apnn_status apnn_quant_pack_out(const int32_t *Y, int M, int N, const apnn_epilogue *epi,
                                 uint32_t *out, apnn_stream_t stream);
+
+/* Stand-alone pooling + element-wise routine over an NHWC int32 conv output
+ * (the unfused counterpart of the fused conv epilogue):
+ *   Y:   device int32 [B][H][W][N]  (H, W = the conv output size Ho, Wo)
+ *   epi: host; pool >= 1 required (see apnn_epilogue)
+ *   out: device packed [B*Hp*Wp][out_bits][roundup(N,128)/32] */
+apnn_status apnn_pool_quant_pack_out(const int32_t *Y, int B, int H, int W, int N,
+                                     const apnn_epilogue *epi, uint32_t *out, apnn_stream_t stream);
 
 /* Which variant APNN_VARIANT_AUTO resolves to for this problem (no launch). */
 apnn_variant apnn_select_variant(int M, int N, int K, int a_bits, int w_bits, apnn_encoding enc);

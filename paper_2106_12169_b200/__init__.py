@@ -46,7 +46,8 @@ class ApnnError(RuntimeError):
 
 class _Epi(ctypes.Structure):
     _fields_ = [("out_bits", ctypes.c_int32), ("alpha", ctypes.c_void_p), ("beta", ctypes.c_void_p),
-                ("divisor", ctypes.c_int32), ("pool", ctypes.c_int32)]
+                ("divisor", ctypes.c_int32), ("pool", ctypes.c_int32), ("pool_stride", ctypes.c_int32),
+                ("pool_avg", ctypes.c_int32)]
 
 
 class _Conv(ctypes.Structure):
@@ -83,6 +84,8 @@ def lib() -> ctypes.CDLL:
             L.apnn_conv2d_ex.restype = st
             L.apnn_quant_pack_out.argtypes = [vp, ci, ci, ctypes.POINTER(_Epi), vp, vp]
             L.apnn_quant_pack_out.restype = st
+            L.apnn_pool_quant_pack_out.argtypes = [vp, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp, vp]
+            L.apnn_pool_quant_pack_out.restype = st
             L.apnn_select_variant.argtypes = [ci, ci, ci, ci, ci, ci]
             L.apnn_select_variant.restype = ci
             L.apnn_status_string.argtypes = [ci]
@@ -98,7 +101,8 @@ def lib() -> ctypes.CDLL:
 
 
 ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
-               "apnn_conv2d", "apnn_conv2d_ex", "apnn_quant_pack_out", "apnn_select_variant",
+               "apnn_conv2d", "apnn_conv2d_ex", "apnn_quant_pack_out", "apnn_pool_quant_pack_out",
+               "apnn_select_variant",
                "apnn_status_string", "apnn_variant_name", "apnn_launch_count", "apnn_version")
 
 
@@ -148,11 +152,19 @@ def packed_shape(rows: int, K: int, bits: int):
 
 @dataclass
 class Epilogue:
-    """Fused element-wise routine: q = clamp(floor((alpha*y+beta)/divisor), 0, 2^out_bits-1)."""
+    """Fused element-wise routine: q = clamp(floor((alpha*y+beta)/divisor), 0, 2^out_bits-1),
+    optionally after k x k pooling of alpha*y+beta (conv only: pool = k, max or average)."""
     out_bits: int
     alpha: Optional[torch.Tensor] = None  # int32 [N] on the device, or None (= 1)
     beta: Optional[torch.Tensor] = None   # int32 [N] on the device, or None (= 0)
     divisor: int = 1
+    pool: int = 0
+    pool_stride: int = 0                  # 0 -> = pool
+    pool_avg: bool = False
+
+    def pooled(self, Ho: int, Wo: int):
+        st = self.pool_stride or self.pool
+        return ((Ho - self.pool) // st + 1, (Wo - self.pool) // st + 1) if self.pool else (Ho, Wo)
 
     def _c(self):
         for name in ("alpha", "beta"):
@@ -160,7 +172,8 @@ class Epilogue:
             if t is not None:
                 _cuda(t, name, torch.int32)
         return _Epi(self.out_bits, None if self.alpha is None else self.alpha.data_ptr(),
-                    None if self.beta is None else self.beta.data_ptr(), self.divisor, 0)
+                    None if self.beta is None else self.beta.data_ptr(), self.divisor, self.pool,
+                    self.pool_stride, 1 if self.pool_avg else 0)
 
 
 @dataclass
@@ -217,20 +230,27 @@ def gemm(A: torch.Tensor, W: torch.Tensor, M: int, N: int, K: int, a_bits: int, 
 def conv2d(X: torch.Tensor, W: torch.Tensor, shape: ConvShape, a_bits: int, w_bits: int, enc: int,
            epi: Optional[Epilogue] = None, variant: int = VARIANT_AUTO,
            out: Optional[torch.Tensor] = None) -> torch.Tensor:
-    """APConv (implicit GEMM): int32 NHWC [B, Ho, Wo, C_out] or packed [B*Ho*Wo, out_bits, Kw(C_out)]."""
+    """APConv (implicit GEMM): int32 NHWC [B, Ho, Wo, C_out] or packed [B*Hp*Wp, out_bits, Kw(C_out)]
+    (Hp, Wp = Ho, Wo without pooling).  Pooling the library cannot fuse (apnn_conv2d returns
+    APNN_ERR_UNSUPPORTED) runs as the unfused GPU pair: int32 conv + apnn_pool_quant_pack_out."""
     _cuda(X, "X", torch.int32)
     _cuda(W, "W", torch.int32)
     if out is None:
         if epi is None:
             oshape = (shape.B, shape.Ho, shape.Wo, shape.C_out)
         else:
-            oshape = packed_shape(shape.B * shape.Ho * shape.Wo, shape.C_out, epi.out_bits)
+            Hp, Wp = epi.pooled(shape.Ho, shape.Wo)
+            oshape = packed_shape(shape.B * Hp * Wp, shape.C_out, epi.out_bits)
         out = torch.empty(oshape, dtype=torch.int32, device=X.device)
     _cuda(out, "out", torch.int32)
     ce = None if epi is None else ctypes.byref(epi._c())
     cs = shape._c()
-    _check(lib().apnn_conv2d_ex(_ptr(X), _ptr(W), ctypes.byref(cs), a_bits, w_bits, enc, ce, _ptr(out),
-                                variant, _stream(X)), "apnn_conv2d_ex")
+    st = lib().apnn_conv2d_ex(_ptr(X), _ptr(W), ctypes.byref(cs), a_bits, w_bits, enc, ce, _ptr(out),
+                              variant, _stream(X))
+    if st == 7 and epi is not None and epi.pool:  # APNN_ERR_UNSUPPORTED: unfused pooling pair
+        Y = conv2d(X, W, shape, a_bits, w_bits, enc, None, variant)
+        return pool_quant_pack_out(Y, epi, out=out)
+    _check(st, "apnn_conv2d_ex")
     return out
 
 
@@ -243,6 +263,20 @@ def quant_pack_out(Y: torch.Tensor, epi: Epilogue, out: Optional[torch.Tensor] =
     _cuda(out, "out", torch.int32)
     _check(lib().apnn_quant_pack_out(_ptr(Y), M, N, ctypes.byref(epi._c()), _ptr(out), _stream(Y)),
            "apnn_quant_pack_out")
+    return out
+
+
+def pool_quant_pack_out(Y: torch.Tensor, epi: Epilogue, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Stand-alone pooling + requantise + pack of an NHWC int32 conv output [B, H, W, N]
+    (apnn_pool_quant_pack_out) -> packed [B*Hp*Wp, out_bits, Kw(N)]."""
+    _cuda(Y, "Y", torch.int32)
+    B, H, Wd, N = Y.shape
+    Hp, Wp = epi.pooled(H, Wd)
+    if out is None:
+        out = torch.empty(packed_shape(B * Hp * Wp, N, epi.out_bits), dtype=torch.int32, device=Y.device)
+    _cuda(out, "out", torch.int32)
+    _check(lib().apnn_pool_quant_pack_out(_ptr(Y), B, H, Wd, N, ctypes.byref(epi._c()), _ptr(out), _stream(Y)),
+           "apnn_pool_quant_pack_out")
     return out
 
 

@@ -18,6 +18,9 @@ cudaError_t launch_pack_bits(const uint8_t* codes, int rows, int K, int bits, ui
                              cudaStream_t s);
 cudaError_t launch_quant_pack(const int32_t* Y, int M, int N, const Epi& e, uint32_t* out, int sms,
                               cudaStream_t s);
+cudaError_t launch_pool_quant_pack(const int32_t* Y, int B, int H, int W, int N, const Epi& e, uint32_t* out,
+                                  int sms, cudaStream_t s);
+bool tc_i8_pool_fusable(const Geom& g, const Epi& e);
 cudaError_t launch_popc(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
                         cudaStream_t s);
 cudaError_t launch_b1mma(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
@@ -83,7 +86,8 @@ static apnn_status make_epi(const apnn_epilogue* epi, Epi* e) {
     std::memset(e, 0, sizeof(*e));
     if (!epi) return APNN_OK;
     if (epi->out_bits < 1 || epi->out_bits > 8) return APNN_ERR_BITS;
-    if (epi->divisor <= 0 || epi->pool != 0) return APNN_ERR_INVALID_ARG;
+    if (epi->divisor <= 0 || epi->pool < 0 || epi->pool_stride < 0 || (epi->pool_avg != 0 && epi->pool_avg != 1))
+        return APNN_ERR_INVALID_ARG;
     if ((epi->alpha && !aligned16(epi->alpha)) || (epi->beta && !aligned16(epi->beta)))
         return APNN_ERR_ALIGNMENT;
     e->alpha = epi->alpha;
@@ -92,6 +96,9 @@ static apnn_status make_epi(const apnn_epilogue* epi, Epi* e) {
     e->out_bits = epi->out_bits;
     e->qmax = (1 << epi->out_bits) - 1;
     e->invS = 1.0f / (float)epi->divisor;
+    e->pool = epi->pool;
+    e->pool_stride = epi->pool ? (epi->pool_stride ? epi->pool_stride : epi->pool) : 0;
+    e->pool_avg = epi->pool_avg;
     return APNN_OK;
 }
 
@@ -171,6 +178,7 @@ apnn_status apnn_gemm_ex(const uint32_t* A, const uint32_t* W, int M, int N, int
     if ((st = check_overflow(K, a_bits, w_bits, enc)) != APNN_OK) return st;
     Epi e;
     if ((st = make_epi(epi, &e)) != APNN_OK) return st;
+    if (e.pool) return APNN_ERR_INVALID_ARG;  // pooling is a conv epilogue
     if ((unsigned)variant > (unsigned)APNN_VARIANT_B1MMA) return APNN_ERR_INVALID_ARG;
     Geom g;
     gemm_geom(&g, M, N, K, a_bits, w_bits, enc);
@@ -222,6 +230,10 @@ apnn_status apnn_conv2d_ex(const uint32_t* X, const uint32_t* W, const apnn_conv
     g.nchunks = g.RS * g.CB;
     g.conv = 1;
     g.H = c.H; g.W = c.W; g.Ho = Ho; g.Wo = Wo; g.S = c.S; g.stride = c.stride; g.pad = c.pad;
+    if (e.pool) {
+        if (e.pool > Ho || e.pool > Wo) return APNN_ERR_SHAPE;
+        if (resolve(variant, g) != APNN_VARIANT_TC_I8 || !tc_i8_pool_fusable(g, e)) return APNN_ERR_UNSUPPORTED;
+    }
     return run(X, W, g, e, Y, variant, (cudaStream_t)stream);
 }
 
@@ -240,9 +252,29 @@ apnn_status apnn_quant_pack_out(const int32_t* Y, int M, int N, const apnn_epilo
     Epi e;
     apnn_status st = make_epi(epi, &e);
     if (st != APNN_OK) return st;
+    if (e.pool) return APNN_ERR_INVALID_ARG;  // pooled: apnn_pool_quant_pack_out
     DevInfo d;
     if ((st = device_info(&d)) != APNN_OK) return st;
     cudaError_t err = launch_quant_pack(Y, M, N, e, out, d.sms, (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_status apnn_pool_quant_pack_out(const int32_t* Y, int B, int H, int W, int N, const apnn_epilogue* epi,
+                                     uint32_t* out, apnn_stream_t stream) {
+    if (B < 0 || H < 1 || W < 1 || N < 0) return APNN_ERR_SHAPE;
+    if (!epi) return APNN_ERR_INVALID_ARG;
+    Epi e;
+    apnn_status st = make_epi(epi, &e);
+    if (st != APNN_OK) return st;
+    if (e.pool < 1) return APNN_ERR_INVALID_ARG;
+    if (e.pool > H || e.pool > W) return APNN_ERR_SHAPE;
+    const int Hp = (H - e.pool) / e.pool_stride + 1, Wp = (W - e.pool) / e.pool_stride + 1;
+    if ((long long)B * Hp * Wp > 2147483647LL) return APNN_ERR_SHAPE;
+    if ((B > 0 && N > 0 && !Y) || (B > 0 && !out)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(Y) || !aligned16(out)) return APNN_ERR_ALIGNMENT;
+    DevInfo d;
+    if ((st = device_info(&d)) != APNN_OK) return st;
+    cudaError_t err = launch_pool_quant_pack(Y, B, H, W, N, e, out, d.sms, (cudaStream_t)stream);
     return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }
 
@@ -279,6 +311,6 @@ const char* apnn_variant_name(apnn_variant v) {
 
 uint64_t apnn_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
-int apnn_version(void) { return 100; }
+int apnn_version(void) { return 200; }
 
 }  // extern "C"

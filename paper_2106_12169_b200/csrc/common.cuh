@@ -100,7 +100,22 @@ struct Epi {
     int32_t out_bits;      // 0 -> raw int32 output
     int32_t qmax;
     float invS;            // 1/S (rounded), used for a first guess only
+    int32_t pool;          // conv pooling window k (0 = none)
+    int32_t pool_stride;
+    int32_t pool_avg;      // 0 max, 1 average
 };
+
+// q = clamp(floor(v / S), 0, qmax) for an int64 v (the quantisation step alone)
+__device__ __forceinline__ uint32_t quantise_v(const Epi& e, long long v) {
+    if (v < 0) return 0;
+    long long lim = (long long)(e.qmax + 1) * e.S;
+    if (v >= lim) return (uint32_t)e.qmax;
+    int q = __float2int_rz((float)v * e.invS);
+    long long r = v - (long long)q * e.S;
+    while (r < 0) { q -= 1; r += e.S; }
+    while (r >= e.S) { q += 1; r -= e.S; }
+    return (uint32_t)q;
+}
 
 __device__ __forceinline__ uint32_t requant(const Epi& e, int32_t y, int32_t alpha, int32_t beta) {
     long long v = (long long)alpha * y + beta;

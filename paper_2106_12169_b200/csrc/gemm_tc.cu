@@ -64,6 +64,8 @@ struct Params {
     int tab_mode;       // fused epilogue: kTabNone / kTabQ3 / kTabHybrid (tc_common.cuh)
     int out_mode;       // epilogue stores: kOutDirect / kOutTma (tensor map tmapY) / kOutLsu (coalesced)
     int nwb;            // packed TMA store box width in words (2-CTA kernel)
+    int pool_fused;     // conv: 2x2/2 max pooling fused into the epilogue (pooled output Hp x Wp)
+    int Hp, Wp;
     int acc_shift;      // scaled operands: accumulator = Y << acc_shift (2-CTA kernel)
     // conv A-row tiling of the 2-CTA kernel (TMA row boxes):
     //   conv_k > 0: a CTA tile is conv_k whole output rows (conv_k * Wo <= 128 pixels)
@@ -113,6 +115,63 @@ __device__ __forceinline__ void cta_tile_rows(const Params& p, int ct, int& m_ba
     }
     if (m_base + len > g.M) len = g.M - m_base;
     if (len < 0) len = 0;
+}
+
+// ------------------------------------------------- fused 2x2/2 max pooling
+// (fused conv + pool + quantisation 641-647).  q is non-decreasing in
+// v = alpha*y + beta, so the max over a grid of q equals q of the max v (reading R15):
+// every row (output pixel) requantises its own 32 channels, the four codes of a 2x2
+// grid are combined with a byte-wise max through shared memory, and the grid's
+// top-left pixel ("anchor") packs and stores the pooled codes.  The CTA tile holds
+// conv_k (even) whole output rows and Ho is even, so every grid lies in one tile.
+__device__ __forceinline__ bool pool_anchor(int t, int len, int mb, const Geom& g, const Params& p, long long& prow) {
+    if (t >= len) return false;
+    const int i = t / g.Wo, wo = t - i * g.Wo;
+    if ((i & 1) || (wo & 1) || wo + 1 >= g.Wo) return false;
+    const int gr = mb / g.Wo + i;          // global output row b*Ho + ho (ho even)
+    const int b = gr / g.Ho, ho = gr - b * g.Ho;
+    prow = ((long long)b * p.Hp + (ho >> 1)) * p.Wp + (wo >> 1);
+    return true;
+}
+
+__device__ __forceinline__ void pool_chunk(const uint32_t (&acc)[32], int nb, int lc, int t, int len, int mb,
+                                           const Geom& g, const Params& p, const int32_t* tab, uint8_t* buf) {
+    uint32_t qb[8];
+    requant_chunk_bytes(acc, nb, lc, g, p.e, tab, p.tab_mode, qb);
+    uint4* row = reinterpret_cast<uint4*>(buf + t * 32);
+    row[0] = make_uint4(qb[0], qb[1], qb[2], qb[3]);
+    row[1] = make_uint4(qb[4], qb[5], qb[6], qb[7]);
+    sm100::named_bar_sync(2, 128);
+    long long prow;
+    if (!pool_anchor(t, len, mb, g, p, prow)) return;
+    const int nbrs[3] = {t + 1, t + g.Wo, t + g.Wo + 1};
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        const uint4* r = reinterpret_cast<const uint4*>(buf + nbrs[k] * 32);
+        const uint4 a = r[0], b = r[1];
+        qb[0] = __vmaxu4(qb[0], a.x); qb[1] = __vmaxu4(qb[1], a.y);
+        qb[2] = __vmaxu4(qb[2], a.z); qb[3] = __vmaxu4(qb[3], a.w);
+        qb[4] = __vmaxu4(qb[4], b.x); qb[5] = __vmaxu4(qb[5], b.y);
+        qb[6] = __vmaxu4(qb[6], b.z); qb[7] = __vmaxu4(qb[7], b.w);
+    }
+    uint32_t w[8];
+    bytes_to_words(qb, p.e.out_bits, w);
+    const int Nw = (g.N + 127) / 128 * 4;
+    uint32_t* o = reinterpret_cast<uint32_t*>(p.Y) + prow * p.e.out_bits * Nw + nb / 32;
+#pragma unroll
+    for (int tb = 0; tb < 8; tb++)
+        if (tb < p.e.out_bits) o[(long long)tb * Nw] = w[tb];
+}
+
+// zero the N padding words [w_from, Nw) of the pooled rows anchored in this tile
+__device__ __forceinline__ void pool_pad_words(int n_end, int t, int len, int mb, const Geom& g, const Params& p) {
+    const int Nw = (g.N + 127) / 128 * 4;
+    if (n_end < g.N) return;
+    long long prow;
+    if (!pool_anchor(t, len, mb, g, p, prow)) return;
+    uint32_t* o = reinterpret_cast<uint32_t*>(p.Y) + prow * p.e.out_bits * Nw;
+    for (int tb = 0; tb < p.e.out_bits; tb++)
+        for (int w = n_end / 32; w < Nw; w++) o[(long long)tb * Nw + w] = 0u;
 }
 
 // ============================================================== 2-CTA kernel
@@ -334,7 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
         uint8_t* stg = sStg + q * kStgWarpBytes;
         const uint32_t stg_addr = smem_u32(stg);
         int tc = 0;
-        uint32_t nst = 0;
+        uint32_t nst = 0, npc = 0;
         for (int tile = cid; tile < p.num_tiles; tile += ncl, tc++) {
             int mb, len;
             cta_tile_rows(p, (tile % p.tiles_m) * 2 + rank, mb, len);
@@ -365,6 +424,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 if (SCALED) {
 #pragma unroll
                     for (int i = 0; i < 32; i++) acc[i] = (uint32_t)((int32_t)acc[i] >> p.acc_shift);
+                }
+                if (p.pool_fused) {  // uniform across the 4 epilogue warps (named barrier inside)
+                    pool_chunk(acc, n0 + c, c, t, len, mb, g, p, sTab, sStg + (npc & 1) * 4096);
+                    __syncwarp();  // reconverge before the next .sync.aligned TMEM load
+                    npc++;
+                    continue;
                 }
                 if (!any || p.exp_nostore) continue;
                 if (ob == 0) {
@@ -399,7 +464,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(accum_empty0);
-            if (ob && any && !p.exp_nostore) {
+            if (p.pool_fused) {
+                pool_pad_words(n0 + T2_BN, t, len, mb, g, p);
+            } else if (ob && any && !p.exp_nostore) {
                 if (use_tma || use_lsu) {
                     const uint32_t zero8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                     for (int wi = T2_BN / 32; wi < p.nwb; wi++)  // box words past the tile: N padding
@@ -749,6 +816,14 @@ static cudaError_t launch1_bn(int BN, const CUtensorMap& ta, const CUtensorMap& 
 
 }  // namespace tc
 
+static int tc_kernel_override();
+
+// 2x2/2 max pooling fused into the 2-CTA kernel's epilogue (see pool_chunk)
+bool tc_i8_pool_fusable(const Geom& g, const Epi& e) {
+    return g.conv && e.pool == 2 && e.pool_stride == 2 && !e.pool_avg && e.out_bits > 0 && g.Ho % 2 == 0 &&
+           g.Wo >= 2 && g.Wo <= 64 && g.M > 128 && tc_kernel_override() != 1;
+}
+
 bool tc_i8_supports(const Geom& g) {
     // GEMM and implicit-GEMM conv; K = 0 has no MMA to issue (handled by the popc variant)
     return g.K > 0 && g.M > 0 && g.N > 0;
@@ -806,6 +881,9 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     }
     p.out_mode = kOutDirect;
     p.nwb = 0;
+    p.pool_fused = e.pool ? 1 : 0;  // the ABI only forwards fusable pooling (tc_i8_pool_fusable)
+    p.Hp = g.Ho / 2;
+    p.Wp = g.Wo / 2;
     const int want_mode = epi_store_mode(e.out_bits > 0);
     p.acc_shift = 0;
     p.trace = nullptr;
@@ -826,7 +904,9 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         p.b_bytes = 16u * brows * g.w_bits;
         p.conv_box_stride = 0;
         if (g.conv) {
-            const int bw = g.Wo <= 128 ? g.Wo : 128, nbox = g.Wo <= 128 ? 128 / g.Wo : 1;
+            // row boxes per stage = output rows per CTA tile (conv_k below; even when pooling)
+            const int bw = g.Wo <= 128 ? g.Wo : 128;
+            const int nbox = g.Wo <= 128 ? (p.pool_fused ? (128 / g.Wo) & ~1 : 128 / g.Wo) : 1;
             p.conv_box_stride = (16 * bw * g.a_bits + 127) / 128 * 128;
             p.a_bytes = (uint32_t)(nbox * p.conv_box_stride);
             p.a_tx_bytes = (uint32_t)(nbox * 16 * bw * g.a_bits);
@@ -869,6 +949,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         if (g.conv) {
             if (g.Wo <= 128) {
                 p.conv_k = 128 / g.Wo;
+                if (p.pool_fused) p.conv_k &= ~1;  // whole 2x2 grids per tile
                 p.conv_bw = g.Wo;
                 p.conv_nbox = p.conv_k;
                 cta_tiles = (g.M / g.Wo + p.conv_k - 1) / p.conv_k;

@@ -109,6 +109,55 @@ __global__ void __launch_bounds__(256) quant_pack_kernel(const int32_t* __restri
     }
 }
 
+// Y [B][H][W][N] int32 (NHWC conv output) -> out [B*Hp*Wp][ob][Nw]: k x k pooling of
+// v = alpha*y + beta (max, or floor of the average), then quantisation and packing
+// (reading R15).  One thread per (pooled pixel, output word).
+__global__ void __launch_bounds__(256) pool_quant_pack_kernel(const int32_t* __restrict__ Y, int B, int H, int W,
+                                                              int N, int Hp, int Wp, int Nw, Epi e,
+                                                              uint32_t* __restrict__ out) {
+    const long long total = (long long)B * Hp * Wp * Nw;
+    const int k = e.pool, st = e.pool_stride;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long pix = idx / Nw;
+        const int w = (int)(idx - pix * Nw);
+        const int b = (int)(pix / ((long long)Hp * Wp));
+        const int rem = (int)(pix - (long long)b * Hp * Wp);
+        const int i = rem / Wp, j = rem - (rem / Wp) * Wp;
+        uint32_t qb[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) qb[q] = 0;
+        for (int c = 0; c < 32; c++) {
+            const int n = w * 32 + c;
+            if (n >= N) break;
+            const long long al = epi_alpha(e, n), be = epi_beta(e, n);
+            long long best = 0, sum = 0;
+            for (int r = 0; r < k; r++) {
+                const int32_t* row = Y + (((long long)b * H + i * st + r) * W + j * st) * N + n;
+                for (int s2 = 0; s2 < k; s2++) {
+                    const long long v = al * __ldg(row + (long long)s2 * N) + be;
+                    best = (r == 0 && s2 == 0) ? v : (v > best ? v : best);
+                    sum += v;
+                }
+            }
+            long long P = best;
+            if (e.pool_avg) {
+                const long long kk = (long long)k * k;
+                P = sum / kk;
+                if (sum % kk != 0 && sum < 0) P -= 1;  // floor toward -inf
+            }
+            qb[c >> 2] |= quantise_v(e, P) << (8 * (c & 3));
+        }
+        uint32_t* o = out + pix * e.out_bits * Nw + w;
+        for (int t = 0; t < e.out_bits; t++) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int q = 0; q < 8; q++) word |= byte_bits_to_nibble(qb[q], t) << (4 * q);
+            o[(long long)t * Nw] = word;
+        }
+    }
+}
+
 static int stream_grid(long long total, int sms) {
     long long blocks = (total + 255) / 256;
     long long cap = (long long)sms * 8;  // 8 resident 256-thread CTAs per SM, grid-stride beyond
@@ -141,4 +190,17 @@ cudaError_t launch_quant_pack(const int32_t* Y, int M, int N, const Epi& e, uint
     return cudaGetLastError();
 }
 
+}  // namespace apnn
+
+namespace apnn {
+cudaError_t launch_pool_quant_pack(const int32_t* Y, int B, int H, int W, int N, const Epi& e, uint32_t* out,
+                                  int sms, cudaStream_t s) {
+    const int Hp = (H - e.pool) / e.pool_stride + 1, Wp = (W - e.pool) / e.pool_stride + 1;
+    const int Nw = (N + 127) / 128 * 4;
+    const long long total = (long long)B * Hp * Wp * Nw;
+    if (total == 0) return cudaSuccess;
+    pool_quant_pack_kernel<<<stream_grid(total, sms), 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nw, e, out);
+    count_launch();
+    return cudaGetLastError();
+}
 }  // namespace apnn

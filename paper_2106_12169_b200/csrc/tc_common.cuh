@@ -400,6 +400,49 @@ __device__ __forceinline__ uint32_t requant_hybrid(const int32_t* row, int32_t y
     return yp > h.y ? q : 0u;
 }
 
+// 32 accumulators -> 32 codes as bytes (byte i of qb[j] = q of column nb + 4j + i)
+__device__ __forceinline__ void requant_chunk_bytes(const uint32_t (&acc)[32], int nb, int lc, const Geom& g,
+                                                    const Epi& e, const int32_t* tab, int tab_mode,
+                                                    uint32_t (&qb)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) qb[i] = 0;
+    if (tab_mode == kTabQ3) {
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            const int4 h = *reinterpret_cast<const int4*>(tab + (lc + i) * kTabStride);
+            const int32_t yp = (int32_t)acc[i] * h.x;
+            const uint32_t q = (uint32_t)(yp > h.y) + (uint32_t)(yp > h.z) + (uint32_t)(yp > h.w);
+            qb[i >> 2] |= q << (8 * (i & 3));
+        }
+    } else if (tab_mode == kTabHybrid) {
+        const uint32_t S = (uint32_t)e.S, Q = (uint32_t)e.qmax;
+#pragma unroll
+        for (int i = 0; i < 32; i++)
+            qb[i >> 2] |= requant_hybrid(tab + (lc + i) * kTabStride, (int32_t)acc[i], S, e.invS, Q) << (8 * (i & 3));
+    } else {
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            const int n = nb + i;
+            uint32_t qv = 0;
+            if (n < g.N) qv = requant(e, (int32_t)acc[i], epi_alpha(e, n), epi_beta(e, n));
+            qb[i >> 2] |= qv << (8 * (i & 3));
+        }
+    }
+}
+
+// plane words of 32 byte codes
+__device__ __forceinline__ void bytes_to_words(const uint32_t (&qb)[8], int out_bits, uint32_t (&words)[8]) {
+#pragma unroll
+    for (int tb = 0; tb < 8; tb++) {
+        uint32_t wv = 0;
+        if (tb < out_bits) {
+#pragma unroll
+            for (int qq = 0; qq < 8; qq++) wv |= byte_bits_to_nibble(qb[qq], tb) << (4 * qq);
+        }
+        words[tb] = wv;
+    }
+}
+
 // 32 accumulators of row m, columns nb..nb+31 (lc = tile-local column of nb) ->
 // plane words: words[t] bit i = bit t of q(column nb + i), t < out_bits.
 __device__ __forceinline__ void requant_chunk(const uint32_t (&acc)[32], int nb, int lc, const Geom& g,

@@ -2,6 +2,7 @@
 zero tolerance).  All calls go through the C ABI (paper_2106_12169_b200 is a
 ctypes binding of libapnn.so).  Inputs are the seeded synthetic codes of
 paper_2106_12169_b200.synth; expected values come only from oracle/."""
+import ctypes
 import numpy as np
 import pytest
 import torch
@@ -331,3 +332,43 @@ def test_tc_narrow_pair_tiles_repeatable():
         ref = ap.gemm(Ap, Wp, M, N, K, a, w, e, variant=ap.VARIANT_B1MMA)
         for _ in range(6):
             assert torch.equal(ap.gemm(Ap, Wp, M, N, K, a, w, e, variant=ap.VARIANT_TC_I8), ref)
+
+
+# ----------------------------------------------------------------- pooling (row f2)
+
+POOL_CASES = [  # (B, H, W, C, Co, stride, pool, pool_stride, avg, fused expected)
+    (4, 14, 14, 64, 64, 1, 2, 2, False, True),     # Wo = 14: conv_k 9 -> 8 rows per tile
+    (2, 28, 28, 128, 96, 1, 2, 2, False, True),    # Wo = 28, ragged C_out
+    (2, 16, 17, 64, 130, 1, 2, 2, False, True),    # odd Wo (last column dropped), N > 128
+    (2, 56, 56, 64, 64, 1, 2, 2, False, True),     # ResNet-L1-sized map, conv_k = 2
+    (3, 7, 7, 64, 40, 1, 2, 2, False, False),      # odd Ho -> unfused pair
+    (1, 66, 66, 64, 32, 1, 2, 2, False, False),    # Wo > 64 -> unfused pair
+    (2, 12, 12, 64, 64, 1, 3, 2, False, False),    # AlexNet-style 3x3/2 -> unfused
+    (2, 14, 14, 64, 64, 1, 2, 2, True, False),     # average -> unfused
+    (1, 8, 8, 64, 64, 1, 2, 2, False, False),      # M = 64 <= 128: 1-CTA kernel -> unfused
+]
+
+
+@pytest.mark.parametrize("case", POOL_CASES)
+@pytest.mark.parametrize("a_bits,w_bits,enc,out_bits", [(2, 1, 2, 2), (2, 2, 0, 1), (1, 1, 1, 5)])
+def test_conv_pool_fused_and_unfused(case, a_bits, w_bits, enc, out_bits):
+    B, H, Wd, C, Co, st, k, ps, avg, fused = case
+    X, Wt = synth.conv_inputs(B, H, Wd, C, Co, 3, 3, a_bits, w_bits, tag="pool")
+    Y = oracle.conv2d(X, Wt, st, 1, a_bits, w_bits, enc)
+    alpha, beta, S = epi_case(Co, out_bits, "poolepi")
+    q = oracle.pool_epilogue(Y, alpha, beta, S, out_bits, k, ps, avg=avg)
+    want = oracle.pack(q.reshape(-1, Co), out_bits)
+    Xp = ap.pack_bits(cuda(X.reshape(-1, C)), a_bits)
+    Wp = ap.pack_bits(cuda(Wt.reshape(-1, C)), w_bits)
+    cs = ap.ConvShape(B, H, Wd, C, Co, 3, 3, st, 1)
+    epi = ap.Epilogue(out_bits, cuda(alpha), cuda(beta), S, pool=k, pool_stride=ps, pool_avg=avg)
+    got = ap.conv2d(Xp, Wp, cs, a_bits, w_bits, enc, epi=epi)
+    np.testing.assert_array_equal(u32(got), want)
+    # the library fuses exactly the documented cases (else APNN_ERR_UNSUPPORTED, nothing launched)
+    out = torch.empty_like(got)
+    st_ = ap.lib().apnn_conv2d_ex(ap._ptr(Xp), ap._ptr(Wp), ctypes.byref(cs._c()), a_bits, w_bits, enc,
+                                  ctypes.byref(epi._c()), ap._ptr(out), 0, ap._stream(Xp))
+    assert st_ == (0 if fused else 7)
+    # the unfused pair gives the same bytes (fusion equivalence)
+    Y32 = ap.conv2d(Xp, Wp, cs, a_bits, w_bits, enc)
+    np.testing.assert_array_equal(u32(ap.pool_quant_pack_out(Y32, epi)), want)
