@@ -44,6 +44,7 @@ namespace apnn {
 namespace tc {
 
 constexpr int BM = 128;
+constexpr int T1_THREADS = 10 * 32;
 constexpr int MAX_STAGES = 8;     // operand stages (A in TMEM: 32 columns each)
 constexpr int MAX_PSTAGES = 16;   // packed-plane stages of the 2-CTA kernel
 constexpr int kStgWarpBytes = 8192;  // store staging per epilogue warp (1024-aligned)
@@ -65,6 +66,8 @@ struct Params {
     int out_mode;       // epilogue stores: kOutDirect / kOutTma (tensor map tmapY) / kOutLsu (coalesced)
     int nwb;            // packed TMA store box width in words (2-CTA kernel)
     int pool_fused;     // conv: 2x2/2 max pooling fused into the epilogue (pooled output Hp x Wp)
+    int stg_warp;       // 2-CTA kernel: store staging bytes per epilogue warp (multiple of 1024)
+    int ksplit;         // 1-CTA kernel: split-K factor Z (cluster of Z CTAs along z, DSMEM reduction)
     int Hp, Wp;
     int acc_shift;      // scaled operands: accumulator = Y << acc_shift (2-CTA kernel)
     // conv A-row tiling of the 2-CTA kernel (TMA row boxes):
@@ -90,8 +93,16 @@ __device__ __forceinline__ void trace_at(const Params& p, int ev, int idx) {
 }
 // per-CTA %globaltimer stamps (ns): 0 entry, 1 after the prologue, 2 work done, 3 exit
 constexpr int kCtaTraceMax = 1024;
+// CTA-0 event stamps (ns), slots 0..31 (development)
+__device__ __forceinline__ void dbg_stamp(const Params& p, int slot) {
+    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[kTraceN * TR_N + 4 * kCtaTraceMax + slot] = t;
+    }
+}
 __device__ __forceinline__ void cta_stamp(const Params& p, int k) {
-    const int b = blockIdx.x + blockIdx.y * gridDim.x;
+    const int b = blockIdx.x + (blockIdx.y + blockIdx.z * gridDim.y) * gridDim.x;
     if (p.trace && threadIdx.x == 0 && b < kCtaTraceMax) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -196,7 +207,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     const int S = p.stages, SP = p.pstages;
     uint8_t* sBop = smem;                                        // S x BROWS rows x 128 B
     uint8_t* sStg = sBop + (size_t)S * BOP_STAGE;                // 4 epilogue warps x 8 KB TMA-store staging
-    uint8_t* sApl = sStg + 4 * kStgWarpBytes;                    // SP x a_bytes
+    uint8_t* sApl = sStg + 4 * p.stg_warp;                       // SP x a_bytes
     uint8_t* sBpl = sApl + (size_t)SP * p.a_bytes;               // SP x b_bytes
     int32_t* sTab = reinterpret_cast<int32_t*>(sBpl + (size_t)SP * p.b_bytes);  // 256 x 16 int32
     uint64_t* bars = reinterpret_cast<uint64_t*>(sTab + T2_BN * kTabStride);
@@ -390,7 +401,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
         const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
         const uint32_t accum_empty0 = mapa(smem_u32(accum_empty), 0);
         const int ob = p.e.out_bits;
-        uint8_t* stg = sStg + q * kStgWarpBytes;
+        uint8_t* stg = sStg + q * p.stg_warp;
         const uint32_t stg_addr = smem_u32(stg);
         int tc = 0;
         uint32_t nst = 0, npc = 0;
@@ -504,8 +515,81 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     cta_stamp(p, 3);
 }
 
+// ------------------------------------------------ split-K reduction (row f4)
+// Small problems (few output tiles) leave most SMs idle.  The 1-CTA kernel then runs
+// Z = ksplit CTAs per output tile as one thread-block cluster along z; CTA z reduces
+// k-blocks [z*nkb/Z, (z+1)*nkb/Z).  Each CTA parks its 128 x BN int32 partial sums in
+// a reduction region of its own shared memory (16-byte chunks XOR-swizzled by row:
+// conflict-free row-per-thread stores), the cluster synchronises, and CTA z sums rows
+// [z*128/Z, (z+1)*128/Z) over all Z partials through distributed shared memory
+// (ld.shared::cluster, all Z loads in flight; measured faster than pushing the
+// partials with st.shared::cluster), then applies the epilogue: one warp per (row, 32-column chunk), lane = column, so int32
+// stores are coalesced and packed words come from __ballot_sync.
+__device__ __forceinline__ int split_red_index(int row, int col, int BN) {
+    return row * BN + ((((col >> 2) ^ (row & 7))) << 2) + (col & 3);
+}
+__device__ __forceinline__ int32_t ld_cluster_s32(uint32_t cluster_addr) {
+    int32_t v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(cluster_addr));
+    return v;
+}
+
+template <int BN>
+__device__ __forceinline__ void split_reduce_store(const Params& p, uint8_t* smem, int m0, int n0,
+                                                   const int32_t* tab, int warp, int lane) {
+    using namespace sm100;
+    const Geom& g = p.g;
+    const int Z = p.ksplit;
+    const uint32_t z = cluster_ctarank();
+    if (threadIdx.x == 64) dbg_stamp(p, 4);
+    cluster_sync();  // every partial of the cluster is in shared memory
+    if (threadIdx.x == 64) dbg_stamp(p, 5);
+    const uint32_t red0 = smem_u32(smem);
+    const int rows = BM / Z;
+    const int nch = BN / 32;
+    const int units = rows * nch;
+    const int ob = p.e.out_bits;
+    const int Nw = (g.N + 127) / 128 * 4;
+    for (int u = warp; u < units; u += T1_THREADS / 32) {
+        const int row = (int)z * rows + u / nch, ch = u - (u / nch) * nch;
+        const int col = ch * 32 + lane;
+        const uint32_t off = red0 + 4u * (uint32_t)split_red_index(row, col, BN);
+        int32_t part[8];  // all Z remote loads in flight before the sum
+#pragma unroll
+        for (int r = 0; r < 8; r++) part[r] = r < Z ? ld_cluster_s32(mapa(off, (uint32_t)r)) : 0;
+        int32_t y = 0;
+#pragma unroll
+        for (int r = 0; r < 8; r++) y += part[r];
+        const int m = m0 + row, n = n0 + col;
+        if (m >= g.M) continue;  // warp-uniform
+        if (ob == 0) {
+            if (n < g.N) reinterpret_cast<int32_t*>(p.Y)[(long long)m * g.N + n] = y;
+        } else {
+            uint32_t q = 0;
+            if (n < g.N) {
+                if (p.tab_mode == kTabQ3) {
+                    const int4 h = *reinterpret_cast<const int4*>(tab + col * kTabStride);
+                    const int32_t yp = y * h.x;
+                    q = (uint32_t)(yp > h.y) + (uint32_t)(yp > h.z) + (uint32_t)(yp > h.w);
+                } else if (p.tab_mode == kTabHybrid) {
+                    q = requant_hybrid(tab + col * kTabStride, y, (uint32_t)p.e.S, p.e.invS, (uint32_t)p.e.qmax);
+                } else {
+                    q = requant(p.e, y, epi_alpha(p.e, n), epi_beta(p.e, n));
+                }
+            }
+            const int word = (n0 >> 5) + ch;
+            uint32_t* o = reinterpret_cast<uint32_t*>(p.Y) + (long long)m * ob * Nw + word;
+            for (int tb = 0; tb < ob; tb++) {
+                const uint32_t wv = __ballot_sync(0xFFFFFFFFu, (q >> tb) & 1u);
+                if (lane == tb && word < Nw) o[(long long)tb * Nw] = wv;
+            }
+        }
+    }
+    if (threadIdx.x == 64) dbg_stamp(p, 6);
+    cluster_sync();  // remote reads done before any CTA of the cluster exits
+}
+
 // ============================================================== 1-CTA kernel
-constexpr int T1_THREADS = 10 * 32;
 
 template <int BN, bool A_PM1, bool W_PM1>
 __global__ void __launch_bounds__(T1_THREADS, 1)
@@ -514,7 +598,9 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
     using namespace sm100;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = p.stages;
-    uint8_t* sBop = smem;                                    // S x BN x 128 B
+    // split-K: a dedicated reduction region first (other CTAs of the cluster push into it
+    // while this CTA may still be in its main loop), then the pipeline buffers
+    uint8_t* sBop = smem + (p.ksplit > 1 ? BM * BN * 4 : 0);  // S x BN x 128 B
     uint8_t* sApl = sBop + (size_t)S * BN * 128;             // S x a_bytes
     uint8_t* sBpl = sApl + (size_t)S * p.a_bytes;            // S x b_bytes
     int32_t* sTab = reinterpret_cast<int32_t*>(sBpl + (size_t)S * p.b_bytes);  // BN x 16 int32
@@ -530,7 +616,9 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
     const Geom& g = p.g;
-    const int nkb = p.nkb;
+    // split-K (f4, small problems): CTA z of the cluster reduces k-blocks [kb0, kb0 + nkb)
+    const int kb0 = (int)(((long long)blockIdx.z * p.nkb) / p.ksplit);
+    const int nkb = (int)(((long long)(blockIdx.z + 1) * p.nkb) / p.ksplit) - kb0;  // >= 1 (ksplit <= nkb)
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmapA);
@@ -560,14 +648,16 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
 #pragma unroll
                 for (int i = 0; i < 4; i++) rc[i] = make_row(g, m0 + lane + 32 * i);
             }
-            for (int kb = 0; kb < nkb; kb++) {
-                const int s = kb % S;
-                const uint32_t ph = (kb / S) & 1;
+            for (int i = 0; i < nkb; i++) {
+                const int kb = kb0 + i;
+                const int s = i % S;
+                const uint32_t ph = (i / S) & 1;
                 mbar_wait(&plane_empty[s], ph ^ 1);
                 if (lane == 0) {
                     const int rs = conv ? kb / g.CB : 0;
                     const int cb = conv ? kb - rs * g.CB : kb;
                     mbar_arrive_expect_tx(&plane_full[s], (conv ? 0u : p.a_bytes) + p.b_bytes);
+                    if (i == 0) dbg_stamp(p, 0);
                     if (!conv) tma_load_4d(sApl + (size_t)s * p.a_bytes, &tmapA, &plane_full[s], kb * 4, m0, 0, 0);
                     tma_load_4d(sBpl + (size_t)s * p.b_bytes, &tmapB, &plane_full[s], cb * 4, n0, 0, rs);
                 }
@@ -577,7 +667,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
     } else if (warp == 1) {
         if (lane == 0) {
             const uint32_t idesc = idesc_i8(BM, BN, A_PM1, W_PM1);
-            for (int kb = 0; kb < nkb; kb++) {
+            for (int kb = 0; kb < nkb; kb++) {  // local k-block index
                 const int s = kb % S;
                 const uint32_t ph = (kb / S) & 1;
                 mbar_wait(&op_full[s], ph);
@@ -601,9 +691,10 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
         if (p.tab_mode && et < BN) build_threshold_row(sTab + et * kTabStride, n0 + et, g.N, p.e);
         RowCtx rc;
         if (A_PM1 && g.conv) rc = make_row(g, m0 + t);
-        for (int kb = 0; kb < nkb; kb++) {
-            const int s = kb % S;
-            const uint32_t ph = (kb / S) & 1;
+        for (int i = 0; i < nkb; i++) {
+            const int kb = kb0 + i;
+            const int s = i % S;
+            const uint32_t ph = (i / S) & 1;
             int kvalid = 128;
             if (A_PM1) {
                 if (g.conv) {
@@ -614,8 +705,9 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
                 }
             }
             mbar_wait(&plane_full[s], ph);
+            if (i == 0 && threadIdx.x == 64) dbg_stamp(p, 1);
             mbar_wait(&op_empty[s], ph ^ 1);
-            if ((kb & 1) == grp) {
+            if ((i & 1) == grp) {
                 a_job_any<A_PM1>(g.a_bits, sApl + (size_t)s * p.a_bytes, BM, t, tmem_lane + A_COL + s * 32, kvalid);
                 tmem_wait_st();
             } else {
@@ -632,9 +724,11 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
                 mbar_arrive(&op_full[s]);
             }
         }
+        if (threadIdx.x == 64) dbg_stamp(p, 2);
         named_bar_sync(1, 256);  // threshold table complete (built before the mainloop)
         mbar_wait(accum_full, 0);
         tc_fence_after();
+        if (threadIdx.x == 64) dbg_stamp(p, 3);
         const int m = m0 + t;
         constexpr int half = BN / 2;
         // int32 output: TMA stores from per-warp staging that reuses the (now idle)
@@ -648,6 +742,14 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
             uint32_t acc[32];
             tmem_ld32(tmem_lane + c, acc);
             tmem_wait_ld();
+            if (p.ksplit > 1) {  // partial sums -> this CTA's reduction buffer (reduced below)
+                int32_t* red = reinterpret_cast<int32_t*>(smem);
+#pragma unroll
+                for (int j = 0; j < 8; j++)
+                    *reinterpret_cast<uint4*>(red + split_red_index(t, c + 4 * j, BN)) =
+                        make_uint4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+                continue;
+            }
             if (p.exp_nostore) continue;
             if (use_tma) {
                 uint8_t* b = stg + (nst & 1) * 4096;
@@ -673,6 +775,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
         if (use_tma && lane == 0) bulk_wait<0>();
     }
 
+    if (p.ksplit > 1) split_reduce_store<BN>(p, smem, m0, n0, sTab, warp, lane);
     tc_fence_before();
     __syncthreads();
     cta_stamp(p, 2);
@@ -802,8 +905,25 @@ static cudaError_t launch1(const CUtensorMap& ta, const CUtensorMap& tb, const C
     auto kfn = tc1_kernel<BN, AP, WP>;
     cudaError_t e = set_smem(kfn);
     if (e != cudaSuccess) return e;
-    kfn<<<grid, T1_THREADS, smem, s>>>(ta, tb, ty, p);
-    return cudaGetLastError();
+    if (p.ksplit <= 1) {
+        kfn<<<grid, T1_THREADS, smem, s>>>(ta, tb, ty, p);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(T1_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = (unsigned)p.ksplit;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kfn, ta, tb, ty, p);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <bool AP, bool WP>
@@ -854,6 +974,19 @@ static int epi_store_mode(bool packed) {
     return v >= 0 ? v : (packed ? tc::kOutLsu : tc::kOutTma);
 }
 
+// largest split-K cluster (experiment knob APNN_SPLITZ).  Default 4: the paper's FC layer
+// (M = 64, N = K = 1024, w1a2) measured 10.1 / 7.9 / 8.1 us at Z = 1 / 4 / 8.
+static int split_zmax() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("APNN_SPLITZ");
+        v = s ? atoi(s) : 4;
+        if (v < 1) v = 1;
+        if (v > 8) v = 8;
+    }
+    return v;
+}
+
 // variant knob for experiments: APNN_TC_KERNEL=1 forces the 1-CTA kernel
 static int tc_kernel_override() {
     static int v = -1;
@@ -881,6 +1014,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     }
     p.out_mode = kOutDirect;
     p.nwb = 0;
+    p.ksplit = 1;
     p.pool_fused = e.pool ? 1 : 0;  // the ABI only forwards fusable pooling (tc_i8_pool_fusable)
     p.Hp = g.Ho / 2;
     p.Wp = g.Wo / 2;
@@ -890,11 +1024,18 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     p.exp_nostore = getenv("APNN_EXP_NOSTORE") ? 1 : 0;
     const char* trace_path = getenv("APNN_TRACE");
     if (trace_path) {
-        cudaMalloc(&p.trace, sizeof(unsigned long long) * (kTraceN * TR_N + 4 * kCtaTraceMax));
-        cudaMemset(p.trace, 0, sizeof(unsigned long long) * (kTraceN * TR_N + 4 * kCtaTraceMax));
+        cudaMalloc(&p.trace, sizeof(unsigned long long) * (kTraceN * TR_N + 4 * kCtaTraceMax + 32));
+        cudaMemset(p.trace, 0, sizeof(unsigned long long) * (kTraceN * TR_N + 4 * kCtaTraceMax + 32));
     }
     const int ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
-    const bool two = (g.M > 128) && tc_kernel_override() != 1;
+    bool two = (g.M > 128) && tc_kernel_override() != 1;
+    // small GEMMs (row f4): when the 2-CTA grid would occupy <= 1/4 of the SMs, run the
+    // 1-CTA kernel with split-K clusters instead (latency: more CTAs, fewer k-blocks each)
+    if (two && !g.conv && g.M <= 1024 && g.nchunks >= 4 && tc_kernel_override() != 2) {
+        const int BNP = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
+        const long long pair_tiles = (long long)((g.M + 255) / 256) * ((g.N + BNP - 1) / BNP);
+        if (pair_tiles * 2 * 4 <= sms) two = false;
+    }
     CUtensorMap ta, tb, ty;
     std::memset(&ty, 0, sizeof(ty));
     cudaError_t err;
@@ -914,8 +1055,17 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
             p.a_bytes = 16u * 128 * g.a_bits;
             p.a_tx_bytes = p.a_bytes;
         }
+        {   // store staging per epilogue warp: int32 TMA 2 x 4 KB, int32 LSU 4 KB, packed one
+            // {nwb, bits, 32} box; fused pooling uses 2 x 4 KB across the four warps
+            const int nwb = BNP / 32 < 4 ? 4 : BNP / 32;
+            int sw = 0;
+            if (e.out_bits == 0) sw = want_mode == kOutTma ? 8192 : (want_mode == kOutLsu ? 4096 : 0);
+            else if (want_mode != kOutDirect) sw = (e.out_bits * nwb * 128 + 1023) / 1024 * 1024;
+            if (p.pool_fused && sw < 2048) sw = 2048;
+            p.stg_warp = sw;
+        }
         const size_t fixed = (size_t)256 * kTabStride * 4 + (2 * MAX_PSTAGES + 2 * MAX_STAGES + 4) * 8 +
-                             T2_RECOMB_WARPS * 32 * 4 + 4 * kStgWarpBytes + 1024;
+                             T2_RECOMB_WARPS * 32 * 4 + 4 * (size_t)p.stg_warp + 1024;
         const size_t budget = 227 * 1024 - fixed;
         const size_t op_stage = (size_t)brows * 128, pl_stage = p.a_bytes + p.b_bytes;
         // Both ring depths must be EVEN: the two recombination teams take alternating
@@ -992,12 +1142,35 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         default: err = launch2_bn<true, false>(BNP, ta, tb, ty, p, clusters * 2, smem, s); break;
         }
     } else {
-        const int BN = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
+        int BN = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
+        // split-K over a cluster of Z CTAs when the output tiles alone leave SMs idle
+        p.ksplit = 1;
+        if (tc_kernel_override() != 3) {
+            const int BNs = g.N > 1024 ? 128 : 64;
+            const long long tiles = (long long)((g.M + BM - 1) / BM) * ((ncols + BNs - 1) / BNs);
+            int Z = 1;
+            const int zmax = split_zmax();
+            while (Z < zmax && 2 * Z <= g.nchunks && tiles * 2 * Z <= sms) Z *= 2;
+            if (Z > 1) {
+                p.ksplit = Z;
+                BN = BNs;
+            }
+        }
         p.a_bytes = 16u * BM * g.a_bits;
         p.b_bytes = 16u * BN * g.w_bits;
         const size_t fixed = (size_t)BN * kTabStride * 4 + (4 * MAX_STAGES + 4) * 8 + 1024;
-        const int S = stage_count((size_t)BN * 128 + p.a_bytes + p.b_bytes, fixed);
+        int S = stage_count((size_t)BN * 128 + p.a_bytes + p.b_bytes, fixed);
         if (S < 2) return cudaErrorInvalidConfiguration;
+        if (p.ksplit > 1) {
+            // a split CTA runs only ~nkb/Z k-blocks: a shallow ring keeps TMEM (BN + 32 S
+            // columns) and shared memory small, so co-resident CTAs never wait on tcgen05.alloc
+            const int per = (g.nchunks + p.ksplit - 1) / p.ksplit;
+            const size_t stage = (size_t)BN * 128 + p.a_bytes + p.b_bytes, red = (size_t)BM * BN * 4;
+            const int fit = (int)((227 * 1024 - fixed - red) / stage);
+            S = per < 2 ? 2 : (per < S ? per : S);
+            if (S > fit) S = fit;
+            if (S < 2) return cudaErrorInvalidConfiguration;
+        }
         p.stages = S;
         p.pstages = S;
         uint32_t cols = BN + 32 * S, pow2 = 32;
@@ -1005,10 +1178,12 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         p.tmem_cols = pow2;
         p.tiles_m = 0;
         p.num_tiles = 0;
-        const size_t smem = (size_t)S * ((size_t)BN * 128 + p.a_bytes + p.b_bytes) + fixed - 1024 + 64;
+        const size_t smem = (size_t)S * ((size_t)BN * 128 + p.a_bytes + p.b_bytes) + fixed - 1024 + 64 +
+                            (p.ksplit > 1 ? (size_t)BM * BN * 4 : 0);
+        if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         if (!make_plane_map(&ta, A, g.conv ? 1 : g.M, g.a_bits, g.Cw, 1, BM)) return cudaErrorInvalidValue;
         if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, g.RS, BN)) return cudaErrorInvalidValue;
-        dim3 grid((g.M + BM - 1) / BM, (ncols + BN - 1) / BN);
+        dim3 grid((g.M + BM - 1) / BM, (ncols + BN - 1) / BN, p.ksplit);
         // int32 output through TMA stores, staged in the idle pipeline buffers (8 warps x 8 KB)
         if (e.out_bits == 0 && g.N % 4 == 0 && want_mode != kOutDirect &&
             (size_t)S * ((size_t)BN * 128 + p.a_bytes + p.b_bytes) >= 8 * kStgWarpBytes) {
@@ -1023,7 +1198,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         }
     }
     if (p.trace) {  // development only: synchronous dump
-        static unsigned long long host[kTraceN * TR_N + 4 * kCtaTraceMax];
+        static unsigned long long host[kTraceN * TR_N + 4 * kCtaTraceMax + 32];
         cudaStreamSynchronize(s);
         cudaMemcpy(host, p.trace, sizeof(host), cudaMemcpyDeviceToHost);
         cudaFree(p.trace);

@@ -111,25 +111,27 @@ __global__ void __launch_bounds__(256) quant_pack_kernel(const int32_t* __restri
 
 // Y [B][H][W][N] int32 (NHWC conv output) -> out [B*Hp*Wp][ob][Nw]: k x k pooling of
 // v = alpha*y + beta (max, or floor of the average), then quantisation and packing
-// (reading R15).  One thread per (pooled pixel, output word).
+// (reading R15).  One warp per (pooled pixel, output word):
+// lane = channel (coalesced 128-byte loads, k*k independent loads per lane), and the
+// plane words are formed with __ballot_sync as in the paper's output packing
+// (PAPER.md:1582-1587).
 __global__ void __launch_bounds__(256) pool_quant_pack_kernel(const int32_t* __restrict__ Y, int B, int H, int W,
                                                               int N, int Hp, int Wp, int Nw, Epi e,
                                                               uint32_t* __restrict__ out) {
-    const long long total = (long long)B * Hp * Wp * Nw;
+    const long long total = (long long)B * Hp * Wp * Nw;  // warps of work
     const int k = e.pool, st = e.pool_stride;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const long long wstride = (long long)gridDim.x * (blockDim.x / 32);
+    for (long long idx = blockIdx.x * (long long)(blockDim.x / 32) + (threadIdx.x >> 5); idx < total;
+         idx += wstride) {
         const long long pix = idx / Nw;
         const int w = (int)(idx - pix * Nw);
         const int b = (int)(pix / ((long long)Hp * Wp));
         const int rem = (int)(pix - (long long)b * Hp * Wp);
         const int i = rem / Wp, j = rem - (rem / Wp) * Wp;
-        uint32_t qb[8];
-#pragma unroll
-        for (int q = 0; q < 8; q++) qb[q] = 0;
-        for (int c = 0; c < 32; c++) {
-            const int n = w * 32 + c;
-            if (n >= N) break;
+        const int n = w * 32 + lane;
+        uint32_t q = 0;
+        if (n < N) {
             const long long al = epi_alpha(e, n), be = epi_beta(e, n);
             long long best = 0, sum = 0;
             for (int r = 0; r < k; r++) {
@@ -146,14 +148,12 @@ __global__ void __launch_bounds__(256) pool_quant_pack_kernel(const int32_t* __r
                 P = sum / kk;
                 if (sum % kk != 0 && sum < 0) P -= 1;  // floor toward -inf
             }
-            qb[c >> 2] |= quantise_v(e, P) << (8 * (c & 3));
+            q = quantise_v(e, P);
         }
         uint32_t* o = out + pix * e.out_bits * Nw + w;
         for (int t = 0; t < e.out_bits; t++) {
-            uint32_t word = 0;
-#pragma unroll
-            for (int q = 0; q < 8; q++) word |= byte_bits_to_nibble(qb[q], t) << (4 * q);
-            o[(long long)t * Nw] = word;
+            const uint32_t word = __ballot_sync(0xFFFFFFFFu, (q >> t) & 1u);
+            if (lane == t) o[(long long)t * Nw] = word;
         }
     }
 }
@@ -199,7 +199,7 @@ cudaError_t launch_pool_quant_pack(const int32_t* Y, int B, int H, int W, int N,
     const int Nw = (N + 127) / 128 * 4;
     const long long total = (long long)B * Hp * Wp * Nw;
     if (total == 0) return cudaSuccess;
-    pool_quant_pack_kernel<<<stream_grid(total, sms), 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nw, e, out);
+    pool_quant_pack_kernel<<<stream_grid(total * 32, sms), 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nw, e, out);
     count_launch();
     return cudaGetLastError();
 }

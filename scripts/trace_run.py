@@ -16,7 +16,11 @@ raw = open(path, "rb").read()
 n, nev, nkb, S = struct.unpack("4i", raw[:16])
 allv = np.frombuffer(raw[16:], dtype=np.uint64).astype(np.int64)
 t = allv[:nev * n].reshape(nev, n)
-ct = allv[nev * n:].reshape(-1, 4)
+ct = allv[nev * n:nev * n + 4096].reshape(-1, 4)
+dbg = allv[nev * n + 4096:nev * n + 4096 + 32]
+if (dbg > 0).any():
+    c0 = ct[ct[:, 0] > 0][:, 0].min() if (ct[:, 0] > 0).any() else dbg[dbg > 0].min()
+    print("cta0 stamps (ns from first entry):", [(i, int(v - c0)) for i, v in enumerate(dbg) if v > 0])
 ct = ct[ct[:, 0] > 0]
 if len(ct):
     g0 = ct[:, 0].min()

@@ -372,3 +372,23 @@ def test_conv_pool_fused_and_unfused(case, a_bits, w_bits, enc, out_bits):
     # the unfused pair gives the same bytes (fusion equivalence)
     Y32 = ap.conv2d(Xp, Wp, cs, a_bits, w_bits, enc)
     np.testing.assert_array_equal(u32(ap.pool_quant_pack_out(Y32, epi)), want)
+
+
+# -------------------------------------------- split-K clusters for small problems (row f4)
+
+@pytest.mark.parametrize("M,N,K", [(64, 1024, 1024), (1, 33, 4096), (100, 130, 1500), (300, 64, 640),
+                                   (1000, 100, 1024), (128, 1000, 9216), (256, 4096, 1024)])
+@pytest.mark.parametrize("a_bits,w_bits,enc", [(2, 1, 2), (8, 8, 0), (1, 1, 1)])
+@pytest.mark.parametrize("out_bits", [0, 2, 5])
+def test_split_k_small_problems(M, N, K, a_bits, w_bits, enc, out_bits):
+    A, W = synth.gemm_inputs(M, N, K, a_bits, w_bits, tag="splitk")
+    Y = oracle.gemm(A, W, a_bits, w_bits, enc)
+    if out_bits == 0:
+        got = run_gemm(A, W, a_bits, w_bits, enc, ap.VARIANT_TC_I8)
+        np.testing.assert_array_equal(got.cpu().numpy(), Y)
+    else:
+        alpha, beta, S = epi_case(N, out_bits, "splitk")
+        want = oracle.pack(oracle.epilogue(Y, alpha, beta, S, out_bits), out_bits)
+        got = run_gemm(A, W, a_bits, w_bits, enc, ap.VARIANT_TC_I8,
+                       epi=ap.Epilogue(out_bits, cuda(alpha), cuda(beta), S))
+        np.testing.assert_array_equal(u32(got), want)
