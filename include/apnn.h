@@ -129,6 +129,27 @@ size_t apnn_packed_bytes(int rows, int K, int bits);
 apnn_status apnn_pack_bits(const uint8_t *codes, int rows, int K, int bits, uint32_t *dst,
                            apnn_stream_t stream);
 
+/* Implicit-GEMM rows made explicit for a thin first layer (C_in = 3 images; the paper
+ * blames the first layer for most of AlexNet's latency): bit-decompose
+ * and pack the im2col matrix of NHWC uint8 codes (APConv as GEMM).
+ *   X:   device uint8 [B][H][W][C_in] codes < 2^bits (higher bits ignored)
+ *   dst: device packed [B*Ho*Wo][bits][roundup(R*S*C_in,128)/32]; row (b,ho,wo), element
+ *        k = (r*S + s)*C_in + c holds the code of X[b][ho*st+r-pad][wo*st+s-pad][c], and
+ *        0 for out-of-frame taps (the value 0 of a 0/1 encoding; +-1 activations cannot
+ *        be padded this way and must use apnn_conv2d).
+ * The GEMM weights are then the OHWI codes flattened to [C_out][R*S*C_in]. */
+apnn_status apnn_im2col_pack(const uint8_t *X, const apnn_conv_shape *shape, int bits, uint32_t *dst,
+                             apnn_stream_t stream);
+
+/* Flatten a packed feature map for the first fully connected layer: per image b,
+ *   src [B][P][bits][Cw]  (P pixels, packed rows of the conv output, Cw = roundup(C,128)/32)
+ *   dst [B][bits][P*Cw]   (one packed row of K = P * Cw * 32 elements per image, pixel-major,
+ *                          i.e. the HWC flattening; channel padding stays zero inside K)
+ * A pure permutation of 32-bit words (no arithmetic); the FC weights are packed with the
+ * same [P][Cw*32] element order (zero codes in the padded channels). */
+apnn_status apnn_flatten_packed(const uint32_t *src, int B, int P, int bits, int Cw, uint32_t *dst,
+                                apnn_stream_t stream);
+
 /* APMM with 32-bit output:
  *   Y[m][n] = sum_{k<K} dec_A(a[m][k]) * dec_W(w[n][k])
  *   A: device packed [M][a_bits][Kw];  W: device packed [N][w_bits][Kw];

@@ -71,6 +71,10 @@ def lib() -> ctypes.CDLL:
             L.apnn_packed_bytes.restype = ctypes.c_size_t
             L.apnn_pack_bits.argtypes = [vp, ci, ci, ci, vp, vp]
             L.apnn_pack_bits.restype = st
+            L.apnn_flatten_packed.argtypes = [vp, ci, ci, ci, ci, vp, vp]
+            L.apnn_flatten_packed.restype = st
+            L.apnn_im2col_pack.argtypes = [vp, ctypes.POINTER(_Conv), ci, vp, vp]
+            L.apnn_im2col_pack.restype = st
             L.apnn_gemm.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, vp, vp]
             L.apnn_gemm.restype = st
             L.apnn_gemm_fused.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp, vp]
@@ -100,7 +104,7 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
-ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
+ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_im2col_pack", "apnn_flatten_packed", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
                "apnn_conv2d", "apnn_conv2d_ex", "apnn_quant_pack_out", "apnn_pool_quant_pack_out",
                "apnn_select_variant",
                "apnn_status_string", "apnn_variant_name", "apnn_launch_count", "apnn_version")
@@ -208,6 +212,31 @@ def pack_bits(codes: torch.Tensor, bits: int, out: Optional[torch.Tensor] = None
         out = torch.empty(packed_shape(rows, K, bits), dtype=torch.int32, device=codes.device)
     _cuda(out, "out", torch.int32)
     _check(lib().apnn_pack_bits(_ptr(codes), rows, K, bits, _ptr(out), _stream(codes)), "apnn_pack_bits")
+    return out
+
+
+def im2col_pack(X: torch.Tensor, shape: ConvShape, bits: int, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """NHWC uint8 codes [B, H, W, C_in] -> packed im2col rows [B*Ho*Wo, bits, Kw(R*S*C_in)]
+    (apnn_im2col_pack; out-of-frame taps are code 0)."""
+    _cuda(X, "X", torch.uint8)
+    K = shape.R * shape.S * shape.C_in
+    if out is None:
+        out = torch.empty(packed_shape(shape.B * shape.Ho * shape.Wo, K, bits), dtype=torch.int32, device=X.device)
+    _cuda(out, "out", torch.int32)
+    cs = shape._c()
+    _check(lib().apnn_im2col_pack(_ptr(X), ctypes.byref(cs), bits, _ptr(out), _stream(X)), "apnn_im2col_pack")
+    return out
+
+
+def flatten_packed(X: torch.Tensor, B: int, P: int, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Packed feature map [B*P, bits, Cw] -> one packed row per image [B, bits, P*Cw]
+    (apnn_flatten_packed; HWC flattening for the first FC layer)."""
+    _cuda(X, "X", torch.int32)
+    _, bits, Cw = X.shape
+    if out is None:
+        out = torch.empty((B, bits, P * Cw), dtype=torch.int32, device=X.device)
+    _cuda(out, "out", torch.int32)
+    _check(lib().apnn_flatten_packed(_ptr(X), B, P, bits, Cw, _ptr(out), _stream(X)), "apnn_flatten_packed")
     return out
 
 

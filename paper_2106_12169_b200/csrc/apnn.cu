@@ -21,6 +21,10 @@ cudaError_t launch_quant_pack(const int32_t* Y, int M, int N, const Epi& e, uint
 cudaError_t launch_pool_quant_pack(const int32_t* Y, int B, int H, int W, int N, const Epi& e, uint32_t* out,
                                   int sms, cudaStream_t s);
 bool tc_i8_pool_fusable(const Geom& g, const Epi& e);
+cudaError_t launch_flatten_packed(const uint32_t* src, int B, int P, int bits, int Cw, uint32_t* dst, int sms,
+                                  cudaStream_t s);
+cudaError_t launch_im2col_pack(const uint8_t* X, int B, int H, int W, int C, int R, int S, int stride, int pad,
+                               int Ho, int Wo, int bits, uint32_t* dst, int sms, cudaStream_t s);
 cudaError_t launch_popc(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
                         cudaStream_t s);
 cudaError_t launch_b1mma(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
@@ -163,6 +167,42 @@ apnn_status apnn_pack_bits(const uint8_t* codes, int rows, int K, int bits, uint
     apnn_status st = device_info(&d);
     if (st != APNN_OK) return st;
     cudaError_t err = launch_pack_bits(codes, rows, K, bits, dst, d.sms, (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_status apnn_flatten_packed(const uint32_t* src, int B, int P, int bits, int Cw, uint32_t* dst,
+                                apnn_stream_t stream) {
+    if (B < 0 || P < 1 || Cw < 1 || (Cw & 3)) return APNN_ERR_SHAPE;
+    if (bits < 1 || bits > 8) return APNN_ERR_BITS;
+    if ((long long)P * Cw * 32 > 2147483647LL) return APNN_ERR_SHAPE;
+    if (B > 0 && (!src || !dst)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(src) || !aligned16(dst)) return APNN_ERR_ALIGNMENT;
+    DevInfo d;
+    apnn_status st = device_info(&d);
+    if (st != APNN_OK) return st;
+    cudaError_t err = launch_flatten_packed(src, B, P, bits, Cw, dst, d.sms, (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_status apnn_im2col_pack(const uint8_t* X, const apnn_conv_shape* shp, int bits, uint32_t* dst,
+                             apnn_stream_t stream) {
+    if (!shp) return APNN_ERR_INVALID_ARG;
+    const apnn_conv_shape c = *shp;
+    if (c.B < 0 || c.H < 1 || c.W < 1 || c.C_in < 1 || c.R < 1 || c.S < 1 || c.stride < 1 || c.pad < 0)
+        return APNN_ERR_SHAPE;
+    if (bits < 1 || bits > 8) return APNN_ERR_BITS;
+    if (c.H + 2 * c.pad < c.R || c.W + 2 * c.pad < c.S) return APNN_ERR_SHAPE;
+    const int Ho = (c.H + 2 * c.pad - c.R) / c.stride + 1;
+    const int Wo = (c.W + 2 * c.pad - c.S) / c.stride + 1;
+    const long long rows = (long long)c.B * Ho * Wo, K = (long long)c.R * c.S * c.C_in;
+    if (rows > 2147483647LL || K > 2147483647LL - 127) return APNN_ERR_SHAPE;
+    if (rows > 0 && (!X || !dst)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(dst)) return APNN_ERR_ALIGNMENT;
+    DevInfo d;
+    apnn_status st = device_info(&d);
+    if (st != APNN_OK) return st;
+    cudaError_t err = launch_im2col_pack(X, c.B, c.H, c.W, c.C_in, c.R, c.S, c.stride, c.pad, Ho, Wo, bits, dst,
+                                         d.sms, (cudaStream_t)stream);
     return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }
 

@@ -165,9 +165,10 @@ __device__ __forceinline__ void pool_chunk(const uint32_t (&acc)[32], int nb, in
         qb[4] = __vmaxu4(qb[4], b.x); qb[5] = __vmaxu4(qb[5], b.y);
         qb[6] = __vmaxu4(qb[6], b.z); qb[7] = __vmaxu4(qb[7], b.w);
     }
+    const int Nw = (g.N + 127) / 128 * 4;
+    if (nb / 32 >= Nw) return;  // chunk entirely in the last tile's overhang past the N padding
     uint32_t w[8];
     bytes_to_words(qb, p.e.out_bits, w);
-    const int Nw = (g.N + 127) / 128 * 4;
     uint32_t* o = reinterpret_cast<uint32_t*>(p.Y) + prow * p.e.out_bits * Nw + nb / 32;
 #pragma unroll
     for (int tb = 0; tb < 8; tb++)

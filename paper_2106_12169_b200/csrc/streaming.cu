@@ -158,6 +158,56 @@ __global__ void __launch_bounds__(256) pool_quant_pack_kernel(const int32_t* __r
     }
 }
 
+// im2col + bit decomposition + packing of NHWC uint8 codes: one thread per (row, 32-element
+// word); element k = (r*S + s)*C + c of row (b, ho, wo); out-of-frame taps are code 0.
+__global__ void __launch_bounds__(256) im2col_pack_kernel(const uint8_t* __restrict__ X, int B, int H, int W,
+                                                          int C, int R, int S, int stride, int pad, int Ho, int Wo,
+                                                          int bits, int Kw, uint32_t* __restrict__ dst) {
+    const long long rows = (long long)B * Ho * Wo;
+    const long long total = rows * Kw;
+    const int K = R * S * C;
+    const uint32_t keep = (1u << bits) - 1u;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long m = idx / Kw;
+        const int w = (int)(idx - m * Kw);
+        const int b = (int)(m / ((long long)Ho * Wo));
+        const int rem = (int)(m - (long long)b * Ho * Wo);
+        const int ho = rem / Wo, wo = rem - (rem / Wo) * Wo;
+        uint32_t planes[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int k = w * 32;
+        int tap = k / C, c = k - tap * C;
+        for (int i = 0; i < 32 && k < K; i++, k++) {
+            const int r = tap / S, s2 = tap - (tap / S) * S;
+            const int hi = ho * stride + r - pad, wi = wo * stride + s2 - pad;
+            uint32_t code = 0;
+            if (hi >= 0 && hi < H && wi >= 0 && wi < W)
+                code = __ldg(X + (((long long)b * H + hi) * W + wi) * C + c) & keep;
+#pragma unroll
+            for (int t = 0; t < 8; t++) planes[t] |= ((code >> t) & 1u) << i;
+            if (++c == C) { c = 0; tap++; }
+        }
+        uint32_t* o = dst + m * bits * Kw + w;
+        for (int t = 0; t < bits; t++) o[(long long)t * Kw] = planes[t];
+    }
+}
+
+// [B][P][bits][Cw] -> [B][bits][P*Cw] word permutation; thread = one destination word
+__global__ void __launch_bounds__(256) flatten_packed_kernel(const uint32_t* __restrict__ src, int B, int P,
+                                                             int bits, int Cw, uint32_t* __restrict__ dst) {
+    const long long total = (long long)B * P * bits * Cw;
+    const long long rowlen = (long long)P * Cw;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long b = idx / (bits * rowlen);
+        long long r = idx - b * bits * rowlen;
+        const int t = (int)(r / rowlen);
+        r -= (long long)t * rowlen;
+        const int pix = (int)(r / Cw), w = (int)(r - (long long)pix * Cw);
+        dst[idx] = __ldg(src + (((b * P + pix) * bits + t) * Cw + w));
+    }
+}
+
 static int stream_grid(long long total, int sms) {
     long long blocks = (total + 255) / 256;
     long long cap = (long long)sms * 8;  // 8 resident 256-thread CTAs per SM, grid-stride beyond
@@ -200,6 +250,30 @@ cudaError_t launch_pool_quant_pack(const int32_t* Y, int B, int H, int W, int N,
     const long long total = (long long)B * Hp * Wp * Nw;
     if (total == 0) return cudaSuccess;
     pool_quant_pack_kernel<<<stream_grid(total * 32, sms), 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nw, e, out);
+    count_launch();
+    return cudaGetLastError();
+}
+}  // namespace apnn
+
+namespace apnn {
+cudaError_t launch_im2col_pack(const uint8_t* X, int B, int H, int W, int C, int R, int S, int stride, int pad,
+                               int Ho, int Wo, int bits, uint32_t* dst, int sms, cudaStream_t s) {
+    const int Kw = (R * S * C + 127) / 128 * 4;
+    const long long total = (long long)B * Ho * Wo * Kw;
+    if (total == 0) return cudaSuccess;
+    im2col_pack_kernel<<<stream_grid(total, sms), 256, 0, s>>>(X, B, H, W, C, R, S, stride, pad, Ho, Wo, bits, Kw,
+                                                               dst);
+    count_launch();
+    return cudaGetLastError();
+}
+}  // namespace apnn
+
+namespace apnn {
+cudaError_t launch_flatten_packed(const uint32_t* src, int B, int P, int bits, int Cw, uint32_t* dst, int sms,
+                                  cudaStream_t s) {
+    const long long total = (long long)B * P * bits * Cw;
+    if (total == 0) return cudaSuccess;
+    flatten_packed_kernel<<<stream_grid(total, sms), 256, 0, s>>>(src, B, P, bits, Cw, dst);
     count_launch();
     return cudaGetLastError();
 }

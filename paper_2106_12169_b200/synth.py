@@ -50,3 +50,103 @@ def epilogue_params(N: int, tag: str = "epi", alpha_range=(-3, 8), beta_range=(-
     alpha = g.integers(alpha_range[0], alpha_range[1] + 1, size=N, dtype=np.int32)
     beta = g.integers(beta_range[0], beta_range[1] + 1, size=N, dtype=np.int32)
     return alpha, beta
+
+
+# ------------------------------------------------------------------ end-to-end models (row f1)
+# Architectures of BASELINE.json configs[3]/[4] as plain layer tables (input shapes, no
+# arithmetic).  The paper names the models but not their layer tables;
+# these are the readings of DESIGN.md (R26): AlexNet = Krizhevsky's single-tower network,
+# VGG-Variant = the SURVEY §8(d) reading (unverified).  Every conv/FC of a model uses the
+# model's (w_bits, a_bits); the first layer consumes the image quantised to a_bits codes
+# (reading R23).  Pooling follows the conv it is attached to: (k, stride).
+#   conv: dict(kind="conv", Co, R, stride, pad, pool=(k, st) or None)
+#   fc:   dict(kind="fc", N)        (the first FC consumes the flattened HWC feature map)
+
+MODELS = {
+    "alexnet": dict(input=(224, 224, 3), classes=1000, layers=[
+        dict(kind="conv", Co=96, R=11, stride=4, pad=2, pool=(3, 2)),
+        dict(kind="conv", Co=256, R=5, stride=1, pad=2, pool=(3, 2)),
+        dict(kind="conv", Co=384, R=3, stride=1, pad=1, pool=None),
+        dict(kind="conv", Co=384, R=3, stride=1, pad=1, pool=None),
+        dict(kind="conv", Co=256, R=3, stride=1, pad=1, pool=(3, 2)),
+        dict(kind="fc", N=4096), dict(kind="fc", N=4096), dict(kind="fc", N=1000)]),
+    "vgg_variant": dict(input=(224, 224, 3), classes=1000, layers=[
+        dict(kind="conv", Co=96, R=7, stride=2, pad=3, pool=(2, 2)),
+        dict(kind="conv", Co=256, R=3, stride=1, pad=1, pool=None),
+        dict(kind="conv", Co=256, R=3, stride=1, pad=1, pool=None),
+        dict(kind="conv", Co=256, R=3, stride=1, pad=1, pool=(2, 2)),
+        dict(kind="conv", Co=384, R=3, stride=1, pad=1, pool=None),
+        dict(kind="conv", Co=384, R=3, stride=1, pad=1, pool=None),
+        dict(kind="conv", Co=384, R=3, stride=1, pad=1, pool=(2, 2)),
+        dict(kind="conv", Co=768, R=3, stride=1, pad=1, pool=None),
+        dict(kind="conv", Co=768, R=3, stride=1, pad=1, pool=None),
+        dict(kind="conv", Co=768, R=3, stride=1, pad=1, pool=(2, 2)),
+        dict(kind="fc", N=4096), dict(kind="fc", N=4096), dict(kind="fc", N=1000)]),
+}
+
+# (w_bits, a_bits) -> encoding: 1-bit weights are +-1 with 0/1 activations (Case III,
+# PAPER.md:1462-1476), otherwise both are unsigned 0/1 codes (Case I)
+def model_encoding(w_bits: int, a_bits: int) -> int:
+    return 2 if w_bits == 1 and a_bits > 1 else (1 if w_bits == 1 and a_bits == 1 else 0)
+
+
+def model_layers(name: str, batch: int):
+    """Layer table with every shape resolved: per layer dict(kind, B, H, W, C, Co, R, S,
+    stride, pad, Ho, Wo, pool, Hp, Wp, K) (fc layers: H = W = R = S = feature-map side,
+    i.e. the flattened map is one R x R tap window with pad 0)."""
+    m = MODELS[name]
+    H, W, C = m["input"]
+    out = []
+    for L in m["layers"]:
+        if L["kind"] == "conv":
+            R, st, pad = L["R"], L["stride"], L["pad"]
+            Ho, Wo = (H + 2 * pad - R) // st + 1, (W + 2 * pad - R) // st + 1
+            Hp, Wp = Ho, Wo
+            if L["pool"]:
+                k, ps = L["pool"]
+                Hp, Wp = (Ho - k) // ps + 1, (Wo - k) // ps + 1
+            out.append(dict(kind="conv", B=batch, H=H, W=W, C=C, Co=L["Co"], R=R, S=R, stride=st, pad=pad,
+                            Ho=Ho, Wo=Wo, pool=L["pool"], Hp=Hp, Wp=Wp, K=R * R * C))
+            H, W, C = Hp, Wp, L["Co"]
+        else:
+            out.append(dict(kind="fc", B=batch, H=H, W=W, C=C, Co=L["N"], R=H, S=W, stride=1, pad=0,
+                            Ho=1, Wo=1, pool=None, Hp=1, Wp=1, K=H * W * C))
+            H, W, C = 1, 1, L["N"]
+    return out
+
+
+def model_params(name: str, w_bits: int, a_bits: int, tag: str = "model"):
+    """Synthetic weights (OHWI codes [Co, R, S, C]) and a folded-BN requantisation per layer
+    (reading R12): alpha = 1, per-channel beta and a per-layer divisor S chosen from the
+    weights so that, for uniform input codes, alpha*y + beta spans [0, 4 sigma) and the
+    a_bits output codes are not degenerate.  Integer inputs to both the CUDA path and the
+    oracle; the last layer has no requantisation (int32 logits)."""
+    enc = model_encoding(w_bits, a_bits)
+    a_pm1 = enc == 1
+    w_pm1 = enc in (1, 2)
+    layers = model_layers(name, 1)
+    params = []
+    for i, L in enumerate(layers):
+        g = rng(f"{tag}:{name}:w{w_bits}a{a_bits}:{i}")
+        Wt = g.integers(0, 1 << w_bits, size=(L["Co"], L["R"], L["S"], L["C"]), dtype=np.uint8)
+        if i == len(layers) - 1:
+            params.append(dict(W=Wt, alpha=None, beta=None, S=None))
+            continue
+        wv = Wt.reshape(L["Co"], -1).astype(np.float64)
+        if w_pm1:
+            wv = 2 * wv - 1
+        ma, va = (0.0, 1.0) if a_pm1 else ((2 ** a_bits - 1) / 2, (4 ** a_bits - 1) / 12)
+        mu = ma * wv.sum(1)
+        sd = np.sqrt(va * (wv ** 2).sum(1)) + 1.0
+        S = int(max(1, np.ceil(4 * np.median(sd) / (1 << a_bits))))
+        # max pooling over k*k outputs shifts the level up by about E[max of k*k normals] sigma
+        shift = {1: 0.0, 4: 1.03, 9: 1.49}.get(L["pool"][0] ** 2 if L["pool"] else 1, 1.5)
+        beta = np.round((2 - shift) * sd - mu).astype(np.int32)
+        params.append(dict(W=Wt, alpha=np.ones(L["Co"], np.int32), beta=beta, S=S))
+    return params
+
+
+def model_input(name: str, batch: int, a_bits: int, tag: str = "img"):
+    """The image batch quantised to a_bits codes, NHWC uint8 (reading R23)."""
+    H, W, C = MODELS[name]["input"]
+    return codes((batch, H, W, C), a_bits, f"{tag}:{name}:{batch}:a{a_bits}")

@@ -341,6 +341,8 @@ POOL_CASES = [  # (B, H, W, C, Co, stride, pool, pool_stride, avg, fused expecte
     (2, 28, 28, 128, 96, 1, 2, 2, False, True),    # Wo = 28, ragged C_out
     (2, 16, 17, 64, 130, 1, 2, 2, False, True),    # odd Wo (last column dropped), N > 128
     (2, 56, 56, 64, 64, 1, 2, 2, False, True),     # ResNet-L1-sized map, conv_k = 2
+    (1, 14, 14, 128, 384, 1, 2, 2, False, True),   # several N tiles, the last one overhangs N
+    (1, 28, 28, 64, 768, 1, 2, 2, False, True),
     (3, 7, 7, 64, 40, 1, 2, 2, False, False),      # odd Ho -> unfused pair
     (1, 66, 66, 64, 32, 1, 2, 2, False, False),    # Wo > 64 -> unfused pair
     (2, 12, 12, 64, 64, 1, 3, 2, False, False),    # AlexNet-style 3x3/2 -> unfused

@@ -284,3 +284,52 @@ def test_oracle_independent_of_product():
                 src = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "apnn_oracle" not in src, f
+
+
+# ------------------------------------------------------------ end-to-end models (row f1)
+
+def test_model_tables_match_survey_shapes():
+    L = synth.model_layers("alexnet", 1)
+    assert [l["Hp"] for l in L[:5]] == [27, 13, 13, 13, 6] and L[5]["K"] == 9216   # 6*6*256
+    V = synth.model_layers("vgg_variant", 1)
+    assert V[0]["Ho"] == 112 and V[0]["Hp"] == 56 and V[10]["K"] == 37632           # 7*7*768
+    assert abs(sum(l["Ho"] * l["Wo"] * l["Co"] * l["K"] for l in L) / 1e9 - 1.135) < 0.01
+
+
+def test_model_runner_vs_torch_float64():
+    """oracle.models.run_model on a tiny layer table against torch float64 conv2d /
+    max_pool2d / linear with floor-and-clamp requantisation (exact at these magnitudes)."""
+    import torch
+    import torch.nn.functional as F
+    from oracle import models as om
+    layers = [dict(kind="conv", B=2, H=9, W=9, C=3, Co=8, R=3, S=3, stride=1, pad=1, pool=(2, 2), K=27),
+              dict(kind="conv", B=2, H=4, W=4, C=8, Co=6, R=3, S=3, stride=1, pad=1, pool=(3, 1), K=72),
+              dict(kind="fc", B=2, H=2, W=2, C=6, Co=5, R=2, S=2, stride=1, pad=0, pool=None, K=24),
+              dict(kind="fc", B=2, H=1, W=1, C=5, Co=4, R=1, S=1, stride=1, pad=0, pool=None, K=5)]
+    g = synth.rng("tinymodel")
+    params = []
+    for i, L in enumerate(layers):
+        Wt = g.integers(0, 2, size=(L["Co"], L["R"], L["S"], L["C"]), dtype=np.uint8)
+        if i == len(layers) - 1:
+            params.append(dict(W=Wt, alpha=None, beta=None, S=None))
+        else:
+            params.append(dict(W=Wt, alpha=g.integers(-2, 4, size=L["Co"]).astype(np.int32),
+                               beta=g.integers(-6, 9, size=L["Co"]).astype(np.int32), S=3))
+    x = synth.codes((2, 9, 9, 3), 2, "tinymodel:x")
+    got = om.run_model(layers, params, x, 1, 2, 2)
+    act = torch.from_numpy(x.astype(np.float64)).permute(0, 3, 1, 2)
+    for i, (L, P) in enumerate(zip(layers, params)):
+        w = 2.0 * torch.from_numpy(P["W"].astype(np.float64)) - 1.0          # +-1 weights (Case III)
+        if L["kind"] == "conv":
+            y = F.conv2d(act, w.permute(0, 3, 1, 2), stride=L["stride"], padding=L["pad"])
+        else:
+            y = (act.permute(0, 2, 3, 1).reshape(2, -1) @ w.reshape(L["Co"], -1).T)[:, :, None, None]
+        if i == len(layers) - 1:
+            want = y.reshape(2, -1).numpy()
+            break
+        v = y * torch.from_numpy(P["alpha"].astype(np.float64))[None, :, None, None] + \
+            torch.from_numpy(P["beta"].astype(np.float64))[None, :, None, None]
+        if L["pool"]:
+            v = F.max_pool2d(v, L["pool"][0], L["pool"][1])
+        act = torch.clamp(torch.floor(v / P["S"]), 0, 3)
+    np.testing.assert_array_equal(got, want.astype(np.int32))
