@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(256) quant_pack_kernel(const int32_t* __restri
                             (requant(e, v.w, epi_alpha(e, n + 3), epi_beta(e, n + 3)) << 24);
                 }
             } else {
-                for (int i = 0; i < 32; i++) {
+#pragma unroll
+                for (int i = 0; i < 32; i++) {  // static qb[] indices: no local-memory array
                     int n = n0 + i;
                     if (n < N) qb[i >> 2] |= requant(e, __ldg(src + i), epi_alpha(e, n), epi_beta(e, n))
                                              << (8 * (i & 3));
@@ -115,30 +116,32 @@ __global__ void __launch_bounds__(256) quant_pack_kernel(const int32_t* __restri
 // lane = channel (coalesced 128-byte loads, k*k independent loads per lane), and the
 // plane words are formed with __ballot_sync as in the paper's output packing
 // (PAPER.md:1582-1587).
+template <int KP>  // KP > 0: compile-time window (unrolled, all loads in flight); 0: runtime e.pool
 __global__ void __launch_bounds__(256) pool_quant_pack_kernel(const int32_t* __restrict__ Y, int B, int H, int W,
                                                               int N, int Hp, int Wp, int Nw, Epi e,
                                                               uint32_t* __restrict__ out) {
-    const long long total = (long long)B * Hp * Wp * Nw;  // warps of work
-    const int k = e.pool, st = e.pool_stride;
+    const int total = B * Hp * Wp * Nw;  // warps of work (host-checked < 2^31)
+    const int k = KP > 0 ? KP : e.pool, st = e.pool_stride;
     const int lane = threadIdx.x & 31;
-    const long long wstride = (long long)gridDim.x * (blockDim.x / 32);
-    for (long long idx = blockIdx.x * (long long)(blockDim.x / 32) + (threadIdx.x >> 5); idx < total;
-         idx += wstride) {
-        const long long pix = idx / Nw;
-        const int w = (int)(idx - pix * Nw);
-        const int b = (int)(pix / ((long long)Hp * Wp));
-        const int rem = (int)(pix - (long long)b * Hp * Wp);
+    const int wstride = gridDim.x * (blockDim.x >> 5);
+    for (int idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); idx < total; idx += wstride) {
+        const int pix = idx / Nw;
+        const int w = idx - pix * Nw;
+        const int b = pix / (Hp * Wp);
+        const int rem = pix - b * Hp * Wp;
         const int i = rem / Wp, j = rem - (rem / Wp) * Wp;
         const int n = w * 32 + lane;
         uint32_t q = 0;
         if (n < N) {
             const long long al = epi_alpha(e, n), be = epi_beta(e, n);
+            const int32_t* base = Y + (((long long)b * H + i * st) * W + j * st) * N + n;
             long long best = 0, sum = 0;
-            for (int r = 0; r < k; r++) {
-                const int32_t* row = Y + (((long long)b * H + i * st + r) * W + j * st) * N + n;
-                for (int s2 = 0; s2 < k; s2++) {
-                    const long long v = al * __ldg(row + (long long)s2 * N) + be;
-                    best = (r == 0 && s2 == 0) ? v : (v > best ? v : best);
+#pragma unroll
+            for (int rr = 0; rr < k; rr++) {
+#pragma unroll
+                for (int ss = 0; ss < k; ss++) {
+                    const long long v = al * __ldg(base + ((long long)rr * W + ss) * N) + be;
+                    best = (rr == 0 && ss == 0) ? v : (v > best ? v : best);
                     sum += v;
                 }
             }
@@ -150,45 +153,78 @@ __global__ void __launch_bounds__(256) pool_quant_pack_kernel(const int32_t* __r
             }
             q = quantise_v(e, P);
         }
-        uint32_t* o = out + pix * e.out_bits * Nw + w;
+        uint32_t* o = out + (long long)pix * e.out_bits * Nw + w;
+        uint32_t mine = 0;
         for (int t = 0; t < e.out_bits; t++) {
             const uint32_t word = __ballot_sync(0xFFFFFFFFu, (q >> t) & 1u);
-            if (lane == t) o[(long long)t * Nw] = word;
+            if (lane == t) mine = word;
         }
+        if (lane < e.out_bits) o[(long long)lane * Nw] = mine;
     }
 }
 
-// im2col + bit decomposition + packing of NHWC uint8 codes: one thread per (row, 32-element
-// word); element k = (r*S + s)*C + c of row (b, ho, wo); out-of-frame taps are code 0.
+// im2col + bit decomposition + packing of NHWC uint8 codes.  One CTA per output image
+// row (b, ho): the R input rows it needs are staged in shared memory with the zero
+// padding materialised (R x (W + 2 pad) x C bytes, coalesced 4-byte loads), then each
+// thread packs (pixel wo, word w) tasks: 32 consecutive elements k = (r*S + s)*C + c
+// walked with incremental counters (no per-element division), one shared-memory byte
+// read and `bits` shift-ors each; the CTA's Wo output rows are one contiguous range,
+// so the words are staged in shared memory and written out coalesced.
 __global__ void __launch_bounds__(256) im2col_pack_kernel(const uint8_t* __restrict__ X, int B, int H, int W,
                                                           int C, int R, int S, int stride, int pad, int Ho, int Wo,
                                                           int bits, int Kw, uint32_t* __restrict__ dst) {
-    const long long rows = (long long)B * Ho * Wo;
-    const long long total = rows * Kw;
+    extern __shared__ __align__(16) uint8_t sm[];
+    const int Wp = W + 2 * pad, rowb = Wp * C;       // padded input row bytes
+    uint8_t* rows = sm;                              // R x rowb
+    uint32_t* outw = reinterpret_cast<uint32_t*>(sm + ((R * rowb + 15) & ~15));  // Wo x bits x Kw
     const int K = R * S * C;
     const uint32_t keep = (1u << bits) - 1u;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const long long m = idx / Kw;
-        const int w = (int)(idx - m * Kw);
-        const int b = (int)(m / ((long long)Ho * Wo));
-        const int rem = (int)(m - (long long)b * Ho * Wo);
-        const int ho = rem / Wo, wo = rem - (rem / Wo) * Wo;
-        uint32_t planes[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        int k = w * 32;
-        int tap = k / C, c = k - tap * C;
-        for (int i = 0; i < 32 && k < K; i++, k++) {
-            const int r = tap / S, s2 = tap - (tap / S) * S;
-            const int hi = ho * stride + r - pad, wi = wo * stride + s2 - pad;
-            uint32_t code = 0;
-            if (hi >= 0 && hi < H && wi >= 0 && wi < W)
-                code = __ldg(X + (((long long)b * H + hi) * W + wi) * C + c) & keep;
-#pragma unroll
-            for (int t = 0; t < 8; t++) planes[t] |= ((code >> t) & 1u) << i;
-            if (++c == C) { c = 0; tap++; }
+    for (int br = blockIdx.x; br < B * Ho; br += gridDim.x) {
+        const int b = br / Ho, ho = br - b * Ho;
+        __syncthreads();  // previous row's smem readers are done
+        for (int i = threadIdx.x; i < R * Wp; i += blockDim.x) {  // one padded pixel (C bytes) per step
+            const int r = i / Wp, px = i - r * Wp;
+            const int hi = ho * stride - pad + r, wi = px - pad;
+            uint8_t* d = rows + r * rowb + px * C;
+            if (hi >= 0 && hi < H && wi >= 0 && wi < W) {
+                const uint8_t* src = X + (((long long)b * H + hi) * W + wi) * C;
+                for (int c = 0; c < C; c++) d[c] = __ldg(src + c) & keep;
+            } else {
+                for (int c = 0; c < C; c++) d[c] = 0;
+            }
         }
-        uint32_t* o = dst + m * bits * Kw + w;
-        for (int t = 0; t < bits; t++) o[(long long)t * Kw] = planes[t];
+        __syncthreads();
+        for (int task = threadIdx.x; task < Wo * Kw; task += blockDim.x) {
+            const int wo = task / Kw, w = task - wo * Kw;
+            int k = w * 32;
+            int r = k / (S * C), sc = k - r * S * C, s2 = sc / C, c = sc - s2 * C;
+            const uint8_t* base = rows + wo * stride * C;
+            uint32_t qb[8];  // byte i of qb[j] = code of element 4j + i (as in pack_bits_kernel)
+#pragma unroll
+            for (int j = 0; j < 8; j++) qb[j] = 0;
+#pragma unroll
+            for (int e = 0; e < 32; e++) {
+                if (k < K) qb[e >> 2] |= (uint32_t)base[r * rowb + s2 * C + c] << (8 * (e & 3));
+                k++;
+                if (++c == C) {
+                    c = 0;
+                    if (++s2 == S) { s2 = 0; r++; }
+                }
+            }
+            uint32_t* o = outw + wo * bits * Kw + w;
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                if (t < bits) {
+                    uint32_t word = 0;
+#pragma unroll
+                    for (int q = 0; q < 8; q++) word |= byte_bits_to_nibble(qb[q], t) << (4 * q);
+                    o[t * Kw] = word;
+                }
+            }
+        }
+        __syncthreads();
+        uint32_t* g = dst + (long long)br * Wo * bits * Kw;  // rows (b, ho, 0..Wo-1) are contiguous
+        for (int i = threadIdx.x; i < Wo * bits * Kw; i += blockDim.x) g[i] = outw[i];
     }
 }
 
@@ -249,7 +285,11 @@ cudaError_t launch_pool_quant_pack(const int32_t* Y, int B, int H, int W, int N,
     const int Nw = (N + 127) / 128 * 4;
     const long long total = (long long)B * Hp * Wp * Nw;
     if (total == 0) return cudaSuccess;
-    pool_quant_pack_kernel<<<stream_grid(total * 32, sms), 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nw, e, out);
+    if ((long long)B * Hp * Wp * Nw > 2147483647LL) return cudaErrorInvalidValue;
+    const int grid = stream_grid(total * 32, sms);
+    if (e.pool == 2) pool_quant_pack_kernel<2><<<grid, 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nw, e, out);
+    else if (e.pool == 3) pool_quant_pack_kernel<3><<<grid, 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nw, e, out);
+    else pool_quant_pack_kernel<0><<<grid, 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nw, e, out);
     count_launch();
     return cudaGetLastError();
 }
@@ -259,10 +299,18 @@ namespace apnn {
 cudaError_t launch_im2col_pack(const uint8_t* X, int B, int H, int W, int C, int R, int S, int stride, int pad,
                                int Ho, int Wo, int bits, uint32_t* dst, int sms, cudaStream_t s) {
     const int Kw = (R * S * C + 127) / 128 * 4;
-    const long long total = (long long)B * Ho * Wo * Kw;
+    const long long total = (long long)B * Ho * Wo;
     if (total == 0) return cudaSuccess;
-    im2col_pack_kernel<<<stream_grid(total, sms), 256, 0, s>>>(X, B, H, W, C, R, S, stride, pad, Ho, Wo, bits, Kw,
-                                                               dst);
+    const size_t smem = (((size_t)R * (W + 2 * pad) * C + 15) & ~(size_t)15) + (size_t)Wo * bits * Kw * 4;
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(im2col_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const long long ctas = (long long)B * Ho;
+    const int grid = (int)(ctas < (long long)sms * 4 ? ctas : (long long)sms * 4);
+    im2col_pack_kernel<<<grid, 256, smem, s>>>(X, B, H, W, C, R, S, stride, pad, Ho, Wo, bits, Kw, dst);
     count_launch();
     return cudaGetLastError();
 }
