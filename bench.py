@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-models", action="store_true")
+    ap.add_argument("--model-batch", type=int, default=256, help="global batch of the end-to-end models")
     return ap.parse_args()
 
 
@@ -186,6 +188,47 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------- end-to-end models
+def time_models(args, world, rank, dev, dist):
+    """BASELINE.json configs[3]: AlexNet and VGG-Variant w1a2 end-to-end inference, global
+    batch sharded over the ranks (strong scaling: each rank runs batch/world images), the
+    whole forward captured in one CUDA graph; latency = max over ranks of the best of 5
+    replays (CUDA events).  Row f1; the logits are checked against the oracle in
+    tests/test_models.py."""
+    import torch
+    from paper_2106_12169_b200 import synth
+    from paper_2106_12169_b200.models import APNNModel
+    out = {}
+    per = max(1, args.model_batch // world)
+    for name in ("alexnet", "vgg_variant"):
+        m = APNNModel(name, per, 1, 2, device=dev)
+        x = torch.from_numpy(synth.model_input(name, per, 2, tag=f"img-rank{rank}")).to(dev)
+        m.run(x)
+        m.capture()
+        for _ in range(3):
+            m.run()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = 1e30
+        for _ in range(5):
+            e0.record()
+            m.run()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            best = min(best, e0.elapsed_time(e1))
+        if dist is not None:
+            t = torch.tensor([best], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            best = float(t.item())
+        macs = m.macs_per_image() * per * world
+        out[f"{name}_w1a2"] = {"global_batch": per * world, "batch_per_gpu": per, "latency_ms": best,
+                               "images_per_s": per * world / (best * 1e-3),
+                               "effective_tops": 2.0 * macs / (best * 1e-3) / 1e12, "scaling": "strong",
+                               "timing": "CUDA graph of the whole forward, best of 5, max over ranks"}
+        del m
+    return out
+
+
 # ------------------------------------------------------------------------ ours
 def run_ours(args):
     import numpy as np
@@ -306,6 +349,8 @@ def run_ours(args):
                "h2d_bytes_per_step": int(A_host.numel()), "d2h_bytes_per_step": int(Y_host.numel() * 4),
                "steps": n_e2e}
 
+    models = None if args.no_models else time_models(args, world, rank, dev, dist)
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -339,6 +384,8 @@ def run_ours(args):
         "e2e": e2e,
         "gpu_launches": launches,
     }
+    if models is not None:
+        line["models"] = models
     if not args.no_cpu:
         line["cpu_baseline"] = oracle_sample(A_np, W_np, args, args.cpu_seconds, out_bits, alpha_np, beta_np, S)
     print(json.dumps(line), flush=True)
