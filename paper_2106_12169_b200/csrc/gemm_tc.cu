@@ -48,6 +48,10 @@ constexpr int T1_THREADS = 10 * 32;
 constexpr int MAX_STAGES = 8;     // operand stages (A in TMEM: 32 columns each)
 constexpr int MAX_PSTAGES = 16;   // packed-plane stages of the 2-CTA kernel
 constexpr int kStgWarpBytes = 8192;  // store staging per epilogue warp (1024-aligned)
+#ifndef APNN_PROD_LANES
+#define APNN_PROD_LANES 4
+#endif
+constexpr int kProdLanes = APNN_PROD_LANES;  // TMA-issuing lanes of the producer warp (2-CTA kernel)
 enum { kOutDirect = 0, kOutTma = 1, kOutLsu = 2 };
 
 struct Params {
@@ -257,38 +261,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
         // ---------------------------------------------------- TMA producer
         // (conv: one strided TMA box per output row of the tile and filter tap;
         //  out-of-frame pixels are zero-filled by the TMA unit)
+        // Lanes 0..kProdLanes-1 issue consecutive k-blocks side by side: one warp
+        // instruction carries kProdLanes expect_tx arrivals and box loads, which hides
+        // the ~200-cycle per-stage barrier round trip of a single issuing thread
+        // (scripts/tma_rate.cu: 330 -> 137 cycles per 128-row box with 4 lanes; the TMA
+        // unit then runs at about one 16-byte box row per cycle).
         const bool conv = g.conv;
-        if (lane == 0) {
-            int s = 0, tr_it = 0;
-            uint32_t ph = 0;
-            for (int tile = cid; tile < p.num_tiles; tile += ncl) {
+        const int my_tiles = p.num_tiles > cid ? (p.num_tiles - cid + ncl - 1) / ncl : 0;
+        const int total = my_tiles * nkb;
+        for (int base = 0; base < total; base += kProdLanes) {
+            const int it = base + lane;
+            if (lane < kProdLanes && it < total) {
+                const int s = it % SP;
+                const uint32_t ph = (uint32_t)(it / SP) & 1u;
+                const int ti = it / nkb, kb = it - ti * nkb;
+                const int tile = cid + ti * ncl;
                 const int ct = (tile % p.tiles_m) * 2 + rank;
                 const int m0 = ct * 128;
                 const int nr0 = (tile / p.tiles_m) * T2_BN + rank * BROWS;
-                for (int kb = 0; kb < nkb; kb++, s = (s + 1 == SP) ? 0 : s + 1, ph ^= (s == 0)) {
-                    mbar_wait(&plane_empty[s], ph ^ 1);
-                    trace_at(p, TR_PROD, tr_it++);
-                    const int rs = conv ? kb / g.CB : 0;
-                    const int cb = conv ? kb - rs * g.CB : kb;
-                    mbar_arrive_expect_tx(&plane_full[s], p.a_tx_bytes + p.b_bytes);
-                    uint8_t* adst = sApl + (size_t)s * p.a_bytes;
-                    if (!conv) {
-                        tma_load_4d(adst, &tmapA, &plane_full[s], kb * 4, m0, 0, 0);
-                    } else {
-                        const int r = rs / g.S, sx = rs - r * g.S;
-                        const int box_bytes = p.conv_box_stride;
-                        for (int i = 0; i < p.conv_nbox; i++) {
-                            int gr, wo0;
-                            if (p.conv_k > 0) { gr = ct * p.conv_k + i; wo0 = 0; }
-                            else { gr = ct / p.conv_segs; wo0 = (ct - gr * p.conv_segs) * 128; }
-                            const int b = gr / g.Ho, ho = gr - b * g.Ho;  // b >= B -> whole box out of bounds (zeros)
-                            tma_load_5d(adst + i * box_bytes, &tmapA, &plane_full[s], cb * 4,
-                                        wo0 * g.stride + sx - g.pad, 0, ho * g.stride + r - g.pad, b);
-                        }
+                mbar_wait(&plane_empty[s], ph ^ 1);
+                if (lane == 0) trace_at(p, TR_PROD, it);
+                const int rs = conv ? kb / g.CB : 0;
+                const int cb = conv ? kb - rs * g.CB : kb;
+                mbar_arrive_expect_tx(&plane_full[s], p.a_tx_bytes + p.b_bytes);
+                uint8_t* adst = sApl + (size_t)s * p.a_bytes;
+                if (!conv) {
+                    tma_load_4d(adst, &tmapA, &plane_full[s], kb * 4, m0, 0, 0);
+                } else {
+                    const int r = rs / g.S, sx = rs - r * g.S;
+                    const int box_bytes = p.conv_box_stride;
+                    for (int i = 0; i < p.conv_nbox; i++) {
+                        int gr, wo0;
+                        if (p.conv_k > 0) { gr = ct * p.conv_k + i; wo0 = 0; }
+                        else { gr = ct / p.conv_segs; wo0 = (ct - gr * p.conv_segs) * 128; }
+                        const int b = gr / g.Ho, ho = gr - b * g.Ho;  // b >= B -> whole box out of bounds (zeros)
+                        tma_load_5d(adst + i * box_bytes, &tmapA, &plane_full[s], cb * 4,
+                                    wo0 * g.stride + sx - g.pad, 0, ho * g.stride + r - g.pad, b);
                     }
-                    tma_load_4d(sBpl + (size_t)s * p.b_bytes, &tmapB, &plane_full[s], cb * 4, nr0, 0, rs);
                 }
+                tma_load_4d(sBpl + (size_t)s * p.b_bytes, &tmapB, &plane_full[s], cb * 4, nr0, 0, rs);
             }
+            __syncwarp();
         }
     } else if (warp == T2_MMA_WARP) {
         // ---------------------------------------------------- MMA issuer (CTA 0)
