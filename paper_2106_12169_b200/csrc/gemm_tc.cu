@@ -79,6 +79,8 @@ struct Params {
     //   conv_k = 0: a CTA tile is a 128-pixel segment of one output row (Wo > 128)
     int conv_k, conv_bw, conv_segs, conv_nbox;
     int conv_box_stride;  // bytes between row boxes in a plane stage (16*bw*bits rounded up to 128: TMA dst alignment)
+    int conv_merged;      // C_in <= 128: a pixel's planes are one contiguous record, fetched as ONE box row
+                          // ({4*bits words, pixels} box, smem [pixel][plane][16 B]) instead of bits rows
     uint32_t a_tx_bytes;  // bytes the A loads of one stage actually deliver (expect_tx; excludes slot padding)
     unsigned long long* trace;  // development trace (APNN_TRACE), nullptr normally
     int exp_nostore;            // experiment knob (APNN_EXP_NOSTORE): skip the epilogue stores
@@ -220,9 +222,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     uint64_t* plane_empty = bars + MAX_PSTAGES;                    // [MAX_PSTAGES]
     uint64_t* op_full = bars + 2 * MAX_PSTAGES;                    // [MAX_STAGES], used in CTA 0
     uint64_t* op_empty = op_full + MAX_STAGES;                     // [MAX_STAGES]
-    uint64_t* accum_full = op_empty + MAX_STAGES;
-    uint64_t* accum_empty = accum_full + 1;                        // used in CTA 0
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accum_empty + 1);
+    // accumulators: NACC = 2 TMEM buffers when the pair tile is <= 128 columns wide (the
+    // epilogue of tile i then overlaps the MMAs of tile i+1), else 1 (A stages fill the rest)
+    constexpr int NACC = T2_BN <= 128 ? 2 : 1;
+    uint64_t* accum_full = op_empty + MAX_STAGES;                  // [2]
+    uint64_t* accum_empty = accum_full + 2;                        // [2], used in CTA 0
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accum_empty + 2);
     volatile uint32_t* dep_slots = tmem_holder + 1;                // [T2_RECOMB_WARPS * 32]
 
     cta_stamp(p, 0);
@@ -244,8 +249,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             mbar_init(&op_full[s], 16);   // 8 recombination warps x 2 CTAs
             mbar_init(&op_empty[s], 1);
         }
-        mbar_init(accum_full, 1);
-        mbar_init(accum_empty, 8);        // 4 epilogue warps x 2 CTAs
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&accum_full[i], 1);
+            mbar_init(&accum_empty[i], 8);  // 4 epilogue warps x 2 CTAs
+        }
         fence_mbar_init();
     }
     if (warp == T2_MMA_WARP) tmem_alloc2(tmem_holder, p.tmem_cols);
@@ -295,8 +302,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                         if (p.conv_k > 0) { gr = ct * p.conv_k + i; wo0 = 0; }
                         else { gr = ct / p.conv_segs; wo0 = (ct - gr * p.conv_segs) * 128; }
                         const int b = gr / g.Ho, ho = gr - b * g.Ho;  // b >= B -> whole box out of bounds (zeros)
-                        tma_load_5d(adst + i * box_bytes, &tmapA, &plane_full[s], cb * 4,
-                                    wo0 * g.stride + sx - g.pad, 0, ho * g.stride + r - g.pad, b);
+                        if (p.conv_merged)
+                            tma_load_4d(adst + i * box_bytes, &tmapA, &plane_full[s], 0, wo0 * g.stride + sx - g.pad,
+                                        ho * g.stride + r - g.pad, b);
+                        else
+                            tma_load_5d(adst + i * box_bytes, &tmapA, &plane_full[s], cb * 4,
+                                        wo0 * g.stride + sx - g.pad, 0, ho * g.stride + r - g.pad, b);
                     }
                 }
                 tma_load_4d(sBpl + (size_t)s * p.b_bytes, &tmapB, &plane_full[s], cb * 4, nr0, 0, rs);
@@ -312,7 +323,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             int s = 0, tc = 0;
             uint32_t ph = 0;
             for (int tile = cid; tile < p.num_tiles; tile += ncl, tc++) {
-                mbar_wait_cluster(accum_empty, (tc & 1) ^ 1);
+                const int buf = tc % NACC;
+                const uint32_t dtm = tmem + (uint32_t)(buf * T2_BN);
+                mbar_wait_cluster(&accum_empty[buf], ((tc / NACC) & 1) ^ 1);
                 tc_fence_after();
                 for (int kb = 0; kb < nkb; kb++) {
                     mbar_wait_cluster(&op_full[s], ph);
@@ -322,12 +335,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                     const uint32_t as = a_col0 + s * 32;
 #pragma unroll
                     for (int kk = 0; kk < 4; kk++)
-                        mma2_i8_ts(tmem, as + kk * 8, bd + (uint64_t)(kk * kBDescKStep), idesc, (kb | kk) != 0);
+                        mma2_i8_ts(dtm, as + kk * 8, bd + (uint64_t)(kk * kBDescKStep), idesc, (kb | kk) != 0);
                     mma2_commit_mc(&op_empty[s], 0x3);
                     trace_at(p, TR_MMA_ISSUED, tc * nkb + kb);
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
-                mma2_commit_mc(accum_full, 0x3);
+                mma2_commit_mc(&accum_full[buf], 0x3);
             }
         }
     } else if (warp < T2_EPI0) {
@@ -374,13 +387,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 mbar_wait(&plane_full[ps], pph);
                 if (warp == 0 && lane == 0) trace_at(p, TR_A_PLANE, it >> 1);
                 if (grp == 0) {
-                    recomb_step_any<A_PM1, true, SCALED>(g.a_bits, sApl + (size_t)ps * p.a_bytes + a_box_off, a_rows,
+                    recomb_step_any<A_PM1, true, SCALED>(g.a_bits, sApl + (size_t)ps * p.a_bytes + a_box_off,
+                                                         p.conv_merged ? 1 : a_rows, p.conv_merged ? g.a_bits : 1,
                                                          a_row, &plane_empty[ps],
                                                  &op_empty[s], ph ^ 1, tmem_lane + A_COL + s * 32, nullptr, kvalid,
                                                  lane, dep_slots + threadIdx.x);
                     tmem_wait_st();
                 } else if (t < BROWS) {  // warp-uniform: BROWS is a multiple of 32
-                    recomb_step_any<W_PM1, false, SCALED>(g.w_bits, sBpl + (size_t)ps * p.b_bytes, BROWS, t,
+                    recomb_step_any<W_PM1, false, SCALED>(g.w_bits, sBpl + (size_t)ps * p.b_bytes, BROWS, 1, t,
                                                           &plane_empty[ps], &op_empty[s], ph ^ 1, 0,
                                                           sBop + (size_t)s * BOP_STAGE, 128, lane,
                                                           dep_slots + threadIdx.x);
@@ -413,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
         const int t = q * 32 + lane;               // row in this CTA's 128
         const int et = threadIdx.x - T2_EPI0 * 32;  // 0..127
         const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
-        const uint32_t accum_empty0 = mapa(smem_u32(accum_empty), 0);
+        const uint32_t accum_empty0 = mapa(smem_u32(accum_empty), 0);  // + 8 * buf
         const int ob = p.e.out_bits;
         uint8_t* stg = sStg + q * p.stg_warp;
         const uint32_t stg_addr = smem_u32(stg);
@@ -438,13 +452,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 if (lane == 0) bulk_wait_read<0>();
                 __syncwarp();
             }
-            mbar_wait(accum_full, tc & 1);
+            const int buf = tc % NACC;
+            mbar_wait(&accum_full[buf], (tc / NACC) & 1);
             if (warp == T2_EPI0 && lane == 0) trace_at(p, TR_EPI_FULL, tc);
             tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < T2_BN; c += 32) {
                 uint32_t acc[32];
-                tmem_ld32(tmem_lane + c, acc);
+                tmem_ld32(tmem_lane + (uint32_t)(buf * T2_BN) + c, acc);
                 tmem_wait_ld();
                 if (SCALED) {
 #pragma unroll
@@ -488,7 +503,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(accum_empty0);
+            if (lane == 0) mbar_arrive_cluster(accum_empty0 + 8u * (uint32_t)buf);
             if (p.pool_fused) {
                 pool_pad_words(n0 + T2_BN, t, len, mb, g, p);
             } else if (ob && any && !p.exp_nostore) {
@@ -884,6 +899,25 @@ static bool make_out_map_packed(CUtensorMap* m, void* Y, int M, int Nw, int bits
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// C_in <= 128 (one channel block): the pixel record [bits][4 words] is contiguous, so
+// the activations are viewed as a 4-D tensor {4*bits words, W, H, B} and one box row is
+// a whole pixel (bits x 16 B): half (a2) to an eighth (a8) of the box rows of the
+// plane-wise map, and the TMA unit's cost is per box row (scripts/tma_rate.cu).
+static bool make_conv_act_map_merged(CUtensorMap* m, const uint32_t* base, const Geom& g, int bw) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    const cuuint64_t pix = (cuuint64_t)g.a_bits * g.Cw * 4;
+    cuuint64_t dims[4] = {(cuuint64_t)g.a_bits * g.Cw, (cuuint64_t)g.W, (cuuint64_t)g.H,
+                          (cuuint64_t)(g.M / (g.Ho * g.Wo))};
+    cuuint64_t strides[3] = {pix, pix * g.W, pix * g.W * g.H};
+    cuuint32_t box[4] = {(cuuint32_t)(g.a_bits * g.Cw), (cuuint32_t)(bw * g.stride), 1, 1};
+    cuuint32_t estr[4] = {1, (cuuint32_t)g.stride, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint32_t*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 static int stage_count(size_t per_stage, size_t fixed) {
     const size_t budget = 227 * 1024 - fixed;
     int S = (int)(budget / per_stage);
@@ -988,6 +1022,17 @@ static int epi_store_mode(bool packed) {
     return v >= 0 ? v : (packed ? tc::kOutLsu : tc::kOutTma);
 }
 
+// merged pixel-record boxes for C_in <= 128 convs (experiment knob APNN_CONV_MERGE=0 disables)
+constexpr int kMergedMaxBits = 4;  // [pixel][plane] rows of 16 B: up to 4-way LDS conflicts
+static bool conv_merge_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("APNN_CONV_MERGE");
+        v = s ? atoi(s) : 1;
+    }
+    return v != 0;
+}
+
 // largest split-K cluster (experiment knob APNN_SPLITZ).  Default 4: the paper's FC layer
 // (M = 64, N = K = 1024, w1a2) measured 10.1 / 7.9 / 8.1 us at Z = 1 / 4 / 8.
 static int split_zmax() {
@@ -1029,6 +1074,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     p.out_mode = kOutDirect;
     p.nwb = 0;
     p.ksplit = 1;
+    p.conv_merged = 0;
     p.pool_fused = e.pool ? 1 : 0;  // the ABI only forwards fusable pooling (tc_i8_pool_fusable)
     p.Hp = g.Ho / 2;
     p.Wp = g.Wo / 2;
@@ -1078,7 +1124,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
             if (p.pool_fused && sw < 2048) sw = 2048;
             p.stg_warp = sw;
         }
-        const size_t fixed = (size_t)256 * kTabStride * 4 + (2 * MAX_PSTAGES + 2 * MAX_STAGES + 4) * 8 +
+        const size_t fixed = (size_t)256 * kTabStride * 4 + (2 * MAX_PSTAGES + 2 * MAX_STAGES + 6) * 8 +
                              T2_RECOMB_WARPS * 32 * 4 + 4 * (size_t)p.stg_warp + 1024;
         const size_t budget = 227 * 1024 - fixed;
         const size_t op_stage = (size_t)brows * 128, pl_stage = p.a_bytes + p.b_bytes;
@@ -1133,7 +1179,10 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         if (clusters > p.num_tiles) clusters = p.num_tiles;
         const size_t smem = (size_t)S * op_stage + (size_t)SP * pl_stage + fixed - 1024 + 64;
         if (g.conv) {
-            if (!make_conv_act_map(&ta, A, g, p.conv_bw)) return cudaErrorInvalidValue;
+            p.conv_merged = (g.CB == 1 && g.a_bits <= kMergedMaxBits && conv_merge_enabled()) ? 1 : 0;
+            if (p.conv_merged ? !make_conv_act_map_merged(&ta, A, g, p.conv_bw)
+                              : !make_conv_act_map(&ta, A, g, p.conv_bw))
+                return cudaErrorInvalidValue;
         } else if (!make_plane_map(&ta, A, g.M, g.a_bits, g.Cw, 1, 128)) {
             return cudaErrorInvalidValue;
         }

@@ -180,14 +180,18 @@ __device__ __forceinline__ void b_job(const uint8_t* planes, int rows, int row, 
 // right after issuing the LDS raced with the TMA refill: whole rows read the next
 // use of the stage), release the plane stage (the TMA can refill it), then wait
 // for the operand stage to be free and store.
+// Plane pl of row `row` is the 16-byte chunk src[pl * pstride + row * rstride] of the
+// stage: [plane][row][16 B] (pstride = rows, rstride = 1; GEMM and the W operand) or
+// [row][plane][16 B] (pstride = 1, rstride = NB; conv rows fetched as whole pixel records).
 template <int NB, bool PM1, bool IS_A, bool SCALED>
-__device__ __forceinline__ void recomb_step(const uint8_t* planes, int rows, int row, uint64_t* plane_empty,
-                                            uint64_t* op_empty, uint32_t op_parity, uint32_t taddr, uint8_t* bop,
-                                            int kvalid, int lane, volatile uint32_t* dep_slot) {
+__device__ __forceinline__ void recomb_step(const uint8_t* planes, int pstride, int rstride, int row,
+                                            uint64_t* plane_empty, uint64_t* op_empty, uint32_t op_parity,
+                                            uint32_t taddr, uint8_t* bop, int kvalid, int lane,
+                                            volatile uint32_t* dep_slot) {
     const uint4* src = reinterpret_cast<const uint4*>(planes);
     uint4 v[NB];
 #pragma unroll
-    for (int pl = 0; pl < NB; pl++) v[pl] = src[pl * rows + row];
+    for (int pl = 0; pl < NB; pl++) v[pl] = src[pl * pstride + row * rstride];
     // The release below must not overtake the plane loads: neither mbarrier.arrive's
     // release semantics nor program order make the hardware wait for in-flight LDS.
     // A store of a value that depends on one register of every LDS.128 forces all of
@@ -219,12 +223,12 @@ __device__ __forceinline__ void recomb_step(const uint8_t* planes, int rows, int
 }
 
 template <bool PM1, bool IS_A, bool SCALED>
-__device__ __forceinline__ void recomb_step_any(int nb, const uint8_t* planes, int rows, int row,
+__device__ __forceinline__ void recomb_step_any(int nb, const uint8_t* planes, int pstride, int rstride, int row,
                                                 uint64_t* plane_empty, uint64_t* op_empty, uint32_t op_parity,
                                                 uint32_t taddr, uint8_t* bop, int kvalid, int lane,
                                                 volatile uint32_t* dep_slot) {
-#define APNN_RS(N_) recomb_step<N_, PM1, IS_A, SCALED>(planes, rows, row, plane_empty, op_empty, op_parity, taddr, bop, kvalid, lane, dep_slot)
-    if (PM1) { recomb_step<1, true, IS_A, SCALED>(planes, rows, row, plane_empty, op_empty, op_parity, taddr, bop, kvalid, lane, dep_slot); return; }
+#define APNN_RS(N_) recomb_step<N_, PM1, IS_A, SCALED>(planes, pstride, rstride, row, plane_empty, op_empty, op_parity, taddr, bop, kvalid, lane, dep_slot)
+    if (PM1) { recomb_step<1, true, IS_A, SCALED>(planes, pstride, rstride, row, plane_empty, op_empty, op_parity, taddr, bop, kvalid, lane, dep_slot); return; }
     switch (nb) {  // warp-uniform
     case 1: APNN_RS(1); break;
     case 2: APNN_RS(2); break;
