@@ -208,6 +208,21 @@ apnn_status apnn_quant_pack_out(const int32_t *Y, int M, int N, const apnn_epilo
 apnn_status apnn_pool_quant_pack_out(const int32_t *Y, int B, int H, int W, int N,
                                      const apnn_epilogue *epi, uint32_t *out, apnn_stream_t stream);
 
+/* Residual element-wise routine (ResNet basic block; reading R24 -- the paper does not
+ * describe residual connections): the shortcut is added to the folded-BN value before
+ * the quantisation,
+ *   v = alpha[n] * Y[m][n] + beta[n] + rho[n] * Z[m][n]
+ *   q = clamp(floor(v / divisor), 0, 2^out_bits - 1)   -> packed like apnn_quant_pack_out
+ *   Y:  device int32 [M][N] (the block's second conv)
+ *   Z:  the shortcut, either device int32 [M][N] (z_bits = 0: a 1x1 downsample conv's
+ *       accumulator) or device packed codes [M][z_bits][roundup(N,128)/32] (z_bits 1..8:
+ *       the block input itself, 0/1 codes)
+ *   rho: device int32 [N] or NULL (= 1);  epi: host, pool must be 0.
+ *   out: device packed [M][out_bits][roundup(N,128)/32]. */
+apnn_status apnn_residual_quant_pack(const int32_t *Y, int M, int N, const void *Z, int z_bits,
+                                     const int32_t *rho, const apnn_epilogue *epi, uint32_t *out,
+                                     apnn_stream_t stream);
+
 /* Which variant APNN_VARIANT_AUTO resolves to for this problem (no launch). */
 apnn_variant apnn_select_variant(int M, int N, int K, int a_bits, int w_bits, apnn_encoding enc);
 

@@ -169,6 +169,20 @@ def pool_epilogue(Y, alpha, beta, S, out_bits, k, stride=None, avg=False):
     return q
 
 
+def residual_epilogue(Y, Z, alpha, beta, rho, S, out_bits):
+    """Residual requantisation (reading R24; ResNet blocks are not described in the paper):
+    v = alpha[n]*Y + beta[n] + rho[n]*Z in int64, q = clamp(floor(v / S), 0, 2^out_bits - 1).
+    Y, Z: [M, N] integers (Z = shortcut codes or a 1x1 conv accumulator)."""
+    Y = np.asarray(Y, dtype=np.int64)
+    Z = np.asarray(Z, dtype=np.int64)
+    N = Y.shape[-1]
+    a = np.ones(N, np.int64) if alpha is None else np.asarray(alpha, np.int64)
+    b = np.zeros(N, np.int64) if beta is None else np.asarray(beta, np.int64)
+    r = np.ones(N, np.int64) if rho is None else np.asarray(rho, np.int64)
+    v = a * Y + b + r * Z
+    return np.clip(v // int(S), 0, (1 << out_bits) - 1).astype(np.uint8)  # // floors toward -inf
+
+
 def pack(codes, bits):
     """Codes [rows, K] -> packed planes uint32 [rows, bits, roundup(K,128)/32]."""
     codes = _u8(codes)

@@ -90,3 +90,71 @@ def calibrate(layers, params, x, w_bits, a_bits, enc, threads=0):
         else:
             act = epilogue(Y.reshape(-1, L["Co"]), alpha, beta, S, a_bits).reshape(Y.shape)
     return out
+
+
+def run_resnet18(ops, params, x, w_bits, a_bits, enc, threads=0, trace=None):
+    """ResNet-18 in the oracle (synth.resnet18_ops / resnet18_params): basic blocks with the
+    shortcut added before the residual requantisation (reading R24)."""
+    from . import residual_epilogue
+    act = np.ascontiguousarray(x, dtype=np.uint8)
+    B = act.shape[0]
+    for (kind, op), P in zip(ops, params):
+        if kind == "stem":
+            Y = conv2d(act, P["W"], op["stride"], op["pad"], a_bits, w_bits, enc, threads=threads)
+            act = pool_epilogue(Y, P["alpha"], P["beta"], P["S"], a_bits, op["pool"][0], op["pool"][1])
+        elif kind == "block":
+            La, Lb, Ld = op["a"], op["b"], op["down"]
+            Ya = conv2d(act, P["Wa"], La["stride"], La["pad"], a_bits, w_bits, enc, threads=threads)
+            qa = epilogue(Ya.reshape(-1, La["Co"]), P["alpha_a"], P["beta_a"], P["S_a"], a_bits).reshape(Ya.shape)
+            Yb = conv2d(qa, P["Wb"], 1, 1, a_bits, w_bits, enc, threads=threads)
+            Z = act if Ld is None else conv2d(act, P["Wd"], Ld["stride"], 0, a_bits, w_bits, enc, threads=threads)
+            C = Lb["Co"]
+            act = residual_epilogue(Yb.reshape(-1, C), Z.reshape(-1, C), P["alpha"], P["beta"], P["rho"], P["S"],
+                                    a_bits).reshape(Yb.shape)
+        else:
+            return gemm(act.reshape(B, -1), P["W"].reshape(op["Co"], -1), a_bits, w_bits, enc, threads=threads)
+        if trace is not None:
+            trace.append(act)
+    raise ValueError("no classifier")
+
+
+def calibrate_resnet18(ops, params, x, w_bits, a_bits, enc, threads=0):
+    """calibrate() for ResNet-18: per-channel median centring of every requantisation
+    (stem pooled values, conv_a outputs, y_b + rho*shortcut) on one input batch."""
+    from . import residual_epilogue
+
+    def center(V, Co):
+        V = V.reshape(-1, Co).astype(np.int64)
+        if V.shape[0] >= 16:
+            med = np.median(V, axis=0)
+            spread = np.percentile(V, 90, axis=0) - np.percentile(V, 10, axis=0)
+        else:
+            med, spread = np.full(Co, np.median(V)), np.full(Co, np.percentile(V, 90) - np.percentile(V, 10))
+        S = int(max(1, np.ceil(np.median(spread) / (1 << a_bits))))
+        return np.ones(Co, np.int32), np.round(-med + (1 << (a_bits - 1)) * S).astype(np.int32), S
+
+    act = np.ascontiguousarray(x, dtype=np.uint8)
+    out = []
+    for (kind, op), P in zip(ops, params):
+        P = dict(P)
+        if kind == "stem":
+            Y = conv2d(act, P["W"], op["stride"], op["pad"], a_bits, w_bits, enc, threads=threads)
+            Y64 = Y.astype(np.int64)
+            pooled = np.maximum(np.maximum(Y64[:, 0::2, 0::2], Y64[:, 0::2, 1::2]),
+                                np.maximum(Y64[:, 1::2, 0::2], Y64[:, 1::2, 1::2]))
+            P["alpha"], P["beta"], P["S"] = center(pooled, op["Co"])
+            act = pool_epilogue(Y, P["alpha"], P["beta"], P["S"], a_bits, 2, 2)
+        elif kind == "block":
+            La, Lb, Ld = op["a"], op["b"], op["down"]
+            Ya = conv2d(act, P["Wa"], La["stride"], La["pad"], a_bits, w_bits, enc, threads=threads)
+            P["alpha_a"], P["beta_a"], P["S_a"] = center(Ya, La["Co"])
+            qa = epilogue(Ya.reshape(-1, La["Co"]), P["alpha_a"], P["beta_a"], P["S_a"], a_bits).reshape(Ya.shape)
+            Yb = conv2d(qa, P["Wb"], 1, 1, a_bits, w_bits, enc, threads=threads)
+            Z = act if Ld is None else conv2d(act, P["Wd"], Ld["stride"], 0, a_bits, w_bits, enc, threads=threads)
+            C = Lb["Co"]
+            V = Yb.reshape(-1, C).astype(np.int64) + P["rho"].astype(np.int64) * Z.reshape(-1, C)
+            P["alpha"], P["beta"], P["S"] = center(V, C)
+            act = residual_epilogue(Yb.reshape(-1, C), Z.reshape(-1, C), P["alpha"], P["beta"], P["rho"], P["S"],
+                                    a_bits).reshape(Yb.shape)
+        out.append(P)
+    return out

@@ -71,6 +71,8 @@ def lib() -> ctypes.CDLL:
             L.apnn_packed_bytes.restype = ctypes.c_size_t
             L.apnn_pack_bits.argtypes = [vp, ci, ci, ci, vp, vp]
             L.apnn_pack_bits.restype = st
+            L.apnn_residual_quant_pack.argtypes = [vp, ci, ci, vp, ci, vp, ctypes.POINTER(_Epi), vp, vp]
+            L.apnn_residual_quant_pack.restype = st
             L.apnn_flatten_packed.argtypes = [vp, ci, ci, ci, ci, vp, vp]
             L.apnn_flatten_packed.restype = st
             L.apnn_im2col_pack.argtypes = [vp, ctypes.POINTER(_Conv), ci, vp, vp]
@@ -106,6 +108,7 @@ def lib() -> ctypes.CDLL:
 
 ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_im2col_pack", "apnn_flatten_packed", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
                "apnn_conv2d", "apnn_conv2d_ex", "apnn_quant_pack_out", "apnn_pool_quant_pack_out",
+               "apnn_residual_quant_pack",
                "apnn_select_variant",
                "apnn_status_string", "apnn_variant_name", "apnn_launch_count", "apnn_version")
 
@@ -306,6 +309,25 @@ def pool_quant_pack_out(Y: torch.Tensor, epi: Epilogue, out: Optional[torch.Tens
     _cuda(out, "out", torch.int32)
     _check(lib().apnn_pool_quant_pack_out(_ptr(Y), B, H, Wd, N, ctypes.byref(epi._c()), _ptr(out), _stream(Y)),
            "apnn_pool_quant_pack_out")
+    return out
+
+
+def residual_quant_pack(Y: torch.Tensor, Z: torch.Tensor, z_bits: int, epi: Epilogue,
+                        rho: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """q = requant(alpha*Y + beta + rho*Z) packed (apnn_residual_quant_pack).  Y int32 [M, N];
+    Z int32 [M, N] (z_bits = 0) or packed codes [M, z_bits, Kw(N)]."""
+    _cuda(Y, "Y", torch.int32)
+    _cuda(Z, "Z", torch.int32)
+    if rho is not None:
+        _cuda(rho, "rho", torch.int32)
+    N = Y.shape[-1]
+    Y2 = Y.reshape(-1, N)  # NHWC conv output -> [B*H*W, N]
+    M = Y2.shape[0]
+    if out is None:
+        out = torch.empty(packed_shape(M, N, epi.out_bits), dtype=torch.int32, device=Y.device)
+    _cuda(out, "out", torch.int32)
+    _check(lib().apnn_residual_quant_pack(_ptr(Y2), M, N, _ptr(Z), z_bits, _ptr(rho), ctypes.byref(epi._c()),
+                                          _ptr(out), _stream(Y)), "apnn_residual_quant_pack")
     return out
 
 

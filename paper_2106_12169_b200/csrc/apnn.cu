@@ -21,6 +21,8 @@ cudaError_t launch_quant_pack(const int32_t* Y, int M, int N, const Epi& e, uint
 cudaError_t launch_pool_quant_pack(const int32_t* Y, int B, int H, int W, int N, const Epi& e, uint32_t* out,
                                   int sms, cudaStream_t s);
 bool tc_i8_pool_fusable(const Geom& g, const Epi& e);
+cudaError_t launch_residual_quant_pack(const int32_t* Y, int M, int N, const void* Z, int z_bits,
+                                       const int32_t* rho, const Epi& e, uint32_t* out, int sms, cudaStream_t s);
 cudaError_t launch_flatten_packed(const uint32_t* src, int B, int P, int bits, int Cw, uint32_t* dst, int sms,
                                   cudaStream_t s);
 cudaError_t launch_im2col_pack(const uint8_t* X, int B, int H, int W, int C, int R, int S, int stride, int pad,
@@ -315,6 +317,24 @@ apnn_status apnn_pool_quant_pack_out(const int32_t* Y, int B, int H, int W, int 
     DevInfo d;
     if ((st = device_info(&d)) != APNN_OK) return st;
     cudaError_t err = launch_pool_quant_pack(Y, B, H, W, N, e, out, d.sms, (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_status apnn_residual_quant_pack(const int32_t* Y, int M, int N, const void* Z, int z_bits,
+                                     const int32_t* rho, const apnn_epilogue* epi, uint32_t* out,
+                                     apnn_stream_t stream) {
+    if (M < 0 || N < 0) return APNN_ERR_SHAPE;
+    if (!epi) return APNN_ERR_INVALID_ARG;
+    if (z_bits < 0 || z_bits > 8) return APNN_ERR_BITS;
+    if ((M > 0 && N > 0 && (!Y || !Z)) || (M > 0 && !out)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(Y) || !aligned16(Z) || !aligned16(out) || (rho && !aligned16(rho))) return APNN_ERR_ALIGNMENT;
+    Epi e;
+    apnn_status st = make_epi(epi, &e);
+    if (st != APNN_OK) return st;
+    if (e.pool) return APNN_ERR_INVALID_ARG;
+    DevInfo d;
+    if ((st = device_info(&d)) != APNN_OK) return st;
+    cudaError_t err = launch_residual_quant_pack(Y, M, N, Z, z_bits, rho, e, out, d.sms, (cudaStream_t)stream);
     return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }
 

@@ -244,6 +244,44 @@ __global__ void __launch_bounds__(256) flatten_packed_kernel(const uint32_t* __r
     }
 }
 
+// Residual routine: one warp per (row, 32-column word), lane = column (coalesced int32
+// loads), ballot packing.  v = alpha*y + beta + rho*z in int64 (reading R24).
+__global__ void __launch_bounds__(256) residual_quant_pack_kernel(const int32_t* __restrict__ Y, int M, int N,
+                                                                  const void* __restrict__ Z, int z_bits,
+                                                                  const int32_t* __restrict__ rho, int Nw, Epi e,
+                                                                  uint32_t* __restrict__ out) {
+    const long long total = (long long)M * Nw;
+    const int lane = threadIdx.x & 31;
+    const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long idx = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); idx < total;
+         idx += wstride) {
+        const long long m = idx / Nw;
+        const int w = (int)(idx - m * Nw);
+        const int n = w * 32 + lane;
+        uint32_t q = 0;
+        if (n < N) {
+            long long z;
+            if (z_bits == 0) {
+                z = __ldg(reinterpret_cast<const int32_t*>(Z) + m * N + n);
+            } else {
+                const uint32_t* zp = reinterpret_cast<const uint32_t*>(Z) + m * z_bits * Nw + w;
+                uint32_t code = 0;
+                for (int t = 0; t < z_bits; t++) code |= ((__ldg(zp + (long long)t * Nw) >> lane) & 1u) << t;
+                z = code;
+            }
+            const long long r = rho ? __ldg(rho + n) : 1;
+            const long long v = (long long)epi_alpha(e, n) * __ldg(Y + m * N + n) + epi_beta(e, n) + r * z;
+            q = quantise_v(e, v);
+        }
+        uint32_t mine = 0;
+        for (int t = 0; t < e.out_bits; t++) {
+            const uint32_t word = __ballot_sync(0xFFFFFFFFu, (q >> t) & 1u);
+            if (lane == t) mine = word;
+        }
+        if (lane < e.out_bits) out[(m * e.out_bits + lane) * Nw + w] = mine;
+    }
+}
+
 static int stream_grid(long long total, int sms) {
     long long blocks = (total + 255) / 256;
     long long cap = (long long)sms * 8;  // 8 resident 256-thread CTAs per SM, grid-stride beyond
@@ -322,6 +360,18 @@ cudaError_t launch_flatten_packed(const uint32_t* src, int B, int P, int bits, i
     const long long total = (long long)B * P * bits * Cw;
     if (total == 0) return cudaSuccess;
     flatten_packed_kernel<<<stream_grid(total, sms), 256, 0, s>>>(src, B, P, bits, Cw, dst);
+    count_launch();
+    return cudaGetLastError();
+}
+}  // namespace apnn
+
+namespace apnn {
+cudaError_t launch_residual_quant_pack(const int32_t* Y, int M, int N, const void* Z, int z_bits,
+                                       const int32_t* rho, const Epi& e, uint32_t* out, int sms, cudaStream_t s) {
+    const int Nw = (N + 127) / 128 * 4;
+    const long long total = (long long)M * Nw;
+    if (total == 0) return cudaSuccess;
+    residual_quant_pack_kernel<<<stream_grid(total * 32, sms), 256, 0, s>>>(Y, M, N, Z, z_bits, rho, Nw, e, out);
     count_launch();
     return cudaGetLastError();
 }

@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import (ConvShape, Epilogue, conv2d, flatten_packed, gemm, im2col_pack, pack_bits, pool_quant_pack_out,
-               synth)
+               residual_quant_pack, synth)
 
 
 class APNNModel:
@@ -135,3 +135,101 @@ class APNNModel:
 
     def macs_per_image(self) -> int:
         return sum(L["Ho"] * L["Wo"] * L["Co"] * L["K"] for L in synth.model_layers(self.name, 1))
+
+
+class APNNResNet18:
+    """ResNet-18 (BASELINE.json configs[4]; synth.resnet18_ops, reading R24) over the C ABI:
+    stem = im2col GEMM (int32) + 2x2 pooling routine; basic block = conv_a with the fused
+    requantisation, conv_b (int32), the shortcut (the block input's packed codes, or a 1x1
+    stride-s downsample conv's int32 accumulator) and apnn_residual_quant_pack; head =
+    flatten + FC (int32 logits).  Static buffers; capture()/run() as APNNModel."""
+
+    def __init__(self, batch: int, w_bits: int, a_bits: int, device="cuda", params=None):
+        self.B, self.w_bits, self.a_bits = batch, w_bits, a_bits
+        self.name = "resnet18"
+        self.dev = torch.device(device)
+        self.enc = synth.model_encoding(w_bits, a_bits)
+        self.ops = synth.resnet18_ops(batch)
+        params = params if params is not None else synth.resnet18_params(w_bits, a_bits)
+        d, a = self.dev, a_bits
+
+        def t(x):
+            return torch.from_numpy(np.ascontiguousarray(x)).to(d)
+
+        def packed(rows, N):
+            return torch.empty((rows, a, (N + 127) // 128 * 4), dtype=torch.int32, device=d)
+
+        self.steps = []
+        for (kind, L), P in zip(self.ops, params):
+            st = dict(kind=kind, L=L)
+            if kind == "stem":
+                st["W"] = pack_bits(t(P["W"].reshape(L["Co"], -1)), w_bits)
+                st["shape"] = ConvShape(batch, L["H"], L["W"], L["C"], L["Co"], L["R"], L["S"], L["stride"], L["pad"])
+                st["A"] = torch.empty((batch * L["Ho"] * L["Wo"], a, (L["K"] + 127) // 128 * 4), dtype=torch.int32,
+                                      device=d)
+                st["Y32"] = torch.empty((batch, L["Ho"], L["Wo"], L["Co"]), dtype=torch.int32, device=d)
+                st["epi"] = Epilogue(a, t(P["alpha"]), t(P["beta"]), int(P["S"]), pool=2, pool_stride=2)
+                st["out"] = packed(batch * L["Hp"] * L["Wp"], L["Co"])
+            elif kind == "block":
+                La, Lb, Ld = L["a"], L["b"], L["down"]
+                st["Wa"] = pack_bits(t(P["Wa"].reshape(-1, La["C"])), w_bits)
+                st["Wb"] = pack_bits(t(P["Wb"].reshape(-1, Lb["C"])), w_bits)
+                st["sa"] = ConvShape(batch, La["H"], La["W"], La["C"], La["Co"], 3, 3, La["stride"], 1)
+                st["sb"] = ConvShape(batch, Lb["H"], Lb["W"], Lb["C"], Lb["Co"], 3, 3, 1, 1)
+                st["epi_a"] = Epilogue(a, t(P["alpha_a"]), t(P["beta_a"]), int(P["S_a"]))
+                st["qa"] = packed(batch * La["Ho"] * La["Wo"], La["Co"])
+                st["Yb"] = torch.empty((batch, Lb["Ho"], Lb["Wo"], Lb["Co"]), dtype=torch.int32, device=d)
+                if Ld is not None:
+                    st["Wd"] = pack_bits(t(P["Wd"].reshape(-1, Ld["C"])), w_bits)
+                    st["sd"] = ConvShape(batch, Ld["H"], Ld["W"], Ld["C"], Ld["Co"], 1, 1, Ld["stride"], 0)
+                    st["Zd"] = torch.empty((batch, Ld["Ho"], Ld["Wo"], Ld["Co"]), dtype=torch.int32, device=d)
+                st["epi"] = Epilogue(a, t(P["alpha"]), t(P["beta"]), int(P["S"]))
+                st["rho"] = t(P["rho"])
+                st["out"] = packed(batch * Lb["Ho"] * Lb["Wo"], Lb["Co"])
+            else:
+                Pn, C = L["H"] * L["W"], L["C"]
+                Cp = (C + 127) // 128 * 128
+                Wf = np.zeros((L["Co"], Pn, Cp), np.uint8)
+                Wf[:, :, :C] = P["W"].reshape(L["Co"], Pn, C)
+                st["K"] = Pn * Cp
+                st["W"] = pack_bits(t(Wf.reshape(L["Co"], -1)), w_bits)
+                st["A"] = torch.empty((batch, a, Pn * Cp // 32), dtype=torch.int32, device=d)
+                st["out"] = torch.empty((batch, L["Co"]), dtype=torch.int32, device=d)
+            self.steps.append(st)
+        self.x = torch.empty((batch, 224, 224, 3), dtype=torch.uint8, device=d)
+        self.graph: Optional[torch.cuda.CUDAGraph] = None
+
+    def forward(self, x: Optional[torch.Tensor] = None) -> torch.Tensor:
+        if x is not None and x.data_ptr() != self.x.data_ptr():
+            self.x.copy_(x)
+        a, w, enc, B = self.a_bits, self.w_bits, self.enc, self.B
+        act = None
+        for st in self.steps:
+            L = st["L"]
+            if st["kind"] == "stem":
+                im2col_pack(self.x, st["shape"], a, out=st["A"])
+                M = B * L["Ho"] * L["Wo"]
+                gemm(st["A"], st["W"], M, L["Co"], L["K"], a, w, enc, out=st["Y32"].view(M, L["Co"]))
+                act = pool_quant_pack_out(st["Y32"], st["epi"], out=st["out"])
+            elif st["kind"] == "block":
+                qa = conv2d(act, st["Wa"], st["sa"], a, w, enc, epi=st["epi_a"], out=st["qa"])
+                conv2d(qa, st["Wb"], st["sb"], a, w, enc, out=st["Yb"])
+                if L["down"] is not None:
+                    Z, zb = conv2d(act, st["Wd"], st["sd"], a, w, enc, out=st["Zd"]).view(-1, L["b"]["Co"]), 0
+                else:
+                    Z, zb = act, a
+                act = residual_quant_pack(st["Yb"], Z, zb, st["epi"], rho=st["rho"], out=st["out"])
+            else:
+                A = flatten_packed(act, B, L["H"] * L["W"], out=st["A"])
+                act = gemm(A, st["W"], B, L["Co"], st["K"], a, w, enc, out=st["out"])
+        return act
+
+    capture = APNNModel.capture
+    run = APNNModel.run
+
+    def macs_per_image(self) -> int:
+        tot = 0
+        for kind, L in synth.resnet18_ops(1):
+            for l in ([L["a"], L["b"]] + ([L["down"]] if L["down"] else []) if kind == "block" else [L]):
+                tot += l["Ho"] * l["Wo"] * l["Co"] * l["K"]
+        return tot

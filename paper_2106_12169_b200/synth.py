@@ -148,5 +148,75 @@ def model_params(name: str, w_bits: int, a_bits: int, tag: str = "model"):
 
 def model_input(name: str, batch: int, a_bits: int, tag: str = "img"):
     """The image batch quantised to a_bits codes, NHWC uint8 (reading R23)."""
-    H, W, C = MODELS[name]["input"]
+    H, W, C = MODELS[name]["input"] if name in MODELS else (224, 224, 3)
     return codes((batch, H, W, C), a_bits, f"{tag}:{name}:{batch}:a{a_bits}")
+
+
+# ResNet-18 (BASELINE.json configs[4]; He et al.'s basic-block network, reading R24 for the
+# residual integer form).  Deviations, labelled: the stem max-pool is 2x2/2 (no pool padding
+# in this library) instead of 3x3/2 pad 1 (same 56 x 56 output); the head is an FC over the
+# flattened 7 x 7 x 512 map instead of global average pooling + FC (both are linear maps of
+# the last block's codes).
+RESNET18_STAGES = [(64, 1), (128, 2), (256, 2), (512, 2)]
+
+
+def resnet18_ops(batch: int):
+    """[("stem", L), ("block", {"a": L, "b": L, "down": L or None}) x 8, ("fc", L)] with the
+    conv layer dict format of model_layers."""
+    def conv(H, C, Co, R, st, pad, pool=None):
+        Ho = (H + 2 * pad - R) // st + 1
+        Hp = Ho if not pool else (Ho - pool[0]) // pool[1] + 1
+        return dict(kind="conv", B=batch, H=H, W=H, C=C, Co=Co, R=R, S=R, stride=st, pad=pad, Ho=Ho, Wo=Ho,
+                    pool=pool, Hp=Hp, Wp=Hp, K=R * R * C)
+    ops = [("stem", conv(224, 3, 64, 7, 2, 3, (2, 2)))]
+    H, C = 56, 64
+    for Co, st in RESNET18_STAGES:
+        for blk in range(2):
+            s_ = st if blk == 0 else 1
+            a = conv(H, C, Co, 3, s_, 1)
+            b = conv(a["Ho"], Co, Co, 3, 1, 1)
+            down = conv(H, C, Co, 1, s_, 0) if (s_ != 1 or C != Co) else None
+            ops.append(("block", dict(a=a, b=b, down=down)))
+            H, C = a["Ho"], Co
+    ops.append(("fc", dict(kind="fc", B=batch, H=H, W=H, C=C, Co=1000, R=H, S=H, stride=1, pad=0, Ho=1, Wo=1,
+                           pool=None, Hp=1, Wp=1, K=H * H * C)))
+    return ops
+
+
+def resnet18_params(w_bits: int, a_bits: int, tag: str = "resnet18"):
+    """Synthetic weights per conv and integer (alpha, beta, S[, rho]) per requantisation,
+    analytical as in model_params (uniform input codes); blocks: "a" = first conv's
+    requant, "res" = the residual requant of alpha*y_b + beta + rho*shortcut."""
+    enc = model_encoding(w_bits, a_bits)
+    w_pm1 = enc in (1, 2)
+    ma, va = (2 ** a_bits - 1) / 2, (4 ** a_bits - 1) / 12
+
+    def weights(L, t):
+        return rng(f"{tag}:w{w_bits}a{a_bits}:{t}").integers(0, 1 << w_bits, size=(L["Co"], L["R"], L["S"], L["C"]),
+                                                            dtype=np.uint8)
+
+    def requant(Wt, pooled=False):
+        wv = Wt.reshape(Wt.shape[0], -1).astype(np.float64)
+        if w_pm1:
+            wv = 2 * wv - 1
+        mu, sd = ma * wv.sum(1), np.sqrt(va * (wv ** 2).sum(1)) + 1.0
+        S = int(max(1, np.ceil(4 * np.median(sd) / (1 << a_bits))))
+        shift = 1.03 if pooled else 0.0
+        return np.ones(len(mu), np.int32), np.round((2 - shift) * sd - mu).astype(np.int32), S
+
+    out = []
+    for i, (kind, op) in enumerate(resnet18_ops(1)):
+        if kind == "stem":
+            Wt = weights(op, i)
+            a_, b_, S = requant(Wt, pooled=True)
+            out.append(dict(W=Wt, alpha=a_, beta=b_, S=S))
+        elif kind == "block":
+            Wa, Wb = weights(op["a"], f"{i}a"), weights(op["b"], f"{i}b")
+            Wd = weights(op["down"], f"{i}d") if op["down"] else None
+            aa, ba, Sa = requant(Wa)
+            ab, bb, Sb = requant(Wb)
+            out.append(dict(Wa=Wa, alpha_a=aa, beta_a=ba, S_a=Sa, Wb=Wb, Wd=Wd, alpha=ab, beta=bb, S=Sb,
+                            rho=np.ones(op["b"]["Co"], np.int32)))
+        else:
+            out.append(dict(W=weights(op, i), alpha=None, beta=None, S=None))
+    return out

@@ -57,3 +57,45 @@ def test_im2col_pack_and_flatten_match_oracle_layouts():
     Fp = ap.pack_bits(torch.from_numpy(F).cuda(), 2)
     flat = ap.flatten_packed(Fp, 3, 4).cpu().numpy().view(np.uint32)
     np.testing.assert_array_equal(flat, oracle.pack(F.reshape(3, 4 * 256), 2))
+
+
+def test_residual_quant_pack_matches_oracle():
+    g = synth.rng("resgpu")
+    M, N = 300, 200
+    Y = g.integers(-2**20, 2**20, size=(M, N)).astype(np.int32)
+    Zi = g.integers(-2**20, 2**20, size=(M, N)).astype(np.int32)
+    Zc = synth.codes((M, N), 3, "resgpu:z")
+    alpha = g.integers(-3, 4, size=N).astype(np.int32)
+    beta = g.integers(-5000, 5000, size=N).astype(np.int32)
+    rho = g.integers(-2, 3, size=N).astype(np.int32)
+    for ob, S in ((2, 4099), (8, 97)):
+        epi = ap.Epilogue(ob, torch.from_numpy(alpha).cuda(), torch.from_numpy(beta).cuda(), S)
+        got = ap.residual_quant_pack(torch.from_numpy(Y).cuda(), torch.from_numpy(Zi).cuda(), 0, epi,
+                                     rho=torch.from_numpy(rho).cuda())
+        want = oracle.pack(oracle.residual_epilogue(Y, Zi, alpha, beta, rho, S, ob), ob)
+        np.testing.assert_array_equal(got.cpu().numpy().view(np.uint32), want)
+        Zp = ap.pack_bits(torch.from_numpy(Zc).cuda(), 3)
+        got = ap.residual_quant_pack(torch.from_numpy(Y).cuda(), Zp, 3, epi, rho=torch.from_numpy(rho).cuda())
+        want = oracle.pack(oracle.residual_epilogue(Y, Zc, alpha, beta, rho, S, ob), ob)
+        np.testing.assert_array_equal(got.cpu().numpy().view(np.uint32), want)
+
+
+@pytest.mark.parametrize("B,w,a", [(1, 2, 8), (2, 1, 2)])
+def test_resnet18_logits_match_oracle(B, w, a):
+    from paper_2106_12169_b200.models import APNNResNet18
+    ops = synth.resnet18_ops(B)
+    x = synth.model_input("resnet18", B, a)
+    enc = synth.model_encoding(w, a)
+    params = om.calibrate_resnet18(ops, synth.resnet18_params(w, a), x, w, a, enc)
+    trace = []
+    want = om.run_resnet18(ops, params, x, w, a, enc, trace=trace)
+    for t in trace:
+        assert len(np.unique(t)) >= 2
+    model = APNNResNet18(B, w, a, params=params)
+    got = model.forward(torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+    model.capture()
+    again = model.run(torch.from_numpy(x).cuda()).clone()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(again.cpu().numpy(), want)

@@ -333,3 +333,27 @@ def test_model_runner_vs_torch_float64():
             v = F.max_pool2d(v, L["pool"][0], L["pool"][1])
         act = torch.clamp(torch.floor(v / P["S"]), 0, 3)
     np.testing.assert_array_equal(got, want.astype(np.int32))
+
+
+def test_residual_epilogue_pins():
+    """Residual requantisation (reading R24): rho = 0 reduces to the plain epilogue, and a
+    Python-integer brute force on random values (floor toward -inf)."""
+    g = synth.rng("respin")
+    Y = g.integers(-2**20, 2**20, size=(9, 7)).astype(np.int32)
+    Z = g.integers(-2**20, 2**20, size=(9, 7)).astype(np.int32)
+    alpha = g.integers(-3, 4, size=7).astype(np.int32)
+    beta = g.integers(-5000, 5000, size=7).astype(np.int32)
+    rho = g.integers(-2, 3, size=7).astype(np.int32)
+    np.testing.assert_array_equal(oracle.residual_epilogue(Y, Z, alpha, beta, np.zeros(7, np.int32), 13, 3),
+                                  oracle.epilogue(Y, alpha, beta, 13, 3))
+    q = oracle.residual_epilogue(Y, Z, alpha, beta, rho, 777, 5)
+    for m in range(9):
+        for n in range(7):
+            v = int(alpha[n]) * int(Y[m, n]) + int(beta[n]) + int(rho[n]) * int(Z[m, n])
+            assert q[m, n] == min(max(v // 777, 0), 31)
+
+
+def test_resnet18_table():
+    ops = synth.resnet18_ops(1)
+    assert [k for k, _ in ops].count("block") == 8 and ops[-1][1]["K"] == 7 * 7 * 512
+    assert sum(1 for k, o in ops if k == "block" and o["down"] is not None) == 3
