@@ -53,7 +53,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-models", action="store_true")
-    ap.add_argument("--model-batch", type=int, default=256, help="global batch of the end-to-end models")
+    ap.add_argument("--model-batch", type=int, default=256, help="global batch of AlexNet / VGG-Variant")
+    ap.add_argument("--resnet-batch", type=int, default=1024, help="global batch of ResNet-18 w2a8")
     return ap.parse_args()
 
 
@@ -190,19 +191,20 @@ def run_reference(args):
 
 # ------------------------------------------------------------- end-to-end models
 def time_models(args, world, rank, dev, dist):
-    """BASELINE.json configs[3]: AlexNet and VGG-Variant w1a2 end-to-end inference, global
-    batch sharded over the ranks (strong scaling: each rank runs batch/world images), the
+    """BASELINE.json configs[3]/[4]: AlexNet and VGG-Variant w1a2 (global batch 256) and
+    ResNet-18 w2a8 (global batch 1024) end-to-end inference, global batch sharded over the ranks (strong scaling: each rank runs batch/world images), the
     whole forward captured in one CUDA graph; latency = max over ranks of the best of 5
     replays (CUDA events).  Row f1; the logits are checked against the oracle in
     tests/test_models.py."""
     import torch
     from paper_2106_12169_b200 import synth
-    from paper_2106_12169_b200.models import APNNModel
+    from paper_2106_12169_b200.models import APNNModel, APNNResNet18
     out = {}
-    per = max(1, args.model_batch // world)
-    for name in ("alexnet", "vgg_variant"):
-        m = APNNModel(name, per, 1, 2, device=dev)
-        x = torch.from_numpy(synth.model_input(name, per, 2, tag=f"img-rank{rank}")).to(dev)
+    for name, w, a, gb in (("alexnet", 1, 2, args.model_batch), ("vgg_variant", 1, 2, args.model_batch),
+                           ("resnet18", 2, 8, args.resnet_batch)):
+        per = max(1, gb // world)
+        m = APNNResNet18(per, w, a, device=dev) if name == "resnet18" else APNNModel(name, per, w, a, device=dev)
+        x = torch.from_numpy(synth.model_input(name, per, a, tag=f"img-rank{rank}")).to(dev)
         m.run(x)
         m.capture()
         for _ in range(3):
@@ -221,7 +223,7 @@ def time_models(args, world, rank, dev, dist):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             best = float(t.item())
         macs = m.macs_per_image() * per * world
-        out[f"{name}_w1a2"] = {"global_batch": per * world, "batch_per_gpu": per, "latency_ms": best,
+        out[f"{name}_w{w}a{a}"] = {"global_batch": per * world, "batch_per_gpu": per, "latency_ms": best,
                                "images_per_s": per * world / (best * 1e-3),
                                "effective_tops": 2.0 * macs / (best * 1e-3) / 1e12, "scaling": "strong",
                                "timing": "CUDA graph of the whole forward, best of 5, max over ranks"}

@@ -4,11 +4,12 @@ import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2106_12169_b200 import synth
-from paper_2106_12169_b200.models import APNNModel
+from paper_2106_12169_b200.models import APNNModel, APNNResNet18
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 256
-for name, w, a in [("alexnet", 1, 2), ("vgg_variant", 1, 2), ("alexnet", 2, 2), ("vgg_variant", 2, 2)]:
-    m = APNNModel(name, B, w, a)
+for name, w, a in [("alexnet", 1, 2), ("vgg_variant", 1, 2), ("alexnet", 2, 2), ("vgg_variant", 2, 2),
+                   ("resnet18", 2, 8), ("resnet18", 1, 2)]:
+    m = APNNResNet18(B, w, a) if name == "resnet18" else APNNModel(name, B, w, a)
     x = torch.from_numpy(synth.model_input(name, B, a)).cuda()
     m.run(x); m.capture()
     for _ in range(3): m.run()
