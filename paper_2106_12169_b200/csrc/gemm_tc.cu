@@ -84,6 +84,7 @@ struct Params {
     uint32_t a_tx_bytes;  // bytes the A loads of one stage actually deliver (expect_tx; excludes slot padding)
     unsigned long long* trace;  // development trace (APNN_TRACE), nullptr normally
     int exp_nostore;            // experiment knob (APNN_EXP_NOSTORE): skip the epilogue stores
+    int exp_nob;                // experiment knob (APNN_EXP_NOB): B warps skip the decode (wrong results)
 };
 
 // development trace of CTA 0: clock64 stamps per k-block / tile (APNN_TRACE=<file>)
@@ -393,7 +394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                                                  &op_empty[s], ph ^ 1, tmem_lane + A_COL + s * 32, nullptr, kvalid,
                                                  lane, dep_slots + threadIdx.x);
                     tmem_wait_st();
-                } else if (t < BROWS) {  // warp-uniform: BROWS is a multiple of 32
+                } else if (t < BROWS && !p.exp_nob) {  // warp-uniform: BROWS is a multiple of 32
                     recomb_step_any<W_PM1, false, SCALED>(g.w_bits, sBpl + (size_t)ps * p.b_bytes, BROWS, 1, t,
                                                           &plane_empty[ps], &op_empty[s], ph ^ 1, 0,
                                                           sBop + (size_t)s * BOP_STAGE, 128, lane,
@@ -1082,6 +1083,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     p.acc_shift = 0;
     p.trace = nullptr;
     p.exp_nostore = getenv("APNN_EXP_NOSTORE") ? 1 : 0;
+    p.exp_nob = getenv("APNN_EXP_NOB") ? 1 : 0;
     const char* trace_path = getenv("APNN_TRACE");
     if (trace_path) {
         cudaMalloc(&p.trace, sizeof(unsigned long long) * (kTraceN * TR_N + 4 * kCtaTraceMax + 32));
