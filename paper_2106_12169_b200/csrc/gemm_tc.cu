@@ -85,6 +85,7 @@ struct Params {
     unsigned long long* trace;  // development trace (APNN_TRACE), nullptr normally
     int exp_nostore;            // experiment knob (APNN_EXP_NOSTORE): skip the epilogue stores
     int exp_nob;                // experiment knob (APNN_EXP_NOB): B warps skip the decode (wrong results)
+    int halves;                 // 256-wide pair tiles: two N = 128 MMA halves (APNN_HALVES, default 0)
 };
 
 // development trace of CTA 0: clock64 stamps per k-block / tile (APNN_TRACE=<file>)
@@ -226,6 +227,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     // accumulators: NACC = 2 TMEM buffers when the pair tile is <= 128 columns wide (the
     // epilogue of tile i then overlaps the MMAs of tile i+1), else 1 (A stages fill the rest)
     constexpr int NACC = T2_BN <= 128 ? 2 : 1;
+    // 256-wide tiles: the MMA runs as two N = 128 halves (accumulator columns [0,128) and
+    // [128,256), B rows [0,64) / [64,128) of each CTA), released separately by the epilogue,
+    // so the next tile's first MMAs start after half the epilogue.  Experiment only
+    // (APNN_HALVES=1): the N = 128 instructions made the main loop slower than the exposure saved
+    constexpr bool HALVES = T2_BN == 256;
     uint64_t* accum_full = op_empty + MAX_STAGES;                  // [2]
     uint64_t* accum_empty = accum_full + 2;                        // [2], used in CTA 0
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accum_empty + 2);
@@ -318,7 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     } else if (warp == T2_MMA_WARP) {
         // ---------------------------------------------------- MMA issuer (CTA 0)
         if (rank == 0 && lane == 0) {
-            const uint32_t idesc = idesc_i8(256, T2_BN, A_PM1, W_PM1);
+            const uint32_t idesc = idesc_i8(256, (HALVES && p.halves) ? 128 : T2_BN, A_PM1, W_PM1);
             const uint64_t bdesc0 = b_desc(smem_u32(sBop), 0);
             const uint32_t a_col0 = tmem + A_COL;
             int s = 0, tc = 0;
@@ -326,7 +332,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             for (int tile = cid; tile < p.num_tiles; tile += ncl, tc++) {
                 const int buf = tc % NACC;
                 const uint32_t dtm = tmem + (uint32_t)(buf * T2_BN);
-                mbar_wait_cluster(&accum_empty[buf], ((tc / NACC) & 1) ^ 1);
+                const bool halves = HALVES && p.halves;
+                mbar_wait_cluster(&accum_empty[buf], ((tc / NACC) & 1) ^ 1);  // halves: the low half
                 tc_fence_after();
                 for (int kb = 0; kb < nkb; kb++) {
                     mbar_wait_cluster(&op_full[s], ph);
@@ -334,9 +341,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                     tc_fence_after();
                     const uint64_t bd = bdesc0 + (uint64_t)(s * (BOP_STAGE / 16));
                     const uint32_t as = a_col0 + s * 32;
+                    if (!halves) {
 #pragma unroll
-                    for (int kk = 0; kk < 4; kk++)
-                        mma2_i8_ts(dtm, as + kk * 8, bd + (uint64_t)(kk * kBDescKStep), idesc, (kb | kk) != 0);
+                        for (int kk = 0; kk < 4; kk++)
+                            mma2_i8_ts(dtm, as + kk * 8, bd + (uint64_t)(kk * kBDescKStep), idesc, (kb | kk) != 0);
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < 4; kk++)
+                            mma2_i8_ts(dtm, as + kk * 8, bd + (uint64_t)(kk * kBDescKStep), idesc, (kb | kk) != 0);
+                        if (kb == 0) {  // the high half of the accumulator must be drained too
+                            mbar_wait_cluster(&accum_empty[1], (tc & 1) ^ 1);
+                            tc_fence_after();
+                        }
+                        const uint64_t bdh = bd + (uint64_t)(64 * 128 / 16);  // B rows 64..127 of each CTA
+#pragma unroll
+                        for (int kk = 0; kk < 4; kk++)
+                            mma2_i8_ts(dtm + 128, as + kk * 8, bdh + (uint64_t)(kk * kBDescKStep), idesc,
+                                       (kb | kk) != 0);
+                    }
                     mma2_commit_mc(&op_empty[s], 0x3);
                     trace_at(p, TR_MMA_ISSUED, tc * nkb + kb);
                     if (++s == S) { s = 0; ph ^= 1; }
@@ -457,11 +479,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             mbar_wait(&accum_full[buf], (tc / NACC) & 1);
             if (warp == T2_EPI0 && lane == 0) trace_at(p, TR_EPI_FULL, tc);
             tc_fence_after();
+            const bool halves = HALVES && p.halves;
 #pragma unroll 1
-            for (int c = 0; c < T2_BN; c += 32) {
+            for (int cc = 0; cc < T2_BN; cc += 32) {
                 uint32_t acc[32];
-                tmem_ld32(tmem_lane + (uint32_t)(buf * T2_BN) + c, acc);
+                tmem_ld32(tmem_lane + (uint32_t)(buf * T2_BN) + cc, acc);
                 tmem_wait_ld();
+                // accumulator column cc -> tile-local output column c (halves: [0,64) CTA0 B rows
+                // 0-63, [64,128) CTA1 rows 0-63, [128,192) CTA0 rows 64-127, [192,256) CTA1 rows 64-127)
+                int c = cc;
+                if (halves) {
+                    const int h = cc >> 7, j = cc & 127;
+                    c = j < 64 ? 64 * h + j : 128 + 64 * h + (j - 64);
+                    if (cc == 96) {  // the low half has been read out: release it to the next tile
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(accum_empty0);
+                    }
+                }
                 if (SCALED) {
 #pragma unroll
                     for (int i = 0; i < 32; i++) acc[i] = (uint32_t)((int32_t)acc[i] >> p.acc_shift);
@@ -504,7 +539,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(accum_empty0 + 8u * (uint32_t)buf);
+            if (lane == 0) mbar_arrive_cluster(accum_empty0 + 8u * (uint32_t)(halves ? 1 : buf));
             if (p.pool_fused) {
                 pool_pad_words(n0 + T2_BN, t, len, mb, g, p);
             } else if (ob && any && !p.exp_nostore) {
@@ -1084,6 +1119,10 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     p.trace = nullptr;
     p.exp_nostore = getenv("APNN_EXP_NOSTORE") ? 1 : 0;
     p.exp_nob = getenv("APNN_EXP_NOB") ? 1 : 0;
+    {
+        const char* h = getenv("APNN_HALVES");
+        p.halves = h ? atoi(h) : 0;  // measured slower (8192^3 w1a2: 564 vs 455 us): N = 128 MMAs cost more
+    }
     const char* trace_path = getenv("APNN_TRACE");
     if (trace_path) {
         cudaMalloc(&p.trace, sizeof(unsigned long long) * (kTraceN * TR_N + 4 * kCtaTraceMax + 32));
