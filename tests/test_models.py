@@ -99,3 +99,19 @@ def test_resnet18_logits_match_oracle(B, w, a):
     again = model.run(torch.from_numpy(x).cuda()).clone()
     torch.cuda.synchronize()
     np.testing.assert_array_equal(again.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("name,B", [("alexnet", 256), ("vgg_variant", 256)])
+def test_bench_batch_sampled_images(name, B):
+    """The bench configuration (w1a2, global batch 256 on one GPU, synth.model_params, CUDA
+    graph): images are independent, so sampled images' logits are compared with the oracle
+    run on those images alone."""
+    params = synth.model_params(name, 1, 2)
+    x = synth.model_input(name, B, 2, tag="img-rank0")
+    model = APNNModel(name, B, 1, 2, params=params)
+    model.run(torch.from_numpy(x).cuda())
+    model.capture()
+    got = model.run().cpu().numpy()
+    for i in (0, B - 1):
+        want = om.run_model(synth.model_layers(name, 1), params, x[i:i + 1], 1, 2, 2)
+        np.testing.assert_array_equal(got[i:i + 1], want, err_msg=f"image {i}")
