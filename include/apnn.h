@@ -109,6 +109,15 @@ typedef struct {
                               apnn_pool_quant_pack_out only; APNN_ERR_INVALID_ARG elsewhere) */
     int32_t pool_stride;   /* 0: = pool */
     int32_t pool_avg;      /* 0: max pooling, 1: average (floor of the sum / k^2) */
+    /* Residual shortcut (ResNet blocks, reading R24), apnn_gemm_fused / apnn_conv2d only:
+     *   v = alpha[n]*y + beta[n] + rho[n]*z[m][n]  before the pooling-free quantisation.
+     * residual == NULL: none.  Otherwise z is device int32 [M][N] (residual_bits = 0) or
+     * device packed 0/1 codes [M][residual_bits][roundup(N,128)/32] (1..8).  Fused only by
+     * the 2-CTA tensor-core kernel (M > 128, no pooling); elsewhere APNN_ERR_UNSUPPORTED:
+     * use apnn_residual_quant_pack after an int32 GEMM/conv. */
+    const void *residual;
+    int32_t residual_bits;
+    const int32_t *rho;    /* device [N] or NULL (= 1) */
 } apnn_epilogue;
 
 /* NHWC convolution geometry.  Ho = (H + 2 pad - R)/stride + 1, Wo likewise. */

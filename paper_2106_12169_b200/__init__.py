@@ -47,7 +47,8 @@ class ApnnError(RuntimeError):
 class _Epi(ctypes.Structure):
     _fields_ = [("out_bits", ctypes.c_int32), ("alpha", ctypes.c_void_p), ("beta", ctypes.c_void_p),
                 ("divisor", ctypes.c_int32), ("pool", ctypes.c_int32), ("pool_stride", ctypes.c_int32),
-                ("pool_avg", ctypes.c_int32)]
+                ("pool_avg", ctypes.c_int32), ("residual", ctypes.c_void_p), ("residual_bits", ctypes.c_int32),
+                ("rho", ctypes.c_void_p)]
 
 
 class _Conv(ctypes.Structure):
@@ -168,19 +169,24 @@ class Epilogue:
     pool: int = 0
     pool_stride: int = 0                  # 0 -> = pool
     pool_avg: bool = False
+    residual: Optional[torch.Tensor] = None  # shortcut z: int32 [M, N] or packed codes [M, bits, Kw(N)]
+    residual_bits: int = 0                   # 0: int32 shortcut; 1..8: packed codes
+    rho: Optional[torch.Tensor] = None       # int32 [N] or None (= 1)
 
     def pooled(self, Ho: int, Wo: int):
         st = self.pool_stride or self.pool
         return ((Ho - self.pool) // st + 1, (Wo - self.pool) // st + 1) if self.pool else (Ho, Wo)
 
     def _c(self):
-        for name in ("alpha", "beta"):
+        for name in ("alpha", "beta", "residual", "rho"):
             t = getattr(self, name)
             if t is not None:
                 _cuda(t, name, torch.int32)
         return _Epi(self.out_bits, None if self.alpha is None else self.alpha.data_ptr(),
                     None if self.beta is None else self.beta.data_ptr(), self.divisor, self.pool,
-                    self.pool_stride, 1 if self.pool_avg else 0)
+                    self.pool_stride, 1 if self.pool_avg else 0,
+                    None if self.residual is None else self.residual.data_ptr(), self.residual_bits,
+                    None if self.rho is None else self.rho.data_ptr())
 
 
 @dataclass
@@ -282,6 +288,10 @@ def conv2d(X: torch.Tensor, W: torch.Tensor, shape: ConvShape, a_bits: int, w_bi
     if st == 7 and epi is not None and epi.pool:  # APNN_ERR_UNSUPPORTED: unfused pooling pair
         Y = conv2d(X, W, shape, a_bits, w_bits, enc, None, variant)
         return pool_quant_pack_out(Y, epi, out=out)
+    if st == 7 and epi is not None and epi.residual is not None:  # unfused residual pair
+        Y = conv2d(X, W, shape, a_bits, w_bits, enc, None, variant)
+        plain = Epilogue(epi.out_bits, epi.alpha, epi.beta, epi.divisor)
+        return residual_quant_pack(Y, epi.residual, epi.residual_bits, plain, rho=epi.rho, out=out)
     _check(st, "apnn_conv2d_ex")
     return out
 

@@ -105,6 +105,14 @@ static apnn_status make_epi(const apnn_epilogue* epi, Epi* e) {
     e->pool = epi->pool;
     e->pool_stride = epi->pool ? (epi->pool_stride ? epi->pool_stride : epi->pool) : 0;
     e->pool_avg = epi->pool_avg;
+    if (epi->residual) {
+        if (epi->residual_bits < 0 || epi->residual_bits > 8) return APNN_ERR_BITS;
+        if (!aligned16(epi->residual) || (epi->rho && !aligned16(epi->rho))) return APNN_ERR_ALIGNMENT;
+        if (epi->pool) return APNN_ERR_INVALID_ARG;
+    }
+    e->res = epi->residual;
+    e->res_bits = epi->residual_bits;
+    e->rho = epi->rho;
     return APNN_OK;
 }
 
@@ -224,6 +232,7 @@ apnn_status apnn_gemm_ex(const uint32_t* A, const uint32_t* W, int M, int N, int
     if ((unsigned)variant > (unsigned)APNN_VARIANT_B1MMA) return APNN_ERR_INVALID_ARG;
     Geom g;
     gemm_geom(&g, M, N, K, a_bits, w_bits, enc);
+    if (e.res && (resolve(variant, g) != APNN_VARIANT_TC_I8 || M <= 128)) return APNN_ERR_UNSUPPORTED;
     return run(A, W, g, e, Y, variant, (cudaStream_t)stream);
 }
 
@@ -272,6 +281,7 @@ apnn_status apnn_conv2d_ex(const uint32_t* X, const uint32_t* W, const apnn_conv
     g.nchunks = g.RS * g.CB;
     g.conv = 1;
     g.H = c.H; g.W = c.W; g.Ho = Ho; g.Wo = Wo; g.S = c.S; g.stride = c.stride; g.pad = c.pad;
+    if (e.res && (resolve(variant, g) != APNN_VARIANT_TC_I8 || g.M <= 128)) return APNN_ERR_UNSUPPORTED;
     if (e.pool) {
         if (e.pool > Ho || e.pool > Wo) return APNN_ERR_SHAPE;
         if (resolve(variant, g) != APNN_VARIANT_TC_I8 || !tc_i8_pool_fusable(g, e)) return APNN_ERR_UNSUPPORTED;
@@ -295,6 +305,7 @@ apnn_status apnn_quant_pack_out(const int32_t* Y, int M, int N, const apnn_epilo
     apnn_status st = make_epi(epi, &e);
     if (st != APNN_OK) return st;
     if (e.pool) return APNN_ERR_INVALID_ARG;  // pooled: apnn_pool_quant_pack_out
+    if (e.res) return APNN_ERR_INVALID_ARG;  // residual: apnn_residual_quant_pack
     DevInfo d;
     if ((st = device_info(&d)) != APNN_OK) return st;
     cudaError_t err = launch_quant_pack(Y, M, N, e, out, d.sms, (cudaStream_t)stream);
@@ -308,7 +319,7 @@ apnn_status apnn_pool_quant_pack_out(const int32_t* Y, int B, int H, int W, int 
     Epi e;
     apnn_status st = make_epi(epi, &e);
     if (st != APNN_OK) return st;
-    if (e.pool < 1) return APNN_ERR_INVALID_ARG;
+    if (e.pool < 1 || e.res) return APNN_ERR_INVALID_ARG;
     if (e.pool > H || e.pool > W) return APNN_ERR_SHAPE;
     const int Hp = (H - e.pool) / e.pool_stride + 1, Wp = (W - e.pool) / e.pool_stride + 1;
     if ((long long)B * Hp * Wp > 2147483647LL) return APNN_ERR_SHAPE;
@@ -331,7 +342,7 @@ apnn_status apnn_residual_quant_pack(const int32_t* Y, int M, int N, const void*
     Epi e;
     apnn_status st = make_epi(epi, &e);
     if (st != APNN_OK) return st;
-    if (e.pool) return APNN_ERR_INVALID_ARG;
+    if (e.pool || e.res) return APNN_ERR_INVALID_ARG;  // the shortcut is the Z argument here
     DevInfo d;
     if ((st = device_info(&d)) != APNN_OK) return st;
     cudaError_t err = launch_residual_quant_pack(Y, M, N, Z, z_bits, rho, e, out, d.sms, (cudaStream_t)stream);

@@ -103,6 +103,9 @@ struct Epi {
     int32_t pool;          // conv pooling window k (0 = none)
     int32_t pool_stride;
     int32_t pool_avg;      // 0 max, 1 average
+    const void* res;       // residual shortcut z (reading R24) or nullptr: int32 [M][N] (res_bits 0)
+    int32_t res_bits;      //   or packed codes [M][res_bits][Nw]
+    const int32_t* rho;    // per-column residual scale or nullptr (= 1)
 };
 
 // q = clamp(floor(v / S), 0, qmax) for an int64 v (the quantisation step alone)

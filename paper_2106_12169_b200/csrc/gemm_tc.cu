@@ -465,7 +465,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             const bool use_tma = p.out_mode == kOutTma && any && (!g.conv || q * 32 + 32 <= len) && !p.exp_nostore;
             const bool use_lsu = p.out_mode == kOutLsu && any && !p.exp_nostore;
             const int row0 = mb + q * 32, row_end = mb + len;
-            if (p.tab_mode) {
+            if (p.tab_mode == kTabQ3 || p.tab_mode == kTabHybrid) {
                 named_bar_sync(1, 128);  // previous tile's readers are done
                 if (et < T2_BN) build_threshold_row(sTab + et * kTabStride, n0 + et, g.N, p.e);
                 if (et + 128 < T2_BN) build_threshold_row(sTab + (et + 128) * kTabStride, n0 + et + 128, g.N, p.e);
@@ -531,7 +531,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                     }
                 } else if (use_tma || use_lsu) {
                     uint32_t w[8];
-                    requant_chunk(acc, n0 + c, c, g, p.e, sTab, p.tab_mode, w);
+                    requant_chunk(acc, n0 + c, c, g, p.e, sTab, p.tab_mode, w, m);
                     stage_words(w, ob, p.nwb, c >> 5, reinterpret_cast<uint32_t*>(stg), lane);
                 } else {
                     epilogue_chunk(acc, m, n0 + c, c, g, p.e, p.Y, sTab, p.tab_mode);
@@ -753,7 +753,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
         const int t = q * 32 + lane;
         const int et = threadIdx.x - 64;  // 0..255
         const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
-        if (p.tab_mode && et < BN) build_threshold_row(sTab + et * kTabStride, n0 + et, g.N, p.e);
+        if ((p.tab_mode == kTabQ3 || p.tab_mode == kTabHybrid) && et < BN) build_threshold_row(sTab + et * kTabStride, n0 + et, g.N, p.e);
         RowCtx rc;
         if (A_PM1 && g.conv) rc = make_row(g, m0 + t);
         for (int i = 0; i < nkb; i++) {
@@ -1102,7 +1102,9 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     p.A = A;
     p.nkb = g.nchunks;
     p.tab_mode = kTabNone;
-    if (e.out_bits > 0 && e.out_bits <= 2) {
+    if (e.res) {
+        p.tab_mode = kTabResidual;  // v depends on the shortcut: no per-column thresholds
+    } else if (e.out_bits > 0 && e.out_bits <= 2) {
         p.tab_mode = kTabQ3;
     } else if (e.out_bits > 2 && (unsigned long long)e.qmax * (unsigned long long)e.S <= 0xFFFFFFFFull) {
         p.tab_mode = kTabHybrid;  // 32-bit in-range division is exact (requant_hybrid)
@@ -1130,9 +1132,10 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     }
     const int ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
     bool two = (g.M > 128) && tc_kernel_override() != 1;
+    if (e.res && !two) return cudaErrorNotSupported;  // residual epilogue: 2-CTA kernel only (ABI checks first)
     // small GEMMs (row f4): when the 2-CTA grid would occupy <= 1/4 of the SMs, run the
     // 1-CTA kernel with split-K clusters instead (latency: more CTAs, fewer k-blocks each)
-    if (two && !g.conv && g.M <= 1024 && g.nchunks >= 4 && tc_kernel_override() != 2) {
+    if (two && !g.conv && !e.res && g.M <= 1024 && g.nchunks >= 4 && tc_kernel_override() != 2) {
         const int BNP = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
         const long long pair_tiles = (long long)((g.M + 255) / 256) * ((g.N + BNP - 1) / BNP);
         if (pair_tiles * 2 * 4 <= sms) two = false;

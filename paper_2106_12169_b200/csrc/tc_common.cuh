@@ -336,7 +336,7 @@ __device__ __forceinline__ void conv_gather_kb(const uint32_t* X, const Geom& g,
 //   [0] sign  [1] U_1  [2] U_2  [3] U_3  [4] U_Q  [5] alpha  [6] beta  [7] unused
 // Padding columns (n >= N) get all thresholds INT32_MAX and alpha = beta = 0: q = 0.
 constexpr int kTabStride = 8;
-enum { kTabNone = 0, kTabQ3 = 1, kTabHybrid = 2 };
+enum { kTabNone = 0, kTabQ3 = 1, kTabHybrid = 2, kTabResidual = 3 };
 
 __device__ __forceinline__ long long floor_div64(long long a, long long b) {
     long long q = a / b;
@@ -449,9 +449,56 @@ __device__ __forceinline__ void bytes_to_words(const uint32_t (&qb)[8], int out_
 
 // 32 accumulators of row m, columns nb..nb+31 (lc = tile-local column of nb) ->
 // plane words: words[t] bit i = bit t of q(column nb + i), t < out_bits.
+// Residual requantisation of a 32-column chunk of row m (reading R24):
+// q = clamp(floor((alpha*y + beta + rho*z) / S)), z = int32 shortcut or a packed code.
+__device__ __forceinline__ void residual_chunk_bytes(const uint32_t (&acc)[32], int m, int nb, const Geom& g,
+                                                     const Epi& e, uint32_t (&qb)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) qb[i] = 0;
+    if (m >= g.M) return;
+    const int Nw = (g.N + 127) / 128 * 4;
+    uint32_t zw[8];
+    if (e.res_bits > 0) {
+        const uint32_t* zp = reinterpret_cast<const uint32_t*>(e.res) + (long long)m * e.res_bits * Nw + nb / 32;
+#pragma unroll
+        for (int t = 0; t < 8; t++) zw[t] = t < e.res_bits ? __ldg(zp + (long long)t * Nw) : 0u;
+    }
+    const int32_t* zr = reinterpret_cast<const int32_t*>(e.res) + (long long)m * g.N + nb;
+#pragma unroll
+    for (int g8 = 0; g8 < 4; g8++) {  // 8 columns at a time (register pressure)
+        int32_t z[8];
+        if (e.res_bits > 0) {
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                uint32_t code = 0;
+#pragma unroll
+                for (int t = 0; t < 8; t++) code |= ((zw[t] >> (8 * g8 + i)) & 1u) << t;
+                z[i] = (int32_t)code;
+            }
+        } else if ((g.N & 3) == 0 && nb + 8 * g8 + 8 <= g.N) {
+            const int4 a = __ldg(reinterpret_cast<const int4*>(zr + 8 * g8));
+            const int4 b = __ldg(reinterpret_cast<const int4*>(zr + 8 * g8 + 4));
+            z[0] = a.x; z[1] = a.y; z[2] = a.z; z[3] = a.w; z[4] = b.x; z[5] = b.y; z[6] = b.z; z[7] = b.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; i++) z[i] = nb + 8 * g8 + i < g.N ? __ldg(zr + 8 * g8 + i) : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const int n = nb + 8 * g8 + i;
+            uint32_t q = 0;
+            if (n < g.N) {
+                const long long r = e.rho ? __ldg(e.rho + n) : 1;
+                q = quantise_v(e, (long long)epi_alpha(e, n) * (int32_t)acc[8 * g8 + i] + epi_beta(e, n) + r * z[i]);
+            }
+            qb[2 * g8 + (i >> 2)] |= q << (8 * (i & 3));
+        }
+    }
+}
+
 __device__ __forceinline__ void requant_chunk(const uint32_t (&acc)[32], int nb, int lc, const Geom& g,
                                               const Epi& e, const int32_t* tab, int tab_mode,
-                                              uint32_t (&words)[8]) {
+                                              uint32_t (&words)[8], int m = 0) {
     if (tab_mode == kTabQ3) {
         requant_chunk_words_q3(acc, tab, lc, words[0], words[1]);
         return;
@@ -459,7 +506,9 @@ __device__ __forceinline__ void requant_chunk(const uint32_t (&acc)[32], int nb,
     uint32_t qb[8];
 #pragma unroll
     for (int i = 0; i < 8; i++) qb[i] = 0;
-    if (tab_mode == kTabHybrid) {
+    if (tab_mode == kTabResidual) {
+        residual_chunk_bytes(acc, m, nb, g, e, qb);
+    } else if (tab_mode == kTabHybrid) {
         const uint32_t S = (uint32_t)e.S, Q = (uint32_t)e.qmax;
 #pragma unroll
         for (int i = 0; i < 32; i++)
@@ -509,7 +558,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&acc)[32], int m,
     if (word >= Nw) return;
     uint32_t* o = reinterpret_cast<uint32_t*>(Yout) + (long long)m * e.out_bits * Nw + word;
     uint32_t w[8];
-    requant_chunk(acc, nb, lc, g, e, tab, tab_mode, w);
+    requant_chunk(acc, nb, lc, g, e, tab, tab_mode, w, m);
 #pragma unroll
     for (int tb = 0; tb < 8; tb++)
         if (tb < e.out_bits) o[(long long)tb * Nw] = w[tb];

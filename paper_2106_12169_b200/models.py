@@ -140,12 +140,16 @@ class APNNModel:
 class APNNResNet18:
     """ResNet-18 (BASELINE.json configs[4]; synth.resnet18_ops, reading R24) over the C ABI:
     stem = im2col GEMM (int32) + 2x2 pooling routine; basic block = conv_a with the fused
-    requantisation, conv_b (int32), the shortcut (the block input's packed codes, or a 1x1
-    stride-s downsample conv's int32 accumulator) and apnn_residual_quant_pack; head =
+    requantisation, conv_b with the shortcut (the block input's packed codes, or a 1x1
+    stride-s downsample conv's int32 accumulator) added in its fused epilogue (or, unfused,
+    conv_b int32 + apnn_residual_quant_pack); head =
     flatten + FC (int32 logits).  Static buffers; capture()/run() as APNNModel."""
 
-    def __init__(self, batch: int, w_bits: int, a_bits: int, device="cuda", params=None):
+    def __init__(self, batch: int, w_bits: int, a_bits: int, device="cuda", params=None, fuse_residual=False):
+        # fuse_residual: the shortcut in conv_b's epilogue.  Correct (tests) but measured slower at
+        # batch 256 (w2a8 11.5 vs 10.5 ms): the epilogue's per-row shortcut loads are uncoalesced.
         self.B, self.w_bits, self.a_bits = batch, w_bits, a_bits
+        self.fuse_residual = fuse_residual
         self.name = "resnet18"
         self.dev = torch.device(device)
         self.enc = synth.model_encoding(w_bits, a_bits)
@@ -213,12 +217,17 @@ class APNNResNet18:
                 act = pool_quant_pack_out(st["Y32"], st["epi"], out=st["out"])
             elif st["kind"] == "block":
                 qa = conv2d(act, st["Wa"], st["sa"], a, w, enc, epi=st["epi_a"], out=st["qa"])
-                conv2d(qa, st["Wb"], st["sb"], a, w, enc, out=st["Yb"])
                 if L["down"] is not None:
                     Z, zb = conv2d(act, st["Wd"], st["sd"], a, w, enc, out=st["Zd"]).view(-1, L["b"]["Co"]), 0
                 else:
                     Z, zb = act, a
-                act = residual_quant_pack(st["Yb"], Z, zb, st["epi"], rho=st["rho"], out=st["out"])
+                if self.fuse_residual:  # shortcut added in conv_b's epilogue (unfused pair if unsupported)
+                    e = st["epi"]
+                    epi_b = Epilogue(e.out_bits, e.alpha, e.beta, e.divisor, residual=Z, residual_bits=zb, rho=st["rho"])
+                    act = conv2d(qa, st["Wb"], st["sb"], a, w, enc, epi=epi_b, out=st["out"])
+                else:
+                    conv2d(qa, st["Wb"], st["sb"], a, w, enc, out=st["Yb"])
+                    act = residual_quant_pack(st["Yb"], Z, zb, st["epi"], rho=st["rho"], out=st["out"])
             else:
                 A = flatten_packed(act, B, L["H"] * L["W"], out=st["A"])
                 act = gemm(A, st["W"], B, L["Co"], st["K"], a, w, enc, out=st["out"])

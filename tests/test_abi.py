@@ -64,9 +64,9 @@ def test_validation_errors():
     assert gemm_ex(a=8, w=8, enc=0, K=33025) != 6                        # fits int32
     assert gemm_ex(a=8, w=8, enc=0, K=33026) == 6                        # APNN_ERR_OVERFLOW
     assert gemm_ex(variant=9) == 1
-    bad = ap._Epi(9, None, None, 1, 0, 0, 0)
+    bad = ap._Epi(9, None, None, 1, 0, 0, 0, None, 0, None)
     assert gemm_ex(epi=ctypes.byref(bad)) == 2
-    bad = ap._Epi(2, None, None, 0, 0, 0, 0)
+    bad = ap._Epi(2, None, None, 0, 0, 0, 0, None, 0, None)
     assert gemm_ex(epi=ctypes.byref(bad)) == 1
     L = ap.lib()
     cs = ap._Conv(1, 2, 2, 3, 4, 5, 5, 1, 0)  # 5x5 filter on a 2x2 map, no padding
@@ -76,15 +76,15 @@ def test_validation_errors():
 
 def test_pool_validation():
     L = ap.lib()
-    pooled = ap._Epi(2, None, None, 1, 2, 0, 0)
+    pooled = ap._Epi(2, None, None, 1, 2, 0, 0, None, 0, None)
     assert gemm_ex(epi=ctypes.byref(pooled)) == 1                       # pooling is a conv epilogue
     assert L.apnn_quant_pack_out(FAKE, 4, 4, ctypes.byref(pooled), FAKE, None) == 1
-    plain = ap._Epi(2, None, None, 1, 0, 0, 0)
+    plain = ap._Epi(2, None, None, 1, 0, 0, 0, None, 0, None)
     assert L.apnn_pool_quant_pack_out(FAKE, 1, 4, 4, 8, ctypes.byref(plain), FAKE, None) == 1  # needs pool >= 1
-    big = ap._Epi(2, None, None, 1, 5, 0, 0)
+    big = ap._Epi(2, None, None, 1, 5, 0, 0, None, 0, None)
     assert L.apnn_pool_quant_pack_out(FAKE, 1, 4, 4, 8, ctypes.byref(big), FAKE, None) == 4    # window > map
     for bad in (ap._Epi(2, None, None, 1, -1, 0, 0), ap._Epi(2, None, None, 1, 2, -1, 0),
-                ap._Epi(2, None, None, 1, 2, 0, 2)):
+                ap._Epi(2, None, None, 1, 2, 0, 2, None, 0, None)):
         assert L.apnn_pool_quant_pack_out(FAKE, 1, 4, 4, 8, ctypes.byref(bad), FAKE, None) == 1
     cs = ap._Conv(1, 4, 4, 8, 8, 3, 3, 1, 1)
     assert L.apnn_conv2d_ex(FAKE, FAKE, ctypes.byref(cs), 2, 1, 2, ctypes.byref(big), FAKE, 0, None) == 4

@@ -394,3 +394,33 @@ def test_split_k_small_problems(M, N, K, a_bits, w_bits, enc, out_bits):
         got = run_gemm(A, W, a_bits, w_bits, enc, ap.VARIANT_TC_I8,
                        epi=ap.Epilogue(out_bits, cuda(alpha), cuda(beta), S))
         np.testing.assert_array_equal(u32(got), want)
+
+
+
+# ------------------------------------------- fused residual epilogue (ResNet, reading R24)
+
+@pytest.mark.parametrize("M,N,K,zb", [(300, 200, 384, 0), (300, 200, 384, 3), (1000, 64, 640, 8),
+                                      (257, 520, 1152, 0), (60, 64, 256, 2)])
+def test_fused_residual_epilogue(M, N, K, zb):
+    A, W = synth.gemm_inputs(M, N, K, 2, 2, tag="fres")
+    Y = oracle.gemm(A, W, 2, 2, 0)
+    g = synth.rng(f"fres:{M}:{zb}")
+    Z = (g.integers(-5000, 5000, size=(M, N)).astype(np.int32) if zb == 0
+         else synth.codes((M, N), zb, f"fres:z:{M}:{zb}"))
+    alpha = g.integers(-3, 4, size=N).astype(np.int32)
+    beta = g.integers(-3000, 3000, size=N).astype(np.int32)
+    rho = g.integers(-2, 3, size=N).astype(np.int32)
+    S, ob = 37, 3
+    want = oracle.pack(oracle.residual_epilogue(Y, Z, alpha, beta, rho, S, ob), ob)
+    Zd = cuda(Z) if zb == 0 else ap.pack_bits(cuda(Z), zb)
+    epi = ap.Epilogue(ob, cuda(alpha), cuda(beta), S, residual=Zd, residual_bits=zb, rho=cuda(rho))
+    Ap, Wp = ap.pack_bits(cuda(A), 2), ap.pack_bits(cuda(W), 2)
+    out = torch.empty(ap.packed_shape(M, N, ob), dtype=torch.int32, device="cuda")
+    st = ap.lib().apnn_gemm_ex(ap._ptr(Ap), ap._ptr(Wp), M, N, K, 2, 2, 0, ctypes.byref(epi._c()), ap._ptr(out),
+                               0, ap._stream(Ap))
+    if M <= 128:
+        assert st == 7  # fused only by the 2-CTA kernel
+        return
+    assert st == 0
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(u32(out), want)

@@ -80,8 +80,8 @@ def test_residual_quant_pack_matches_oracle():
         np.testing.assert_array_equal(got.cpu().numpy().view(np.uint32), want)
 
 
-@pytest.mark.parametrize("B,w,a", [(1, 2, 8), (2, 1, 2)])
-def test_resnet18_logits_match_oracle(B, w, a):
+@pytest.mark.parametrize("B,w,a,fuse", [(1, 2, 8, True), (2, 1, 2, True), (1, 2, 8, False)])
+def test_resnet18_logits_match_oracle(B, w, a, fuse):
     from paper_2106_12169_b200.models import APNNResNet18
     ops = synth.resnet18_ops(B)
     x = synth.model_input("resnet18", B, a)
@@ -91,7 +91,7 @@ def test_resnet18_logits_match_oracle(B, w, a):
     want = om.run_resnet18(ops, params, x, w, a, enc, trace=trace)
     for t in trace:
         assert len(np.unique(t)) >= 2
-    model = APNNResNet18(B, w, a, params=params)
+    model = APNNResNet18(B, w, a, params=params, fuse_residual=fuse)
     got = model.forward(torch.from_numpy(x).cuda())
     torch.cuda.synchronize()
     np.testing.assert_array_equal(got.cpu().numpy(), want)
