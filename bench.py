@@ -69,11 +69,14 @@ def load_peaks():
         return None
 
 
-def int8_peak_tops(peaks):
-    """Dense int8 tensor-core peak: measured bf16 burst x the guide's nominal int8:bf16 ratio (4.5/2.25)."""
+def int8_peak_tops(peaks, fp4=False):
+    """Dense tensor-core peak of the pipe the GEMM runs on: measured bf16 burst x the guide's
+    nominal ratio (int8 4.5 / bf16 2.25 = 2; fp4 9 / 2.25 = 4 for the kind::mxf4 variant)."""
+    r = 4.0 if fp4 else 2.0
+    name = "fp4" if fp4 else "int8"
     if peaks and peaks.get("bf16_tflops"):
-        return float(peaks["bf16_tflops"]) * 2.0, "MEASURED_PEAKS.json bf16_tflops (burst) x 2 (nominal int8/bf16)"
-    return 1590.0 * 2.0, "fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md) x 2"
+        return float(peaks["bf16_tflops"]) * r, f"MEASURED_PEAKS.json bf16_tflops (burst) x {r:g} (nominal {name}/bf16)"
+    return 1590.0 * r, f"fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md) x {r:g}"
 
 
 class ClockSampler:
@@ -267,7 +270,7 @@ def run_ours(args):
     if args.allgather and dist is not None:
         from paper_2106_12169_b200.dist import gather_rows
         gathered = True
-    resolved = variant if variant else ap.select_variant(M, N, K, a, w, enc)
+    resolved = variant if variant else ap.select_variant(M, N, K, a, w, enc, out_bits)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
@@ -384,12 +387,12 @@ def run_ours(args):
         return
 
     peaks = load_peaks()
-    peak, peak_src = int8_peak_tops(peaks)
+    peak, peak_src = int8_peak_tops(peaks, fp4=resolved == ap.VARIANT_TC_FP4)
     achieved = ops / (gemm_avg_ms * 1e-3) / 1e12
     traffic = None
     try:
         summ = json.load(open(NCU_SUMMARY))
-        key = f"{M}x{N}x{K}_w{w}a{a}_enc{enc}"
+        key = f"{M}x{N}x{K}_w{w}a{a}_enc{enc}_{ap.variant_name(resolved)}"
         traffic = summ.get("traffic_bytes_per_launch", {}).get(key)
     except Exception:
         pass

@@ -87,7 +87,9 @@ typedef enum {
     APNN_VARIANT_AUTO = 0,  /* library picks (apnn_select_variant) */
     APNN_VARIANT_TC_I8 = 1, /* planes -> int8 recombination, tcgen05.mma kind::i8, TMEM accumulators */
     APNN_VARIANT_POPC = 2,  /* CUDA-core AND/XOR + POPC bit-plane products, shift-add combination */
-    APNN_VARIANT_B1MMA = 3  /* legacy mma.sync m16n8k256 b1 .and/.xor.popc (the paper's bmma) */
+    APNN_VARIANT_B1MMA = 3, /* legacy mma.sync m16n8k256 b1 .and/.xor.popc (the paper's bmma) */
+    APNN_VARIANT_TC_FP4 = 4 /* exact e2m1 formulation, tcgen05.mma kind::mxf4 with unit block scales:
+                               GEMM with a_bits, w_bits <= 2 and K*max|a|*max|w| < 2^24 only */
 } apnn_variant;
 
 /* Element-wise routine fused after the contraction:
@@ -232,8 +234,11 @@ apnn_status apnn_residual_quant_pack(const int32_t *Y, int M, int N, const void 
                                      const int32_t *rho, const apnn_epilogue *epi, uint32_t *out,
                                      apnn_stream_t stream);
 
-/* Which variant APNN_VARIANT_AUTO resolves to for this problem (no launch). */
+/* Which variant APNN_VARIANT_AUTO resolves to for this problem (no launch): int32 output,
+ * or the fused element-wise routine with out_bits (1..8) packed output. */
 apnn_variant apnn_select_variant(int M, int N, int K, int a_bits, int w_bits, apnn_encoding enc);
+apnn_variant apnn_select_variant_fused(int M, int N, int K, int a_bits, int w_bits, apnn_encoding enc,
+                                       int out_bits);
 
 const char *apnn_status_string(apnn_status status);
 const char *apnn_variant_name(apnn_variant variant);

@@ -31,8 +31,8 @@ LIB_PATH = os.environ.get("APNN_LIB", os.path.join(_HERE, "libapnn.so"))  # APNN
 ENC_01_01, ENC_PM1_PM1, ENC_W_PM1_A_01, ENC_W_01_A_PM1 = 0, 1, 2, 3
 ENCODINGS = {"01_01": 0, "pm1_pm1": 1, "w_pm1_a_01": 2, "w_01_a_pm1": 3}
 # apnn_variant
-VARIANT_AUTO, VARIANT_TC_I8, VARIANT_POPC, VARIANT_B1MMA = 0, 1, 2, 3
-VARIANTS = {"auto": 0, "tc_i8": 1, "popc": 2, "b1mma": 3}
+VARIANT_AUTO, VARIANT_TC_I8, VARIANT_POPC, VARIANT_B1MMA, VARIANT_TC_FP4 = 0, 1, 2, 3, 4
+VARIANTS = {"auto": 0, "tc_i8": 1, "popc": 2, "b1mma": 3, "tc_fp4": 4}
 # apnn_status
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "BITS", 3: "ENCODING", 4: "SHAPE", 5: "ALIGNMENT",
           6: "OVERFLOW", 7: "UNSUPPORTED", 8: "CUDA"}
@@ -95,6 +95,8 @@ def lib() -> ctypes.CDLL:
             L.apnn_pool_quant_pack_out.restype = st
             L.apnn_select_variant.argtypes = [ci, ci, ci, ci, ci, ci]
             L.apnn_select_variant.restype = ci
+            L.apnn_select_variant_fused.argtypes = [ci, ci, ci, ci, ci, ci, ci]
+            L.apnn_select_variant_fused.restype = ci
             L.apnn_status_string.argtypes = [ci]
             L.apnn_status_string.restype = ctypes.c_char_p
             L.apnn_variant_name.argtypes = [ci]
@@ -110,7 +112,7 @@ def lib() -> ctypes.CDLL:
 ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_im2col_pack", "apnn_flatten_packed", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
                "apnn_conv2d", "apnn_conv2d_ex", "apnn_quant_pack_out", "apnn_pool_quant_pack_out",
                "apnn_residual_quant_pack",
-               "apnn_select_variant",
+               "apnn_select_variant", "apnn_select_variant_fused",
                "apnn_status_string", "apnn_variant_name", "apnn_launch_count", "apnn_version")
 
 
@@ -341,5 +343,8 @@ def residual_quant_pack(Y: torch.Tensor, Z: torch.Tensor, z_bits: int, epi: Epil
     return out
 
 
-def select_variant(M, N, K, a_bits, w_bits, enc) -> int:
+def select_variant(M, N, K, a_bits, w_bits, enc, out_bits: int = 0) -> int:
+    """Variant APNN_VARIANT_AUTO runs for this GEMM (out_bits > 0: the fused epilogue)."""
+    if out_bits:
+        return int(lib().apnn_select_variant_fused(M, N, K, a_bits, w_bits, enc, out_bits))
     return int(lib().apnn_select_variant(M, N, K, a_bits, w_bits, enc))

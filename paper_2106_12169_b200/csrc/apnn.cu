@@ -34,6 +34,9 @@ cudaError_t launch_b1mma(const uint32_t* A, const uint32_t* W, const Geom& g, co
 cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
                          int sms, cudaStream_t s);
 bool tc_i8_supports(const Geom& g);
+bool tc_fp4_supports(const Geom& g);
+cudaError_t launch_tc_fp4(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
+                          cudaStream_t s);
 bool b1mma_supports(const Geom& g);
 
 // ---- device properties (cached per device ordinal)
@@ -116,8 +119,28 @@ static apnn_status make_epi(const apnn_epilogue* epi, Epi* e) {
     return APNN_OK;
 }
 
-static apnn_variant resolve(apnn_variant v, const Geom& g) {
+// AUTO dispatch (measured, scripts/fp4_time.py, profiles/r01_fp4.json): the exact FP4
+// formulation wins every fused (requantised) GEMM with operands <= 2 bits above one CTA
+// row-tile, and int32-output w1a2 / w2a1 GEMMs from 2048^2; the int8 tensor-core variant
+// everything else (conv, wider codes, small-M split-K, residual / pooling epilogues).
+static bool fp4_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("APNN_FP4");
+        v = s ? atoi(s) : 1;
+    }
+    return v != 0;
+}
+
+static apnn_variant resolve(apnn_variant v, const Geom& g, const Epi* e = nullptr) {
     if (v != APNN_VARIANT_AUTO) return v;
+    const bool fused = e && e->out_bits > 0;
+    // the FP4 kernel is one CTA per 128 x 256 tile without split-K: require enough tiles to
+    // fill the SMs, else the int8 variant's split-K clusters win (VGG FC at batch 256)
+    const long long fp4_tiles = (long long)((g.M + 127) / 128) * ((g.N + 255) / 256);
+    if (fp4_enabled() && tc_fp4_supports(g) && fp4_tiles >= 64 && !(e && (e->res || e->pool)) &&
+        (fused || (g.a_bits + g.w_bits == 3 && g.M >= 2048 && g.N >= 2048)))
+        return APNN_VARIANT_TC_FP4;
     if (tc_i8_supports(g)) return APNN_VARIANT_TC_I8;
     return APNN_VARIANT_POPC;
 }
@@ -129,12 +152,16 @@ static apnn_status run(const uint32_t* A, const uint32_t* W, const Geom& g, cons
     if (st != APNN_OK) return st;
     if (g.M == 0 || g.N == 0) return APNN_OK;
     cudaError_t err;
-    switch (resolve(variant, g)) {
+    switch (resolve(variant, g, &e)) {
     case APNN_VARIANT_TC_I8:
         if (!tc_i8_supports(g)) return APNN_ERR_UNSUPPORTED;
         err = launch_tc_i8(A, W, g, e, Y, d.sms, s);
         break;
     case APNN_VARIANT_POPC: err = launch_popc(A, W, g, e, Y, s); break;
+    case APNN_VARIANT_TC_FP4:
+        if (!tc_fp4_supports(g) || e.res || e.pool) return APNN_ERR_UNSUPPORTED;
+        err = launch_tc_fp4(A, W, g, e, Y, s);
+        break;
     case APNN_VARIANT_B1MMA:
         if (!b1mma_supports(g)) return APNN_ERR_UNSUPPORTED;
         err = launch_b1mma(A, W, g, e, Y, s);
@@ -229,10 +256,12 @@ apnn_status apnn_gemm_ex(const uint32_t* A, const uint32_t* W, int M, int N, int
     Epi e;
     if ((st = make_epi(epi, &e)) != APNN_OK) return st;
     if (e.pool) return APNN_ERR_INVALID_ARG;  // pooling is a conv epilogue
-    if ((unsigned)variant > (unsigned)APNN_VARIANT_B1MMA) return APNN_ERR_INVALID_ARG;
+    if ((unsigned)variant > (unsigned)APNN_VARIANT_TC_FP4) return APNN_ERR_INVALID_ARG;
     Geom g;
     gemm_geom(&g, M, N, K, a_bits, w_bits, enc);
-    if (e.res && (resolve(variant, g) != APNN_VARIANT_TC_I8 || M <= 128)) return APNN_ERR_UNSUPPORTED;
+    if (e.res && (resolve(variant, g, &e) != APNN_VARIANT_TC_I8 || M <= 128 || enc == APNN_ENC_PM1_PM1 ||
+                  enc == APNN_ENC_W_01_A_PM1))
+        return APNN_ERR_UNSUPPORTED;  // fused residual: 2-CTA int8 kernel, 0/1 activations
     return run(A, W, g, e, Y, variant, (cudaStream_t)stream);
 }
 
@@ -269,7 +298,7 @@ apnn_status apnn_conv2d_ex(const uint32_t* X, const uint32_t* W, const apnn_conv
     if ((st = check_overflow(Kll, a_bits, w_bits, enc)) != APNN_OK) return st;
     Epi e;
     if ((st = make_epi(epi, &e)) != APNN_OK) return st;
-    if ((unsigned)variant > (unsigned)APNN_VARIANT_B1MMA) return APNN_ERR_INVALID_ARG;
+    if ((unsigned)variant > (unsigned)APNN_VARIANT_TC_FP4) return APNN_ERR_INVALID_ARG;
     Geom g;
     std::memset(&g, 0, sizeof(g));
     g.M = (int)Mll; g.N = c.C_out; g.K = (int)Kll;
@@ -281,7 +310,9 @@ apnn_status apnn_conv2d_ex(const uint32_t* X, const uint32_t* W, const apnn_conv
     g.nchunks = g.RS * g.CB;
     g.conv = 1;
     g.H = c.H; g.W = c.W; g.Ho = Ho; g.Wo = Wo; g.S = c.S; g.stride = c.stride; g.pad = c.pad;
-    if (e.res && (resolve(variant, g) != APNN_VARIANT_TC_I8 || g.M <= 128)) return APNN_ERR_UNSUPPORTED;
+    if (e.res && (resolve(variant, g, &e) != APNN_VARIANT_TC_I8 || g.M <= 128 || enc == APNN_ENC_PM1_PM1 ||
+                  enc == APNN_ENC_W_01_A_PM1))
+        return APNN_ERR_UNSUPPORTED;
     if (e.pool) {
         if (e.pool > Ho || e.pool > Wo) return APNN_ERR_SHAPE;
         if (resolve(variant, g) != APNN_VARIANT_TC_I8 || !tc_i8_pool_fusable(g, e)) return APNN_ERR_UNSUPPORTED;
@@ -355,6 +386,16 @@ apnn_variant apnn_select_variant(int M, int N, int K, int a_bits, int w_bits, ap
     return resolve(APNN_VARIANT_AUTO, g);
 }
 
+apnn_variant apnn_select_variant_fused(int M, int N, int K, int a_bits, int w_bits, apnn_encoding enc,
+                                       int out_bits) {
+    Geom g;
+    gemm_geom(&g, M, N, K, a_bits, w_bits, enc);
+    Epi e;
+    std::memset(&e, 0, sizeof(e));
+    e.out_bits = out_bits;
+    return resolve(APNN_VARIANT_AUTO, g, &e);
+}
+
 const char* apnn_status_string(apnn_status s) {
     switch (s) {
     case APNN_OK: return "ok";
@@ -376,6 +417,7 @@ const char* apnn_variant_name(apnn_variant v) {
     case APNN_VARIANT_TC_I8: return "tc_i8";
     case APNN_VARIANT_POPC: return "popc";
     case APNN_VARIANT_B1MMA: return "b1mma";
+    case APNN_VARIANT_TC_FP4: return "tc_fp4";
     }
     return "unknown";
 }

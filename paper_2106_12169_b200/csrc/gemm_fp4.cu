@@ -1,0 +1,367 @@
+// gemm_fp4.cu -- exact FP4 formulation of the AP-bit contraction (row f3, APNN_VARIANT_TC_FP4).
+//
+// For operands of at most 2 bits (0/1 codes 0..3, or +-1), every value is exactly
+// representable in e2m1 (0, 1, 2, 3 = 0x0, 0x2, 0x4, 0x5; +-1 = 0x2 / 0xA), every product
+// is an integer of magnitude <= 9, and an fp32 accumulator is exact while |Y| < 2^24
+// (host check K * max|a| * max|w| < 2^24).  So the bit combination of PAPER.md:1426-1429,
+// applied to the operands as in the int8 path, can feed
+// `tcgen05.mma kind::mxf4.block_scale` with all block scales 2^0 (E8M0 127): the fp4 pipe,
+// twice the int8 rate on B200, and half the operand bytes the recombination writes.
+//
+// Kernel (one CTA, 128 x BN output tile, BN = 128 or 256):
+//   warp 0      TMA producer: planes of 2 k-blocks (256 K elements) per stage
+//   warp 1      TMEM allocator, single-thread MMA issuer (4 x 128xBNx64 per stage)
+//   warps 2-9   recombination planes -> e2m1 nibbles into the K-major SWIZZLE_128B operand
+//               tiles (A and B both in shared memory), then the epilogue (fp32 -> int32,
+//               int32 store or the fused requantisation of tc_common.cuh)
+// Element order: 16-byte chunk (kb2*4 + gi) of a row holds the 32 elements of group gi of
+// k-block kb2; word j of it holds elements {j, j+4, ..., j+28} (nibble n = element j+4n):
+// the same permutation for A and B, so the dot product is unchanged.
+#include <cuda.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "tc_common.cuh"
+
+namespace apnn {
+namespace fp4 {
+
+using namespace sm100;
+
+constexpr int BM = 128;
+constexpr int THREADS = 10 * 32;
+constexpr int MAXS = 6;
+constexpr uint32_t kSfCols = 16;  // scale-factor TMEM columns per operand (all bytes 0x7F = 2^0)
+
+struct Params {
+    Geom g;
+    Epi e;
+    void* Y;
+    int stages;
+    int nst;             // stages (of 2 k-blocks) along K
+    uint32_t a_bytes;    // plane bytes per stage (A: 128 rows x a_bits x 32 B)
+    uint32_t b_bytes;    // (B: BN rows x w_bits x 32 B)
+    uint32_t tmem_cols;
+    int tab_mode;
+};
+
+// block-scaled instruction descriptor: E2M1 x E2M1 (MXF4 format 1), fp32 D, K-major,
+// E8M0 scales, M = 128, N, dense K = 64 (cute::UMMA::InstrDescriptorBlockScaled layout)
+__host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
+    return (1u << 7)                      // A format: E2M1
+           | (1u << 10)                   // B format: E2M1
+           | ((uint32_t)(N >> 3) << 17)   // N / 8
+           | (1u << 23)                   // scale format: E8M0
+           | ((uint32_t)(M >> 4) << 24);  // M / 16
+}
+
+__device__ __forceinline__ void mma_mxf4(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+            d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+        : "memory");
+}
+
+// 32 elements of one plane group -> 4 words of e2m1 nibbles (word j: elements j + 4n)
+template <int NB, bool PM1>
+__device__ __forceinline__ void decode_group_fp4(const uint32_t (&pw)[2], uint32_t vm, bool masked,
+                                                 uint32_t (&o)[4]) {
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const uint32_t b0 = (pw[0] >> j) & 0x11111111u;
+        uint32_t w;
+        if (PM1) {  // +1 -> 0x2, -1 -> 0xA; elements outside vm -> 0
+            w = 0x22222222u | ((b0 ^ 0x11111111u) << 3);
+            if (masked) w &= ((vm >> j) & 0x11111111u) * 0xFu;
+        } else if (NB == 1) {  // 0 -> 0x0, 1 -> 0x2
+            w = b0 << 1;
+        } else {  // 0, 1, 2, 3 -> 0x0, 0x2, 0x4, 0x5
+            const uint32_t b1 = (pw[1] >> j) & 0x11111111u;
+            w = (b1 << 2) | ((b0 & ~b1) << 1) | (b0 & b1);
+        }
+        o[j] = w;
+    }
+}
+
+// one operand row of a stage (2 k-blocks): planes smem [plane][rows][32 B] -> 128-byte
+// K-major SWIZZLE_128B row of e2m1 nibbles
+template <int NB, bool PM1>
+__device__ __forceinline__ void recomb_row(const uint8_t* planes, int rows, int row, uint8_t* op, int kvalid0) {
+    const uint4* src = reinterpret_cast<const uint4*>(planes);
+    uint4 v[NB][2];
+#pragma unroll
+    for (int pl = 0; pl < NB; pl++) {
+        v[pl][0] = src[(pl * rows + row) * 2];
+        v[pl][1] = src[(pl * rows + row) * 2 + 1];
+    }
+#pragma unroll
+    for (int kb2 = 0; kb2 < 2; kb2++) {
+        const int kvalid = kvalid0 - kb2 * 128;
+#pragma unroll
+        for (int gi = 0; gi < 4; gi++) {
+            uint32_t pw[2] = {0u, 0u};
+#pragma unroll
+            for (int pl = 0; pl < NB; pl++) pw[pl] = tc::sel4(v[pl][kb2], gi);
+            uint32_t o[4];
+            decode_group_fp4<NB, PM1>(pw, tc::valid_mask(kvalid, gi), PM1 && kvalid < 128, o);
+            *reinterpret_cast<uint4*>(op + tc::b_chunk_offset(row, kb2 * 4 + gi)) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    }
+}
+
+template <bool PM1>
+__device__ __forceinline__ void recomb_row_any(int nb, const uint8_t* planes, int rows, int row, uint8_t* op,
+                                               int kvalid) {
+    if (PM1) recomb_row<1, true>(planes, rows, row, op, kvalid);
+    else if (nb == 1) recomb_row<1, false>(planes, rows, row, op, kvalid);
+    else recomb_row<2, false>(planes, rows, row, op, kvalid);
+}
+
+template <int BN, bool A_PM1, bool W_PM1>
+__global__ void __launch_bounds__(THREADS, 1)
+    fp4_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB, const Params p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int S = p.stages;
+    uint8_t* sAop = smem;                                   // S x 128 x 128 B
+    uint8_t* sBop = sAop + (size_t)S * BM * 128;            // S x BN x 128 B
+    uint8_t* sApl = sBop + (size_t)S * BN * 128;            // S x a_bytes
+    uint8_t* sBpl = sApl + (size_t)S * p.a_bytes;           // S x b_bytes
+    int32_t* sTab = reinterpret_cast<int32_t*>(sBpl + (size_t)S * p.b_bytes);  // BN x kTabStride
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sTab + BN * tc::kTabStride);
+    uint64_t* plane_full = bars;
+    uint64_t* plane_empty = bars + MAXS;
+    uint64_t* op_full = bars + 2 * MAXS;
+    uint64_t* op_empty = bars + 3 * MAXS;
+    uint64_t* accum_full = bars + 4 * MAXS;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * MAXS + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    const Geom& g = p.g;
+    const int nst = p.nst;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmapA);
+        tma_prefetch(&tmapB);
+        for (int s = 0; s < S; s++) {
+            mbar_init(&plane_full[s], 1);
+            mbar_init(&plane_empty[s], 8);
+            mbar_init(&op_full[s], 8);
+            mbar_init(&op_empty[s], 1);
+        }
+        mbar_init(accum_full, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc_dyn(tmem_holder, p.tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_holder;
+    const uint32_t sfa = tmem + BN, sfb = tmem + BN + kSfCols;
+    if (warp >= 2 && warp < 6) {  // every scale factor byte = E8M0 127 (2^0), all 128 lanes
+        const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // warp w owns lanes 32*(w%4)..
+        const uint32_t ones[8] = {0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu,
+                                  0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu};
+#pragma unroll
+        for (uint32_t c = 0; c < 2 * kSfCols; c += 8) tmem_st8(lane_base + BN + c, ones);
+        tmem_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < nst; i++) {
+                const int s = i % S;
+                const uint32_t ph = (i / S) & 1;
+                mbar_wait(&plane_empty[s], ph ^ 1);
+                mbar_arrive_expect_tx(&plane_full[s], p.a_bytes + p.b_bytes);
+                tma_load_4d(sApl + (size_t)s * p.a_bytes, &tmapA, &plane_full[s], i * 8, m0, 0, 0);
+                tma_load_4d(sBpl + (size_t)s * p.b_bytes, &tmapB, &plane_full[s], i * 8, n0, 0, 0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = idesc_mxf4(BM, BN);
+            for (int i = 0; i < nst; i++) {
+                const int s = i % S;
+                const uint32_t ph = (i / S) & 1;
+                mbar_wait(&op_full[s], ph);
+                tc_fence_after();
+                const uint32_t abase = smem_u32(sAop + (size_t)s * BM * 128);
+                const uint32_t bbase = smem_u32(sBop + (size_t)s * BN * 128);
+#pragma unroll
+                for (int kk = 0; kk < 4; kk++)  // K = 64 fp4 elements = 32 bytes per MMA
+                    mma_mxf4(tmem, tc::b_desc(abase, kk), tc::b_desc(bbase, kk), idesc, sfa, sfb, (i | kk) != 0);
+                mma_commit(&op_empty[s]);
+            }
+            mma_commit(accum_full);
+        }
+    } else {
+        const int q = warp & 3;
+        const int grp = (warp - 2) >> 2;  // 0: A rows, 1: B rows (BN = 128) / B rows t, t+128
+        const int t = q * 32 + lane;
+        const int et = threadIdx.x - 64;
+        const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
+        if ((p.tab_mode == tc::kTabQ3 || p.tab_mode == tc::kTabHybrid) && et < BN)
+            tc::build_threshold_row(sTab + et * tc::kTabStride, n0 + et, g.N, p.e);
+        for (int i = 0; i < nst; i++) {
+            const int s = i % S;
+            const uint32_t ph = (i / S) & 1;
+            int kvalid = 256;  // +-1 x +-1: padded K decodes to 0
+            if (A_PM1 && W_PM1) {
+                const int rem = g.K - i * 256;
+                kvalid = rem < 256 ? rem : 256;
+            }
+            mbar_wait(&plane_full[s], ph);
+            mbar_wait(&op_empty[s], ph ^ 1);
+            if (grp == 0) {
+                recomb_row_any<A_PM1>(g.a_bits, sApl + (size_t)s * p.a_bytes, BM, t, sAop + (size_t)s * BM * 128,
+                                      kvalid);
+            } else {
+                const uint8_t* bpl = sBpl + (size_t)s * p.b_bytes;
+                uint8_t* bop = sBop + (size_t)s * BN * 128;
+                recomb_row_any<W_PM1>(g.w_bits, bpl, BN, t, bop, kvalid);
+                if (BN > 128) recomb_row_any<W_PM1>(g.w_bits, bpl, BN, t + 128, bop, kvalid);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&plane_empty[s]);
+                mbar_arrive(&op_full[s]);
+            }
+        }
+        named_bar_sync(1, 256);  // threshold table complete
+        mbar_wait(accum_full, 0);
+        tc_fence_after();
+        const int m = m0 + t;
+        constexpr int half = BN / 2;
+#pragma unroll 1
+        for (int c = grp * half; c < (grp + 1) * half; c += 32) {
+            uint32_t acc[32];
+            tmem_ld32(tmem_lane + c, acc);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 32; k++) acc[k] = (uint32_t)__float2int_rn(__uint_as_float(acc[k]));  // exact
+            tc::epilogue_chunk(acc, m, n0 + c, c, g, p.e, p.Y, sTab, p.tab_mode);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, p.tmem_cols);
+    }
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(ptr);
+        else
+            cudaGetLastError();
+    });
+    return fn;
+}
+
+// packed [rows][bits][Kw] as {Kw, rows, bits}; box {8 words = 2 k-blocks, box_rows, bits}
+// lands as [plane][row][32 B]
+static bool make_map(CUtensorMap* m, const uint32_t* base, int rows, int bits, int Kw, int box_rows) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)Kw, (cuuint64_t)rows, (cuuint64_t)bits, 1};
+    cuuint64_t strides[3] = {(cuuint64_t)bits * Kw * 4, (cuuint64_t)Kw * 4, (cuuint64_t)bits * Kw * 4 * rows};
+    cuuint32_t box[4] = {8, (cuuint32_t)box_rows, (cuuint32_t)bits, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint32_t*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, bool AP, bool WP>
+static cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, dim3 grid, size_t smem,
+                          cudaStream_t s) {
+    auto kfn = fp4_kernel<BN, AP, WP>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    kfn<<<grid, THREADS, smem, s>>>(ta, tb, p);
+    return cudaGetLastError();
+}
+
+template <int BN>
+static cudaError_t launch_enc(int enc, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, dim3 grid,
+                              size_t smem, cudaStream_t s) {
+    switch (enc) {
+    case APNN_ENC_01_01: return launch<BN, false, false>(ta, tb, p, grid, smem, s);
+    case APNN_ENC_PM1_PM1: return launch<BN, true, true>(ta, tb, p, grid, smem, s);
+    case APNN_ENC_W_PM1_A_01: return launch<BN, false, true>(ta, tb, p, grid, smem, s);
+    default: return launch<BN, true, false>(ta, tb, p, grid, smem, s);
+    }
+}
+
+}  // namespace fp4
+
+// GEMM with both operands of at most 2 bits and |Y| < 2^24 (exact fp32 accumulation)
+bool tc_fp4_supports(const Geom& g) {
+    if (g.conv || g.K <= 0 || g.M <= 0 || g.N <= 0 || g.a_bits > 2 || g.w_bits > 2) return false;
+    const long long ma = (g.enc == APNN_ENC_PM1_PM1 || g.enc == APNN_ENC_W_01_A_PM1) ? 1 : (1 << g.a_bits) - 1;
+    const long long mw = (g.enc == APNN_ENC_PM1_PM1 || g.enc == APNN_ENC_W_PM1_A_01) ? 1 : (1 << g.w_bits) - 1;
+    return (long long)g.K * ma * mw < (1LL << 24);
+}
+
+cudaError_t launch_tc_fp4(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
+                          cudaStream_t s) {
+    using namespace fp4;
+    Params p;
+    std::memset(&p, 0, sizeof(p));
+    p.g = g;
+    p.e = e;
+    p.Y = Y;
+    const int Kw = (g.K + 127) / 128 * 4;
+    p.nst = (Kw + 7) / 8;  // stages of 2 k-blocks (the TMA zero-fills a missing second k-block)
+    p.tab_mode = tc::kTabNone;
+    if (e.out_bits > 0 && e.out_bits <= 2) p.tab_mode = tc::kTabQ3;
+    else if (e.out_bits > 2 && (unsigned long long)e.qmax * (unsigned long long)e.S <= 0xFFFFFFFFull)
+        p.tab_mode = tc::kTabHybrid;
+    const int ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
+    const int BN = g.N > 128 ? 256 : 128;
+    p.a_bytes = 32u * BM * g.a_bits;
+    p.b_bytes = 32u * BN * g.w_bits;
+    const size_t per = (size_t)(BM + BN) * 128 + p.a_bytes + p.b_bytes;
+    const size_t fixed = (size_t)BN * tc::kTabStride * 4 + (4 * MAXS + 4) * 8 + 1024;
+    int S = (int)((227 * 1024 - fixed) / per);
+    if (S > MAXS) S = MAXS;
+    if (S < 2) return cudaErrorInvalidConfiguration;
+    p.stages = S;
+    uint32_t cols = BN + 2 * kSfCols, pow2 = 32;
+    while (pow2 < cols) pow2 <<= 1;
+    p.tmem_cols = pow2;
+    const size_t smem = (size_t)S * per + fixed - 1024 + 64;
+    CUtensorMap ta, tb;
+    if (!make_map(&ta, A, g.M, g.a_bits, Kw, BM) || !make_map(&tb, W, g.N, g.w_bits, Kw, BN))
+        return cudaErrorInvalidValue;
+    dim3 grid((g.M + BM - 1) / BM, (ncols + BN - 1) / BN);
+    cudaError_t err = BN == 256 ? launch_enc<256>(g.enc, ta, tb, p, grid, smem, s)
+                                : launch_enc<128>(g.enc, ta, tb, p, grid, smem, s);
+    count_launch();
+    return err;
+}
+
+}  // namespace apnn

@@ -204,7 +204,7 @@ constexpr int T2_MMA_WARP = T2_TMA_WARP + 1;        // warp 21: TMEM allocator +
 constexpr int T2_THREADS = (T2_MMA_WARP + 1) * 32;
 
 // BNP = N of the pair tile (256 / 128 / 64); each CTA holds BNP/2 B rows.
-template <int BNP, bool A_PM1, bool W_PM1, bool SCALED>
+template <int BNP, bool A_PM1, bool W_PM1, bool SCALED, bool RES = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     tc2_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
                const __grid_constant__ CUtensorMap tmapY, const Params p) {
@@ -531,10 +531,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                     }
                 } else if (use_tma || use_lsu) {
                     uint32_t w[8];
-                    requant_chunk(acc, n0 + c, c, g, p.e, sTab, p.tab_mode, w, m);
+                    requant_chunk<RES>(acc, n0 + c, c, g, p.e, sTab, p.tab_mode, w, m);
                     stage_words(w, ob, p.nwb, c >> 5, reinterpret_cast<uint32_t*>(stg), lane);
                 } else {
-                    epilogue_chunk(acc, m, n0 + c, c, g, p.e, p.Y, sTab, p.tab_mode);
+                    epilogue_chunk<RES>(acc, m, n0 + c, c, g, p.e, p.Y, sTab, p.tab_mode);
                 }
             }
             tc_fence_before();
@@ -969,6 +969,10 @@ template <int BNP, bool AP, bool WP>
 static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, const Params& p,
                            int grid, size_t smem, cudaStream_t s) {
     auto kfn = p.acc_shift > 0 ? tc2_kernel<BNP, AP, WP, true> : tc2_kernel<BNP, AP, WP, false>;
+    if constexpr (!AP) {  // fused residual instances (0/1 activations: the ResNet encodings)
+        if (p.tab_mode == kTabResidual)
+            kfn = p.acc_shift > 0 ? tc2_kernel<BNP, AP, WP, true, true> : tc2_kernel<BNP, AP, WP, false, true>;
+    }
     cudaError_t e = set_smem(kfn);
     if (e != cudaSuccess) return e;
     kfn<<<grid, T2_THREADS, smem, s>>>(ta, tb, ty, p);

@@ -496,6 +496,10 @@ __device__ __forceinline__ void residual_chunk_bytes(const uint32_t (&acc)[32], 
     }
 }
 
+// RES: compile the residual branch (kTabResidual) in -- only the residual kernel instances,
+// so the others keep their register allocation (the residual code cost the 2-CTA kernel
+// ~100 bytes of spills per thread when always present)
+template <bool RES = false>
 __device__ __forceinline__ void requant_chunk(const uint32_t (&acc)[32], int nb, int lc, const Geom& g,
                                               const Epi& e, const int32_t* tab, int tab_mode,
                                               uint32_t (&words)[8], int m = 0) {
@@ -506,7 +510,7 @@ __device__ __forceinline__ void requant_chunk(const uint32_t (&acc)[32], int nb,
     uint32_t qb[8];
 #pragma unroll
     for (int i = 0; i < 8; i++) qb[i] = 0;
-    if (tab_mode == kTabResidual) {
+    if (RES) {
         residual_chunk_bytes(acc, m, nb, g, e, qb);
     } else if (tab_mode == kTabHybrid) {
         const uint32_t S = (uint32_t)e.S, Q = (uint32_t)e.qmax;
@@ -536,6 +540,7 @@ __device__ __forceinline__ void requant_chunk(const uint32_t (&acc)[32], int nb,
 // Direct (per-thread) stores of one 32-column chunk of row m: int32 row segment, or
 // the out_bits plane words.  Used where a TMA store box does not fit (partial conv
 // row slabs, the one-CTA kernel's packed output).
+template <bool RES = false>
 __device__ __forceinline__ void epilogue_chunk(const uint32_t (&acc)[32], int m, int nb, int lc, const Geom& g,
                                                const Epi& e, void* Yout, const int32_t* tab, int tab_mode) {
     if (m >= g.M) return;
@@ -558,7 +563,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&acc)[32], int m,
     if (word >= Nw) return;
     uint32_t* o = reinterpret_cast<uint32_t*>(Yout) + (long long)m * e.out_bits * Nw + word;
     uint32_t w[8];
-    requant_chunk(acc, nb, lc, g, e, tab, tab_mode, w, m);
+    requant_chunk<RES>(acc, nb, lc, g, e, tab, tab_mode, w, m);
 #pragma unroll
     for (int tb = 0; tb < 8; tb++)
         if (tb < e.out_bits) o[(long long)tb * Nw] = w[tb];

@@ -264,10 +264,12 @@ def _sample_rows(M, n, tag):
 
 
 @pytest.mark.parametrize("fused", [False, True])
-def test_full_size_bench_config_sampled_rows(fused):
+@pytest.mark.parametrize("variant", [ap.VARIANT_AUTO, ap.VARIANT_TC_I8, ap.VARIANT_TC_FP4])
+def test_full_size_bench_config_sampled_rows(fused, variant):
     # BASELINE.json configs[1] at its largest point, exactly as bench.py runs it:
-    # M = N = K = 8192, w1a2, Case III, auto variant (tcgen05 2-CTA kernel); rows
-    # sampled (first/last 4 + random) and checked against the oracle one by one.
+    # M = N = K = 8192, w1a2, Case III, auto variant (the exact-FP4 kernel for the fused
+    # bench step) and both tensor-core variants explicitly; rows sampled
+    # (first/last 4 + random) and checked against the oracle one by one.
     M = N = K = 8192
     a, w, enc = 2, 1, 2
     A, W = synth.gemm_inputs(M, N, K, a, w, tag="bench")
@@ -276,8 +278,8 @@ def test_full_size_bench_config_sampled_rows(fused):
     epi = ap.Epilogue(a, cuda(alpha), cuda(beta), S) if fused else None
     Ap = ap.pack_bits(cuda(A), a)
     Wp = ap.pack_bits(cuda(W), w)
-    assert ap.select_variant(M, N, K, a, w, enc) == ap.VARIANT_TC_I8
-    Y = ap.gemm(Ap, Wp, M, N, K, a, w, enc, epi=epi)
+    assert ap.select_variant(M, N, K, a, w, enc, a if fused else 0) == ap.VARIANT_TC_FP4
+    Y = ap.gemm(Ap, Wp, M, N, K, a, w, enc, epi=epi, variant=variant)
     torch.cuda.synchronize()
     rows = _sample_rows(M, 24, "fullsize")
     want = oracle.gemm(A[rows], W, a, w, enc)
@@ -424,3 +426,24 @@ def test_fused_residual_epilogue(M, N, K, zb):
     assert st == 0
     torch.cuda.synchronize()
     np.testing.assert_array_equal(u32(out), want)
+
+
+# ------------------------------------------------ exact FP4 formulation (row f3)
+
+@pytest.mark.parametrize("M,N,K", [(150, 270, 300), (256, 256, 1024), (7, 33, 129), (300, 100, 2048)])
+@pytest.mark.parametrize("a_bits,w_bits,enc", [(2, 1, 2), (2, 2, 0), (1, 1, 1), (1, 2, 3), (1, 1, 0)])
+def test_fp4_variant_exact(M, N, K, a_bits, w_bits, enc):
+    A, W = synth.gemm_inputs(M, N, K, a_bits, w_bits, tag="fp4")
+    Y = oracle.gemm(A, W, a_bits, w_bits, enc)
+    got = run_gemm(A, W, a_bits, w_bits, enc, ap.VARIANT_TC_FP4)
+    np.testing.assert_array_equal(got.cpu().numpy(), Y)
+    alpha, beta, S = epi_case(N, 2, "fp4")
+    want = oracle.pack(oracle.epilogue(Y, alpha, beta, S, 2), 2)
+    got = run_gemm(A, W, a_bits, w_bits, enc, ap.VARIANT_TC_FP4, epi=ap.Epilogue(2, cuda(alpha), cuda(beta), S))
+    np.testing.assert_array_equal(u32(got), want)
+
+
+def test_fp4_variant_rejects_wide_codes():
+    A, W = synth.gemm_inputs(64, 64, 128, 4, 1, tag="fp4rej")
+    with pytest.raises(ap.ApnnError):
+        run_gemm(A, W, 4, 1, 2, ap.VARIANT_TC_FP4)
