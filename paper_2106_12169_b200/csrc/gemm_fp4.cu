@@ -32,7 +32,8 @@ using namespace sm100;
 
 constexpr int BM = 128;
 constexpr int THREADS = 10 * 32;
-constexpr int MAXS = 6;
+constexpr int MAXS = 6;    // operand stages
+constexpr int MAXSP = 12;  // packed-plane stages (a deeper ring: TMA latency)
 constexpr uint32_t kSfCols = 16;  // scale-factor TMEM columns per operand (all bytes 0x7F = 2^0)
 
 struct Params {
@@ -40,6 +41,7 @@ struct Params {
     Epi e;
     void* Y;
     int stages;
+    int pstages;
     int nst;             // stages (of 2 k-blocks) along K
     uint32_t a_bytes;    // plane bytes per stage (A: 128 rows x a_bits x 32 B)
     uint32_t b_bytes;    // (B: BN rows x w_bits x 32 B)
@@ -127,19 +129,19 @@ template <int BN, bool A_PM1, bool W_PM1>
 __global__ void __launch_bounds__(THREADS, 1)
     fp4_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB, const Params p) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int S = p.stages;
+    const int S = p.stages, SP = p.pstages;
     uint8_t* sAop = smem;                                   // S x 128 x 128 B
     uint8_t* sBop = sAop + (size_t)S * BM * 128;            // S x BN x 128 B
-    uint8_t* sApl = sBop + (size_t)S * BN * 128;            // S x a_bytes
-    uint8_t* sBpl = sApl + (size_t)S * p.a_bytes;           // S x b_bytes
-    int32_t* sTab = reinterpret_cast<int32_t*>(sBpl + (size_t)S * p.b_bytes);  // BN x kTabStride
+    uint8_t* sApl = sBop + (size_t)S * BN * 128;            // SP x a_bytes
+    uint8_t* sBpl = sApl + (size_t)SP * p.a_bytes;          // SP x b_bytes
+    int32_t* sTab = reinterpret_cast<int32_t*>(sBpl + (size_t)SP * p.b_bytes);  // BN x kTabStride
     uint64_t* bars = reinterpret_cast<uint64_t*>(sTab + BN * tc::kTabStride);
-    uint64_t* plane_full = bars;
-    uint64_t* plane_empty = bars + MAXS;
-    uint64_t* op_full = bars + 2 * MAXS;
-    uint64_t* op_empty = bars + 3 * MAXS;
-    uint64_t* accum_full = bars + 4 * MAXS;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * MAXS + 2);
+    uint64_t* plane_full = bars;                            // [MAXSP]
+    uint64_t* plane_empty = bars + MAXSP;                   // [MAXSP]
+    uint64_t* op_full = bars + 2 * MAXSP;                   // [MAXS]
+    uint64_t* op_empty = op_full + MAXS;                    // [MAXS]
+    uint64_t* accum_full = op_empty + MAXS;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accum_full + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
@@ -149,9 +151,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmapA);
         tma_prefetch(&tmapB);
-        for (int s = 0; s < S; s++) {
+        for (int s = 0; s < SP; s++) {
             mbar_init(&plane_full[s], 1);
             mbar_init(&plane_empty[s], 8);
+        }
+        for (int s = 0; s < S; s++) {
             mbar_init(&op_full[s], 8);
             mbar_init(&op_empty[s], 1);
         }
@@ -178,9 +182,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            for (int i = 0; i < nst; i++) {
-                const int s = i % S;
-                const uint32_t ph = (i / S) & 1;
+            int s = 0;
+            uint32_t ph = 0;
+            for (int i = 0; i < nst; i++, s = (s + 1 == SP) ? 0 : s + 1, ph ^= (s == 0)) {  // no divisions
                 mbar_wait(&plane_empty[s], ph ^ 1);
                 mbar_arrive_expect_tx(&plane_full[s], p.a_bytes + p.b_bytes);
                 tma_load_4d(sApl + (size_t)s * p.a_bytes, &tmapA, &plane_full[s], i * 8, m0, 0, 0);
@@ -190,9 +194,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else if (warp == 1) {
         if (lane == 0) {
             const uint32_t idesc = idesc_mxf4(BM, BN);
-            for (int i = 0; i < nst; i++) {
-                const int s = i % S;
-                const uint32_t ph = (i / S) & 1;
+            int s = 0;
+            uint32_t ph = 0;
+            for (int i = 0; i < nst; i++, s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
                 mbar_wait(&op_full[s], ph);
                 tc_fence_after();
                 const uint32_t abase = smem_u32(sAop + (size_t)s * BM * 128);
@@ -212,21 +216,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
         if ((p.tab_mode == tc::kTabQ3 || p.tab_mode == tc::kTabHybrid) && et < BN)
             tc::build_threshold_row(sTab + et * tc::kTabStride, n0 + et, g.N, p.e);
-        for (int i = 0; i < nst; i++) {
-            const int s = i % S;
-            const uint32_t ph = (i / S) & 1;
+        int s = 0, ps = 0;
+        uint32_t ph = 0, pph = 0;
+        for (int i = 0; i < nst; i++, s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0),
+                 ps = (ps + 1 == SP) ? 0 : ps + 1, pph ^= (ps == 0)) {
             int kvalid = 256;  // +-1 x +-1: padded K decodes to 0
             if (A_PM1 && W_PM1) {
                 const int rem = g.K - i * 256;
                 kvalid = rem < 256 ? rem : 256;
             }
-            mbar_wait(&plane_full[s], ph);
+            mbar_wait(&plane_full[ps], pph);
             mbar_wait(&op_empty[s], ph ^ 1);
             if (grp == 0) {
-                recomb_row_any<A_PM1>(g.a_bits, sApl + (size_t)s * p.a_bytes, BM, t, sAop + (size_t)s * BM * 128,
+                recomb_row_any<A_PM1>(g.a_bits, sApl + (size_t)ps * p.a_bytes, BM, t, sAop + (size_t)s * BM * 128,
                                       kvalid);
             } else {
-                const uint8_t* bpl = sBpl + (size_t)s * p.b_bytes;
+                const uint8_t* bpl = sBpl + (size_t)ps * p.b_bytes;
                 uint8_t* bop = sBop + (size_t)s * BN * 128;
                 recomb_row_any<W_PM1>(g.w_bits, bpl, BN, t, bop, kvalid);
                 if (BN > 128) recomb_row_any<W_PM1>(g.w_bits, bpl, BN, t + 128, bop, kvalid);
@@ -234,7 +239,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(&plane_empty[s]);
+                mbar_arrive(&plane_empty[ps]);
                 mbar_arrive(&op_full[s]);
             }
         }
@@ -318,6 +323,17 @@ static cudaError_t launch_enc(int enc, const CUtensorMap& ta, const CUtensorMap&
 
 }  // namespace fp4
 
+static int fp4_op_stages() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("APNN_FP4_S");
+        v = s ? atoi(s) : 3;  // measured (8192^3 w1a2 fused): S = 2 / 3 / 4 -> 2616 / 2922 / 2926 TOPS
+        if (v < 2) v = 2;
+        if (v > fp4::MAXS) v = fp4::MAXS;
+    }
+    return v;
+}
+
 // GEMM with both operands of at most 2 bits and |Y| < 2^24 (exact fp32 accumulation)
 bool tc_fp4_supports(const Geom& g) {
     if (g.conv || g.K <= 0 || g.M <= 0 || g.N <= 0 || g.a_bits > 2 || g.w_bits > 2) return false;
@@ -344,16 +360,24 @@ cudaError_t launch_tc_fp4(const uint32_t* A, const uint32_t* W, const Geom& g, c
     const int BN = g.N > 128 ? 256 : 128;
     p.a_bytes = 32u * BM * g.a_bits;
     p.b_bytes = 32u * BN * g.w_bits;
-    const size_t per = (size_t)(BM + BN) * 128 + p.a_bytes + p.b_bytes;
-    const size_t fixed = (size_t)BN * tc::kTabStride * 4 + (4 * MAXS + 4) * 8 + 1024;
-    int S = (int)((227 * 1024 - fixed) / per);
-    if (S > MAXS) S = MAXS;
+    const size_t op = (size_t)(BM + BN) * 128, pl = p.a_bytes + p.b_bytes;
+    const size_t fixed = (size_t)BN * tc::kTabStride * 4 + (2 * MAXSP + 2 * MAXS + 4) * 8 + 1024;
+    const size_t budget = 227 * 1024 - fixed;
+    // operand ring S (3 stages), plane ring SP as deep
+    // as the rest of shared memory allows (it hides the TMA latency); APNN_FP4_S overrides S
+    int S = fp4_op_stages();
+    if (S * op + 2 * pl > budget) S = (int)((budget - 2 * pl) / op);
     if (S < 2) return cudaErrorInvalidConfiguration;
+    int SP = (int)((budget - S * op) / pl);
+    if (SP > MAXSP) SP = MAXSP;
+    if (SP < 2) return cudaErrorInvalidConfiguration;
     p.stages = S;
+    p.pstages = SP;
+    const size_t per_total = S * op + SP * pl;
     uint32_t cols = BN + 2 * kSfCols, pow2 = 32;
     while (pow2 < cols) pow2 <<= 1;
     p.tmem_cols = pow2;
-    const size_t smem = (size_t)S * per + fixed - 1024 + 64;
+    const size_t smem = per_total + fixed - 1024 + 64;
     CUtensorMap ta, tb;
     if (!make_map(&ta, A, g.M, g.a_bits, Kw, BM) || !make_map(&tb, W, g.N, g.w_bits, Kw, BN))
         return cudaErrorInvalidValue;
