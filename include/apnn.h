@@ -234,6 +234,22 @@ apnn_status apnn_residual_quant_pack(const int32_t *Y, int M, int N, const void 
                                      const int32_t *rho, const apnn_epilogue *epi, uint32_t *out,
                                      apnn_stream_t stream);
 
+/* Prepared weights for the exact-FP4 variant (weights are static): the
+ * operand-side bit combination of W done once, at load time, instead of per output tile.
+ *   W:  device packed [N][w_bits][roundup(K,128)/32] (w_bits <= 2, or 1-bit +-1)
+ *   Wp: device, apnn_prepared_bytes(N, K) bytes: e2m1 nibbles [N][roundup(K,128)/2] in the
+ *       kernel's element order (an opaque layout for apnn_gemm_prepared); padding is value 0.
+ * APNN_ERR_UNSUPPORTED for w_bits > 2. */
+size_t apnn_prepared_bytes(int N, int K);
+apnn_status apnn_prepare_weights(const uint32_t *W, int N, int K, int w_bits, apnn_encoding enc, uint8_t *Wp,
+                                 apnn_stream_t stream);
+/* apnn_gemm_ex (int32 when epi == NULL, else the fused routine without pooling / residual)
+ * with prepared weights on the exact-FP4 kernel; a_bits <= 2 and K*max|a|*max|w| < 2^24,
+ * else APNN_ERR_UNSUPPORTED.  Same results as apnn_gemm_ex. */
+apnn_status apnn_gemm_prepared(const uint32_t *A, const uint8_t *Wp, int M, int N, int K, int a_bits,
+                               int w_bits, apnn_encoding enc, const apnn_epilogue *epi, void *Y,
+                               apnn_stream_t stream);
+
 /* Which variant APNN_VARIANT_AUTO resolves to for this problem (no launch): int32 output,
  * or the fused element-wise routine with out_bits (1..8) packed output. */
 apnn_variant apnn_select_variant(int M, int N, int K, int a_bits, int w_bits, apnn_encoding enc);

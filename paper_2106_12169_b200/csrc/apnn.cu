@@ -37,6 +37,10 @@ bool tc_i8_supports(const Geom& g);
 bool tc_fp4_supports(const Geom& g);
 cudaError_t launch_tc_fp4(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
                           cudaStream_t s);
+cudaError_t launch_tc_fp4_prepared(const uint32_t* A, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
+                                   cudaStream_t s);
+cudaError_t launch_prepare_weights(const uint32_t* W, int N, int K, int w_bits, int enc, uint8_t* out, int sms,
+                                   cudaStream_t s);
 bool b1mma_supports(const Geom& g);
 
 // ---- device properties (cached per device ordinal)
@@ -263,6 +267,48 @@ apnn_status apnn_gemm_ex(const uint32_t* A, const uint32_t* W, int M, int N, int
                   enc == APNN_ENC_W_01_A_PM1))
         return APNN_ERR_UNSUPPORTED;  // fused residual: 2-CTA int8 kernel, 0/1 activations
     return run(A, W, g, e, Y, variant, (cudaStream_t)stream);
+}
+
+size_t apnn_prepared_bytes(int N, int K) {
+    if (N < 0 || K < 0) return 0;
+    return (size_t)N * (((size_t)K + 127) / 128 * 64);
+}
+
+apnn_status apnn_prepare_weights(const uint32_t* W, int N, int K, int w_bits, apnn_encoding enc, uint8_t* Wp,
+                                 apnn_stream_t stream) {
+    if (N < 0 || K < 0) return APNN_ERR_SHAPE;
+    apnn_status st = APNN_OK;
+    if (w_bits < 1 || w_bits > 8) return APNN_ERR_BITS;
+    if (enc < 0 || enc > 3) return APNN_ERR_ENCODING;
+    const bool wpm = enc == APNN_ENC_PM1_PM1 || enc == APNN_ENC_W_PM1_A_01;
+    if (wpm && w_bits != 1) return APNN_ERR_ENCODING;
+    if (w_bits > 2) return APNN_ERR_UNSUPPORTED;
+    if (N > 0 && K > 0 && (!W || !Wp)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(W) || !aligned16(Wp)) return APNN_ERR_ALIGNMENT;
+    DevInfo d;
+    if ((st = device_info(&d)) != APNN_OK) return st;
+    cudaError_t err = launch_prepare_weights(W, N, K, w_bits, enc, Wp, d.sms, (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_status apnn_gemm_prepared(const uint32_t* A, const uint8_t* Wp, int M, int N, int K, int a_bits, int w_bits,
+                               apnn_encoding enc, const apnn_epilogue* epi, void* Y, apnn_stream_t stream) {
+    if (M < 0 || N < 0 || K < 0) return APNN_ERR_SHAPE;
+    apnn_status st = check_bits_enc(a_bits, w_bits, enc);
+    if (st != APNN_OK) return st;
+    if ((M > 0 && K > 0 && !A) || (N > 0 && K > 0 && !Wp) || (M > 0 && N > 0 && !Y)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(A) || !aligned16(Wp) || !aligned16(Y)) return APNN_ERR_ALIGNMENT;
+    Epi e;
+    if ((st = make_epi(epi, &e)) != APNN_OK) return st;
+    if (e.pool || e.res) return APNN_ERR_INVALID_ARG;
+    Geom g;
+    gemm_geom(&g, M, N, K, a_bits, w_bits, enc);
+    if (!tc_fp4_supports(g)) return APNN_ERR_UNSUPPORTED;
+    DevInfo d;
+    if ((st = device_info(&d)) != APNN_OK) return st;
+    if (M == 0 || N == 0) return APNN_OK;
+    cudaError_t err = launch_tc_fp4_prepared(A, Wp, g, e, Y, (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }
 
 apnn_status apnn_gemm(const uint32_t* A, const uint32_t* W, int M, int N, int K, int a_bits,

@@ -70,6 +70,14 @@ __device__ __forceinline__ void mma_mxf4(uint32_t d_tmem, uint64_t a_desc, uint6
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d_sw(void* dst, const void* tmap, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
 // 32 elements of one plane group -> 4 words of e2m1 nibbles (word j: elements j + 4n)
 template <int NB, bool PM1>
 __device__ __forceinline__ void decode_group_fp4(const uint32_t (&pw)[2], uint32_t vm, bool masked,
@@ -117,6 +125,31 @@ __device__ __forceinline__ void recomb_row(const uint8_t* planes, int rows, int 
     }
 }
 
+// apnn_prepare_weights: packed W [N][w_bits][Kw] -> e2m1 [N][Kw*16 bytes]; 16 bytes per
+// 32-element group g at byte 16*g (the kernel's chunk order), elements >= K are value 0.
+template <int NB, bool PM1>
+__global__ void __launch_bounds__(256) prepare_kernel(const uint32_t* __restrict__ W, int N, int K, int Kw,
+                                                      uint8_t* __restrict__ out) {
+    const long long total = (long long)N * Kw;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long n = idx / Kw;
+        const int gidx = (int)(idx - n * Kw);
+        uint32_t pw[2] = {0u, 0u};
+#pragma unroll
+        for (int pl = 0; pl < NB; pl++) pw[pl] = __ldg(W + (n * NB + pl) * Kw + gidx);
+        const int nv = K - gidx * 32;
+        const uint32_t vm = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
+        uint32_t o[4];
+        decode_group_fp4<NB, PM1>(pw, vm, true, o);
+        if (!PM1) {  // 0/1 codes: padding bits are zero already; mask anyway (robust to dirty padding)
+#pragma unroll
+            for (int j = 0; j < 4; j++) o[j] &= ((vm >> j) & 0x11111111u) * 0xFu;
+        }
+        *reinterpret_cast<uint4*>(out + n * (long long)Kw * 16 + gidx * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
 template <bool PM1>
 __device__ __forceinline__ void recomb_row_any(int nb, const uint8_t* planes, int rows, int row, uint8_t* op,
                                                int kvalid) {
@@ -125,7 +158,30 @@ __device__ __forceinline__ void recomb_row_any(int nb, const uint8_t* planes, in
     else recomb_row<2, false>(planes, rows, row, op, kvalid);
 }
 
-template <int BN, bool A_PM1, bool W_PM1>
+// one k-block (kb2 of the stage) of one A row (prepared-weights mode: the 8 recombination
+// warps split the stage's two k-blocks)
+template <int NB, bool PM1>
+__device__ __forceinline__ void recomb_row_kb(const uint8_t* planes, int rows, int row, uint8_t* op, int kb2,
+                                              int kvalid) {
+    const uint4* src = reinterpret_cast<const uint4*>(planes);
+    uint4 v[NB];
+#pragma unroll
+    for (int pl = 0; pl < NB; pl++) v[pl] = src[(pl * rows + row) * 2 + kb2];
+#pragma unroll
+    for (int gi = 0; gi < 4; gi++) {
+        uint32_t pw[2] = {0u, 0u};
+#pragma unroll
+        for (int pl = 0; pl < NB; pl++) pw[pl] = tc::sel4(v[pl], gi);
+        uint32_t o[4];
+        decode_group_fp4<NB, PM1>(pw, tc::valid_mask(kvalid, gi), PM1 && kvalid < 128, o);
+        *reinterpret_cast<uint4*>(op + tc::b_chunk_offset(row, kb2 * 4 + gi)) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+// PREP: W arrives pre-recombined (apnn_prepare_weights: e2m1 nibbles in the kernel's element
+// order, padding = value 0) and is loaded by TMA straight into the SWIZZLE_128B operand tile;
+// only A is recombined per tile.
+template <int BN, bool A_PM1, bool W_PM1, bool PREP = false>
 __global__ void __launch_bounds__(THREADS, 1)
     fp4_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB, const Params p) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -141,7 +197,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* op_full = bars + 2 * MAXSP;                   // [MAXS]
     uint64_t* op_empty = op_full + MAXS;                    // [MAXS]
     uint64_t* accum_full = op_empty + MAXS;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accum_full + 2);
+    uint64_t* b_full = accum_full + 2;                      // [MAXS] (PREP: B operand landed)
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(b_full + MAXS);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
@@ -158,6 +215,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int s = 0; s < S; s++) {
             mbar_init(&op_full[s], 8);
             mbar_init(&op_empty[s], 1);
+            mbar_init(&b_full[s], 1);
         }
         mbar_init(accum_full, 1);
         fence_mbar_init();
@@ -184,11 +242,20 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            for (int i = 0; i < nst; i++, s = (s + 1 == SP) ? 0 : s + 1, ph ^= (s == 0)) {  // no divisions
+            int os = 0;
+            uint32_t oph = 0;
+            for (int i = 0; i < nst; i++, s = (s + 1 == SP) ? 0 : s + 1, ph ^= (s == 0),
+                     os = (os + 1 == S) ? 0 : os + 1, oph ^= (os == 0)) {  // no divisions
                 mbar_wait(&plane_empty[s], ph ^ 1);
-                mbar_arrive_expect_tx(&plane_full[s], p.a_bytes + p.b_bytes);
+                mbar_arrive_expect_tx(&plane_full[s], p.a_bytes + (PREP ? 0u : p.b_bytes));
                 tma_load_4d(sApl + (size_t)s * p.a_bytes, &tmapA, &plane_full[s], i * 8, m0, 0, 0);
-                tma_load_4d(sBpl + (size_t)s * p.b_bytes, &tmapB, &plane_full[s], i * 8, n0, 0, 0);
+                if (!PREP) {
+                    tma_load_4d(sBpl + (size_t)s * p.b_bytes, &tmapB, &plane_full[s], i * 8, n0, 0, 0);
+                } else {  // prepared W: 128 bytes (256 e2m1) x BN rows straight into operand stage os
+                    mbar_wait(&op_empty[os], oph ^ 1);
+                    mbar_arrive_expect_tx(&b_full[os], (uint32_t)BN * 128);
+                    tma_load_2d_sw(sBop + (size_t)os * BN * 128, &tmapB, &b_full[os], i * 128, n0);
+                }
             }
         }
     } else if (warp == 1) {
@@ -198,6 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             uint32_t ph = 0;
             for (int i = 0; i < nst; i++, s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
                 mbar_wait(&op_full[s], ph);
+                if (PREP) mbar_wait(&b_full[s], ph);
                 tc_fence_after();
                 const uint32_t abase = smem_u32(sAop + (size_t)s * BM * 128);
                 const uint32_t bbase = smem_u32(sBop + (size_t)s * BN * 128);
@@ -227,7 +295,13 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             mbar_wait(&plane_full[ps], pph);
             mbar_wait(&op_empty[s], ph ^ 1);
-            if (grp == 0) {
+            if (PREP) {  // prepared W has value-0 padding: A needs no mask; grp = k-block of the stage
+                const uint8_t* apl = sApl + (size_t)ps * p.a_bytes;
+                uint8_t* aop = sAop + (size_t)s * BM * 128;
+                if (A_PM1) recomb_row_kb<1, true>(apl, BM, t, aop, grp, 128);
+                else if (g.a_bits == 1) recomb_row_kb<1, false>(apl, BM, t, aop, grp, 128);
+                else recomb_row_kb<2, false>(apl, BM, t, aop, grp, 128);
+            } else if (grp == 0) {
                 recomb_row_any<A_PM1>(g.a_bits, sApl + (size_t)ps * p.a_bytes, BM, t, sAop + (size_t)s * BM * 128,
                                       kvalid);
             } else {
@@ -300,24 +374,38 @@ static bool make_map(CUtensorMap* m, const uint32_t* base, int rows, int bits, i
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool AP, bool WP>
+// prepared W [N][Kw*16 bytes] as a 2-D byte tensor; box {128 bytes, BN rows} with
+// SWIZZLE_128B lands exactly in the UMMA K-major SWIZZLE_128B operand layout
+static bool make_map_prep(CUtensorMap* m, const uint8_t* base, int N, int Kw, int box_rows) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)Kw * 16, (cuuint64_t)N};
+    cuuint64_t strides[1] = {(cuuint64_t)Kw * 16};
+    cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, bool AP, bool WP, bool PREP>
 static cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, dim3 grid, size_t smem,
                           cudaStream_t s) {
-    auto kfn = fp4_kernel<BN, AP, WP>;
+    auto kfn = fp4_kernel<BN, AP, WP, PREP>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     kfn<<<grid, THREADS, smem, s>>>(ta, tb, p);
     return cudaGetLastError();
 }
 
-template <int BN>
+template <int BN, bool PREP>
 static cudaError_t launch_enc(int enc, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, dim3 grid,
                               size_t smem, cudaStream_t s) {
     switch (enc) {
-    case APNN_ENC_01_01: return launch<BN, false, false>(ta, tb, p, grid, smem, s);
-    case APNN_ENC_PM1_PM1: return launch<BN, true, true>(ta, tb, p, grid, smem, s);
-    case APNN_ENC_W_PM1_A_01: return launch<BN, false, true>(ta, tb, p, grid, smem, s);
-    default: return launch<BN, true, false>(ta, tb, p, grid, smem, s);
+    case APNN_ENC_01_01: return launch<BN, false, false, PREP>(ta, tb, p, grid, smem, s);
+    case APNN_ENC_PM1_PM1: return launch<BN, true, true, PREP>(ta, tb, p, grid, smem, s);
+    case APNN_ENC_W_PM1_A_01: return launch<BN, false, true, PREP>(ta, tb, p, grid, smem, s);
+    default: return launch<BN, true, false, PREP>(ta, tb, p, grid, smem, s);
     }
 }
 
@@ -342,8 +430,8 @@ bool tc_fp4_supports(const Geom& g) {
     return (long long)g.K * ma * mw < (1LL << 24);
 }
 
-cudaError_t launch_tc_fp4(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
-                          cudaStream_t s) {
+static cudaError_t launch_fp4_impl(const uint32_t* A, const void* W, bool prep, const Geom& g, const Epi& e,
+                                   void* Y, cudaStream_t s) {
     using namespace fp4;
     Params p;
     std::memset(&p, 0, sizeof(p));
@@ -359,9 +447,9 @@ cudaError_t launch_tc_fp4(const uint32_t* A, const uint32_t* W, const Geom& g, c
     const int ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
     const int BN = g.N > 128 ? 256 : 128;
     p.a_bytes = 32u * BM * g.a_bits;
-    p.b_bytes = 32u * BN * g.w_bits;
+    p.b_bytes = prep ? 0u : 32u * BN * g.w_bits;
     const size_t op = (size_t)(BM + BN) * 128, pl = p.a_bytes + p.b_bytes;
-    const size_t fixed = (size_t)BN * tc::kTabStride * 4 + (2 * MAXSP + 2 * MAXS + 4) * 8 + 1024;
+    const size_t fixed = (size_t)BN * tc::kTabStride * 4 + (2 * MAXSP + 3 * MAXS + 4) * 8 + 1024;
     const size_t budget = 227 * 1024 - fixed;
     // operand ring S (3 stages), plane ring SP as deep
     // as the rest of shared memory allows (it hides the TMA latency); APNN_FP4_S overrides S
@@ -379,13 +467,44 @@ cudaError_t launch_tc_fp4(const uint32_t* A, const uint32_t* W, const Geom& g, c
     p.tmem_cols = pow2;
     const size_t smem = per_total + fixed - 1024 + 64;
     CUtensorMap ta, tb;
-    if (!make_map(&ta, A, g.M, g.a_bits, Kw, BM) || !make_map(&tb, W, g.N, g.w_bits, Kw, BN))
+    if (!make_map(&ta, A, g.M, g.a_bits, Kw, BM)) return cudaErrorInvalidValue;
+    if (prep ? !make_map_prep(&tb, reinterpret_cast<const uint8_t*>(W), g.N, Kw, BN)
+             : !make_map(&tb, reinterpret_cast<const uint32_t*>(W), g.N, g.w_bits, Kw, BN))
         return cudaErrorInvalidValue;
     dim3 grid((g.M + BM - 1) / BM, (ncols + BN - 1) / BN);
-    cudaError_t err = BN == 256 ? launch_enc<256>(g.enc, ta, tb, p, grid, smem, s)
-                                : launch_enc<128>(g.enc, ta, tb, p, grid, smem, s);
+    cudaError_t err;
+    if (prep) err = BN == 256 ? launch_enc<256, true>(g.enc, ta, tb, p, grid, smem, s)
+                              : launch_enc<128, true>(g.enc, ta, tb, p, grid, smem, s);
+    else err = BN == 256 ? launch_enc<256, false>(g.enc, ta, tb, p, grid, smem, s)
+                         : launch_enc<128, false>(g.enc, ta, tb, p, grid, smem, s);
     count_launch();
     return err;
+}
+
+cudaError_t launch_tc_fp4(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
+                          cudaStream_t s) {
+    return launch_fp4_impl(A, W, false, g, e, Y, s);
+}
+
+cudaError_t launch_tc_fp4_prepared(const uint32_t* A, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
+                                   cudaStream_t s) {
+    return launch_fp4_impl(A, Wp, true, g, e, Y, s);
+}
+
+cudaError_t launch_prepare_weights(const uint32_t* W, int N, int K, int w_bits, int enc, uint8_t* out, int sms,
+                                   cudaStream_t s) {
+    using namespace fp4;
+    const int Kw = (K + 127) / 128 * 4;
+    const long long total = (long long)N * Kw;
+    if (total == 0) return cudaSuccess;
+    long long blocks = (total + 255) / 256;
+    if (blocks > (long long)sms * 8) blocks = (long long)sms * 8;
+    const bool pm1 = enc == APNN_ENC_PM1_PM1 || enc == APNN_ENC_W_PM1_A_01;
+    if (pm1) prepare_kernel<1, true><<<(int)blocks, 256, 0, s>>>(W, N, K, Kw, out);
+    else if (w_bits == 1) prepare_kernel<1, false><<<(int)blocks, 256, 0, s>>>(W, N, K, Kw, out);
+    else prepare_kernel<2, false><<<(int)blocks, 256, 0, s>>>(W, N, K, Kw, out);
+    count_launch();
+    return cudaGetLastError();
 }
 
 }  // namespace apnn

@@ -447,3 +447,36 @@ def test_fp4_variant_rejects_wide_codes():
     A, W = synth.gemm_inputs(64, 64, 128, 4, 1, tag="fp4rej")
     with pytest.raises(ap.ApnnError):
         run_gemm(A, W, 4, 1, 2, ap.VARIANT_TC_FP4)
+
+
+
+@pytest.mark.parametrize("M,N,K", [(150, 270, 300), (256, 256, 1024), (7, 33, 129), (300, 100, 2048)])
+@pytest.mark.parametrize("a_bits,w_bits,enc", [(2, 1, 2), (2, 2, 0), (1, 1, 1), (1, 2, 3), (1, 1, 0)])
+def test_fp4_prepared_weights_exact(M, N, K, a_bits, w_bits, enc):
+    A, W = synth.gemm_inputs(M, N, K, a_bits, w_bits, tag="fp4p")
+    Y = oracle.gemm(A, W, a_bits, w_bits, enc)
+    Ap = ap.pack_bits(cuda(A), a_bits)
+    Wprep = ap.prepare_weights(ap.pack_bits(cuda(W), w_bits), N, K, w_bits, enc)
+    got = ap.gemm_prepared(Ap, Wprep, M, N, K, a_bits, w_bits, enc)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy(), Y)
+    alpha, beta, S = epi_case(N, 3, "fp4p")
+    want = oracle.pack(oracle.epilogue(Y, alpha, beta, S, 3), 3)
+    got = ap.gemm_prepared(Ap, Wprep, M, N, K, a_bits, w_bits, enc, epi=ap.Epilogue(3, cuda(alpha), cuda(beta), S))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(u32(got), want)
+
+
+def test_fp4_prepared_full_size_sampled_rows():
+    M = N = K = 8192
+    a, w, enc = 2, 1, 2
+    A, W = synth.gemm_inputs(M, N, K, a, w, tag="bench")
+    alpha, beta = synth.epilogue_params(N, tag="bench")
+    S = 1 << 10
+    Ap = ap.pack_bits(cuda(A), a)
+    Wprep = ap.prepare_weights(ap.pack_bits(cuda(W), w), N, K, w, enc)
+    Y = ap.gemm_prepared(Ap, Wprep, M, N, K, a, w, enc, epi=ap.Epilogue(a, cuda(alpha), cuda(beta), S))
+    torch.cuda.synchronize()
+    rows = _sample_rows(M, 24, "fullsize-prep")
+    want = oracle.pack(oracle.epilogue(oracle.gemm(A[rows], W, a, w, enc), alpha, beta, S, a), a)
+    np.testing.assert_array_equal(u32(Y)[rows], want)
