@@ -22,7 +22,8 @@ SO = os.path.join(HERE, "libapnn.so")
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
-         "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+         "--expt-relaxed-constexpr", "--split-compile=0",  # parallel device optimisation (gemm_tc.cu 4.3 -> 1.5 min)
+         "-I", os.path.join(ROOT, "include")]
 
 
 def _sources():
