@@ -250,6 +250,19 @@ apnn_status apnn_gemm_prepared(const uint32_t *A, const uint8_t *Wp, int M, int 
                                int w_bits, apnn_encoding enc, const apnn_epilogue *epi, void *Y,
                                apnn_stream_t stream);
 
+/* Prepared int8 weights for the int8 tensor-core kernel (any w_bits; the B decode that grows
+ * with w_bits is done once at load time):
+ *   Wp: device, apnn_prepared_i8_bytes(N, K) bytes: int8 operand rows [N][roundup(K,128)] in
+ *       the kernel's element order (u8 codes, or s8 +-1 with value-0 padding); opaque layout.
+ * apnn_gemm_prepared_i8: as apnn_gemm_ex on the 2-CTA tcgen05 kernel; GEMM with M > 128 and
+ * no pooling / residual epilogue, else APNN_ERR_UNSUPPORTED. */
+size_t apnn_prepared_i8_bytes(int N, int K);
+apnn_status apnn_prepare_weights_i8(const uint32_t *W, int N, int K, int w_bits, apnn_encoding enc,
+                                    uint8_t *Wp, apnn_stream_t stream);
+apnn_status apnn_gemm_prepared_i8(const uint32_t *A, const uint8_t *Wp, int M, int N, int K, int a_bits,
+                                  int w_bits, apnn_encoding enc, const apnn_epilogue *epi, void *Y,
+                                  apnn_stream_t stream);
+
 /* Which variant APNN_VARIANT_AUTO resolves to for this problem (no launch): int32 output,
  * or the fused element-wise routine with out_bits (1..8) packed output. */
 apnn_variant apnn_select_variant(int M, int N, int K, int a_bits, int w_bits, apnn_encoding enc);

@@ -82,6 +82,12 @@ def lib() -> ctypes.CDLL:
             L.apnn_prepare_weights.restype = st
             L.apnn_gemm_prepared.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp, vp]
             L.apnn_gemm_prepared.restype = st
+            L.apnn_prepared_i8_bytes.argtypes = [ci, ci]
+            L.apnn_prepared_i8_bytes.restype = ctypes.c_size_t
+            L.apnn_prepare_weights_i8.argtypes = [vp, ci, ci, ci, ci, vp, vp]
+            L.apnn_prepare_weights_i8.restype = st
+            L.apnn_gemm_prepared_i8.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp, vp]
+            L.apnn_gemm_prepared_i8.restype = st
             L.apnn_im2col_pack.argtypes = [vp, ctypes.POINTER(_Conv), ci, vp, vp]
             L.apnn_im2col_pack.restype = st
             L.apnn_gemm.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, vp, vp]
@@ -116,7 +122,8 @@ def lib() -> ctypes.CDLL:
 
 
 ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_im2col_pack", "apnn_flatten_packed",
-               "apnn_prepared_bytes", "apnn_prepare_weights", "apnn_gemm_prepared", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
+               "apnn_prepared_bytes", "apnn_prepare_weights", "apnn_gemm_prepared",
+               "apnn_prepared_i8_bytes", "apnn_prepare_weights_i8", "apnn_gemm_prepared_i8", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
                "apnn_conv2d", "apnn_conv2d_ex", "apnn_quant_pack_out", "apnn_pool_quant_pack_out",
                "apnn_residual_quant_pack",
                "apnn_select_variant", "apnn_select_variant_fused",
@@ -298,6 +305,33 @@ def gemm_prepared(A: torch.Tensor, Wp: torch.Tensor, M: int, N: int, K: int, a_b
     ce = None if epi is None else ctypes.byref(epi._c())
     _check(lib().apnn_gemm_prepared(_ptr(A), _ptr(Wp), M, N, K, a_bits, w_bits, enc, ce, _ptr(out), _stream(A)),
            "apnn_gemm_prepared")
+    return out
+
+
+def prepare_weights_i8(W: torch.Tensor, N: int, K: int, w_bits: int, enc: int,
+                       out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Packed weights -> prepared int8 operand rows for the 2-CTA int8 kernel (apnn_prepare_weights_i8)."""
+    _cuda(W, "W", torch.int32)
+    if out is None:
+        out = torch.empty(int(lib().apnn_prepared_i8_bytes(N, K)), dtype=torch.uint8, device=W.device)
+    _cuda(out, "out", torch.uint8)
+    _check(lib().apnn_prepare_weights_i8(_ptr(W), N, K, w_bits, enc, _ptr(out), _stream(W)),
+           "apnn_prepare_weights_i8")
+    return out
+
+
+def gemm_prepared_i8(A: torch.Tensor, Wp: torch.Tensor, M: int, N: int, K: int, a_bits: int, w_bits: int,
+                     enc: int, epi: Optional[Epilogue] = None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """APMM on the int8 tensor-core kernel with prepared weights (apnn_gemm_prepared_i8)."""
+    _cuda(A, "A", torch.int32)
+    _cuda(Wp, "Wp", torch.uint8)
+    if out is None:
+        shape = (M, N) if epi is None else packed_shape(M, N, epi.out_bits)
+        out = torch.empty(shape, dtype=torch.int32, device=A.device)
+    _cuda(out, "out", torch.int32)
+    ce = None if epi is None else ctypes.byref(epi._c())
+    _check(lib().apnn_gemm_prepared_i8(_ptr(A), _ptr(Wp), M, N, K, a_bits, w_bits, enc, ce, _ptr(out), _stream(A)),
+           "apnn_gemm_prepared_i8")
     return out
 
 

@@ -41,6 +41,10 @@ cudaError_t launch_tc_fp4_prepared(const uint32_t* A, const uint8_t* Wp, const G
                                    cudaStream_t s);
 cudaError_t launch_prepare_weights(const uint32_t* W, int N, int K, int w_bits, int enc, uint8_t* out, int sms,
                                    cudaStream_t s);
+cudaError_t launch_prepare_weights_i8(const uint32_t* W, int N, int K, int w_bits, int enc, uint8_t* out, int sms,
+                                      cudaStream_t s);
+cudaError_t launch_tc_i8_prepared(const uint32_t* A, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
+                                  int sms, cudaStream_t s);
 bool b1mma_supports(const Geom& g);
 
 // ---- device properties (cached per device ordinal)
@@ -308,6 +312,48 @@ apnn_status apnn_gemm_prepared(const uint32_t* A, const uint8_t* Wp, int M, int 
     if ((st = device_info(&d)) != APNN_OK) return st;
     if (M == 0 || N == 0) return APNN_OK;
     cudaError_t err = launch_tc_fp4_prepared(A, Wp, g, e, Y, (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+size_t apnn_prepared_i8_bytes(int N, int K) {
+    if (N < 0 || K < 0) return 0;
+    return (size_t)N * (((size_t)K + 127) / 128 * 128);
+}
+
+apnn_status apnn_prepare_weights_i8(const uint32_t* W, int N, int K, int w_bits, apnn_encoding enc, uint8_t* Wp,
+                                    apnn_stream_t stream) {
+    if (N < 0 || K < 0) return APNN_ERR_SHAPE;
+    if (w_bits < 1 || w_bits > 8) return APNN_ERR_BITS;
+    if (enc < 0 || enc > 3) return APNN_ERR_ENCODING;
+    if ((enc == APNN_ENC_PM1_PM1 || enc == APNN_ENC_W_PM1_A_01) && w_bits != 1) return APNN_ERR_ENCODING;
+    if (N > 0 && K > 0 && (!W || !Wp)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(W) || !aligned16(Wp)) return APNN_ERR_ALIGNMENT;
+    DevInfo d;
+    apnn_status st = device_info(&d);
+    if (st != APNN_OK) return st;
+    cudaError_t err = launch_prepare_weights_i8(W, N, K, w_bits, enc, Wp, d.sms, (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_status apnn_gemm_prepared_i8(const uint32_t* A, const uint8_t* Wp, int M, int N, int K, int a_bits,
+                                  int w_bits, apnn_encoding enc, const apnn_epilogue* epi, void* Y,
+                                  apnn_stream_t stream) {
+    if (M < 0 || N < 0 || K < 0) return APNN_ERR_SHAPE;
+    apnn_status st = check_bits_enc(a_bits, w_bits, enc);
+    if (st != APNN_OK) return st;
+    if ((M > 0 && K > 0 && !A) || (N > 0 && K > 0 && !Wp) || (M > 0 && N > 0 && !Y)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(A) || !aligned16(Wp) || !aligned16(Y)) return APNN_ERR_ALIGNMENT;
+    if ((st = check_overflow(K, a_bits, w_bits, enc)) != APNN_OK) return st;
+    Epi e;
+    if ((st = make_epi(epi, &e)) != APNN_OK) return st;
+    if (e.pool || e.res || M <= 128 || K == 0) return APNN_ERR_UNSUPPORTED;
+    Geom g;
+    gemm_geom(&g, M, N, K, a_bits, w_bits, enc);
+    DevInfo d;
+    if ((st = device_info(&d)) != APNN_OK) return st;
+    if (N == 0) return APNN_OK;
+    cudaError_t err = launch_tc_i8_prepared(A, Wp, g, e, Y, d.sms, (cudaStream_t)stream);
+    if (err == cudaErrorNotSupported) return APNN_ERR_UNSUPPORTED;
     return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }
 

@@ -86,6 +86,7 @@ struct Params {
     int exp_nostore;            // experiment knob (APNN_EXP_NOSTORE): skip the epilogue stores
     int exp_nob;                // experiment knob (APNN_EXP_NOB): B warps skip the decode (wrong results)
     int halves;                 // 256-wide pair tiles: two N = 128 MMA halves (APNN_HALVES, default 0)
+    int prep;                   // prepared int8 W (apnn_prepare_weights_i8): B tiles by TMA, no B decode
 };
 
 // development trace of CTA 0: clock64 stamps per k-block / tile (APNN_TRACE=<file>)
@@ -134,6 +135,14 @@ __device__ __forceinline__ void cta_tile_rows(const Params& p, int ct, int& m_ba
     }
     if (m_base + len > g.M) len = g.M - m_base;
     if (len < 0) len = 0;
+}
+
+__device__ __forceinline__ void tma_load_2d_box(void* dst, const void* tmap, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+        "[%2];" ::"r"(sm100::smem_u32(dst)),
+        "l"(tmap), "r"(sm100::smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
 }
 
 // ------------------------------------------------- fused 2x2/2 max pooling
@@ -234,7 +243,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     constexpr bool HALVES = T2_BN == 256;
     uint64_t* accum_full = op_empty + MAX_STAGES;                  // [2]
     uint64_t* accum_empty = accum_full + 2;                        // [2], used in CTA 0
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accum_empty + 2);
+    uint64_t* b_full = accum_empty + 2;                            // [MAX_STAGES] prepared W landed (p.prep)
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(b_full + MAX_STAGES);
     volatile uint32_t* dep_slots = tmem_holder + 1;                // [T2_RECOMB_WARPS * 32]
 
     cta_stamp(p, 0);
@@ -260,6 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             mbar_init(&accum_full[i], 1);
             mbar_init(&accum_empty[i], 8);  // 4 epilogue warps x 2 CTAs
         }
+        for (int i = 0; i < S; i++) mbar_init(&b_full[i], 1);
         fence_mbar_init();
     }
     if (warp == T2_MMA_WARP) tmem_alloc2(tmem_holder, p.tmem_cols);
@@ -297,7 +308,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                 if (lane == 0) trace_at(p, TR_PROD, it);
                 const int rs = conv ? kb / g.CB : 0;
                 const int cb = conv ? kb - rs * g.CB : kb;
-                mbar_arrive_expect_tx(&plane_full[s], p.a_tx_bytes + p.b_bytes);
+                mbar_arrive_expect_tx(&plane_full[s], p.a_tx_bytes + (p.prep ? 0u : p.b_bytes));
                 uint8_t* adst = sApl + (size_t)s * p.a_bytes;
                 if (!conv) {
                     tma_load_4d(adst, &tmapA, &plane_full[s], kb * 4, m0, 0, 0);
@@ -317,7 +328,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                                         wo0 * g.stride + sx - g.pad, 0, ho * g.stride + r - g.pad, b);
                     }
                 }
-                tma_load_4d(sBpl + (size_t)s * p.b_bytes, &tmapB, &plane_full[s], cb * 4, nr0, 0, rs);
+                if (!p.prep) {
+                    tma_load_4d(sBpl + (size_t)s * p.b_bytes, &tmapB, &plane_full[s], cb * 4, nr0, 0, rs);
+                } else {  // prepared int8 W (GEMM): 128 bytes x BROWS rows straight into operand stage os
+                    const int os = it % S;
+                    const uint32_t oph = (uint32_t)(it / S) & 1u;
+                    mbar_wait(&op_empty[os], oph ^ 1);
+                    mbar_arrive_expect_tx(&b_full[os], BOP_STAGE);
+                    tma_load_2d_box(sBop + (size_t)os * BOP_STAGE, &tmapB, &b_full[os], kb * 128, nr0);
+                }
             }
             __syncwarp();
         }
@@ -416,6 +435,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                                                  &op_empty[s], ph ^ 1, tmem_lane + A_COL + s * 32, nullptr, kvalid,
                                                  lane, dep_slots + threadIdx.x);
                     tmem_wait_st();
+                } else if (p.prep) {  // prepared W: the B tile comes from TMA; keep the barrier protocol
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&plane_empty[ps]);
+                    mbar_wait(&b_full[s], ph);
                 } else if (t < BROWS && !p.exp_nob) {  // warp-uniform: BROWS is a multiple of 32
                     recomb_step_any<W_PM1, false, SCALED>(g.w_bits, sBpl + (size_t)ps * p.b_bytes, BROWS, 1, t,
                                                           &plane_empty[ps], &op_empty[s], ph ^ 1, 0,
@@ -954,6 +977,20 @@ static bool make_conv_act_map_merged(CUtensorMap* m, const uint32_t* base, const
     return r == CUDA_SUCCESS;
 }
 
+// prepared int8 W [N][Kp] bytes; box {128 bytes (one k-block), box_rows} with SWIZZLE_128B =
+// the UMMA K-major SWIZZLE_128B operand layout of b_chunk_offset
+static bool make_prep_i8_map(CUtensorMap* m, const uint8_t* base, int N, int Kp, int box_rows) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)N};
+    cuuint64_t strides[1] = {(cuuint64_t)Kp};
+    cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static int stage_count(size_t per_stage, size_t fixed) {
     const size_t budget = 227 * 1024 - fixed;
     int S = (int)(budget / per_stage);
@@ -1032,6 +1069,61 @@ bool tc_i8_pool_fusable(const Geom& g, const Epi& e) {
            g.Wo >= 2 && g.Wo <= 64 && g.M > 128 && tc_kernel_override() != 1;
 }
 
+namespace tc {
+// apnn_prepare_weights_i8: packed W [N][w_bits][Kw] -> unscaled int8 operand rows [N][Kw*32]
+// (u8 codes, or s8 +-1 with value-0 padding), 32 bytes per 32-element group in the
+// recombination's element order (decode_01 / decode_pm1): the B tile of tc2_kernel as-is.
+template <int NB, bool PM1>
+__global__ void __launch_bounds__(256) prepare_i8_kernel(const uint32_t* __restrict__ W, int N, int K, int Kw,
+                                                         uint8_t* __restrict__ out) {
+    const long long total = (long long)N * Kw;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long n = idx / Kw;
+        const int gidx = (int)(idx - n * Kw);
+        uint32_t pw[NB];
+#pragma unroll
+        for (int pl = 0; pl < NB; pl++) pw[pl] = __ldg(W + (n * NB + pl) * Kw + gidx);
+        uint32_t o[8];
+        const int nv = K - gidx * 32;  // valid elements of this 32-element group
+        const uint32_t vm = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
+        if (PM1) decode_pm1<true>(pw[0], vm, o);  // padding -> value 0
+        else decode_01<NB>(pw, o);
+        uint4* dst = reinterpret_cast<uint4*>(out + n * (long long)Kw * 32 + gidx * 32);
+        dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    }
+}
+}  // namespace tc
+
+cudaError_t launch_prepare_weights_i8(const uint32_t* W, int N, int K, int w_bits, int enc, uint8_t* out, int sms,
+                                      cudaStream_t s) {
+    using namespace tc;
+    const int Kw = (K + 127) / 128 * 4;
+    const long long total = (long long)N * Kw;
+    if (total == 0) return cudaSuccess;
+    long long blocks = (total + 255) / 256;
+    if (blocks > (long long)sms * 8) blocks = (long long)sms * 8;
+    const int gb = (int)blocks;
+    const bool pm1 = enc == APNN_ENC_PM1_PM1 || enc == APNN_ENC_W_PM1_A_01;
+    if (pm1) { prepare_i8_kernel<1, true><<<gb, 256, 0, s>>>(W, N, K, Kw, out); }
+    else {
+        switch (w_bits) {
+        case 1: prepare_i8_kernel<1, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
+        case 2: prepare_i8_kernel<2, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
+        case 3: prepare_i8_kernel<3, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
+        case 4: prepare_i8_kernel<4, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
+        case 5: prepare_i8_kernel<5, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
+        case 6: prepare_i8_kernel<6, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
+        case 7: prepare_i8_kernel<7, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
+        default: prepare_i8_kernel<8, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
+        }
+    }
+    count_launch();
+    return cudaGetLastError();
+}
+
+
 bool tc_i8_supports(const Geom& g) {
     // GEMM and implicit-GEMM conv; K = 0 has no MMA to issue (handled by the popc variant)
     return g.K > 0 && g.M > 0 && g.N > 0;
@@ -1096,10 +1188,11 @@ static int tc_kernel_override() {
     return v;
 }
 
-cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y, int sms,
-                         cudaStream_t s) {
+static cudaError_t launch_tc_i8_impl(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
+                                     int sms, cudaStream_t s, const uint8_t* Wprep) {
     using namespace tc;
     Params p;
+    p.prep = Wprep ? 1 : 0;
     p.g = g;
     p.e = e;
     p.Y = Y;
@@ -1139,7 +1232,8 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     if (e.res && !two) return cudaErrorNotSupported;  // residual epilogue: 2-CTA kernel only (ABI checks first)
     // small GEMMs (row f4): when the 2-CTA grid would occupy <= 1/4 of the SMs, run the
     // 1-CTA kernel with split-K clusters instead (latency: more CTAs, fewer k-blocks each)
-    if (two && !g.conv && !e.res && g.M <= 1024 && g.nchunks >= 4 && tc_kernel_override() != 2) {
+    if (Wprep && (!two || g.conv)) return cudaErrorNotSupported;  // prepared W: 2-CTA GEMM only
+    if (two && !g.conv && !e.res && !Wprep && g.M <= 1024 && g.nchunks >= 4 && tc_kernel_override() != 2) {
         const int BNP = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
         const long long pair_tiles = (long long)((g.M + 255) / 256) * ((g.N + BNP - 1) / BNP);
         if (pair_tiles * 2 * 4 <= sms) two = false;
@@ -1150,7 +1244,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     if (two) {
         const int BNP = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);   // pair tile width
         const int brows = BNP / 2;
-        p.b_bytes = 16u * brows * g.w_bits;
+        p.b_bytes = p.prep ? 0u : 16u * brows * g.w_bits;
         p.conv_box_stride = 0;
         if (g.conv) {
             // row boxes per stage = output rows per CTA tile (conv_k below; even when pooling)
@@ -1172,7 +1266,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
             if (p.pool_fused && sw < 2048) sw = 2048;
             p.stg_warp = sw;
         }
-        const size_t fixed = (size_t)256 * kTabStride * 4 + (2 * MAX_PSTAGES + 2 * MAX_STAGES + 6) * 8 +
+        const size_t fixed = (size_t)256 * kTabStride * 4 + (2 * MAX_PSTAGES + 3 * MAX_STAGES + 6) * 8 +
                              T2_RECOMB_WARPS * 32 * 4 + 4 * (size_t)p.stg_warp + 1024;
         const size_t budget = 227 * 1024 - fixed;
         const size_t op_stage = (size_t)brows * 128, pl_stage = p.a_bytes + p.b_bytes;
@@ -1199,7 +1293,7 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
             const long long ma = apm ? 64 : (((1LL << g.a_bits) - 1) << ka);
             const long long mw = wpm ? 64 : (((1LL << g.w_bits) - 1) << kw);
             const bool safe = (long long)g.K * ma * mw < 2147483647LL;
-            p.acc_shift = (safe && ka + kw > 0 && tc_scaled_enabled()) ? ka + kw : 0;
+            p.acc_shift = (safe && ka + kw > 0 && tc_scaled_enabled() && !p.prep) ? ka + kw : 0;  // prepared W is unscaled
         }
         p.tmem_cols = 512;
         int cta_tiles = (g.M + 127) / 128;
@@ -1234,7 +1328,11 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
         } else if (!make_plane_map(&ta, A, g.M, g.a_bits, g.Cw, 1, 128)) {
             return cudaErrorInvalidValue;
         }
-        if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, g.RS, brows)) return cudaErrorInvalidValue;
+        if (p.prep) {
+            if (!make_prep_i8_map(&tb, Wprep, g.N, g.Cw * 32, brows)) return cudaErrorInvalidValue;
+        } else if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, g.RS, brows)) {
+            return cudaErrorInvalidValue;
+        }
         p.nwb = BNP / 32 < 4 ? 4 : BNP / 32;
         if (want_mode == kOutLsu) {
             p.out_mode = (e.out_bits > 0 || g.N % 4 == 0) ? kOutLsu : kOutDirect;
@@ -1322,6 +1420,16 @@ cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, co
     }
     count_launch();
     return err;
+}
+
+cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y, int sms,
+                         cudaStream_t s) {
+    return launch_tc_i8_impl(A, W, g, e, Y, sms, s, nullptr);
+}
+
+cudaError_t launch_tc_i8_prepared(const uint32_t* A, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
+                                  int sms, cudaStream_t s) {
+    return launch_tc_i8_impl(A, nullptr, g, e, Y, sms, s, Wp);
 }
 
 }  // namespace apnn

@@ -480,3 +480,21 @@ def test_fp4_prepared_full_size_sampled_rows():
     rows = _sample_rows(M, 24, "fullsize-prep")
     want = oracle.pack(oracle.epilogue(oracle.gemm(A[rows], W, a, w, enc), alpha, beta, S, a), a)
     np.testing.assert_array_equal(u32(Y)[rows], want)
+
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 270, 300), (257, 520, 2048), (1000, 64, 640), (600, 100, 1152)])
+@pytest.mark.parametrize("a_bits,w_bits,enc", [(2, 1, 2), (8, 8, 0), (4, 4, 0), (1, 1, 1), (1, 3, 3), (3, 5, 0)])
+def test_i8_prepared_weights_exact(M, N, K, a_bits, w_bits, enc):
+    A, W = synth.gemm_inputs(M, N, K, a_bits, w_bits, tag="i8p")
+    Y = oracle.gemm(A, W, a_bits, w_bits, enc)
+    Ap = ap.pack_bits(cuda(A), a_bits)
+    Wprep = ap.prepare_weights_i8(ap.pack_bits(cuda(W), w_bits), N, K, w_bits, enc)
+    got = ap.gemm_prepared_i8(Ap, Wprep, M, N, K, a_bits, w_bits, enc)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy(), Y)
+    alpha, beta, S = epi_case(N, 4, "i8p")
+    want = oracle.pack(oracle.epilogue(Y, alpha, beta, S, 4), 4)
+    got = ap.gemm_prepared_i8(Ap, Wprep, M, N, K, a_bits, w_bits, enc, epi=ap.Epilogue(4, cuda(alpha), cuda(beta), S))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(u32(got), want)
