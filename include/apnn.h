@@ -262,6 +262,12 @@ apnn_status apnn_prepare_weights_i8(const uint32_t *W, int N, int K, int w_bits,
 apnn_status apnn_gemm_prepared_i8(const uint32_t *A, const uint8_t *Wp, int M, int N, int K, int a_bits,
                                   int w_bits, apnn_encoding enc, const apnn_epilogue *epi, void *Y,
                                   apnn_stream_t stream);
+/* apnn_conv2d with prepared conv weights: Wp = apnn_prepare_weights_i8 of the packed OHWI
+ * weights viewed as C_out*R*S rows of C_in (apnn_prepared_i8_bytes(C_out*R*S, C_in) bytes).
+ * 2-CTA kernel only (B*Ho*Wo > 128), else APNN_ERR_UNSUPPORTED; pooling as apnn_conv2d. */
+apnn_status apnn_conv2d_prepared_i8(const uint32_t *X, const uint8_t *Wp, const apnn_conv_shape *shape,
+                                    int a_bits, int w_bits, apnn_encoding enc, const apnn_epilogue *epi,
+                                    void *Y, apnn_stream_t stream);
 
 /* Which variant APNN_VARIANT_AUTO resolves to for this problem (no launch): int32 output,
  * or the fused element-wise routine with out_bits (1..8) packed output. */

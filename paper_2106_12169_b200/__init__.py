@@ -88,6 +88,9 @@ def lib() -> ctypes.CDLL:
             L.apnn_prepare_weights_i8.restype = st
             L.apnn_gemm_prepared_i8.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp, vp]
             L.apnn_gemm_prepared_i8.restype = st
+            L.apnn_conv2d_prepared_i8.argtypes = [vp, vp, ctypes.POINTER(_Conv), ci, ci, ci, ctypes.POINTER(_Epi),
+                                                  vp, vp]
+            L.apnn_conv2d_prepared_i8.restype = st
             L.apnn_im2col_pack.argtypes = [vp, ctypes.POINTER(_Conv), ci, vp, vp]
             L.apnn_im2col_pack.restype = st
             L.apnn_gemm.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, vp, vp]
@@ -123,7 +126,8 @@ def lib() -> ctypes.CDLL:
 
 ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_im2col_pack", "apnn_flatten_packed",
                "apnn_prepared_bytes", "apnn_prepare_weights", "apnn_gemm_prepared",
-               "apnn_prepared_i8_bytes", "apnn_prepare_weights_i8", "apnn_gemm_prepared_i8", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
+               "apnn_prepared_i8_bytes", "apnn_prepare_weights_i8", "apnn_gemm_prepared_i8",
+               "apnn_conv2d_prepared_i8", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
                "apnn_conv2d", "apnn_conv2d_ex", "apnn_quant_pack_out", "apnn_pool_quant_pack_out",
                "apnn_residual_quant_pack",
                "apnn_select_variant", "apnn_select_variant_fused",
@@ -332,6 +336,28 @@ def gemm_prepared_i8(A: torch.Tensor, Wp: torch.Tensor, M: int, N: int, K: int, 
     ce = None if epi is None else ctypes.byref(epi._c())
     _check(lib().apnn_gemm_prepared_i8(_ptr(A), _ptr(Wp), M, N, K, a_bits, w_bits, enc, ce, _ptr(out), _stream(A)),
            "apnn_gemm_prepared_i8")
+    return out
+
+
+def conv2d_prepared_i8(X: torch.Tensor, Wp: torch.Tensor, shape: ConvShape, a_bits: int, w_bits: int, enc: int,
+                       epi: Optional[Epilogue] = None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """APConv with prepared int8 weights (apnn_conv2d_prepared_i8; Wp = prepare_weights_i8 of the
+    packed OHWI weights as C_out*R*S rows of C_in).  Falls back (ApnnError UNSUPPORTED) to the
+    caller; output as conv2d."""
+    _cuda(X, "X", torch.int32)
+    _cuda(Wp, "Wp", torch.uint8)
+    if out is None:
+        if epi is None:
+            oshape = (shape.B, shape.Ho, shape.Wo, shape.C_out)
+        else:
+            Hp, Wpp = epi.pooled(shape.Ho, shape.Wo)
+            oshape = packed_shape(shape.B * Hp * Wpp, shape.C_out, epi.out_bits)
+        out = torch.empty(oshape, dtype=torch.int32, device=X.device)
+    _cuda(out, "out", torch.int32)
+    ce = None if epi is None else ctypes.byref(epi._c())
+    cs = shape._c()
+    _check(lib().apnn_conv2d_prepared_i8(_ptr(X), _ptr(Wp), ctypes.byref(cs), a_bits, w_bits, enc, ce, _ptr(out),
+                                         _stream(X)), "apnn_conv2d_prepared_i8")
     return out
 
 

@@ -369,9 +369,26 @@ apnn_status apnn_gemm_fused(const uint32_t* A, const uint32_t* W, int M, int N, 
     return apnn_gemm_ex(A, W, M, N, K, a_bits, w_bits, enc, epi, Y_packed, APNN_VARIANT_AUTO, stream);
 }
 
+static apnn_status conv_impl(const uint32_t* X, const void* W, bool prepared, const apnn_conv_shape* shp,
+                             int a_bits, int w_bits, apnn_encoding enc, const apnn_epilogue* epi, void* Y,
+                             apnn_variant variant, apnn_stream_t stream);
+
+apnn_status apnn_conv2d_prepared_i8(const uint32_t* X, const uint8_t* Wp, const apnn_conv_shape* shp, int a_bits,
+                                    int w_bits, apnn_encoding enc, const apnn_epilogue* epi, void* Y,
+                                    apnn_stream_t stream) {
+    return conv_impl(X, Wp, true, shp, a_bits, w_bits, enc, epi, Y, APNN_VARIANT_TC_I8, stream);
+}
+
 apnn_status apnn_conv2d_ex(const uint32_t* X, const uint32_t* W, const apnn_conv_shape* shp,
                            int a_bits, int w_bits, apnn_encoding enc, const apnn_epilogue* epi,
                            void* Y, apnn_variant variant, apnn_stream_t stream) {
+    return conv_impl(X, W, false, shp, a_bits, w_bits, enc, epi, Y, variant, stream);
+}
+
+static apnn_status conv_impl(const uint32_t* X, const void* Wv, bool prepared, const apnn_conv_shape* shp,
+                             int a_bits, int w_bits, apnn_encoding enc, const apnn_epilogue* epi, void* Y,
+                             apnn_variant variant, apnn_stream_t stream) {
+    const uint32_t* W = reinterpret_cast<const uint32_t*>(Wv);
     if (!shp) return APNN_ERR_INVALID_ARG;
     const apnn_conv_shape c = *shp;
     if (c.B < 0 || c.H < 1 || c.W < 1 || c.C_in < 1 || c.C_out < 1 || c.R < 1 || c.S < 1 ||
@@ -408,6 +425,16 @@ apnn_status apnn_conv2d_ex(const uint32_t* X, const uint32_t* W, const apnn_conv
     if (e.pool) {
         if (e.pool > Ho || e.pool > Wo) return APNN_ERR_SHAPE;
         if (resolve(variant, g) != APNN_VARIANT_TC_I8 || !tc_i8_pool_fusable(g, e)) return APNN_ERR_UNSUPPORTED;
+    }
+    if (prepared) {
+        if (g.M <= 128 || e.res) return APNN_ERR_UNSUPPORTED;
+        DevInfo d;
+        if ((st = device_info(&d)) != APNN_OK) return st;
+        if (g.M == 0) return APNN_OK;
+        cudaError_t err = launch_tc_i8_prepared(X, reinterpret_cast<const uint8_t*>(Wv), g, e, Y, d.sms,
+                                                (cudaStream_t)stream);
+        if (err == cudaErrorNotSupported) return APNN_ERR_UNSUPPORTED;
+        return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
     }
     return run(X, W, g, e, Y, variant, (cudaStream_t)stream);
 }

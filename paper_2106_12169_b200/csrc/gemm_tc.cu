@@ -1232,7 +1232,7 @@ static cudaError_t launch_tc_i8_impl(const uint32_t* A, const uint32_t* W, const
     if (e.res && !two) return cudaErrorNotSupported;  // residual epilogue: 2-CTA kernel only (ABI checks first)
     // small GEMMs (row f4): when the 2-CTA grid would occupy <= 1/4 of the SMs, run the
     // 1-CTA kernel with split-K clusters instead (latency: more CTAs, fewer k-blocks each)
-    if (Wprep && (!two || g.conv)) return cudaErrorNotSupported;  // prepared W: 2-CTA GEMM only
+    if (Wprep && !two) return cudaErrorNotSupported;  // prepared W: 2-CTA kernel only
     if (two && !g.conv && !e.res && !Wprep && g.M <= 1024 && g.nchunks >= 4 && tc_kernel_override() != 2) {
         const int BNP = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
         const long long pair_tiles = (long long)((g.M + 255) / 256) * ((g.N + BNP - 1) / BNP);
@@ -1329,7 +1329,8 @@ static cudaError_t launch_tc_i8_impl(const uint32_t* A, const uint32_t* W, const
             return cudaErrorInvalidValue;
         }
         if (p.prep) {
-            if (!make_prep_i8_map(&tb, Wprep, g.N, g.Cw * 32, brows)) return cudaErrorInvalidValue;
+            // GEMM: [N][Kp]; conv: [C_out][R*S*Cp] (taps x channel blocks) -- k-block kb at byte kb*128
+            if (!make_prep_i8_map(&tb, Wprep, g.N, g.RS * g.Cw * 32, brows)) return cudaErrorInvalidValue;
         } else if (!make_plane_map(&tb, W, g.N, g.w_bits, g.Cw, g.RS, brows)) {
             return cudaErrorInvalidValue;
         }

@@ -498,3 +498,24 @@ def test_i8_prepared_weights_exact(M, N, K, a_bits, w_bits, enc):
     got = ap.gemm_prepared_i8(Ap, Wprep, M, N, K, a_bits, w_bits, enc, epi=ap.Epilogue(4, cuda(alpha), cuda(beta), S))
     torch.cuda.synchronize()
     np.testing.assert_array_equal(u32(got), want)
+
+
+
+@pytest.mark.parametrize("shape", [CONV_SHAPES[0], CONV_SHAPES[1], CONV_SHAPES[3], (12, 8, 8, 128, 130, 3, 3, 2, 1),
+                                   (2, 28, 28, 96, 256, 3, 3, 1, 1), (4, 14, 14, 64, 128, 1, 1, 2, 0)])
+@pytest.mark.parametrize("a_bits,w_bits,enc", [(2, 1, 2), (8, 2, 0), (1, 1, 1), (2, 2, 0)])
+def test_conv_prepared_weights_exact(shape, a_bits, w_bits, enc):
+    B, H, Wd, C, Co, R, S, st, pad = shape
+    X, Wt = synth.conv_inputs(B, H, Wd, C, Co, R, S, a_bits, w_bits, tag="convprep")
+    want = oracle.conv2d(X, Wt, st, pad, a_bits, w_bits, enc)
+    Xp = ap.pack_bits(cuda(X.reshape(-1, C)), a_bits)
+    Wprep = ap.prepare_weights_i8(ap.pack_bits(cuda(Wt.reshape(-1, C)), w_bits), Co * R * S, C, w_bits, enc)
+    cs = ap.ConvShape(B, H, Wd, C, Co, R, S, st, pad)
+    got = ap.conv2d_prepared_i8(Xp, Wprep, cs, a_bits, w_bits, enc)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+    alpha, beta, Sd = epi_case(Co, 2, "convprep")
+    wantp = oracle.pack(oracle.epilogue(want.reshape(-1, Co), alpha, beta, Sd, 2), 2)
+    got = ap.conv2d_prepared_i8(Xp, Wprep, cs, a_bits, w_bits, enc, epi=ap.Epilogue(2, cuda(alpha), cuda(beta), Sd))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(u32(got), wantp)
