@@ -94,8 +94,10 @@ def main():
                     emit(dict(kind="gemm", n=n, prec=name, fused=fused, error=str(ex)))
                     continue
                 tops = 2.0 * n ** 3 / (ms * 1e-3) / 1e12
-                emit(dict(kind="gemm", n=n, prec=name, fused=fused, variant="tc_i8", us=round(ms * 1e3, 2),
-                          tops=round(tops, 1), frac=round(tops / peak_i8(), 3)))
+                vname = ap.variant_name(ap.select_variant(n, n, n, a, w, enc, a if fused else 0))
+                peak = peak_i8() * (2 if vname == "tc_fp4" else 1)
+                emit(dict(kind="gemm", n=n, prec=name, fused=fused, variant=vname, auto=True, us=round(ms * 1e3, 2),
+                          tops=round(tops, 1), frac=round(tops / peak, 3)))
     # variant comparison (north star: choose by measurement)
     for n in ([1024, 4096] if not quick else [1024]):
         for (a, w, enc, name) in GEMM_COMBOS:
