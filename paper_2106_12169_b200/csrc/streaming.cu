@@ -389,6 +389,65 @@ __global__ void __launch_bounds__(256) residual_quant_pack_kernel(const int32_t*
     }
 }
 
+// Vectorised residual routine (N % 4 == 0): warp = one row's 128 channels, lane = 4
+// consecutive channels (16-byte loads of Y and of an int32 shortcut; packed-code shortcut: the
+// lane's 4 bits of each plane word), nibbles OR-combined over 8 lanes into plane words.
+__global__ void __launch_bounds__(256) residual_quant_pack_v4_kernel(const int32_t* __restrict__ Y, int M, int N,
+                                                                     const void* __restrict__ Z, int z_bits,
+                                                                     const int32_t* __restrict__ rho, int Nw, Epi e,
+                                                                     uint32_t* __restrict__ out) {
+    const int Ng = Nw / 4;
+    const int total = M * Ng;  // host-checked < 2^31
+    const int lane = threadIdx.x & 31;
+    const int wstride = gridDim.x * (blockDim.x >> 5);
+    for (int idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); idx < total; idx += wstride) {
+        const int mi = idx / Ng;
+        const int grp = idx - mi * Ng;
+        const long long m = mi;
+        const int n = grp * 128 + lane * 4;
+        const int w = grp * 4 + (lane >> 3);
+        uint32_t q4 = 0;
+        if (n < N) {
+            const int4 y = __ldg(reinterpret_cast<const int4*>(Y + m * N + n));
+            int32_t z[4];
+            if (z_bits == 0) {
+                const int4 zz = __ldg(reinterpret_cast<const int4*>(reinterpret_cast<const int32_t*>(Z) + m * N + n));
+                z[0] = zz.x; z[1] = zz.y; z[2] = zz.z; z[3] = zz.w;
+            } else {
+                const uint32_t* zp = reinterpret_cast<const uint32_t*>(Z) + m * z_bits * Nw + w;
+                const int sh = (lane & 7) * 4;
+                uint32_t nib[8];
+#pragma unroll
+                for (int t = 0; t < 8; t++) nib[t] = t < z_bits ? (__ldg(zp + (long long)t * Nw) >> sh) & 0xFu : 0u;
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    uint32_t code = 0;
+#pragma unroll
+                    for (int t = 0; t < 8; t++) code |= ((nib[t] >> c) & 1u) << t;
+                    z[c] = (int32_t)code;
+                }
+            }
+            const int32_t yy[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const long long r = rho ? __ldg(rho + n + c) : 1;
+                const long long v = (long long)epi_alpha(e, n + c) * yy[c] + epi_beta(e, n + c) + r * z[c];
+                q4 |= quantise_v(e, v) << (8 * c);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; t++) {
+            if (t < e.out_bits) {
+                uint32_t nb = byte_bits_to_nibble(q4, t) << (4 * (lane & 7));
+                nb |= __shfl_xor_sync(0xFFFFFFFFu, nb, 1);
+                nb |= __shfl_xor_sync(0xFFFFFFFFu, nb, 2);
+                nb |= __shfl_xor_sync(0xFFFFFFFFu, nb, 4);
+                if ((lane & 7) == 0) out[(m * e.out_bits + t) * Nw + w] = nb;
+            }
+        }
+    }
+}
+
 static int stream_grid(long long total, int sms) {
     long long blocks = (total + 255) / 256;
     long long cap = (long long)sms * 8;  // 8 resident 256-thread CTAs per SM, grid-stride beyond
@@ -497,6 +556,13 @@ cudaError_t launch_residual_quant_pack(const int32_t* Y, int M, int N, const voi
     const long long total = (long long)M * Nw;
     if (total == 0) return cudaSuccess;
     if (total > 2147483647LL) return cudaErrorInvalidValue;
+    if (N % 4 == 0 && ((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(Z)) & 15) == 0 &&
+        pool_v4_enabled()) {
+        residual_quant_pack_v4_kernel<<<stream_grid((long long)M * (Nw / 4) * 32, sms), 256, 0, s>>>(
+            Y, M, N, Z, z_bits, rho, Nw, e, out);
+        count_launch();
+        return cudaGetLastError();
+    }
     residual_quant_pack_kernel<<<stream_grid(total * 32, sms), 256, 0, s>>>(Y, M, N, Z, z_bits, rho, Nw, e, out);
     count_launch();
     return cudaGetLastError();
