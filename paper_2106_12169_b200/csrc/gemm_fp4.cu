@@ -415,7 +415,8 @@ static bool fp4_dual() {
     static int v = -1;
     if (v < 0) {
         const char* s = getenv("APNN_FP4_BN192");
-        v = s ? atoi(s) : 1;
+        v = s ? atoi(s) : 0;  // experiment: +4.7 % in the CUDA-graph sweep, -1..2 % in the bench (L2 flushed;
+                              // ncu 376.5 vs 350.8 us: the A decode per MAC grows by 256/192)
     }
     return v != 0;
 }
@@ -455,7 +456,7 @@ static cudaError_t launch_fp4_impl(const uint32_t* A, const void* W, bool prep, 
         p.tab_mode = tc::kTabHybrid;
     const int ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
     // prepared W, fused output: 128 x 192 tiles, two CTAs per SM (one's epilogue overlaps the
-    // other's main loop; TMEM 192 + 32 scale columns -> 256 each); APNN_FP4_BN192=0 disables
+    // other's main loop; TMEM 192 + 32 scale columns -> 256 each); experiment knob APNN_FP4_BN192=1
     const bool dual = prep && g.N > 128 && e.out_bits > 0 && fp4_dual();  // measured: +3-5 % fused, int32 even
     const int BN = dual ? 192 : (g.N > 128 ? 256 : 128);
     p.a_bytes = 32u * BM * g.a_bits;
