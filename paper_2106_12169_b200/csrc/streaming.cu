@@ -279,29 +279,49 @@ __global__ void __launch_bounds__(256) im2col_pack_kernel(const uint8_t* __restr
         __syncthreads();
         for (int task = threadIdx.x; task < Wo * Kw; task += blockDim.x) {
             const int wo = task / Kw, w = task - wo * Kw;
+            // for a filter row r the S*C codes of the window are one contiguous smem run:
+            // element k = r*S*C + j sits at byte r*rowb + wo*stride*C + j
+            const int SC = S * C;
             int k = w * 32;
-            int r = k / (S * C), sc = k - r * S * C, s2 = sc / C, c = sc - s2 * C;
+            int r = k / SC, j = k - r * SC;
             const uint8_t* base = rows + wo * stride * C;
+            int off = r * rowb + j;
             uint32_t qb[8];  // byte i of qb[j] = code of element 4j + i (as in pack_bits_kernel)
 #pragma unroll
-            for (int j = 0; j < 8; j++) qb[j] = 0;
+            for (int q = 0; q < 8; q++) qb[q] = 0;
 #pragma unroll
             for (int e = 0; e < 32; e++) {
-                if (k < K) qb[e >> 2] |= (uint32_t)base[r * rowb + s2 * C + c] << (8 * (e & 3));
-                k++;
-                if (++c == C) {
-                    c = 0;
-                    if (++s2 == S) { s2 = 0; r++; }
-                }
+                if (k + e < K) qb[e >> 2] |= (uint32_t)base[off] << (8 * (e & 3));
+                off++;
+                if (++j == SC) { j = 0; off += rowb - SC; }
             }
             uint32_t* o = outw + wo * bits * Kw + w;
+            if (bits > 4) {  // 8x8 bit-matrix transposes: byte t of group g = plane t of codes 8g..8g+7
+                uint32_t pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-            for (int t = 0; t < 8; t++) {
-                if (t < bits) {
-                    uint32_t word = 0;
+                for (int g = 0; g < 4; g++) {
+                    unsigned long long x = ((unsigned long long)qb[2 * g + 1] << 32) | qb[2 * g];
+                    unsigned long long d = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
+                    x ^= d ^ (d << 7);
+                    d = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
+                    x ^= d ^ (d << 14);
+                    d = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
+                    x ^= d ^ (d << 28);
 #pragma unroll
-                    for (int q = 0; q < 8; q++) word |= byte_bits_to_nibble(qb[q], t) << (4 * q);
-                    o[t * Kw] = word;
+                    for (int t = 0; t < 8; t++) pw[t] |= (uint32_t)((x >> (8 * t)) & 0xFFull) << (8 * g);
+                }
+#pragma unroll
+                for (int t = 0; t < 8; t++)
+                    if (t < bits) o[t * Kw] = pw[t];
+            } else {
+#pragma unroll
+                for (int t = 0; t < 4; t++) {
+                    if (t < bits) {
+                        uint32_t word = 0;
+#pragma unroll
+                        for (int q = 0; q < 8; q++) word |= byte_bits_to_nibble(qb[q], t) << (4 * q);
+                        o[t * Kw] = word;
+                    }
                 }
             }
         }

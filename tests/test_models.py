@@ -37,10 +37,11 @@ def test_model_logits_match_oracle(name, B, w, a):
     np.testing.assert_array_equal(again.cpu().numpy(), want)
 
 
-def test_im2col_pack_and_flatten_match_oracle_layouts():
-    X = synth.codes((2, 11, 13, 3), 2, "im2col")
+@pytest.mark.parametrize("bits", [2, 5, 8])
+def test_im2col_pack_and_flatten_match_oracle_layouts(bits):
+    X = synth.codes((2, 11, 13, 3), bits, "im2col")
     cs = ap.ConvShape(2, 11, 13, 3, 1, 5, 5, 2, 2)
-    got = ap.im2col_pack(torch.from_numpy(X).cuda(), cs, 2).cpu().numpy().view(np.uint32)
+    got = ap.im2col_pack(torch.from_numpy(X).cuda(), cs, bits).cpu().numpy().view(np.uint32)
     # oracle-side im2col by direct indexing, then the oracle packer
     rows = []
     for b in range(2):
@@ -52,7 +53,7 @@ def test_im2col_pack_and_flatten_match_oracle_layouts():
                         h, w_ = ho * 2 + i - 2, wo * 2 + j - 2
                         r.extend(X[b, h, w_] if 0 <= h < 11 and 0 <= w_ < 13 else [0, 0, 0])
                 rows.append(r)
-    np.testing.assert_array_equal(got, oracle.pack(np.array(rows, np.uint8), 2))
+    np.testing.assert_array_equal(got, oracle.pack(np.array(rows, np.uint8), bits))
     F = synth.codes((3 * 4, 256), 2, "flatten")
     Fp = ap.pack_bits(torch.from_numpy(F).cuda(), 2)
     flat = ap.flatten_packed(Fp, 3, 4).cpu().numpy().view(np.uint32)
