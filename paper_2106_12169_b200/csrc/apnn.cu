@@ -128,9 +128,9 @@ static apnn_status make_epi(const apnn_epilogue* epi, Epi* e) {
 }
 
 // AUTO dispatch (measured, scripts/fp4_time.py, profiles/r01_fp4.json): the exact FP4
-// formulation wins every fused (requantised) GEMM with operands <= 2 bits above one CTA
-// row-tile, and int32-output w1a2 / w2a1 GEMMs from 2048^2; the int8 tensor-core variant
-// everything else (conv, wider codes, small-M split-K, residual / pooling epilogues).
+// formulation wins every GEMM with operands <= 2 bits and at least 64 tiles of 128 x 256
+// (fused output, or int32 output with N >= 256); the int8 tensor-core variant everything else
+// (conv, wider codes, narrow int32 outputs, small-M split-K, residual / pooling epilogues).
 static bool fp4_enabled() {
     static int v = -1;
     if (v < 0) {
@@ -146,8 +146,10 @@ static apnn_variant resolve(apnn_variant v, const Geom& g, const Epi* e = nullpt
     // the FP4 kernel is one CTA per 128 x 256 tile without split-K: require enough tiles to
     // fill the SMs, else the int8 variant's split-K clusters win (VGG FC at batch 256)
     const long long fp4_tiles = (long long)((g.M + 127) / 128) * ((g.N + 255) / 256);
+    // int32 outputs: only wide ones (the models' first-layer GEMMs, N = 64..96, measured faster
+    // on the int8 pair kernel)
     if (fp4_enabled() && tc_fp4_supports(g) && fp4_tiles >= 64 && !(e && (e->res || e->pool)) &&
-        (fused || (g.a_bits + g.w_bits == 3 && g.M >= 2048 && g.N >= 2048)))
+        (fused || g.N >= 256))
         return APNN_VARIANT_TC_FP4;
     if (tc_i8_supports(g)) return APNN_VARIANT_TC_I8;
     return APNN_VARIANT_POPC;

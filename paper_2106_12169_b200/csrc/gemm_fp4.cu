@@ -322,6 +322,10 @@ __global__ void __launch_bounds__(THREADS, BN == 192 ? 2 : 1)  // BN = 192: two 
         tc_fence_after();
         const int m = m0 + t;
         constexpr int half = BN / 2;
+        // int32 output: stage each 32 x 32 block in the (now idle) operand smem and write it back
+        // coalesced (4 full 128-byte row segments per store instruction) instead of one row per lane
+        const bool lsu = p.e.out_bits == 0 && (g.N & 3) == 0;
+        uint8_t* stg = smem + (warp - 2) * 4096;
 #pragma unroll 1
         for (int c = grp * half; c < (grp + 1) * half; c += 32) {
             uint32_t acc[32];
@@ -329,6 +333,13 @@ __global__ void __launch_bounds__(THREADS, BN == 192 ? 2 : 1)  // BN = 192: two 
             tmem_wait_ld();
 #pragma unroll
             for (int k = 0; k < 32; k++) acc[k] = (uint32_t)__float2int_rn(__uint_as_float(acc[k]));  // exact
+            if (lsu) {
+                tc::stage_int32_chunk(acc, stg, lane);
+                __syncwarp();
+                tc::writeback_int32_block(stg, lane, reinterpret_cast<int32_t*>(p.Y), m0 + q * 32, g.M, n0 + c, g.N);
+                __syncwarp();
+                continue;
+            }
             tc::epilogue_chunk(acc, m, n0 + c, c, g, p.e, p.Y, sTab, p.tab_mode);
         }
     }

@@ -32,7 +32,7 @@ def supported(variant, M, N, K, a, w, enc, conv=False):
     if variant == ap.VARIANT_TC_I8 and conv:
         return K > 0
     if variant == ap.VARIANT_TC_I8:
-        return ap.select_variant(max(M, 1), max(N, 1), max(K, 1), a, w, enc) == ap.VARIANT_TC_I8
+        return M > 0 and N > 0 and K > 0  # the int8 tensor-core kernels take every shape
     return True
 
 
