@@ -181,7 +181,7 @@ __device__ __forceinline__ void recomb_row_kb(const uint8_t* planes, int rows, i
 // PREP: W arrives pre-recombined (apnn_prepare_weights: e2m1 nibbles in the kernel's element
 // order, padding = value 0) and is loaded by TMA straight into the SWIZZLE_128B operand tile;
 // only A is recombined per tile.
-template <int BN, bool A_PM1, bool W_PM1, bool PREP = false>
+template <int BN, bool A_PM1, bool W_PM1, bool PREP = false, bool I32 = false>
 __global__ void __launch_bounds__(THREADS, BN == 192 ? 2 : 1)  // BN = 192: two CTAs per SM (TMEM 256 cols each)
     fp4_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB, const Params p) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -324,7 +324,8 @@ __global__ void __launch_bounds__(THREADS, BN == 192 ? 2 : 1)  // BN = 192: two 
         constexpr int half = BN / 2;
         // int32 output: stage each 32 x 32 block in the (now idle) operand smem and write it back
         // coalesced (4 full 128-byte row segments per store instruction) instead of one row per lane
-        const bool lsu = p.e.out_bits == 0 && (g.N & 3) == 0;
+        // (compile-time: the branch in the fused instances cost them ~6 % -- register allocation)
+        constexpr bool lsu = I32;
         uint8_t* stg = smem + (warp - 2) * 4096;
 #pragma unroll 1
         for (int c = grp * half; c < (grp + 1) * half; c += 32) {
@@ -402,7 +403,8 @@ static bool make_map_prep(CUtensorMap* m, const uint8_t* base, int N, int Kw, in
 template <int BN, bool AP, bool WP, bool PREP>
 static cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, dim3 grid, size_t smem,
                           cudaStream_t s) {
-    auto kfn = fp4_kernel<BN, AP, WP, PREP>;
+    auto kfn = (p.e.out_bits == 0 && (p.g.N & 3) == 0) ? fp4_kernel<BN, AP, WP, PREP, true>
+                                                        : fp4_kernel<BN, AP, WP, PREP, false>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     kfn<<<grid, THREADS, smem, s>>>(ta, tb, p);
