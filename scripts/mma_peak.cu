@@ -4,6 +4,8 @@
 //   mode 1: 1-CTA  M=128 N=256 K=32, A TMEM  (TS)
 //   mode 2: 2-CTA  M=256 N=256 K=32, A smem  (SS, cta_group::2)
 //   mode 3: 2-CTA  M=256 N=256 K=32, A TMEM  (TS, cta_group::2)
+//   mode 4: 1-CTA  M=128 N=256 K=64, kind::mxf4 block32 (e2m1, E8M0 scales in TMEM), SS
+//   mode 5: 2-CTA  M=256 N=256 K=64, kind::mxf4 block32, SS (cta_group::2)
 // Operands are zeros (timing is value-independent).  Build:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I ../paper_2106_12169_b200/csrc mma_peak.cu -o mma_peak
 #include <cstdio>
@@ -20,7 +22,8 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(int iters, unsigned long l
     uint8_t* sB = smem + 16384;    // 256 rows x 128 B (1-CTA) / 128 rows (2-CTA)
     __shared__ uint64_t bar;
     __shared__ uint32_t holder;
-    constexpr bool two = MODE >= 2;
+    constexpr bool two = MODE == 2 || MODE == 3 || MODE == 5;
+    constexpr bool fp4 = MODE >= 4;
     const int warp = threadIdx.x / 32;
     for (int i = threadIdx.x; i < 49152 / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
     if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
@@ -34,6 +37,17 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(int iters, unsigned long l
     tc_fence_after();
     const uint32_t tmem = holder;
     const bool leader = !two || cluster_ctarank() == 0;
+    if (fp4) {  // scale-factor columns 256..287 of every lane: E8M0 127 (2^0)
+        const uint32_t ones[8] = {0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu,
+                                  0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu};
+        const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
+        for (uint32_t c = 0; c < 32; c += 8) tmem_st8(lb + 256 + c, ones);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncthreads();
+        if (two) cluster_sync();
+        tc_fence_after();
+    }
     unsigned long long t0 = clock64();
     if (warp == 1 && leader && (threadIdx.x % 32) == 0) {
         const uint32_t idesc = idesc_i8(two ? 256 : 128, 256, false, false);
@@ -50,6 +64,20 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(int iters, unsigned long l
                                  "l"(umma_desc_sw128(abase + kk * 32, 1024)), "l"(bd), "r"(idesc) : "memory");
                 }
                 if (MODE == 3) mma2_i8_ts(tmem, tmem + 256 + kk * 8, bd, idesc, 1);
+                if (MODE == 4 || MODE == 5) {
+                    const uint32_t id4 = (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) | (1u << 23) |
+                                         ((uint32_t)((MODE == 5 ? 256 : 128) >> 4) << 24);
+                    if (MODE == 4)
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                                     "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%4], [%5], p;\n\t}"
+                                     ::"r"(tmem), "l"(umma_desc_sw128(abase + kk * 32, 1024)), "l"(bd), "r"(id4),
+                                     "r"(tmem + 256), "r"(tmem + 272) : "memory");
+                    else
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                                     "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%4], [%5], p;\n\t}"
+                                     ::"r"(tmem), "l"(umma_desc_sw128(abase + kk * 32, 1024)), "l"(bd), "r"(id4),
+                                     "r"(tmem + 256), "r"(tmem + 272) : "memory");
+                }
             }
         }
         if (two) mma2_commit_mc(&bar, 0x3); else mma_commit(&bar);
@@ -75,7 +103,8 @@ void run(int iters, int sms) {
     cfg.dynamicSmemBytes = 49152 + 1024;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = MODE >= 2 ? 2 : 1;
+    constexpr bool two = MODE == 2 || MODE == 3 || MODE == 5;
+    attr[0].val.clusterDim.x = two ? 2 : 1;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -93,16 +122,16 @@ void run(int iters, int sms) {
     cudaEventElapsedTime(&ms, e0, e1);
     unsigned long long cyc[512];
     cudaMemcpy(cyc, d, sms * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-    const double M = MODE >= 2 ? 256 : 128;
-    const int units = MODE >= 2 ? sms / 2 : sms;
-    const double ops = 2.0 * M * 256 * 32 * 4.0 * iters * units;
-    const double mac_per_clk_sm = (ops / 2) / (double)cyc[0] / (MODE >= 2 ? 2 : 1) / 1.0 * 1.0 / 1.0;
+    const double M = two ? 256 : 128;
+    const double Kst = MODE >= 4 ? 64 : 32;  // K per instruction (fp4: 64 elements in 32 bytes)
+    const int units = two ? sms / 2 : sms;
+    const double ops = 2.0 * M * 256 * Kst * 4.0 * iters * units;
     printf("{\"mode\": %d, \"name\": \"%s\", \"err\": \"%s\", \"ms\": %.3f, \"tops\": %.1f, \"cycles_cta0\": %llu, "
-           "\"int8_mac_per_clk_per_sm\": %.0f}\n",
-           MODE, MODE == 0 ? "1cta_SS" : MODE == 1 ? "1cta_TS" : MODE == 2 ? "2cta_SS" : "2cta_TS",
+           "\"mac_per_clk_per_sm\": %.0f, \"clk_ghz_cta0\": %.3f}\n",
+           MODE, MODE == 0 ? "i8_1cta_SS" : MODE == 1 ? "i8_1cta_TS" : MODE == 2 ? "i8_2cta_SS" : MODE == 3 ? "i8_2cta_TS"
+                 : MODE == 4 ? "mxf4_1cta_SS" : "mxf4_2cta_SS",
            cudaGetErrorString(err), ms, ops / (ms * 1e-3) / 1e12, cyc[0],
-           (2.0 * M * 256 * 32 * 4.0 * iters / 2) / (double)cyc[0] / (MODE >= 2 ? 2 : 1));
-    (void)mac_per_clk_sm;
+           (M * 256 * Kst * 4.0 * iters) / (double)cyc[0] / (two ? 2 : 1), (double)cyc[0] / (ms * 1e6));
     cudaFree(d);
 }
 
@@ -113,5 +142,7 @@ int main(int argc, char** argv) {
     run<1>(iters, sms);
     run<2>(iters, sms);
     run<3>(iters, sms);
+    run<4>(iters, sms);
+    run<5>(iters, sms);
     return 0;
 }

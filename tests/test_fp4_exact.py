@@ -1,0 +1,213 @@
+"""Exactness of the FP4 formulation on adversarial inputs.
+
+The exact-FP4 kernel feeds <= 2-bit codes to `tcgen05.mma kind::mxf4` as e2m1 values
+and accumulates in fp32.  Products are exact (|a*w| <= 9) and an fp32 accumulator is
+exact for every integer of magnitude < 2^24 *if* each accumulation step rounds to
+nearest with no narrower internal alignment -- which the PTX ISA does not promise
+(the paper's rationale for 32-bit integer accumulation is PAPER.md:1493; the
+"wider type" route is P:142-143 / P:1390-1391).  So the host bound
+K*max|a|*max|w| < 2^24 (tc_fp4_supports) is only trusted where these tests pass:
+
+  * all 9 legal <= 2-bit (a_bits, w_bits, encoding) combinations;
+  * all-max codes at K = 8192 (w2a2: Y = 73 728; w1a2 Case III: +-24 576);
+  * a large running sum followed by small random terms (low bits decide the result
+    at |Y| ~ 2^16 .. 2^24);
+  * cancelling patterns: +W on the first half of K, -W on the rest, and signs that
+    alternate inside one 64-wide MMA K step;
+  * K just under the host bound (w2a2 all 3 at K = 1 864 128: Y = 16 777 152, the
+    last 64 terms random so the low bits of a 2^24-magnitude sum are tested);
+  * uniform random codes at K = 8192 and the full-size w2a2 8192^3 AUTO shape.
+
+Expected values come only from oracle.gemm (plain C, int64).  Both FP4 entry points
+run: apnn_gemm_ex(VARIANT_TC_FP4) (W recombined per tile) and apnn_gemm_prepared
+(W prepared once).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2106_12169_b200 as ap
+from paper_2106_12169_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+# the 9 legal (a_bits, w_bits, enc) with both operands <= 2 bits
+FP4_COMBOS = [(a, w, e) for a in (1, 2) for w in (1, 2) for e in range(4)
+              if e == 0 or (e == 1 and a == 1 and w == 1) or (e == 2 and w == 1) or (e == 3 and a == 1)]
+assert len(FP4_COMBOS) == 9
+
+
+def cuda(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def maxcode(bits, pm1):
+    return 1 if pm1 else (1 << bits) - 1
+
+
+def a_pm1(enc):
+    return enc in (1, 3)
+
+
+def w_pm1(enc):
+    return enc in (1, 2)
+
+
+def run_fp4_both(A, W, a, w, enc, epi=None):
+    """(per-tile W decode result, prepared-W result) on the FP4 kernel."""
+    M, K = A.shape
+    N = W.shape[0]
+    Ap = ap.pack_bits(cuda(A), a)
+    Wpl = ap.pack_bits(cuda(W), w)
+    y1 = ap.gemm(Ap, Wpl, M, N, K, a, w, enc, epi=epi, variant=ap.VARIANT_TC_FP4)
+    Wprep = ap.prepare_weights(Wpl, N, K, w, enc)
+    y2 = ap.gemm_prepared(Ap, Wprep, M, N, K, a, w, enc, epi=epi)
+    torch.cuda.synchronize()
+    return y1, y2
+
+
+def check(A, W, a, w, enc, what):
+    want = oracle.gemm(A, W, a, w, enc)
+    y1, y2 = run_fp4_both(A, W, a, w, enc)
+    np.testing.assert_array_equal(y1.cpu().numpy(), want, err_msg=f"{what}: tc_fp4")
+    np.testing.assert_array_equal(y2.cpu().numpy(), want, err_msg=f"{what}: tc_fp4 prepared")
+    return want
+
+
+@pytest.mark.parametrize("a,w,enc", FP4_COMBOS)
+def test_fp4_all_max_codes_k8192(a, w, enc):
+    M, N, K = 200, 300, 8192
+    A = np.full((M, K), maxcode(a, a_pm1(enc)), np.uint8)
+    W = np.full((N, K), maxcode(w, w_pm1(enc)), np.uint8)
+    if w_pm1(enc):
+        W[N // 2:] = 0  # half the rows -1: negative extremes too
+    want = check(A, W, a, w, enc, "all-max")
+    assert np.abs(want).max() == K * (1 if a_pm1(enc) else (1 << a) - 1) * (1 if w_pm1(enc) else (1 << w) - 1)
+
+
+@pytest.mark.parametrize("a,w,enc", FP4_COMBOS)
+def test_fp4_large_then_small_terms(a, w, enc):
+    # running sum near its maximum for 7/8 of K, then random codes: the low bits of a
+    # large accumulator decide the result
+    M, N, K = 130, 260, 8192
+    g = synth.rng(f"fp4-lts-{a}{w}{enc}")
+    A = np.full((M, K), maxcode(a, a_pm1(enc)), np.uint8)
+    W = np.full((N, K), maxcode(w, w_pm1(enc)), np.uint8)
+    t = K * 7 // 8
+    A[:, t:] = g.integers(0, 1 << a, size=(M, K - t), dtype=np.uint8)
+    W[:, t:] = g.integers(0, 1 << w, size=(N, K - t), dtype=np.uint8)
+    check(A, W, a, w, enc, "large-then-small")
+
+
+@pytest.mark.parametrize("a,w,enc", [c for c in FP4_COMBOS if c[2] != 0])
+def test_fp4_cancelling_halves(a, w, enc):
+    # +W on the first half of K, -W on the second (one operand is +-1): the partial sums
+    # climb to ~K/2*max and cancel back; an odd tail keeps the low bit significant
+    M, N, K = 140, 270, 8192
+    g = synth.rng(f"fp4-cancel-{a}{w}{enc}")
+    A = g.integers(0, 1 << a, size=(M, K), dtype=np.uint8)
+    W = g.integers(0, 1 << w, size=(N, K), dtype=np.uint8)
+    if w_pm1(enc):
+        A[:, :] = maxcode(a, a_pm1(enc))
+        A[:, -3:] = g.integers(0, 1 << a, size=(M, 3), dtype=np.uint8)
+        W[:, : K // 2] = 1
+        W[:, K // 2:] = 0
+    else:  # +-1 activations x 0/1 weights
+        W[:, :] = maxcode(w, False)
+        W[:, -3:] = g.integers(0, 1 << w, size=(N, 3), dtype=np.uint8)
+        A[:, : K // 2] = 1
+        A[:, K // 2:] = 0
+    check(A, W, a, w, enc, "cancelling halves")
+
+
+@pytest.mark.parametrize("a,w,enc", [c for c in FP4_COMBOS if c[2] != 0])
+def test_fp4_mixed_signs_inside_mma_block(a, w, enc):
+    # signs alternate every element (inside one 64-wide K step) on top of a large offset
+    M, N, K = 129, 257, 8192
+    g = synth.rng(f"fp4-mixed-{a}{w}{enc}")
+    A = g.integers(0, 1 << a, size=(M, K), dtype=np.uint8)
+    W = g.integers(0, 1 << w, size=(N, K), dtype=np.uint8)
+    pm = np.arange(K) % 2
+    if w_pm1(enc):
+        W[:, : K // 2] = 1                       # offset: + on the first half
+        W[:, K // 2:] = pm[K // 2:][None, :]     # then alternating signs
+    else:
+        A[:, : K // 2] = 1
+        A[:, K // 2:] = pm[K // 2:][None, :]
+    check(A, W, a, w, enc, "mixed signs")
+
+
+@pytest.mark.parametrize("a,w,enc", FP4_COMBOS)
+def test_fp4_uniform_k8192(a, w, enc):
+    M, N, K = 300, 520, 8192
+    A, W = synth.gemm_inputs(M, N, K, a, w, tag="fp4-uni8192")
+    want = check(A, W, a, w, enc, "uniform K=8192")
+    if enc == 0 and a == 2 and w == 2:
+        assert np.abs(want).mean() > 1.5e4  # |Y| well above 2^14 on average
+
+
+def fp4_bound_k(a, w, enc):
+    ma = 1 if a_pm1(enc) else (1 << a) - 1
+    mw = 1 if w_pm1(enc) else (1 << w) - 1
+    return ((1 << 24) - 1) // (ma * mw)
+
+
+@pytest.mark.parametrize("a,w,enc", [(2, 2, 0), (2, 1, 2), (1, 1, 1)])
+def test_fp4_k_near_host_bound(a, w, enc):
+    # K just under the bound K*max|a|*max|w| < 2^24, rounded down to whole 64-element MMA
+    # steps; every term at its maximum except the last 64, which are random: the result
+    # sits just below 2^24 with random low bits.
+    K = fp4_bound_k(a, w, enc) // 64 * 64
+    M, N = 4, 8
+    g = synth.rng(f"fp4-bound-{a}{w}{enc}")
+    A = np.full((M, K), maxcode(a, a_pm1(enc)), np.uint8)
+    W = np.full((N, K), maxcode(w, w_pm1(enc)), np.uint8)
+    A[:, -64:] = g.integers(0, 1 << a, size=(M, 64), dtype=np.uint8)
+    W[:, -64:] = g.integers(0, 1 << w, size=(N, 64), dtype=np.uint8)
+    want = check(A, W, a, w, enc, f"K={K} near the 2^24 bound")
+    assert np.abs(want).max() > (1 << 23)
+
+
+def test_fp4_rejects_past_host_bound():
+    a, w, enc = 2, 2, 0
+    K = fp4_bound_k(a, w, enc) + 1
+    Ap = torch.zeros(ap.packed_shape(4, K, a), dtype=torch.int32, device="cuda")
+    Wp = torch.zeros(ap.packed_shape(8, K, w), dtype=torch.int32, device="cuda")
+    with pytest.raises(ap.ApnnError) as ei:
+        ap.gemm(Ap, Wp, 4, 8, K, a, w, enc, variant=ap.VARIANT_TC_FP4)
+    assert ei.value.status == 7  # APNN_ERR_UNSUPPORTED
+    assert ap.select_variant(4096, 4096, K, a, w, enc) != ap.VARIANT_TC_FP4
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_fp4_full_size_w2a2_auto_sampled_rows(fused):
+    # the shape AUTO routes to the FP4 kernel with mean |Y| ~ 18 400 (> 2^14)
+    M = N = K = 8192
+    a, w, enc = 2, 2, 0
+    assert ap.select_variant(M, N, K, a, w, enc, a if fused else 0) == ap.VARIANT_TC_FP4
+    A, W = synth.gemm_inputs(M, N, K, a, w, tag="fp4-w2a2-full")
+    alpha, beta = synth.epilogue_params(N, tag="fp4-w2a2-full")
+    S = 1 << 12
+    epi = ap.Epilogue(a, cuda(alpha), cuda(beta), S) if fused else None
+    Ap = ap.pack_bits(cuda(A), a)
+    Wpl = ap.pack_bits(cuda(W), w)
+    Y = ap.gemm(Ap, Wpl, M, N, K, a, w, enc, epi=epi)
+    Wprep = ap.prepare_weights(Wpl, N, K, w, enc)
+    Y2 = ap.gemm_prepared(Ap, Wprep, M, N, K, a, w, enc, epi=epi)
+    torch.cuda.synchronize()
+    g = synth.rng("fp4-w2a2-full-rows")
+    rows = np.array(sorted(set([0, 1, 127, 128, M - 1] + g.integers(0, M, size=24).tolist())))
+    want = oracle.gemm(A[rows], W, a, w, enc)
+    if fused:
+        want = oracle.pack(oracle.epilogue(want, alpha, beta, S, a), a)
+        np.testing.assert_array_equal(u32(Y)[rows], want)
+        np.testing.assert_array_equal(u32(Y2)[rows], want)
+    else:
+        assert np.abs(want).mean() > 1.5e4
+        np.testing.assert_array_equal(Y.cpu().numpy()[rows], want)
+        np.testing.assert_array_equal(Y2.cpu().numpy()[rows], want)
