@@ -41,6 +41,8 @@ cudaError_t launch_tc_fp4_prepared(const uint32_t* A, const uint8_t* Wp, const G
                                    cudaStream_t s);
 cudaError_t launch_prepare_weights(const uint32_t* W, int N, int K, int w_bits, int enc, uint8_t* out, int sms,
                                    cudaStream_t s);
+cudaError_t launch_tc_fp4_pair_prepared(const uint32_t* A, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
+                                        int sms, cudaStream_t s);
 cudaError_t launch_prepare_weights_i8(const uint32_t* W, int N, int K, int w_bits, int enc, uint8_t* out, int sms,
                                       cudaStream_t s);
 cudaError_t launch_tc_i8_prepared(const uint32_t* A, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
@@ -138,6 +140,15 @@ static bool fp4_enabled() {
         v = s ? atoi(s) : 1;
     }
     return v != 0;
+}
+
+static int fp4_kernel_choice() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("APNN_FP4_KERNEL");
+        v = s ? atoi(s) : 0;
+    }
+    return v;
 }
 
 static apnn_variant resolve(apnn_variant v, const Geom& g, const Epi* e = nullptr) {
@@ -313,7 +324,11 @@ apnn_status apnn_gemm_prepared(const uint32_t* A, const uint8_t* Wp, int M, int 
     DevInfo d;
     if ((st = device_info(&d)) != APNN_OK) return st;
     if (M == 0 || N == 0) return APNN_OK;
-    cudaError_t err = launch_tc_fp4_prepared(A, Wp, g, e, Y, (cudaStream_t)stream);
+    // M > 128: the persistent CTA-pair kernel (gemm_fp4_pair.cu); else the one-CTA kernel.
+    // APNN_FP4_KERNEL=1 (read once) forces the one-CTA kernel for A/B measurements.
+    cudaError_t err = (M > 128 && fp4_kernel_choice() != 1)
+                          ? launch_tc_fp4_pair_prepared(A, Wp, g, e, Y, d.sms, (cudaStream_t)stream)
+                          : launch_tc_fp4_prepared(A, Wp, g, e, Y, (cudaStream_t)stream);
     return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }
 

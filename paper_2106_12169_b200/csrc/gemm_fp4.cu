@@ -357,7 +357,7 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-static PFN_encodeTiled get_encode() {
+PFN_encodeTiled get_encode() {
     static PFN_encodeTiled fn = nullptr;
     static std::once_flag once;
     std::call_once(once, [] {
@@ -374,7 +374,7 @@ static PFN_encodeTiled get_encode() {
 
 // packed [rows][bits][Kw] as {Kw, rows, bits}; box {8 words = 2 k-blocks, box_rows, bits}
 // lands as [plane][row][32 B]
-static bool make_map(CUtensorMap* m, const uint32_t* base, int rows, int bits, int Kw, int box_rows) {
+bool make_map(CUtensorMap* m, const uint32_t* base, int rows, int bits, int Kw, int box_rows) {
     PFN_encodeTiled enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[4] = {(cuuint64_t)Kw, (cuuint64_t)rows, (cuuint64_t)bits, 1};
@@ -388,7 +388,7 @@ static bool make_map(CUtensorMap* m, const uint32_t* base, int rows, int bits, i
 
 // prepared W [N][Kw*16 bytes] as a 2-D byte tensor; box {128 bytes, BN rows} with
 // SWIZZLE_128B lands exactly in the UMMA K-major SWIZZLE_128B operand layout
-static bool make_map_prep(CUtensorMap* m, const uint8_t* base, int N, int Kw, int box_rows) {
+bool make_map_prep(CUtensorMap* m, const uint8_t* base, int N, int Kw, int box_rows) {
     PFN_encodeTiled enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)Kw * 16, (cuuint64_t)N};

@@ -211,3 +211,27 @@ def test_fp4_full_size_w2a2_auto_sampled_rows(fused):
         assert np.abs(want).mean() > 1.5e4
         np.testing.assert_array_equal(Y.cpu().numpy()[rows], want)
         np.testing.assert_array_equal(Y2.cpu().numpy()[rows], want)
+
+
+@pytest.mark.parametrize("a,w,enc", [(2, 1, 2), (2, 2, 0), (1, 1, 1), (1, 2, 3)])
+@pytest.mark.parametrize("out_bits", [0, 1, 2, 5])
+def test_fp4_pair_kernel_persistent_tiles(a, w, enc, out_bits):
+    # the prepared-W path runs the persistent CTA-pair kernel for M > 128: 16 x 6 = 96 pair
+    # tiles (more than the 74 pairs: several tiles per pair, both TMEM accumulators), ragged N
+    # (1200 = 5 x 224 + 80), K not a multiple of the 256-element stage
+    M, N, K = 4096, 1200, 1000
+    A, W = synth.gemm_inputs(M, N, K, a, w, tag="fp4-pair")
+    Y = oracle.gemm(A, W, a, w, enc)
+    Ap = ap.pack_bits(cuda(A), a)
+    Wprep = ap.prepare_weights(ap.pack_bits(cuda(W), w), N, K, w, enc)
+    if out_bits == 0:
+        got = ap.gemm_prepared(Ap, Wprep, M, N, K, a, w, enc)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(got.cpu().numpy(), Y)
+    else:
+        alpha, beta = synth.epilogue_params(N, tag="fp4-pair")
+        S = 53
+        want = oracle.pack(oracle.epilogue(Y, alpha, beta, S, out_bits), out_bits)
+        got = ap.gemm_prepared(Ap, Wprep, M, N, K, a, w, enc, epi=ap.Epilogue(out_bits, cuda(alpha), cuda(beta), S))
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(u32(got), want)
