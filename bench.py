@@ -12,10 +12,15 @@ metric: effective TOPS = 2 M N K / step time (logical integer MACs x 2).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--M 8192 --N 8192 --K 8192 --a 2 --w 1 --enc 2] [--variant auto]
+                  [--scaling weak|strong] [--allgather]
 
-N > 1 runs under torchrun, one rank per GPU; every rank processes its own
-M-row batch with replicated W (weak scaling, no data-path collective; the
-optional --allgather adds the output all-gather of the north star).
+N > 1 runs one rank per GPU over NCCL.  Launched as `python bench.py --gpus N` (no
+WORLD_SIZE in the environment) it re-launches itself under torch.distributed.run with N
+ranks; under torchrun it checks WORLD_SIZE == --gpus.  --scaling weak (default): every
+rank processes its own M-row batch with W replicated (no data-path collective).
+--scaling strong: the global M rows are sharded across the ranks (dist.row_range);
+--allgather adds the output all-gather of the north star (NCCL all_gather_into_tensor)
+to every step and reports its bus bandwidth.
 """
 from __future__ import annotations
 
@@ -49,6 +54,7 @@ def parse():
     ap.add_argument("--out-bits", type=int, default=None, help="fused output bits (default a)")
     ap.add_argument("--variant", default="auto")
     ap.add_argument("--allgather", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -185,6 +191,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": full_step_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8 codes, int64 accumulate", "data": "synthetic",
             "impl": "reference",
+            "extrapolated": {"ms_per_step": True, "how": "each step times the oracle on a row sample of A; the "
+                             "full-M step time is the sample time x M / rows (the work is exactly linear in M)"},
             "config": {"workload": f"apmm_w{args.w}a{args.a}_{args.M}x{args.N}x{args.K}_fused_pack",
                        "M": args.M, "N": args.N, "K": args.K, "a_bits": args.a, "w_bits": args.w,
                        "encoding": ENC_NAME[args.enc]},
@@ -245,18 +253,33 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     dist = None
+    comm = None
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # communicator check: every rank contributes rank + 1 (sum = N (N + 1) / 2)
+        t = torch.tensor([rank + 1], dtype=torch.int64, device=torch.device("cuda", local))
+        dist.all_reduce(t)
+        comm = {"backend": dist.get_backend(), "nranks": dist.get_world_size(),
+                "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version()),
+                "comm_nranks_ok": bool(int(t.item()) == world * (world + 1) // 2)}
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    M_global = args.M if args.scaling == "strong" else world * args.M
+    if args.scaling == "strong":  # the global M rows sharded across the ranks (dist.row_range)
+        from paper_2106_12169_b200.dist import row_range
+        r0, r1 = row_range(args.M, world, rank)
+        args.M = r1 - r0
     M, N, K, a, w, enc = args.M, args.N, args.K, args.a, args.w, args.enc
     out_bits = args.out_bits or a
     variant = ap.VARIANTS[args.variant]
 
-    # every rank owns its own M-row batch (weak scaling); W replicated
+    # weak scaling: every rank owns its own M-row batch; strong: its rows of the global
+    # batch.  W replicated.
     A_np, W_np = synth.gemm_inputs(M, N, K, a, w, tag="bench")
     if rank > 0:
         A_np = synth.codes((M, K), a, f"bench-rank{rank}")
@@ -291,8 +314,8 @@ def run_ours(args):
             ap.gemm(A_planes, W_planes, M, N, K, a, w, enc, epi=epi, variant=variant, out=Y_packed)
         if ev_g1 is not None:
             ev_g1.record(stream)
-        if gathered is not None:
-            gather_rows(Y_packed, world * M, None)  # NCCL all-gather: every rank ends with all world*M output rows
+        if gathered is not None:  # NCCL all-gather: every rank ends with all output rows
+            gather_rows(Y_packed, M_global, None)
 
     # correctness spot check on sampled rows against nothing but the oracle happens in tests;
     # here only warm up
@@ -328,8 +351,28 @@ def run_ours(args):
         total_ms = float(t.item())
     ms_per_step = total_ms / K_steps
     ops = 2.0 * M * N * K
-    value = world * ops * K_steps / (total_ms * 1e-3) / 1e12
+    job_ops = 2.0 * M_global * N * K  # every rank's work in one step
+    value = job_ops * K_steps / (total_ms * 1e-3) / 1e12
     gemm_avg_ms = statistics.mean(gemm_ms)
+
+    # the all-gather alone: bus bandwidth (G-1)/G * gathered bytes / t, max over ranks
+    allgather = None
+    if gathered is not None:
+        for _ in range(3):
+            gather_rows(Y_packed, M_global, None)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(10):
+            gather_rows(Y_packed, M_global, None)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        t_ag = torch.tensor([e0.elapsed_time(e1) / 10], dtype=torch.float64, device=dev)
+        dist.all_reduce(t_ag, op=dist.ReduceOp.MAX)
+        total_bytes = M_global * Y_packed[0].numel() * 4
+        allgather = {"bytes_gathered": total_bytes, "ms": float(t_ag.item()),
+                     "busbw_gbs": (world - 1) / world * total_bytes / (float(t_ag.item()) * 1e-3) / 1e9}
 
     # ---------------- e2e: same metric through the public API with host buffers.
     # Every step copies its codes host->device (pinned) and its packed output back; the
@@ -388,7 +431,7 @@ def run_ours(args):
             t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
-        e2e = {"value": world * ops * n_e2e / (e2e_ms * 1e-3) / 1e12, "unit": "TOPS",
+        e2e = {"value": job_ops * n_e2e / (e2e_ms * 1e-3) / 1e12, "unit": "TOPS",
                "h2d_bytes_per_step": int(A_host.numel()), "d2h_bytes_per_step": int(Y_host[0].numel() * 4),
                "steps": n_e2e, "pipelining": "H2D / D2H on separate streams, double-buffered"}
 
@@ -400,38 +443,60 @@ def run_ours(args):
         return
 
     peaks = load_peaks()
-    peak, peak_src = int8_peak_tops(peaks, fp4=resolved == ap.VARIANT_TC_FP4)
+    fp4 = resolved == ap.VARIANT_TC_FP4
+    peak, peak_src = int8_peak_tops(peaks, fp4=fp4)
     achieved = ops / (gemm_avg_ms * 1e-3) / 1e12
+    # which kernel ran (the library's dispatch: prepared W with M > 128 -> the CTA-pair kernel)
+    kname = (("fp4_pair_kernel" if M > 128 else "fp4_kernel") if W_prep is not None
+             else ap.variant_name(resolved))
     traffic = None
     try:
         summ = json.load(open(NCU_SUMMARY))
-        key = f"{M}x{N}x{K}_w{w}a{a}_enc{enc}_{ap.variant_name(resolved)}" + ("_prepared" if W_prep is not None else "")
+        key = f"{M}x{N}x{K}_w{w}a{a}_enc{enc}_{kname}" + ("_prepared" if W_prep is not None else "")
         traffic = summ.get("traffic_bytes_per_launch", {}).get(key)
+    except Exception:
+        pass
+    micro = None  # the tensor pipe's measured issue-rate ceiling (scripts/mma_peak.cu), for context
+    try:
+        pk = json.load(open(os.path.join(ROOT, "profiles", "r02_peaks.json")))["summary"]
+        micro = pk["kind_mxf4_tops"] if fp4 else pk["kind_i8_tops"]
     except Exception:
         pass
     line = {
         "metric": "effective_tops_apmm", "value": value, "unit": "TOPS", "n_gpus": world, "steps": K_steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"apmm_w{w}a{a}_{M}x{N}x{K}_fused_pack", "M": M, "N": N, "K": K, "a_bits": a,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "data": "synthetic",
+        # arithmetic the contraction runs in: e2m1 operands with exact fp32 accumulation (|Y| < 2^24,
+        # tests/test_fp4_exact.py) on the fp4 pipe, else u8/s8 operands with int32 accumulation
+        "dtype": "e2m1 (fp32 accumulate, exact integers)" if fp4 else "u8/s8 (int32 accumulate)",
+        "config": {"workload": f"apmm_w{w}a{a}_{M if args.scaling == 'weak' else M_global}x{N}x{K}_fused_pack",
+                   "M": M_global, "M_per_rank": M, "N": N, "K": K, "a_bits": a,
                    "w_bits": w, "encoding": ENC_NAME[enc], "out": f"packed {out_bits}-bit (fused requant)",
                    "step": "apnn_pack_bits(A) + " + ("apnn_gemm_prepared (W prepared at init)" if W_prep is not None
                                                       else "apnn_gemm_fused"),
                    "variant": ap.variant_name(resolved) + ("_prepared" if W_prep is not None else ""),
-                   "parallelism": f"dp{world} (M-row batch per GPU, W replicated)",
+                   "parallelism": f"dp{world} (" + ("M-row batch per GPU" if args.scaling == "weak"
+                                                    else "global M sharded by rows") + ", W replicated)",
                    "l2": "flushed (512 MB write) between timed steps", "allgather": bool(gathered is not None)},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": f"apnn {ap.variant_name(resolved)} GEMM (fused epilogue"
+                     "kernel": f"{kname} (apnn {ap.variant_name(resolved)} GEMM, fused epilogue"
                                + (", prepared W)" if W_prep is not None else ")"),
                      "kernel_ms": gemm_avg_ms, "kernel_share_of_step": gemm_avg_ms / ms_per_step,
-                     "peak_source": peak_src},
+                     "peak_source": peak_src,
+                     "peak_mma_microbench": micro,
+                     "frac_of_mma_microbench": (achieved / micro) if micro else None,
+                     "traffic_source": "profiles/ncu_summary.json (dram read+write per launch, ncu --set full)"},
         "clocks": clocks,
         "e2e": e2e,
         "gpu_launches": launches,
     }
     if models is not None:
         line["models"] = models
+    if comm is not None:
+        line["comm"] = comm
+    if allgather is not None:
+        line["allgather"] = allgather
     if not args.no_cpu:
         line["cpu_baseline"] = oracle_sample(A_np, W_np, args, args.cpu_seconds, out_bits, alpha_np, beta_np, S)
     print(json.dumps(line), flush=True)
@@ -439,8 +504,23 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def relaunch_distributed(args):
+    """`python bench.py --gpus N` outside torchrun: run N ranks (one per GPU) under
+    torch.distributed.run on this node; its ranks print as usual (rank 0 the JSON line)."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args))
     if args.impl == "reference":
         run_reference(args)
     else:

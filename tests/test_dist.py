@@ -84,3 +84,61 @@ def test_sharded_equals_single_process(world, M, out_bits):
         np.testing.assert_array_equal(g2, want)
         rows.extend(myrows.tolist())
     assert rows == list(range(M))  # shards are contiguous, in rank order, and cover M once
+
+
+def _cuda_worker(rank, world, port, M, N, K, a, w, enc, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2106_12169_b200 as ap
+        torch.cuda.set_device(0)
+        A, W = synth.gemm_inputs(M, N, K, a, w, tag="dist-cuda")
+        op = ShardedAPMM(N, K, a, w, enc, W_planes=ap.pack_bits(torch.from_numpy(W).cuda(), w))
+        cuda_rows = op.kernel  # the library path: apnn_pack_bits + apnn_gemm_ex on cuda:0
+        op.kernel = lambda A_rows: cuda_rows(A_rows.cuda()).cpu()  # gloo gathers host tensors
+        full = op(torch.from_numpy(A), M)
+        torch.cuda.synchronize()
+        q.put((rank, full.numpy(), ap.launch_count()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M", [300, 1000])
+def test_sharded_cuda_kernel_two_ranks(M):
+    # both ranks drive the real CUDA kernel (cuda:0) on their row shard; the gathered result
+    # equals the oracle's single-process result bit for bit
+    world, N, K, a, w, enc = 2, 520, 640, 2, 1, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cuda_worker, args=(r, world, port, M, N, K, a, w, enc, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A, W = synth.gemm_inputs(M, N, K, a, w, tag="dist-cuda")
+    want = oracle.gemm(A, W, a, w, enc)
+    for rank, full, launches in res:
+        assert launches >= 2  # pack + GEMM ran in this rank's library instance
+        np.testing.assert_array_equal(full, want)
+
+
+def test_bench_relaunches_n_ranks():
+    # `python bench.py --gpus 2` outside torchrun runs 2 ranks (here the reference arm, which
+    # needs no GPU: rank 0 times the oracle and prints the one JSON line, rank 1 exits 0)
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--M", "64", "--N", "64", "--K", "256", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    assert lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2
