@@ -169,6 +169,44 @@ def _cuda(t: torch.Tensor, name: str, dtype=None):
     return t
 
 
+def _check_out(out: torch.Tensor, shape, name: str = "out"):
+    """A caller-supplied output must hold exactly the elements the kernel writes (any view shape)."""
+    n = 1
+    for d in shape:
+        n *= int(d)
+    if out.numel() != n:
+        raise ValueError(f"{name} has {out.numel()} elements, the call writes {n} (shape {tuple(shape)})")
+
+
+@dataclass(frozen=True)
+class PreparedWeights:
+    """Weights after the operand-side bit combination (apnn_prepare_weights /
+    apnn_prepare_weights_i8), tagged with what they were prepared for.  The byte layout is
+    only meaningful to the kernel kind and (N, K, w_bits, encoding) it was built for; the
+    prepared-weight calls reject a mismatch instead of computing with the wrong operand."""
+    data: torch.Tensor  # uint8, device
+    kind: str           # "fp4" (e2m1 operand rows) or "i8" (int8 operand rows)
+    N: int
+    K: int
+    w_bits: int
+    enc: int
+
+    def check(self, kind: str, N: int, K: int, w_bits: int, enc: int):
+        got = (self.kind, self.N, self.K, self.w_bits, self.enc)
+        want = (kind, N, K, w_bits, enc)
+        if got != want:
+            raise ValueError(f"prepared weights are (kind, N, K, w_bits, enc) = {got}, the call needs {want}")
+        return self.data
+
+
+def _prepared(Wp, kind, N, K, w_bits, enc) -> torch.Tensor:
+    if not isinstance(Wp, PreparedWeights):
+        raise TypeError("prepared-weight calls take the PreparedWeights returned by prepare_weights[_i8]")
+    t = Wp.check(kind, N, K, w_bits, enc)
+    _cuda(t, "Wp", torch.uint8)
+    return t
+
+
 def kw(K: int) -> int:
     """uint32 words per plane run: roundup(K,128)/32."""
     return (K + 127) // 128 * 4
@@ -240,6 +278,7 @@ def pack_bits(codes: torch.Tensor, bits: int, out: Optional[torch.Tensor] = None
     if out is None:
         out = torch.empty(packed_shape(rows, K, bits), dtype=torch.int32, device=codes.device)
     _cuda(out, "out", torch.int32)
+    _check_out(out, packed_shape(rows, K, bits))
     _check(lib().apnn_pack_bits(_ptr(codes), rows, K, bits, _ptr(out), _stream(codes)), "apnn_pack_bits")
     return out
 
@@ -252,6 +291,7 @@ def im2col_pack(X: torch.Tensor, shape: ConvShape, bits: int, out: Optional[torc
     if out is None:
         out = torch.empty(packed_shape(shape.B * shape.Ho * shape.Wo, K, bits), dtype=torch.int32, device=X.device)
     _cuda(out, "out", torch.int32)
+    _check_out(out, packed_shape(shape.B * shape.Ho * shape.Wo, K, bits))
     cs = shape._c()
     _check(lib().apnn_im2col_pack(_ptr(X), ctypes.byref(cs), bits, _ptr(out), _stream(X)), "apnn_im2col_pack")
     return out
@@ -265,6 +305,7 @@ def flatten_packed(X: torch.Tensor, B: int, P: int, out: Optional[torch.Tensor] 
     if out is None:
         out = torch.empty((B, bits, P * Cw), dtype=torch.int32, device=X.device)
     _cuda(out, "out", torch.int32)
+    _check_out(out, (B, bits, P * Cw))
     _check(lib().apnn_flatten_packed(_ptr(X), B, P, bits, Cw, _ptr(out), _stream(X)), "apnn_flatten_packed")
     return out
 
@@ -275,10 +316,13 @@ def gemm(A: torch.Tensor, W: torch.Tensor, M: int, N: int, K: int, a_bits: int, 
     """APMM: int32 Y [M, N] (epi None) or packed [M, out_bits, Kw(N)]  (apnn_gemm_ex)."""
     _cuda(A, "A", torch.int32)
     _cuda(W, "W", torch.int32)
+    _check_out(A, packed_shape(M, K, a_bits), "A")
+    _check_out(W, packed_shape(N, K, w_bits), "W")
+    shape = (M, N) if epi is None else packed_shape(M, N, epi.out_bits)
     if out is None:
-        shape = (M, N) if epi is None else packed_shape(M, N, epi.out_bits)
         out = torch.empty(shape, dtype=torch.int32, device=A.device)
     _cuda(out, "out", torch.int32)
+    _check_out(out, shape)
     ce = None if epi is None else ctypes.byref(epi._c())
     _check(lib().apnn_gemm_ex(_ptr(A), _ptr(W), M, N, K, a_bits, w_bits, enc, ce, _ptr(out), variant,
                               _stream(A)), "apnn_gemm_ex")
@@ -290,22 +334,27 @@ def prepare_weights(W: torch.Tensor, N: int, K: int, w_bits: int, enc: int,
     """Packed weights [N, w_bits, Kw] -> prepared e2m1 operand bytes for the exact-FP4 kernel
     (apnn_prepare_weights; weights are static)."""
     _cuda(W, "W", torch.int32)
+    _check_out(W, packed_shape(N, K, w_bits), "W")
+    nbytes = int(lib().apnn_prepared_bytes(N, K))
     if out is None:
-        out = torch.empty(int(lib().apnn_prepared_bytes(N, K)), dtype=torch.uint8, device=W.device)
+        out = torch.empty(nbytes, dtype=torch.uint8, device=W.device)
     _cuda(out, "out", torch.uint8)
+    _check_out(out, (nbytes,))
     _check(lib().apnn_prepare_weights(_ptr(W), N, K, w_bits, enc, _ptr(out), _stream(W)), "apnn_prepare_weights")
-    return out
+    return PreparedWeights(out, "fp4", N, K, w_bits, enc)
 
 
-def gemm_prepared(A: torch.Tensor, Wp: torch.Tensor, M: int, N: int, K: int, a_bits: int, w_bits: int, enc: int,
+def gemm_prepared(A: torch.Tensor, Wp: PreparedWeights, M: int, N: int, K: int, a_bits: int, w_bits: int, enc: int,
                   epi: Optional[Epilogue] = None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
     """APMM on the exact-FP4 kernel with prepared weights (apnn_gemm_prepared)."""
     _cuda(A, "A", torch.int32)
-    _cuda(Wp, "Wp", torch.uint8)
+    _check_out(A, packed_shape(M, K, a_bits), "A")
+    Wp = _prepared(Wp, "fp4", N, K, w_bits, enc)
+    shape = (M, N) if epi is None else packed_shape(M, N, epi.out_bits)
     if out is None:
-        shape = (M, N) if epi is None else packed_shape(M, N, epi.out_bits)
         out = torch.empty(shape, dtype=torch.int32, device=A.device)
     _cuda(out, "out", torch.int32)
+    _check_out(out, shape)
     ce = None if epi is None else ctypes.byref(epi._c())
     _check(lib().apnn_gemm_prepared(_ptr(A), _ptr(Wp), M, N, K, a_bits, w_bits, enc, ce, _ptr(out), _stream(A)),
            "apnn_gemm_prepared")
@@ -316,44 +365,51 @@ def prepare_weights_i8(W: torch.Tensor, N: int, K: int, w_bits: int, enc: int,
                        out: Optional[torch.Tensor] = None) -> torch.Tensor:
     """Packed weights -> prepared int8 operand rows for the 2-CTA int8 kernel (apnn_prepare_weights_i8)."""
     _cuda(W, "W", torch.int32)
+    _check_out(W, packed_shape(N, K, w_bits), "W")
+    nbytes = int(lib().apnn_prepared_i8_bytes(N, K))
     if out is None:
-        out = torch.empty(int(lib().apnn_prepared_i8_bytes(N, K)), dtype=torch.uint8, device=W.device)
+        out = torch.empty(nbytes, dtype=torch.uint8, device=W.device)
     _cuda(out, "out", torch.uint8)
+    _check_out(out, (nbytes,))
     _check(lib().apnn_prepare_weights_i8(_ptr(W), N, K, w_bits, enc, _ptr(out), _stream(W)),
            "apnn_prepare_weights_i8")
-    return out
+    return PreparedWeights(out, "i8", N, K, w_bits, enc)
 
 
-def gemm_prepared_i8(A: torch.Tensor, Wp: torch.Tensor, M: int, N: int, K: int, a_bits: int, w_bits: int,
+def gemm_prepared_i8(A: torch.Tensor, Wp: PreparedWeights, M: int, N: int, K: int, a_bits: int, w_bits: int,
                      enc: int, epi: Optional[Epilogue] = None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
     """APMM on the int8 tensor-core kernel with prepared weights (apnn_gemm_prepared_i8)."""
     _cuda(A, "A", torch.int32)
-    _cuda(Wp, "Wp", torch.uint8)
+    _check_out(A, packed_shape(M, K, a_bits), "A")
+    Wp = _prepared(Wp, "i8", N, K, w_bits, enc)
+    shape = (M, N) if epi is None else packed_shape(M, N, epi.out_bits)
     if out is None:
-        shape = (M, N) if epi is None else packed_shape(M, N, epi.out_bits)
         out = torch.empty(shape, dtype=torch.int32, device=A.device)
     _cuda(out, "out", torch.int32)
+    _check_out(out, shape)
     ce = None if epi is None else ctypes.byref(epi._c())
     _check(lib().apnn_gemm_prepared_i8(_ptr(A), _ptr(Wp), M, N, K, a_bits, w_bits, enc, ce, _ptr(out), _stream(A)),
            "apnn_gemm_prepared_i8")
     return out
 
 
-def conv2d_prepared_i8(X: torch.Tensor, Wp: torch.Tensor, shape: ConvShape, a_bits: int, w_bits: int, enc: int,
+def conv2d_prepared_i8(X: torch.Tensor, Wp: PreparedWeights, shape: ConvShape, a_bits: int, w_bits: int, enc: int,
                        epi: Optional[Epilogue] = None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
     """APConv with prepared int8 weights (apnn_conv2d_prepared_i8; Wp = prepare_weights_i8 of the
     packed OHWI weights as C_out*R*S rows of C_in).  Falls back (ApnnError UNSUPPORTED) to the
     caller; output as conv2d."""
     _cuda(X, "X", torch.int32)
-    _cuda(Wp, "Wp", torch.uint8)
+    _check_out(X, packed_shape(shape.B * shape.H * shape.W, shape.C_in, a_bits), "X")
+    Wp = _prepared(Wp, "i8", shape.C_out * shape.R * shape.S, shape.C_in, w_bits, enc)
+    if epi is None:
+        oshape = (shape.B, shape.Ho, shape.Wo, shape.C_out)
+    else:
+        Hp, Wpp = epi.pooled(shape.Ho, shape.Wo)
+        oshape = packed_shape(shape.B * Hp * Wpp, shape.C_out, epi.out_bits)
     if out is None:
-        if epi is None:
-            oshape = (shape.B, shape.Ho, shape.Wo, shape.C_out)
-        else:
-            Hp, Wpp = epi.pooled(shape.Ho, shape.Wo)
-            oshape = packed_shape(shape.B * Hp * Wpp, shape.C_out, epi.out_bits)
         out = torch.empty(oshape, dtype=torch.int32, device=X.device)
     _cuda(out, "out", torch.int32)
+    _check_out(out, oshape)
     ce = None if epi is None else ctypes.byref(epi._c())
     cs = shape._c()
     _check(lib().apnn_conv2d_prepared_i8(_ptr(X), _ptr(Wp), ctypes.byref(cs), a_bits, w_bits, enc, ce, _ptr(out),
@@ -369,14 +425,17 @@ def conv2d(X: torch.Tensor, W: torch.Tensor, shape: ConvShape, a_bits: int, w_bi
     APNN_ERR_UNSUPPORTED) runs as the unfused GPU pair: int32 conv + apnn_pool_quant_pack_out."""
     _cuda(X, "X", torch.int32)
     _cuda(W, "W", torch.int32)
+    _check_out(X, packed_shape(shape.B * shape.H * shape.W, shape.C_in, a_bits), "X")
+    _check_out(W, packed_shape(shape.C_out * shape.R * shape.S, shape.C_in, w_bits), "W")
+    if epi is None:
+        oshape = (shape.B, shape.Ho, shape.Wo, shape.C_out)
+    else:
+        Hp, Wp = epi.pooled(shape.Ho, shape.Wo)
+        oshape = packed_shape(shape.B * Hp * Wp, shape.C_out, epi.out_bits)
     if out is None:
-        if epi is None:
-            oshape = (shape.B, shape.Ho, shape.Wo, shape.C_out)
-        else:
-            Hp, Wp = epi.pooled(shape.Ho, shape.Wo)
-            oshape = packed_shape(shape.B * Hp * Wp, shape.C_out, epi.out_bits)
         out = torch.empty(oshape, dtype=torch.int32, device=X.device)
     _cuda(out, "out", torch.int32)
+    _check_out(out, oshape)
     ce = None if epi is None else ctypes.byref(epi._c())
     cs = shape._c()
     st = lib().apnn_conv2d_ex(_ptr(X), _ptr(W), ctypes.byref(cs), a_bits, w_bits, enc, ce, _ptr(out),
@@ -399,6 +458,7 @@ def quant_pack_out(Y: torch.Tensor, epi: Epilogue, out: Optional[torch.Tensor] =
     if out is None:
         out = torch.empty(packed_shape(M, N, epi.out_bits), dtype=torch.int32, device=Y.device)
     _cuda(out, "out", torch.int32)
+    _check_out(out, packed_shape(M, N, epi.out_bits))
     _check(lib().apnn_quant_pack_out(_ptr(Y), M, N, ctypes.byref(epi._c()), _ptr(out), _stream(Y)),
            "apnn_quant_pack_out")
     return out
@@ -413,6 +473,7 @@ def pool_quant_pack_out(Y: torch.Tensor, epi: Epilogue, out: Optional[torch.Tens
     if out is None:
         out = torch.empty(packed_shape(B * Hp * Wp, N, epi.out_bits), dtype=torch.int32, device=Y.device)
     _cuda(out, "out", torch.int32)
+    _check_out(out, packed_shape(B * Hp * Wp, N, epi.out_bits))
     _check(lib().apnn_pool_quant_pack_out(_ptr(Y), B, H, Wd, N, ctypes.byref(epi._c()), _ptr(out), _stream(Y)),
            "apnn_pool_quant_pack_out")
     return out
@@ -432,6 +493,7 @@ def residual_quant_pack(Y: torch.Tensor, Z: torch.Tensor, z_bits: int, epi: Epil
     if out is None:
         out = torch.empty(packed_shape(M, N, epi.out_bits), dtype=torch.int32, device=Y.device)
     _cuda(out, "out", torch.int32)
+    _check_out(out, packed_shape(M, N, epi.out_bits))
     _check(lib().apnn_residual_quant_pack(_ptr(Y2), M, N, _ptr(Z), z_bits, _ptr(rho), ctypes.byref(epi._c()),
                                           _ptr(out), _stream(Y)), "apnn_residual_quant_pack")
     return out

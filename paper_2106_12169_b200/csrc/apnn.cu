@@ -189,6 +189,7 @@ static apnn_status run(const uint32_t* A, const uint32_t* W, const Geom& g, cons
         break;
     default: return APNN_ERR_INVALID_ARG;
     }
+    if (err == cudaErrorNotSupported) return APNN_ERR_UNSUPPORTED;  // e.g. residual epilogue off the 2-CTA kernel
     return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }
 

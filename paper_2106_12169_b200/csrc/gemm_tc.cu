@@ -52,6 +52,12 @@ constexpr int kStgWarpBytes = 8192;  // store staging per epilogue warp (1024-al
 #define APNN_PROD_LANES 4
 #endif
 constexpr int kProdLanes = APNN_PROD_LANES;  // TMA-issuing lanes of the producer warp (2-CTA kernel)
+// Development-only knobs (pipeline trace, skipped stores / B work -- the latter two give wrong
+// results by design) exist only in experiment builds: build.py --variant NAME -DAPNN_DEV=1.
+#ifndef APNN_DEV
+#define APNN_DEV 0
+#endif
+constexpr bool kDev = APNN_DEV != 0;
 enum { kOutDirect = 0, kOutTma = 1, kOutLsu = 2 };
 
 struct Params {
@@ -94,7 +100,7 @@ constexpr int kTraceN = 2048;
 enum { TR_PROD = 0, TR_A_PLANE = 1, TR_A_OP = 2, TR_A_DONE = 3, TR_MMA_OPFULL = 4, TR_MMA_ISSUED = 5,
        TR_EPI_FULL = 6, TR_EPI_DONE = 7, TR_N = 8 };
 __device__ __forceinline__ void trace_at(const Params& p, int ev, int idx) {
-    if (p.trace && blockIdx.x == 0 && idx < kTraceN) {
+    if (kDev && p.trace && blockIdx.x == 0 && idx < kTraceN) {
         unsigned long long c;
         asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
         p.trace[ev * kTraceN + idx] = c;
@@ -104,7 +110,7 @@ __device__ __forceinline__ void trace_at(const Params& p, int ev, int idx) {
 constexpr int kCtaTraceMax = 1024;
 // CTA-0 event stamps (ns), slots 0..31 (development)
 __device__ __forceinline__ void dbg_stamp(const Params& p, int slot) {
-    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    if (kDev && p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[kTraceN * TR_N + 4 * kCtaTraceMax + slot] = t;
@@ -112,7 +118,7 @@ __device__ __forceinline__ void dbg_stamp(const Params& p, int slot) {
 }
 __device__ __forceinline__ void cta_stamp(const Params& p, int k) {
     const int b = blockIdx.x + (blockIdx.y + blockIdx.z * gridDim.y) * gridDim.x;
-    if (p.trace && threadIdx.x == 0 && b < kCtaTraceMax) {
+    if (kDev && p.trace && threadIdx.x == 0 && b < kCtaTraceMax) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[kTraceN * TR_N + b * 4 + k] = t;
@@ -439,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&plane_empty[ps]);
                     mbar_wait(&b_full[s], ph);
-                } else if (t < BROWS && !p.exp_nob) {  // warp-uniform: BROWS is a multiple of 32
+                } else if (t < BROWS && !(kDev && p.exp_nob)) {  // warp-uniform: BROWS is a multiple of 32
                     recomb_step_any<W_PM1, false, SCALED>(g.w_bits, sBpl + (size_t)ps * p.b_bytes, BROWS, 1, t,
                                                           &plane_empty[ps], &op_empty[s], ph ^ 1, 0,
                                                           sBop + (size_t)s * BOP_STAGE, 128, lane,
@@ -485,8 +491,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             const int m = t < len ? mb + t : g.M;   // rows beyond the tile are not stored
             const int n0 = (tile / p.tiles_m) * T2_BN;
             const bool any = q * 32 < len;
-            const bool use_tma = p.out_mode == kOutTma && any && (!g.conv || q * 32 + 32 <= len) && !p.exp_nostore;
-            const bool use_lsu = p.out_mode == kOutLsu && any && !p.exp_nostore;
+            const bool use_tma = p.out_mode == kOutTma && any && (!g.conv || q * 32 + 32 <= len) && !(kDev && p.exp_nostore);
+            const bool use_lsu = p.out_mode == kOutLsu && any && !(kDev && p.exp_nostore);
             const int row0 = mb + q * 32, row_end = mb + len;
             if (p.tab_mode == kTabQ3 || p.tab_mode == kTabHybrid) {
                 named_bar_sync(1, 128);  // previous tile's readers are done
@@ -530,7 +536,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
                     npc++;
                     continue;
                 }
-                if (!any || p.exp_nostore) continue;
+                if (!any || (kDev && p.exp_nostore)) continue;
                 if (ob == 0) {
                     if (use_tma) {
                         uint8_t* b = stg + (nst & 1) * 4096;
@@ -565,7 +571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
             if (lane == 0) mbar_arrive_cluster(accum_empty0 + 8u * (uint32_t)(halves ? 1 : buf));
             if (p.pool_fused) {
                 pool_pad_words(n0 + T2_BN, t, len, mb, g, p);
-            } else if (ob && any && !p.exp_nostore) {
+            } else if (ob && any && !(kDev && p.exp_nostore)) {
                 if (use_tma || use_lsu) {
                     const uint32_t zero8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                     for (int wi = T2_BN / 32; wi < p.nwb; wi++)  // box words past the tile: N padding
@@ -821,8 +827,8 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
         constexpr int half = BN / 2;
         // int32 output: TMA stores from per-warp staging that reuses the (now idle)
         // pipeline buffers; packed output: direct stores (small problems only)
-        const bool use_tma = p.out_mode == kOutTma && p.e.out_bits == 0 && m0 + q * 32 < g.M && !p.exp_nostore;
-        const bool use_lsu = p.out_mode == kOutLsu && p.e.out_bits == 0 && m0 + q * 32 < g.M && !p.exp_nostore;
+        const bool use_tma = p.out_mode == kOutTma && p.e.out_bits == 0 && m0 + q * 32 < g.M && !(kDev && p.exp_nostore);
+        const bool use_lsu = p.out_mode == kOutLsu && p.e.out_bits == 0 && m0 + q * 32 < g.M && !(kDev && p.exp_nostore);
         uint8_t* stg = smem + (warp - 2) * kStgWarpBytes;
         uint32_t nst = 0;
 #pragma unroll 1
@@ -838,7 +844,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1)
                         make_uint4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
                 continue;
             }
-            if (p.exp_nostore) continue;
+            if (kDev && p.exp_nostore) continue;
             if (use_tma) {
                 uint8_t* b = stg + (nst & 1) * 4096;
                 if (lane == 0) bulk_wait_read<1>();
@@ -1063,10 +1069,19 @@ static cudaError_t launch1_bn(int BN, const CUtensorMap& ta, const CUtensorMap& 
 
 static int tc_kernel_override();
 
+// The 2-CTA conv path fetches each output row's taps as one strided TMA box: the box is
+// min(Wo, 128) pixels wide with element stride `stride`, so it needs width * stride <= 256
+// (the box extent) and stride <= 8 (the largest TMA element stride).  Other convolutions run
+// on the 1-CTA kernel, whose cp.async gathers take any stride.
+static bool conv2_fits(const Geom& g) {
+    const int bw = g.Wo <= 128 ? g.Wo : 128;
+    return bw * g.stride <= 256 && g.stride <= 8;
+}
+
 // 2x2/2 max pooling fused into the 2-CTA kernel's epilogue (see pool_chunk)
 bool tc_i8_pool_fusable(const Geom& g, const Epi& e) {
     return g.conv && e.pool == 2 && e.pool_stride == 2 && !e.pool_avg && e.out_bits > 0 && g.Ho % 2 == 0 &&
-           g.Wo >= 2 && g.Wo <= 64 && g.M > 128 && tc_kernel_override() != 1;
+           g.Wo >= 2 && g.Wo <= 64 && g.M > 128 && conv2_fits(g) && tc_kernel_override() != 1;
 }
 
 namespace tc {
@@ -1188,6 +1203,16 @@ static int tc_kernel_override() {
     return v;
 }
 
+// 256-wide pair tiles as two N = 128 MMA halves (APNN_HALVES=1, read once; correct, slower)
+static int halves_knob() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("APNN_HALVES");
+        v = s ? atoi(s) : 0;
+    }
+    return v;
+}
+
 static cudaError_t launch_tc_i8_impl(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
                                      int sms, cudaStream_t s, const uint8_t* Wprep) {
     using namespace tc;
@@ -1216,19 +1241,20 @@ static cudaError_t launch_tc_i8_impl(const uint32_t* A, const uint32_t* W, const
     const int want_mode = epi_store_mode(e.out_bits > 0);
     p.acc_shift = 0;
     p.trace = nullptr;
+    p.exp_nostore = 0;
+    p.exp_nob = 0;
+    p.halves = halves_knob();  // measured slower (8192^3 w1a2: 564 vs 455 us): N = 128 MMAs cost more
+#if APNN_DEV
     p.exp_nostore = getenv("APNN_EXP_NOSTORE") ? 1 : 0;
     p.exp_nob = getenv("APNN_EXP_NOB") ? 1 : 0;
-    {
-        const char* h = getenv("APNN_HALVES");
-        p.halves = h ? atoi(h) : 0;  // measured slower (8192^3 w1a2: 564 vs 455 us): N = 128 MMAs cost more
-    }
     const char* trace_path = getenv("APNN_TRACE");
-    if (trace_path) {
+    if (trace_path) {  // development only: allocates and synchronises (see the dump below)
         cudaMalloc(&p.trace, sizeof(unsigned long long) * (kTraceN * TR_N + 4 * kCtaTraceMax + 32));
         cudaMemset(p.trace, 0, sizeof(unsigned long long) * (kTraceN * TR_N + 4 * kCtaTraceMax + 32));
     }
+#endif
     const int ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
-    bool two = (g.M > 128) && tc_kernel_override() != 1;
+    bool two = (g.M > 128) && tc_kernel_override() != 1 && (!g.conv || conv2_fits(g));
     if (e.res && !two) return cudaErrorNotSupported;  // residual epilogue: 2-CTA kernel only (ABI checks first)
     // small GEMMs (row f4): when the 2-CTA grid would occupy <= 1/4 of the SMs, run the
     // 1-CTA kernel with split-K clusters instead (latency: more CTAs, fewer k-blocks each)
@@ -1311,7 +1337,7 @@ static cudaError_t launch_tc_i8_impl(const uint32_t* A, const uint32_t* W, const
                 p.conv_nbox = 1;
                 cta_tiles = (g.M / g.Wo) * p.conv_segs;
             }
-            if (p.conv_bw * g.stride > 256 || g.stride > 8) return cudaErrorInvalidConfiguration;
+            if (p.conv_bw * g.stride > 256 || g.stride > 8) return cudaErrorNotSupported;  // conv2_fits said so
         }
         p.tiles_m = (cta_tiles + 1) / 2;
         // tiles cover [0, N); the packed path also writes the N padding words (zero)
@@ -1407,6 +1433,7 @@ static cudaError_t launch_tc_i8_impl(const uint32_t* A, const uint32_t* W, const
         default: err = launch1_bn<true, false>(BN, ta, tb, ty, p, grid, smem, s); break;
         }
     }
+#if APNN_DEV
     if (p.trace) {  // development only: synchronous dump
         static unsigned long long host[kTraceN * TR_N + 4 * kCtaTraceMax + 32];
         cudaStreamSynchronize(s);
@@ -1419,6 +1446,7 @@ static cudaError_t launch_tc_i8_impl(const uint32_t* A, const uint32_t* W, const
             fclose(f);
         }
     }
+#endif
     count_launch();
     return err;
 }

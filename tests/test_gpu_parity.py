@@ -519,3 +519,63 @@ def test_conv_prepared_weights_exact(shape, a_bits, w_bits, enc):
     got = ap.conv2d_prepared_i8(Xp, Wprep, cs, a_bits, w_bits, enc, epi=ap.Epilogue(2, cuda(alpha), cuda(beta), Sd))
     torch.cuda.synchronize()
     np.testing.assert_array_equal(u32(got), wantp)
+
+
+# strides 3 / 4 with wide output rows: the 2-CTA kernel's strided row box (width x stride <= 256,
+# stride <= 8) cannot take these, AUTO / TC_I8 fall back to the 1-CTA kernel
+WIDE_STRIDE_SHAPES = [
+    (1, 4, 400, 16, 32, 3, 3, 3, 1),   # Wo = 134 (box 128 x 3 > 256), M = 268
+    (1, 9, 400, 32, 40, 3, 3, 4, 1),   # Wo = 100 (box 100 x 4 > 256), M = 300
+    (2, 30, 30, 64, 40, 3, 3, 3, 1),   # Wo = 10: the 2-CTA kernel's box fits (30)
+    (2, 33, 33, 64, 24, 5, 5, 4, 2),   # stride 4, 5x5 taps
+]
+
+
+@pytest.mark.parametrize("shape", WIDE_STRIDE_SHAPES)
+@pytest.mark.parametrize("a_bits,w_bits,enc", [(2, 1, 2), (2, 2, 0), (1, 1, 1)])
+def test_conv_large_strides(shape, a_bits, w_bits, enc):
+    B, H, Wd, C, Co, R, S, st, pad = shape
+    X, Wt = synth.conv_inputs(B, H, Wd, C, Co, R, S, a_bits, w_bits, tag="convstride")
+    want = oracle.conv2d(X, Wt, st, pad, a_bits, w_bits, enc)
+    Xp = ap.pack_bits(cuda(X.reshape(-1, C)), a_bits)
+    Wp = ap.pack_bits(cuda(Wt.reshape(-1, C)), w_bits)
+    cs = ap.ConvShape(B, H, Wd, C, Co, R, S, st, pad)
+    for v in (ap.VARIANT_AUTO, ap.VARIANT_TC_I8):
+        got = ap.conv2d(Xp, Wp, cs, a_bits, w_bits, enc, variant=v)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(got.cpu().numpy(), want, err_msg=f"variant {ap.variant_name(v)}")
+        alpha, beta, Sd = epi_case(Co, 2, "convstride")
+        wantp = oracle.pack(oracle.epilogue(want.reshape(-1, Co), alpha, beta, Sd, 2), 2)
+        got = ap.conv2d(Xp, Wp, cs, a_bits, w_bits, enc, epi=ap.Epilogue(2, cuda(alpha), cuda(beta), Sd), variant=v)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(u32(got), wantp)
+    if w_bits > 1:  # prepared int8 weights: the 2-CTA kernel or a clean UNSUPPORTED
+        Wprep = ap.prepare_weights_i8(Wp, Co * R * S, C, w_bits, enc)
+        try:
+            got = ap.conv2d_prepared_i8(Xp, Wprep, cs, a_bits, w_bits, enc)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(got.cpu().numpy(), want)
+        except ap.ApnnError as ex:
+            assert ex.status == 7
+
+
+def test_prepared_weights_tags_checked():
+    # prepared weights carry (kind, N, K, w_bits, enc); a mismatched call is rejected before launch
+    M, N, K = 256, 128, 256
+    A, W = synth.gemm_inputs(M, N, K, 2, 1, tag="tags")
+    Ap = ap.pack_bits(cuda(A), 2)
+    Wpl = ap.pack_bits(cuda(W), 1)
+    Wfp4 = ap.prepare_weights(Wpl, N, K, 1, 2)          # +-1 weights (Case III)
+    with pytest.raises(ValueError):
+        ap.gemm_prepared(Ap, Wfp4, M, N, K, 2, 1, 0)    # used as 0/1 weights
+    with pytest.raises(ValueError):
+        ap.gemm_prepared(Ap, Wfp4, M, N - 1, K, 2, 1, 2)  # wrong N
+    with pytest.raises(ValueError):
+        ap.gemm_prepared_i8(Ap, Wfp4, M, N, K, 2, 1, 2)  # FP4 operand bytes on the int8 kernel
+    with pytest.raises(TypeError):
+        ap.gemm_prepared(Ap, Wfp4.data, M, N, K, 2, 1, 2)  # untagged bytes
+    with pytest.raises(ValueError):                     # output buffer of the wrong size
+        ap.gemm_prepared(Ap, Wfp4, M, N, K, 2, 1, 2, out=torch.empty((M, N - 4), dtype=torch.int32, device="cuda"))
+    got = ap.gemm_prepared(Ap, Wfp4, M, N, K, 2, 1, 2)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy(), oracle.gemm(A, W, 2, 1, 2))
