@@ -215,8 +215,11 @@ def time_models(args, world, rank, dev, dist):
     for name, w, a, gb in (("alexnet", 1, 2, args.model_batch), ("vgg_variant", 1, 2, args.model_batch),
                            ("resnet18", 2, 8, args.resnet_batch)):
         per = max(1, gb // world)
-        m = APNNResNet18(per, w, a, device=dev) if name == "resnet18" else APNNModel(name, per, w, a, device=dev)
-        x = torch.from_numpy(synth.model_input(name, per, a, tag=f"img-rank{rank}")).to(dev)
+        # from the raw 8-bit image: the first layer quantises it on the GPU
+        q = synth.input_quant(a)
+        m = (APNNResNet18(per, w, a, device=dev, input_quant=q) if name == "resnet18"
+             else APNNModel(name, per, w, a, device=dev, input_quant=q))
+        x = torch.from_numpy(synth.model_image(name, per, tag=f"img-rank{rank}")).to(dev)
         m.run(x)
         m.capture()
         for _ in range(3):
@@ -238,6 +241,7 @@ def time_models(args, world, rank, dev, dist):
         out[f"{name}_w{w}a{a}"] = {"global_batch": per * world, "batch_per_gpu": per, "latency_ms": best,
                                "images_per_s": per * world / (best * 1e-3),
                                "effective_tops": 2.0 * macs / (best * 1e-3) / 1e12, "scaling": "strong",
+                               "input": "raw 8-bit image, quantised to a_bits codes in the first layer",
                                "timing": "CUDA graph of the whole forward, best of 5, max over ranks"}
         del m
     return out

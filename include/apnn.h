@@ -152,6 +152,16 @@ apnn_status apnn_pack_bits(const uint8_t *codes, int rows, int K, int bits, uint
 apnn_status apnn_im2col_pack(const uint8_t *X, const apnn_conv_shape *shape, int bits, uint32_t *dst,
                              apnn_stream_t stream);
 
+/* The first layer's input quantisation fused into apnn_im2col_pack: "the first layer
+ * quantizes 8-bit inputs into q-bit activations" with the
+ * quantisation y = floor((x - z) / s) of PAPER.md:1283-1287, clamped to [0, 2^bits - 1]
+ * (reading R10).  X holds the raw 8-bit image (uint8 [B][H][W][C_in], any value); every
+ * element is quantised while it is staged, out-of-frame taps are code 0 (zero padding of
+ * the quantised conv input).  Output layout as apnn_im2col_pack.
+ *   zero_point: z in [-255, 255];  scale: s in [1, 255] (APNN_ERR_INVALID_ARG otherwise). */
+apnn_status apnn_im2col_quant_pack(const uint8_t *X, const apnn_conv_shape *shape, int zero_point, int scale,
+                                   int bits, uint32_t *dst, apnn_stream_t stream);
+
 /* Flatten a packed feature map for the first fully connected layer: per image b,
  *   src [B][P][bits][Cw]  (P pixels, packed rows of the conv output, Cw = roundup(C,128)/32)
  *   dst [B][bits][P*Cw]   (one packed row of K = P * Cw * 32 elements per image, pixel-major,

@@ -183,6 +183,14 @@ def residual_epilogue(Y, Z, alpha, beta, rho, S, out_bits):
     return np.clip(v // int(S), 0, (1 << out_bits) - 1).astype(np.uint8)  # // floors toward -inf
 
 
+def quantize_input(x, zero_point, scale, bits):
+    """The first layer's quantisation of the 8-bit input image to `bits`-bit codes
+    (PAPER.md:1259-1261): y = floor((x - z) / s), clamped to
+    [0, 2^bits - 1] (reading R10).  Plain numpy integer arithmetic (floor division)."""
+    v = np.asarray(x, dtype=np.int64) - int(zero_point)
+    return np.clip(np.floor_divide(v, int(scale)), 0, (1 << bits) - 1).astype(np.uint8)
+
+
 def pack(codes, bits):
     """Codes [rows, K] -> packed planes uint32 [rows, bits, roundup(K,128)/32]."""
     codes = _u8(codes)

@@ -111,8 +111,14 @@ def run_resnet18(ops, params, x, w_bits, a_bits, enc, threads=0, trace=None):
             C = Lb["Co"]
             act = residual_epilogue(Yb.reshape(-1, C), Z.reshape(-1, C), P["alpha"], P["beta"], P["rho"], P["S"],
                                     a_bits).reshape(Yb.shape)
-        else:
-            return gemm(act.reshape(B, -1), P["W"].reshape(op["Co"], -1), a_bits, w_bits, enc, threads=threads)
+        else:  # global average pooling + FC (reading R30): logits = W . sum over positions of q
+            pooled = act.reshape(B, -1, op["C"]).astype(np.int64).sum(axis=1)      # [B, C]
+            w = P["W"].reshape(op["Co"], op["C"]).astype(np.int64)
+            if enc in (1, 2):                                                      # +-1 weights
+                w = 2 * w - 1
+            y = pooled @ w.T
+            assert np.abs(y).max(initial=0) < 2**31
+            return y.astype(np.int32)
         if trace is not None:
             trace.append(act)
     raise ValueError("no classifier")

@@ -93,6 +93,8 @@ def lib() -> ctypes.CDLL:
             L.apnn_conv2d_prepared_i8.restype = st
             L.apnn_im2col_pack.argtypes = [vp, ctypes.POINTER(_Conv), ci, vp, vp]
             L.apnn_im2col_pack.restype = st
+            L.apnn_im2col_quant_pack.argtypes = [vp, ctypes.POINTER(_Conv), ci, ci, ci, vp, vp]
+            L.apnn_im2col_quant_pack.restype = st
             L.apnn_gemm.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, vp, vp]
             L.apnn_gemm.restype = st
             L.apnn_gemm_fused.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp, vp]
@@ -124,7 +126,8 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
-ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_im2col_pack", "apnn_flatten_packed",
+ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_im2col_pack", "apnn_im2col_quant_pack",
+               "apnn_flatten_packed",
                "apnn_prepared_bytes", "apnn_prepare_weights", "apnn_gemm_prepared",
                "apnn_prepared_i8_bytes", "apnn_prepare_weights_i8", "apnn_gemm_prepared_i8",
                "apnn_conv2d_prepared_i8", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
@@ -283,9 +286,11 @@ def pack_bits(codes: torch.Tensor, bits: int, out: Optional[torch.Tensor] = None
     return out
 
 
-def im2col_pack(X: torch.Tensor, shape: ConvShape, bits: int, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+def im2col_pack(X: torch.Tensor, shape: ConvShape, bits: int, out: Optional[torch.Tensor] = None,
+                quant: Optional[tuple] = None) -> torch.Tensor:
     """NHWC uint8 codes [B, H, W, C_in] -> packed im2col rows [B*Ho*Wo, bits, Kw(R*S*C_in)]
-    (apnn_im2col_pack; out-of-frame taps are code 0)."""
+    (apnn_im2col_pack; out-of-frame taps are code 0).  quant = (zero_point, scale): X is the
+    raw 8-bit image, quantised on the fly (apnn_im2col_quant_pack)."""
     _cuda(X, "X", torch.uint8)
     K = shape.R * shape.S * shape.C_in
     if out is None:
@@ -293,7 +298,12 @@ def im2col_pack(X: torch.Tensor, shape: ConvShape, bits: int, out: Optional[torc
     _cuda(out, "out", torch.int32)
     _check_out(out, packed_shape(shape.B * shape.Ho * shape.Wo, K, bits))
     cs = shape._c()
-    _check(lib().apnn_im2col_pack(_ptr(X), ctypes.byref(cs), bits, _ptr(out), _stream(X)), "apnn_im2col_pack")
+    if quant is None:
+        _check(lib().apnn_im2col_pack(_ptr(X), ctypes.byref(cs), bits, _ptr(out), _stream(X)), "apnn_im2col_pack")
+    else:
+        z, sc = quant
+        _check(lib().apnn_im2col_quant_pack(_ptr(X), ctypes.byref(cs), int(z), int(sc), bits, _ptr(out), _stream(X)),
+               "apnn_im2col_quant_pack")
     return out
 
 

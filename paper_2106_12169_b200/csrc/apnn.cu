@@ -26,7 +26,8 @@ cudaError_t launch_residual_quant_pack(const int32_t* Y, int M, int N, const voi
 cudaError_t launch_flatten_packed(const uint32_t* src, int B, int P, int bits, int Cw, uint32_t* dst, int sms,
                                   cudaStream_t s);
 cudaError_t launch_im2col_pack(const uint8_t* X, int B, int H, int W, int C, int R, int S, int stride, int pad,
-                               int Ho, int Wo, int bits, uint32_t* dst, int sms, cudaStream_t s);
+                               int Ho, int Wo, int bits, uint32_t* dst, int sms, cudaStream_t s, int qz = 0,
+                               int qs = 0);
 cudaError_t launch_popc(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
                         cudaStream_t s);
 cudaError_t launch_b1mma(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
@@ -243,8 +244,22 @@ apnn_status apnn_flatten_packed(const uint32_t* src, int B, int P, int bits, int
     return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }
 
+static apnn_status im2col_impl(const uint8_t* X, const apnn_conv_shape* shp, int bits, uint32_t* dst, int qz,
+                               int qs, apnn_stream_t stream);
+
 apnn_status apnn_im2col_pack(const uint8_t* X, const apnn_conv_shape* shp, int bits, uint32_t* dst,
                              apnn_stream_t stream) {
+    return im2col_impl(X, shp, bits, dst, 0, 0, stream);
+}
+
+apnn_status apnn_im2col_quant_pack(const uint8_t* X, const apnn_conv_shape* shp, int zero_point, int scale,
+                                   int bits, uint32_t* dst, apnn_stream_t stream) {
+    if (scale < 1 || scale > 255 || zero_point < -255 || zero_point > 255) return APNN_ERR_INVALID_ARG;
+    return im2col_impl(X, shp, bits, dst, zero_point, scale, stream);
+}
+
+static apnn_status im2col_impl(const uint8_t* X, const apnn_conv_shape* shp, int bits, uint32_t* dst, int qz,
+                               int qs, apnn_stream_t stream) {
     if (!shp) return APNN_ERR_INVALID_ARG;
     const apnn_conv_shape c = *shp;
     if (c.B < 0 || c.H < 1 || c.W < 1 || c.C_in < 1 || c.R < 1 || c.S < 1 || c.stride < 1 || c.pad < 0)
@@ -261,7 +276,7 @@ apnn_status apnn_im2col_pack(const uint8_t* X, const apnn_conv_shape* shp, int b
     apnn_status st = device_info(&d);
     if (st != APNN_OK) return st;
     cudaError_t err = launch_im2col_pack(X, c.B, c.H, c.W, c.C_in, c.R, c.S, c.stride, c.pad, Ho, Wo, bits, dst,
-                                         d.sms, (cudaStream_t)stream);
+                                         d.sms, (cudaStream_t)stream, qz, qs);
     return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }
 

@@ -253,9 +253,14 @@ __global__ void __launch_bounds__(256) pool_quant_pack_v4_kernel(const int32_t* 
 // walked with incremental counters (no per-element division), one shared-memory byte
 // read and `bits` shift-ors each; the CTA's Wo output rows are one contiguous range,
 // so the words are staged in shared memory and written out coalesced.
+// qs > 0: X is the raw 8-bit image and every element is quantised while it is staged,
+// q = clamp(floor((x - qz) / qs), 0, 2^bits - 1) (the first layer's quantisation of the
+// 8-bit input, with the quantisation formula of PAPER.md:1283-1287);
+// out-of-frame taps stay code 0 (zero padding of the conv input).  qs = 0: X holds codes.
 __global__ void __launch_bounds__(256) im2col_pack_kernel(const uint8_t* __restrict__ X, int B, int H, int W,
                                                           int C, int R, int S, int stride, int pad, int Ho, int Wo,
-                                                          int bits, int Kw, uint32_t* __restrict__ dst) {
+                                                          int bits, int Kw, uint32_t* __restrict__ dst, int qz,
+                                                          int qs) {
     extern __shared__ __align__(16) uint8_t sm[];
     const int Wp = W + 2 * pad, rowb = Wp * C;       // padded input row bytes
     uint8_t* rows = sm;                              // R x rowb
@@ -271,7 +276,15 @@ __global__ void __launch_bounds__(256) im2col_pack_kernel(const uint8_t* __restr
             uint8_t* d = rows + r * rowb + px * C;
             if (hi >= 0 && hi < H && wi >= 0 && wi < W) {
                 const uint8_t* src = X + (((long long)b * H + hi) * W + wi) * C;
-                for (int c = 0; c < C; c++) d[c] = __ldg(src + c) & keep;
+                if (qs > 0) {
+                    for (int c = 0; c < C; c++) {
+                        const int v = (int)__ldg(src + c) - qz;  // floor((x - z) / s), clamped
+                        const int q = v < 0 ? 0 : v / qs;
+                        d[c] = (uint8_t)(q > (int)keep ? keep : q);
+                    }
+                } else {
+                    for (int c = 0; c < C; c++) d[c] = __ldg(src + c) & keep;
+                }
             } else {
                 for (int c = 0; c < C; c++) d[c] = 0;
             }
@@ -539,7 +552,7 @@ cudaError_t launch_pool_quant_pack(const int32_t* Y, int B, int H, int W, int N,
 
 namespace apnn {
 cudaError_t launch_im2col_pack(const uint8_t* X, int B, int H, int W, int C, int R, int S, int stride, int pad,
-                               int Ho, int Wo, int bits, uint32_t* dst, int sms, cudaStream_t s) {
+                               int Ho, int Wo, int bits, uint32_t* dst, int sms, cudaStream_t s, int qz, int qs) {
     const int Kw = (R * S * C + 127) / 128 * 4;
     const long long total = (long long)B * Ho * Wo;
     if (total == 0) return cudaSuccess;
@@ -552,7 +565,7 @@ cudaError_t launch_im2col_pack(const uint8_t* X, int B, int H, int W, int C, int
     }
     const long long ctas = (long long)B * Ho;
     const int grid = (int)(ctas < (long long)sms * 4 ? ctas : (long long)sms * 4);
-    im2col_pack_kernel<<<grid, 256, smem, s>>>(X, B, H, W, C, R, S, stride, pad, Ho, Wo, bits, Kw, dst);
+    im2col_pack_kernel<<<grid, 256, smem, s>>>(X, B, H, W, C, R, S, stride, pad, Ho, Wo, bits, Kw, dst, qz, qs);
     count_launch();
     return cudaGetLastError();
 }

@@ -51,8 +51,13 @@ def _conv(X, Wpacked, Wprep, shape, a, w, enc, epi=None, out=None):
 
 
 class APNNModel:
-    def __init__(self, name: str, batch: int, w_bits: int, a_bits: int, device="cuda", params=None):
+    def __init__(self, name: str, batch: int, w_bits: int, a_bits: int, device="cuda", params=None,
+                 input_quant=None):
+        # input_quant = (zero_point, scale): forward() takes the raw 8-bit image and the first
+        # layer quantises it on the fly (apnn_im2col_quant_pack); None:
+        # forward() takes a_bits-bit image codes
         self.name, self.B, self.w_bits, self.a_bits = name, batch, w_bits, a_bits
+        self.input_quant = input_quant
         self.dev = torch.device(device)
         self.enc = synth.model_encoding(w_bits, a_bits)
         self.layers = synth.model_layers(name, batch)
@@ -108,17 +113,20 @@ class APNNModel:
         self.graph: Optional[torch.cuda.CUDAGraph] = None
 
     # ------------------------------------------------------------------ forward
-    def forward(self, x: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """x: NHWC uint8 image codes [B, H, W, 3] (< 2^a_bits) on the device; returns int32
-        logits [B, classes]."""
+    def forward(self, x: Optional[torch.Tensor] = None, mark=None) -> torch.Tensor:
+        """x: NHWC uint8 image codes [B, H, W, 3] (< 2^a_bits), or the raw 8-bit image with
+        input_quant, on the device; returns int32 logits [B, classes].  mark(i) is called after
+        layer i's launches (layer_times)."""
         if x is not None and x.data_ptr() != self.x.data_ptr():
             self.x.copy_(x)
         a, w, enc = self.a_bits, self.w_bits, self.enc
         act = None
-        for st in self.steps:
+        for li, st in enumerate(self.steps):
+            if mark is not None and li > 0:
+                mark(li - 1)
             L, epi = st["L"], st["epi"]
             if st["mode"] == "im2col":
-                im2col_pack(self.x, st["shape"], a, out=st["A"])
+                im2col_pack(self.x, st["shape"], a, out=st["A"], quant=self.input_quant)
                 M = self.B * L["Ho"] * L["Wo"]
                 if L["pool"]:
                     Y = gemm(st["A"], st["W"], M, L["Co"], L["K"], a, w, enc, out=st["Y32"].view(M, L["Co"]))
@@ -132,6 +140,8 @@ class APNNModel:
                 if st["mode"] == "flatten_fc":
                     A = flatten_packed(act, self.B, L["H"] * L["W"], out=st["A"])
                 act = gemm(A, st["W"], self.B, L["Co"], st["K"], a, w, enc, epi=epi, out=st["out"])
+        if mark is not None:
+            mark(len(self.steps) - 1)
         return act
 
     def capture(self):
@@ -165,13 +175,16 @@ class APNNResNet18:
     stem = im2col GEMM (int32) + 2x2 pooling routine; basic block = conv_a with the fused
     requantisation, conv_b with the shortcut (the block input's packed codes, or a 1x1
     stride-s downsample conv's int32 accumulator) added in its fused epilogue (or, unfused,
-    conv_b int32 + apnn_residual_quant_pack); head =
-    flatten + FC (int32 logits).  Static buffers; capture()/run() as APNNModel."""
+    conv_b int32 + apnn_residual_quant_pack); head = global average pooling + FC as one
+    flatten GEMM with the FC weight tiled over the 7 x 7 positions (int32 logits).  Static
+    buffers; capture()/run() as APNNModel."""
 
-    def __init__(self, batch: int, w_bits: int, a_bits: int, device="cuda", params=None, fuse_residual=False):
+    def __init__(self, batch: int, w_bits: int, a_bits: int, device="cuda", params=None, fuse_residual=False,
+                 input_quant=None):
         # fuse_residual: the shortcut in conv_b's epilogue.  Correct (tests) but measured slower at
         # batch 256 (w2a8 11.5 vs 10.5 ms): the epilogue's per-row shortcut loads are uncoalesced.
         self.B, self.w_bits, self.a_bits = batch, w_bits, a_bits
+        self.input_quant = input_quant  # as APNNModel
         self.fuse_residual = fuse_residual
         self.name = "resnet18"
         self.dev = torch.device(device)
@@ -217,10 +230,12 @@ class APNNResNet18:
                 st["rho"] = t(P["rho"])
                 st["out"] = packed(batch * Lb["Ho"] * Lb["Wo"], Lb["Co"])
             else:
+                # global average pooling + FC (reading R30): W . sum_p q_p = [W W ... W] . flatten(q),
+                # so the head is the flatten GEMM with the FC weight tiled over the H x W positions
                 Pn, C = L["H"] * L["W"], L["C"]
                 Cp = (C + 127) // 128 * 128
                 Wf = np.zeros((L["Co"], Pn, Cp), np.uint8)
-                Wf[:, :, :C] = P["W"].reshape(L["Co"], Pn, C)
+                Wf[:, :, :C] = P["W"].reshape(L["Co"], 1, C)
                 st["K"] = Pn * Cp
                 st["W"] = pack_bits(t(Wf.reshape(L["Co"], -1)), w_bits)
                 st["A"] = torch.empty((batch, a, Pn * Cp // 32), dtype=torch.int32, device=d)
@@ -229,15 +244,17 @@ class APNNResNet18:
         self.x = torch.empty((batch, 224, 224, 3), dtype=torch.uint8, device=d)
         self.graph: Optional[torch.cuda.CUDAGraph] = None
 
-    def forward(self, x: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def forward(self, x: Optional[torch.Tensor] = None, mark=None) -> torch.Tensor:
         if x is not None and x.data_ptr() != self.x.data_ptr():
             self.x.copy_(x)
         a, w, enc, B = self.a_bits, self.w_bits, self.enc, self.B
         act = None
-        for st in self.steps:
+        for li, st in enumerate(self.steps):
+            if mark is not None and li > 0:
+                mark(li - 1)
             L = st["L"]
             if st["kind"] == "stem":
-                im2col_pack(self.x, st["shape"], a, out=st["A"])
+                im2col_pack(self.x, st["shape"], a, out=st["A"], quant=self.input_quant)
                 M = B * L["Ho"] * L["Wo"]
                 gemm(st["A"], st["W"], M, L["Co"], L["K"], a, w, enc, out=st["Y32"].view(M, L["Co"]))
                 act = pool_quant_pack_out(st["Y32"], st["epi"], out=st["out"])
@@ -258,6 +275,8 @@ class APNNResNet18:
             else:
                 A = flatten_packed(act, B, L["H"] * L["W"], out=st["A"])
                 act = gemm(A, st["W"], B, L["Co"], st["K"], a, w, enc, out=st["out"])
+        if mark is not None:
+            mark(len(self.steps) - 1)
         return act
 
     capture = APNNModel.capture
@@ -269,3 +288,32 @@ class APNNResNet18:
             for l in ([L["a"], L["b"]] + ([L["down"]] if L["down"] else []) if kind == "block" else [L]):
                 tot += l["Ho"] * l["Wo"] * l["Co"] * l["K"]
         return tot
+
+
+def layer_times(model, x: torch.Tensor, reps: int = 20):
+    """Per-layer device time of one forward (the paper's per-layer latency breakdown,
+    PAPER.md:620-630): CUDA events on the launching stream after every layer of an eager
+    forward, median over `reps` forwards.  Returns [(layer name, ms)]; the sum is the eager
+    forward's time (the CUDA-graph replay the bench times is slightly faster: no launch gaps)."""
+    stream = torch.cuda.current_stream(model.dev)
+    n = len(model.steps)
+    per = [[] for _ in range(n)]
+    model.forward(x)
+    for _ in range(reps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
+        evs[0].record(stream)
+        model.forward(x, mark=lambda i: evs[i + 1].record(stream))
+        torch.cuda.synchronize(model.dev)
+        for i in range(n):
+            per[i].append(evs[i].elapsed_time(evs[i + 1]))
+    names = []
+    for i, st in enumerate(model.steps):
+        L = st["L"]
+        if "kind" in st and st["kind"] == "block":
+            La = L["a"]
+            names.append(f"block{i} {La['C']}->{La['Co']} s{La['stride']} {La['H']}x{La['W']}")
+        elif "kind" in st:
+            names.append(f"{st['kind']} {L['C']}->{L['Co']} {L['H']}x{L['W']}")
+        else:
+            names.append(f"{st['mode']} {L['C']}->{L['Co']} {L['H']}x{L['W']}" + (f" pool{L['pool']}" if L["pool"] else ""))
+    return [(nm, float(np.median(t))) for nm, t in zip(names, per)]

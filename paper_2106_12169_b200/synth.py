@@ -146,6 +146,19 @@ def model_params(name: str, w_bits: int, a_bits: int, tag: str = "model"):
     return params
 
 
+def model_image(name: str, batch: int, tag: str = "img"):
+    """A raw 8-bit image batch (uniform 0..255), NHWC uint8: the first layer's input before
+    its quantisation."""
+    H, W, C = MODELS[name]["input"] if name in MODELS else (224, 224, 3)
+    return rng(f"{tag}:{name}:{batch}:raw").integers(0, 256, size=(batch, H, W, C), dtype=np.uint8)
+
+
+def input_quant(a_bits: int):
+    """(zero_point, scale) of the input quantisation: the 0..255 range split into 2^a_bits
+    equal bins (a synthetic choice; a trained model would calibrate it)."""
+    return 0, 256 >> a_bits if a_bits < 8 else 1
+
+
 def model_input(name: str, batch: int, a_bits: int, tag: str = "img"):
     """The image batch quantised to a_bits codes, NHWC uint8 (reading R23)."""
     H, W, C = MODELS[name]["input"] if name in MODELS else (224, 224, 3)
@@ -153,10 +166,10 @@ def model_input(name: str, batch: int, a_bits: int, tag: str = "img"):
 
 
 # ResNet-18 (BASELINE.json configs[4]; He et al.'s basic-block network, reading R24 for the
-# residual integer form).  Deviations, labelled: the stem max-pool is 2x2/2 (no pool padding
-# in this library) instead of 3x3/2 pad 1 (same 56 x 56 output); the head is an FC over the
-# flattened 7 x 7 x 512 map instead of global average pooling + FC (both are linear maps of
-# the last block's codes).
+# residual integer form).  Deviation, labelled: the stem max-pool is 2x2/2 (no pool padding
+# in this library) instead of 3x3/2 pad 1 (same 56 x 56 output).  The head is He et al.'s
+# global average pooling + FC 512 -> 1000, in integer form (reading R30): the logits are
+# W . sum_p q_p (the 1/49 of the average is a positive scale of every logit, folded away).
 RESNET18_STAGES = [(64, 1), (128, 2), (256, 2), (512, 2)]
 
 
@@ -178,8 +191,9 @@ def resnet18_ops(batch: int):
             down = conv(H, C, Co, 1, s_, 0) if (s_ != 1 or C != Co) else None
             ops.append(("block", dict(a=a, b=b, down=down)))
             H, C = a["Ho"], Co
-    ops.append(("fc", dict(kind="fc", B=batch, H=H, W=H, C=C, Co=1000, R=H, S=H, stride=1, pad=0, Ho=1, Wo=1,
-                           pool=None, Hp=1, Wp=1, K=H * H * C)))
+    # global average pooling + FC: K = C logical MACs per logit (the pooling is H*H*C adds)
+    ops.append(("fc", dict(kind="fc", B=batch, H=H, W=H, C=C, Co=1000, R=1, S=1, stride=1, pad=0, Ho=1, Wo=1,
+                           pool=None, Hp=1, Wp=1, K=C, gap=True)))
     return ops
 
 

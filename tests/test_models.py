@@ -60,6 +60,43 @@ def test_im2col_pack_and_flatten_match_oracle_layouts(bits):
     np.testing.assert_array_equal(flat, oracle.pack(F.reshape(3, 4 * 256), 2))
 
 
+@pytest.mark.parametrize("bits,z,sc", [(2, 0, 64), (3, 17, 23), (8, 0, 1), (1, -5, 200)])
+def test_im2col_quant_pack_matches_oracle(bits, z, sc):
+    # the first layer's input quantisation fused into im2col: raw 8-bit
+    # image -> oracle.quantize_input -> direct-indexing im2col -> oracle packer
+    X = synth.model_image("alexnet", 2, tag="im2colq")[:, :11, :13, :]
+    X = np.ascontiguousarray(X)
+    cs = ap.ConvShape(2, 11, 13, 3, 1, 5, 5, 2, 2)
+    got = ap.im2col_pack(torch.from_numpy(X).cuda(), cs, bits, quant=(z, sc)).cpu().numpy().view(np.uint32)
+    Q = oracle.quantize_input(X, z, sc, bits)
+    rows = []
+    for b in range(2):
+        for ho in range(cs.Ho):
+            for wo in range(cs.Wo):
+                r = []
+                for i in range(5):
+                    for j in range(5):
+                        h, w_ = ho * 2 + i - 2, wo * 2 + j - 2
+                        r.extend(Q[b, h, w_] if 0 <= h < 11 and 0 <= w_ < 13 else [0, 0, 0])
+                rows.append(r)
+    np.testing.assert_array_equal(got, oracle.pack(np.array(rows, np.uint8), bits))
+
+
+@pytest.mark.parametrize("name", ["alexnet", "vgg_variant"])
+def test_model_from_raw_image_matches_oracle(name):
+    # end to end from the raw 8-bit image: GPU quantises in the first layer; the oracle
+    # quantises with oracle.quantize_input and runs the model on the codes
+    B, w, a = 2, 1, 2
+    params = synth.model_params(name, w, a)
+    raw = synth.model_image(name, B)
+    z, sc = synth.input_quant(a)
+    want = om.run_model(synth.model_layers(name, B), params, oracle.quantize_input(raw, z, sc, a), w, a, 2)
+    model = APNNModel(name, B, w, a, params=params, input_quant=(z, sc))
+    got = model.forward(torch.from_numpy(raw).cuda())
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+
+
 def test_residual_quant_pack_matches_oracle():
     g = synth.rng("resgpu")
     M, N = 300, 200

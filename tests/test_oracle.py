@@ -346,6 +346,12 @@ def test_residual_epilogue_pins():
     rho = g.integers(-2, 3, size=7).astype(np.int32)
     np.testing.assert_array_equal(oracle.residual_epilogue(Y, Z, alpha, beta, np.zeros(7, np.int32), 13, 3),
                                   oracle.epilogue(Y, alpha, beta, 13, 3))
+    # reduction to the (separately pinned) plain epilogue: alpha*Y + rho*Z formed first with
+    # numpy int64 (it fits int32 here), then requantised with alpha' = 1
+    comb = (alpha.astype(np.int64) * Y + rho.astype(np.int64) * Z)
+    assert np.abs(comb).max() < 2**31
+    np.testing.assert_array_equal(oracle.residual_epilogue(Y, Z, alpha, beta, rho, 777, 5),
+                                  oracle.epilogue(comb.astype(np.int32), np.ones(7, np.int32), beta, 777, 5))
     q = oracle.residual_epilogue(Y, Z, alpha, beta, rho, 777, 5)
     for m in range(9):
         for n in range(7):
@@ -355,5 +361,73 @@ def test_residual_epilogue_pins():
 
 def test_resnet18_table():
     ops = synth.resnet18_ops(1)
-    assert [k for k, _ in ops].count("block") == 8 and ops[-1][1]["K"] == 7 * 7 * 512
+    assert [k for k, _ in ops].count("block") == 8
+    assert ops[-1][1]["gap"] and ops[-1][1]["K"] == 512 and ops[-1][1]["H"] == 7   # GAP over 7 x 7, FC 512 -> 1000
     assert sum(1 for k, o in ops if k == "block" and o["down"] is not None) == 3
+
+
+def _tiny_resnet(g):
+    """A 4-op ResNet in synth.resnet18_ops' format: stem (7x7/2 conv + 2x2/2 max pool), an
+    identity basic block, a stride-2 block with a 1x1 downsample shortcut, GAP + FC."""
+    def conv(H, C, Co, R, st, pad, pool=None):
+        Ho = (H + 2 * pad - R) // st + 1
+        Hp = Ho if not pool else (Ho - pool[0]) // pool[1] + 1
+        return dict(kind="conv", B=2, H=H, W=H, C=C, Co=Co, R=R, S=R, stride=st, pad=pad, Ho=Ho, Wo=Ho, pool=pool,
+                    Hp=Hp, Wp=Hp, K=R * R * C)
+    ops = [("stem", conv(16, 3, 8, 7, 2, 3, (2, 2))),
+           ("block", dict(a=conv(4, 8, 8, 3, 1, 1), b=conv(4, 8, 8, 3, 1, 1), down=None)),
+           ("block", dict(a=conv(4, 8, 16, 3, 2, 1), b=conv(2, 16, 16, 3, 1, 1), down=conv(4, 8, 16, 1, 2, 0))),
+           ("fc", dict(kind="fc", B=2, H=2, W=2, C=16, Co=10, R=1, S=1, stride=1, pad=0, Ho=1, Wo=1, pool=None,
+                       Hp=1, Wp=1, K=16, gap=True))]
+    w = lambda Co, R, C: g.integers(0, 4, size=(Co, R, R, C), dtype=np.uint8)          # 2-bit weights
+    q = lambda Co: (g.integers(-2, 4, size=Co).astype(np.int32), g.integers(-40, 60, size=Co).astype(np.int32))
+    a0, b0 = q(8); aa1, ba1 = q(8); ab1, bb1 = q(8); aa2, ba2 = q(16); ab2, bb2 = q(16)
+    params = [dict(W=w(8, 7, 3), alpha=a0, beta=b0, S=40),
+              dict(Wa=w(8, 3, 8), alpha_a=aa1, beta_a=ba1, S_a=30, Wb=w(8, 3, 8), Wd=None, alpha=ab1, beta=bb1,
+                   S=30, rho=g.integers(1, 4, size=8).astype(np.int32)),
+              dict(Wa=w(16, 3, 8), alpha_a=aa2, beta_a=ba2, S_a=30, Wb=w(16, 3, 16), Wd=w(16, 1, 8), alpha=ab2,
+                   beta=bb2, S=30, rho=g.integers(1, 4, size=16).astype(np.int32)),
+              dict(W=w(10, 1, 16), alpha=None, beta=None, S=None)]
+    return ops, params
+
+
+def test_resnet18_runner_vs_torch_float64():
+    """oracle.models.run_resnet18 against a textbook basic-block network written with torch
+    float64 ops (conv2d, max_pool2d, mean over positions): conv_a -> BN/requant -> conv_b,
+    shortcut = the block input (identity) or a 1x1 stride-2 conv of it, added before the
+    block's requantisation (reading R24); head = global average pooling + FC (reading R30,
+    the 1/HW scale folded away).  w2a2 0/1 codes (Case I); exact at these magnitudes."""
+    import torch
+    import torch.nn.functional as F
+    from oracle import models as om
+    g = synth.rng("tinyresnet")
+    ops, params = _tiny_resnet(g)
+    x = synth.codes((2, 16, 16, 3), 2, "tinyresnet:x")
+    got = om.run_resnet18(ops, params, x, 2, 2, 0)
+    T = lambda a: torch.from_numpy(np.asarray(a).astype(np.float64))
+    ch = lambda v: T(v)[None, :, None, None]
+    conv = lambda t, W, st, pad: F.conv2d(t, T(W).permute(0, 3, 1, 2), stride=st, padding=pad)
+    quant = lambda v, S: torch.clamp(torch.floor(v / S), 0, 3)
+    act = T(x).permute(0, 3, 1, 2)
+    P = params[0]
+    act = quant(F.max_pool2d(conv(act, P["W"], 2, 3) * ch(P["alpha"]) + ch(P["beta"]), 2, 2), P["S"])
+    for (kind, op), P in zip(ops[1:3], params[1:3]):
+        h = quant(conv(act, P["Wa"], op["a"]["stride"], 1) * ch(P["alpha_a"]) + ch(P["beta_a"]), P["S_a"])
+        y = conv(h, P["Wb"], 1, 1)
+        z = act if P["Wd"] is None else conv(act, P["Wd"], 2, 0)
+        act = quant(y * ch(P["alpha"]) + ch(P["beta"]) + ch(P["rho"]) * z, P["S"])
+    gap = act.mean(dim=(2, 3)) * (act.shape[2] * act.shape[3])     # HW * average = sum of the codes
+    want = gap @ T(params[3]["W"]).reshape(10, 16).T
+    np.testing.assert_array_equal(got, want.numpy().astype(np.int32))
+
+
+def test_quantize_input_brute_force():
+    """First-layer input quantisation (formula P:1283-1287, clamp R10):
+    every 8-bit value against Python floor division."""
+    x = np.arange(256, dtype=np.uint8).reshape(16, 16)
+    for bits in (1, 2, 3, 8):
+        for z, sc in ((0, 1), (0, 64), (17, 23), (-5, 200), (255, 1)):
+            got = oracle.quantize_input(x, z, sc, bits)
+            for v in range(256):
+                assert got.flat[v] == min(max((v - z) // sc, 0), (1 << bits) - 1)
+    assert (oracle.quantize_input(x, 0, 64, 2).reshape(-1) == np.arange(256) // 64).all()
