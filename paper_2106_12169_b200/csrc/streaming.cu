@@ -68,182 +68,286 @@ __global__ void __launch_bounds__(256) pack_bits_kernel(const uint8_t* __restric
     }
 }
 
-// Y [M][N] int32 -> out [M][ob][Nw], Nw = roundup(N,128)/32
-__global__ void __launch_bounds__(256) quant_pack_kernel(const int32_t* __restrict__ Y, int M, int N,
-                                                         int Nw, Epi e, uint32_t* __restrict__ out,
-                                                         bool vec) {
-    const long long total = (long long)M * Nw;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const int m = (int)(idx / Nw);
-        const int w = (int)(idx - (long long)m * Nw);
-        const int n0 = w * 32;
-        uint32_t qb[8];  // 32 codes, 4 per word (byte i of qb[q] = code of column n0+4q+i)
+// ---------------------------------------------------------------------------------------
+// The element-wise routines (unfused forms of the epilogue):
+//   quant_pack      q = requant(alpha*y + beta)                      (apnn_quant_pack_out)
+//   pool_quant_pack q = requant(pool_kxk(alpha*y + beta))            (R15)
+//   residual        q = requant(alpha*y + beta + rho*z)              (reading R24)
+// all writing packed planes [rows][ob][Nw].  Work split: a warp owns ONE output word column
+// w (32 consecutive channels, lane = channel: coalesced 128-byte loads of int32 rows) and
+// walks the rows r0, r0 + rstride, ... (kRows of them in flight), so the per-channel
+// parameters are loaded once per warp; each plane word is one __ballot_sync (the paper's
+// ballot packing).  Only words that hold channels are walked; the
+// warp of the last one also writes the row's zero padding words.  The host sizes the grid
+// so that the number of warps is a multiple of the word count.
+constexpr int kRows = 4;
+
+struct WordWalk {
+    int w, r0, rstride;
+};
+__device__ __forceinline__ WordWalk word_walk(int Nd) {
+    const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+    return WordWalk{gw % Nd, gw / Nd, nwarps / Nd};
+}
+
+// Requantisation constants of one launch: q = clamp(floor(v / S), 0, qmax) of an int64 v.
+struct QuantK {
+    long long lim;  // (qmax + 1) * S: v >= lim -> qmax
+    uint32_t S, qmax;
+    float invS;
+};
+static QuantK quant_k(const Epi& e) {
+    return QuantK{(long long)(e.qmax + 1) * e.S, (uint32_t)e.S, (uint32_t)e.qmax, e.invS};
+}
+// FAST (host: lim <= 2^32): the in-range v fits 32 bits and an fp32 estimate is within one
+// of the floor (relative error < 2^-22 on q <= 255), fixed by one exact integer correction.
+template <bool FAST>
+__device__ __forceinline__ uint32_t quant_v(long long v, const QuantK& k, const Epi& e) {
+    if (v < 0) return 0u;
+    if (v >= k.lim) return k.qmax;
+    if (!FAST) return quantise_v(e, v);
+    const uint32_t u = (uint32_t)v;
+    uint32_t q = __float2uint_rz(__uint2float_rn(u) * k.invS);
+    const int32_t r = (int32_t)(u - q * k.S);
+    return r < 0 ? q - 1 : (r >= (int32_t)k.S ? q + 1 : q);
+}
+
+// planes of 32 lanes' codes -> lane t < ob stores plane t's word of this row; with
+// pad_words > 0 (the row's last data word) lanes also zero the words w+1 .. w+pad_words
+template <int OB>
+__device__ __forceinline__ void ballot_store(uint32_t q, int lane, int ob, uint32_t* row_words, int Nw,
+                                             int pad_words) {
+    const int nb = OB > 0 ? OB : ob;
+    uint32_t mine = 0;
 #pragma unroll
-        for (int q = 0; q < 8; q++) qb[q] = 0;
-        if (n0 < N) {
-            const int32_t* src = Y + (long long)m * N + n0;
-            if (vec && n0 + 32 <= N) {
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    int4 v = __ldg(reinterpret_cast<const int4*>(src) + q);
-                    int n = n0 + 4 * q;
-                    qb[q] = requant(e, v.x, epi_alpha(e, n), epi_beta(e, n)) |
-                            (requant(e, v.y, epi_alpha(e, n + 1), epi_beta(e, n + 1)) << 8) |
-                            (requant(e, v.z, epi_alpha(e, n + 2), epi_beta(e, n + 2)) << 16) |
-                            (requant(e, v.w, epi_alpha(e, n + 3), epi_beta(e, n + 3)) << 24);
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; i++) {  // static qb[] indices: no local-memory array
-                    int n = n0 + i;
-                    if (n < N) qb[i >> 2] |= requant(e, __ldg(src + i), epi_alpha(e, n), epi_beta(e, n))
-                                             << (8 * (i & 3));
-                }
-            }
+    for (int t = 0; t < 8; t++) {
+        if (t < nb) {
+            const uint32_t word = __ballot_sync(0xFFFFFFFFu, (q >> t) & 1u);
+            if (lane == t) mine = word;
         }
-        uint32_t* o = out + (long long)m * e.out_bits * Nw + w;
-        for (int t = 0; t < e.out_bits; t++) {
-            uint32_t word = 0;
+    }
+    if (lane < nb) row_words[(long long)lane * Nw] = mine;
+    for (int i = lane; i < pad_words * nb; i += 32) row_words[(long long)(i / pad_words) * Nw + 1 + i % pad_words] = 0u;
+}
+
+template <bool FAST, int OB>
+__global__ void __launch_bounds__(256) quant_pack_kernel(const int32_t* __restrict__ Y, int M, int N, int Nd,
+                                                         int Nw, Epi e, QuantK qk, uint32_t* __restrict__ out) {
+    const WordWalk k = word_walk(Nd);
+    const int lane = threadIdx.x & 31, n = k.w * 32 + lane, ob = OB > 0 ? OB : e.out_bits;
+    const bool valid = n < N;
+    const int32_t al = valid ? epi_alpha(e, n) : 0, be = valid ? epi_beta(e, n) : 0;
+    const int pad = k.w == Nd - 1 ? Nw - Nd : 0;
+    for (int r = k.r0; r < M; r += kRows * k.rstride) {
+        int32_t y[kRows];
 #pragma unroll
-            for (int q = 0; q < 8; q++) word |= byte_bits_to_nibble(qb[q], t) << (4 * q);
-            o[(long long)t * Nw] = word;
+        for (int u = 0; u < kRows; u++) {
+            const int row = r + u * k.rstride;
+            y[u] = (valid && row < M) ? __ldg(Y + (long long)row * N + n) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kRows; u++) {
+            const int row = r + u * k.rstride;
+            if (row >= M) break;  // warp-uniform
+            const uint32_t q = valid ? quant_v<FAST>((long long)al * y[u] + be, qk, e) : 0u;
+            ballot_store<OB>(q, lane, ob, out + (long long)row * ob * Nw + k.w, Nw, pad);
         }
     }
 }
 
-// Y [B][H][W][N] int32 (NHWC conv output) -> out [B*Hp*Wp][ob][Nw]: k x k pooling of
-// v = alpha*y + beta (max, or floor of the average), then quantisation and packing
-// (reading R15).  One warp per (pooled pixel, output word):
-// lane = channel (coalesced 128-byte loads, k*k independent loads per lane), and the
-// plane words are formed with __ballot_sync as in the paper's output packing
-// (PAPER.md:1582-1587).
-template <int KP>  // KP > 0: compile-time window (unrolled, all loads in flight); 0: runtime e.pool
+// Y [B][H][W][N] (NHWC conv output) -> pooled rows [B*Hp*Wp].  Max pooling of v = alpha*y + beta
+// is alpha*max(y) + beta for alpha >= 0 and alpha*min(y) + beta otherwise (v is monotone in y):
+// the window is reduced in 32-bit and v is formed once per output.  Average: floor of
+// (alpha*sum(y) + k*k*beta) / (k*k) (reading R15).
+template <int KP, bool FAST, int OB>
 __global__ void __launch_bounds__(256) pool_quant_pack_kernel(const int32_t* __restrict__ Y, int B, int H, int W,
-                                                              int N, int Hp, int Wp, int Nw, Epi e,
-                                                              uint32_t* __restrict__ out) {
-    const int total = B * Hp * Wp * Nw;  // warps of work (host-checked < 2^31)
-    const int k = KP > 0 ? KP : e.pool, st = e.pool_stride;
-    const int lane = threadIdx.x & 31;
-    const int wstride = gridDim.x * (blockDim.x >> 5);
-    constexpr int IT = 1;  // work items per warp iteration (4 measured slower: 973 -> 1160 us on the ResNet stem)
-    for (int idx0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); idx0 < total; idx0 += IT * wstride) {
-        long long P[IT];
-        int pixv[IT], wv[IT];
+                                                              int N, int Hp, int Wp, int Nd, int Nw, Epi e,
+                                                              QuantK qk, uint32_t* __restrict__ out) {
+    const WordWalk k = word_walk(Nd);
+    const int lane = threadIdx.x & 31, n = k.w * 32 + lane, ob = OB > 0 ? OB : e.out_bits;
+    const bool valid = n < N;
+    const int32_t al = valid ? epi_alpha(e, n) : 0, be = valid ? epi_beta(e, n) : 0;
+    const int kp = KP > 0 ? KP : e.pool, st = e.pool_stride;
+    const int pad = k.w == Nd - 1 ? Nw - Nd : 0;
+    const int P = B * Hp * Wp;
+    const bool avg = e.pool_avg != 0;
+    for (int r = k.r0; r < P; r += kRows * k.rstride) {
+        int32_t ysel[kRows];  // max (alpha >= 0) or min (alpha < 0) of the window
+        long long ysum[kRows];
 #pragma unroll
-        for (int u = 0; u < IT; u++) {
-            const int idx = idx0 + u * wstride;
-            const int pix = idx / Nw;
-            const int w = idx - pix * Nw;
-            pixv[u] = pix;
-            wv[u] = w;
-            P[u] = 0;
-            const int n = w * 32 + lane;
-            if (idx < total && n < N) {
-                const int b = pix / (Hp * Wp);
-                const int rem = pix - b * Hp * Wp;
+        for (int u = 0; u < kRows; u++) {
+            const int pix = r + u * k.rstride;
+            ysel[u] = 0;
+            ysum[u] = 0;
+            if (valid && pix < P) {
+                const int b = pix / (Hp * Wp), rem = pix - b * Hp * Wp;
                 const int i = rem / Wp, j = rem - (rem / Wp) * Wp;
-                const long long al = epi_alpha(e, n), be = epi_beta(e, n);
                 const int32_t* base = Y + (((long long)b * H + i * st) * W + j * st) * N + n;
-                long long best = 0, sum = 0;
+                int32_t mx = INT32_MIN, mn = INT32_MAX;
+                long long sm = 0;
 #pragma unroll
-                for (int rr = 0; rr < k; rr++) {
+                for (int rr = 0; rr < kp; rr++) {  // kp is the constant KP in the KP > 0 instances
 #pragma unroll
-                    for (int ss = 0; ss < k; ss++) {
-                        const long long v = al * __ldg(base + ((long long)rr * W + ss) * N) + be;
-                        best = (rr == 0 && ss == 0) ? v : (v > best ? v : best);
-                        sum += v;
+                    for (int ss = 0; ss < kp; ss++) {
+                        const int32_t yv = __ldg(base + ((long long)rr * W + ss) * N);
+                        mx = max(mx, yv);
+                        mn = min(mn, yv);
+                        if (avg) sm += yv;
                     }
                 }
-                P[u] = best;
-                if (e.pool_avg) {
-                    const long long kk = (long long)k * k;
-                    long long a = sum / kk;
-                    if (sum % kk != 0 && sum < 0) a -= 1;  // floor toward -inf
-                    P[u] = a;
-                }
+                ysel[u] = al >= 0 ? mx : mn;
+                ysum[u] = sm;
             }
         }
 #pragma unroll
-        for (int u = 0; u < IT; u++) {
-            const int idx = idx0 + u * wstride;
-            if (idx >= total) break;  // warp-uniform
-            const int n = wv[u] * 32 + lane;
-            const uint32_t q = n < N ? quantise_v(e, P[u]) : 0u;
-            uint32_t mine = 0;
-#pragma unroll
-            for (int t = 0; t < 8; t++) {
-                if (t < e.out_bits) {
-                    const uint32_t word = __ballot_sync(0xFFFFFFFFu, (q >> t) & 1u);
-                    if (lane == t) mine = word;
+        for (int u = 0; u < kRows; u++) {
+            const int pix = r + u * k.rstride;
+            if (pix >= P) break;  // warp-uniform
+            uint32_t q = 0;
+            if (valid) {
+                long long v;
+                if (avg) {
+                    const long long kk = (long long)kp * kp, t = (long long)al * ysum[u] + kk * be;
+                    v = t / kk;
+                    if (t % kk != 0 && t < 0) v -= 1;  // floor toward -inf
+                } else {
+                    v = (long long)al * ysel[u] + be;
                 }
+                q = quant_v<FAST>(v, qk, e);
             }
-            if (lane < e.out_bits) out[((long long)pixv[u] * e.out_bits + lane) * Nw + wv[u]] = mine;
+            ballot_store<OB>(q, lane, ob, out + (long long)pix * ob * Nw + k.w, Nw, pad);
         }
     }
 }
 
-// Vectorised pooling routine (N % 4 == 0): a warp handles 128 channels (4 output words) of one
-// pooled pixel, lane = 4 consecutive channels (one 16-byte load per window element: 4x fewer
-// load and index instructions than one channel per lane).  The 4 codes of a lane form one
-// nibble per plane; 8 lanes' nibbles are OR-combined with xor-shuffles into a plane word.
-template <int KP>
-__global__ void __launch_bounds__(256) pool_quant_pack_v4_kernel(const int32_t* __restrict__ Y, int B, int H,
-                                                                 int W, int N, int Hp, int Wp, int Nw, Epi e,
-                                                                 uint32_t* __restrict__ out) {
-    const int Ng = (Nw + 3) / 4;                  // 128-channel groups per pixel
-    const int total = B * Hp * Wp * Ng;           // warp items (host-checked < 2^31)
-    const int k = KP > 0 ? KP : e.pool, st = e.pool_stride;
-    const int lane = threadIdx.x & 31;
-    const int wstride = gridDim.x * (blockDim.x >> 5);
-    for (int idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); idx < total; idx += wstride) {
-        const int pix = idx / Ng;
-        const int grp = idx - pix * Ng;
-        const int b = pix / (Hp * Wp);
-        const int rem = pix - b * Hp * Wp;
-        const int i = rem / Wp, j = rem - (rem / Wp) * Wp;
-        const int n = grp * 128 + lane * 4;       // first of this lane's 4 channels
-        uint32_t q4 = 0;                          // 4 codes, byte c = code of channel n + c
-        if (n < N) {
-            const int32_t* base = Y + (((long long)b * H + i * st) * W + j * st) * N + n;
-            long long best[4], sum[4];
+// shortcut z: int32 [M][N] (ZB = 0) or packed codes [M][z_bits][Nw] (ZB = -1: runtime z_bits)
+template <bool FAST, int OB, int ZB>
+__global__ void __launch_bounds__(256) residual_quant_pack_kernel(const int32_t* __restrict__ Y, int M, int N,
+                                                                  const void* __restrict__ Z, int z_bits,
+                                                                  const int32_t* __restrict__ rho, int Nd, int Nw,
+                                                                  Epi e, QuantK qk, uint32_t* __restrict__ out) {
+    const WordWalk k = word_walk(Nd);
+    const int lane = threadIdx.x & 31, n = k.w * 32 + lane, ob = OB > 0 ? OB : e.out_bits;
+    const bool valid = n < N;
+    const int32_t al = valid ? epi_alpha(e, n) : 0, be = valid ? epi_beta(e, n) : 0;
+    const int32_t rh = valid ? (rho ? __ldg(rho + n) : 1) : 0;
+    const int pad = k.w == Nd - 1 ? Nw - Nd : 0;
+    const int32_t* Zi = reinterpret_cast<const int32_t*>(Z);
+    const uint32_t* Zp = reinterpret_cast<const uint32_t*>(Z);
+    for (int r = k.r0; r < M; r += kRows * k.rstride) {
+        int32_t y[kRows];
+        uint32_t zw[kRows];  // ZB != 0: lane t < z_bits holds plane t's word of the row
+        int32_t zi[kRows];
 #pragma unroll
-            for (int rr = 0; rr < k; rr++) {
-#pragma unroll
-                for (int ss = 0; ss < k; ss++) {
-                    const int4 y = __ldg(reinterpret_cast<const int4*>(base + ((long long)rr * W + ss) * N));
-                    const int32_t yy[4] = {y.x, y.y, y.z, y.w};
-#pragma unroll
-                    for (int c = 0; c < 4; c++) {
-                        const long long v = (long long)epi_alpha(e, n + c) * yy[c] + epi_beta(e, n + c);
-                        if (rr == 0 && ss == 0) { best[c] = v; sum[c] = v; }
-                        else { best[c] = v > best[c] ? v : best[c]; sum[c] += v; }
-                    }
+        for (int u = 0; u < kRows; u++) {
+            const int row = r + u * k.rstride;
+            y[u] = zi[u] = 0;
+            zw[u] = 0;
+            if (row < M) {
+                if (valid) y[u] = __ldg(Y + (long long)row * N + n);
+                if (ZB == 0) {
+                    if (valid) zi[u] = __ldg(Zi + (long long)row * N + n);
+                } else if (lane < z_bits) {
+                    zw[u] = __ldg(Zp + ((long long)row * z_bits + lane) * Nw + k.w);
                 }
-            }
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                long long P = best[c];
-                if (e.pool_avg) {
-                    const long long kk = (long long)k * k;
-                    P = sum[c] / kk;
-                    if (sum[c] % kk != 0 && sum[c] < 0) P -= 1;  // floor toward -inf
-                }
-                q4 |= quantise_v(e, P) << (8 * c);
             }
         }
-        const int w = grp * 4 + (lane >> 3);      // output word of this lane's channels
 #pragma unroll
-        for (int t = 0; t < 8; t++) {
-            if (t < e.out_bits) {
-                uint32_t nib = byte_bits_to_nibble(q4, t) << (4 * (lane & 7));
-                nib |= __shfl_xor_sync(0xFFFFFFFFu, nib, 1);
-                nib |= __shfl_xor_sync(0xFFFFFFFFu, nib, 2);
-                nib |= __shfl_xor_sync(0xFFFFFFFFu, nib, 4);
-                if ((lane & 7) == 0 && w < Nw) out[((long long)pix * e.out_bits + t) * Nw + w] = nib;
+        for (int u = 0; u < kRows; u++) {
+            const int row = r + u * k.rstride;
+            if (row >= M) break;  // warp-uniform
+            int32_t z = zi[u];
+            if (ZB != 0) {  // this lane's code: bit `lane` of every plane word (shuffled from lane t)
+                uint32_t code = 0;
+#pragma unroll
+                for (int t = 0; t < 8; t++) {
+                    if (t < z_bits) code |= ((__shfl_sync(0xFFFFFFFFu, zw[u], t) >> lane) & 1u) << t;
+                }
+                z = (int32_t)code;
             }
+            const uint32_t q = valid ? quant_v<FAST>((long long)al * y[u] + be + (long long)rh * z, qk, e) : 0u;
+            ballot_store<OB>(q, lane, ob, out + (long long)row * ob * Nw + k.w, Nw, pad);
         }
     }
+}
+
+static int stream_grid(long long total, int sms) {
+    long long blocks = (total + 255) / 256;
+    long long cap = (long long)sms * 8;  // 8 resident 256-thread CTAs per SM, grid-stride beyond
+    if (blocks > cap) blocks = cap;
+    return (int)(blocks < 1 ? 1 : blocks);
+}
+
+// grid for the word-walk routines: enough warps to cover rows x Nd (capped at 8 CTAs per SM),
+// rounded up to a multiple of Nd CTAs so the warp count is a multiple of Nd
+static int word_grid(long long rows, int Nd, int sms) {
+    long long blocks = (rows * Nd + 7) / 8;
+    const long long cap = (long long)sms * 8;
+    if (blocks > cap) blocks = cap;
+    blocks = (blocks + Nd - 1) / Nd * Nd;
+    return (int)(blocks < Nd ? Nd : blocks);
+}
+
+static bool quant_fast(const Epi& e) {
+    return (unsigned long long)(e.qmax + 1) * (unsigned long long)e.S <= 0x100000000ull;
+}
+
+cudaError_t launch_quant_pack(const int32_t* Y, int M, int N, const Epi& e, uint32_t* out, int sms,
+                              cudaStream_t s) {
+    const int Nw = (N + 127) / 128 * 4, Nd = (N + 31) / 32;
+    if ((long long)M * Nw == 0) return cudaSuccess;
+    const int grid = word_grid(M, Nd, sms);
+    const QuantK qk = quant_k(e);
+#define APNN_QP(F_, OB_) quant_pack_kernel<F_, OB_><<<grid, 256, 0, s>>>(Y, M, N, Nd, Nw, e, qk, out)
+    if (!quant_fast(e)) APNN_QP(false, 0);
+    else if (e.out_bits == 2) APNN_QP(true, 2);
+    else if (e.out_bits == 8) APNN_QP(true, 8);
+    else APNN_QP(true, 0);
+#undef APNN_QP
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pool_quant_pack(const int32_t* Y, int B, int H, int W, int N, const Epi& e, uint32_t* out,
+                                  int sms, cudaStream_t s) {
+    const int Hp = (H - e.pool) / e.pool_stride + 1, Wp = (W - e.pool) / e.pool_stride + 1;
+    const int Nw = (N + 127) / 128 * 4, Nd = (N + 31) / 32;
+    const long long rows = (long long)B * Hp * Wp;
+    if (rows * Nw == 0) return cudaSuccess;
+    if (rows > 2147483647LL) return cudaErrorInvalidValue;
+    const int grid = word_grid(rows, Nd, sms);
+    const QuantK qk = quant_k(e);
+    const bool f = quant_fast(e);
+#define APNN_POOL(KP_, F_, OB_) \
+    pool_quant_pack_kernel<KP_, F_, OB_><<<grid, 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nd, Nw, e, qk, out)
+    if (!f) APNN_POOL(0, false, 0);
+    else if (e.pool == 2 && e.out_bits == 2) APNN_POOL(2, true, 2);
+    else if (e.pool == 2 && e.out_bits == 8) APNN_POOL(2, true, 8);
+    else if (e.pool == 3 && e.out_bits == 2) APNN_POOL(3, true, 2);
+    else if (e.pool == 2) APNN_POOL(2, true, 0);
+    else if (e.pool == 3) APNN_POOL(3, true, 0);
+    else APNN_POOL(0, true, 0);
+#undef APNN_POOL
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_residual_quant_pack(const int32_t* Y, int M, int N, const void* Z, int z_bits,
+                                       const int32_t* rho, const Epi& e, uint32_t* out, int sms, cudaStream_t s) {
+    const int Nw = (N + 127) / 128 * 4, Nd = (N + 31) / 32;
+    if ((long long)M * Nw == 0) return cudaSuccess;
+    const int grid = word_grid(M, Nd, sms);
+    const QuantK qk = quant_k(e);
+#define APNN_RES(F_, OB_, ZB_) \
+    residual_quant_pack_kernel<F_, OB_, ZB_><<<grid, 256, 0, s>>>(Y, M, N, Z, z_bits, rho, Nd, Nw, e, qk, out)
+    if (!quant_fast(e)) { if (z_bits) APNN_RES(false, 0, -1); else APNN_RES(false, 0, 0); }
+    else if (e.out_bits == 8) { if (z_bits) APNN_RES(true, 8, -1); else APNN_RES(true, 8, 0); }
+    else if (e.out_bits == 2) { if (z_bits) APNN_RES(true, 2, -1); else APNN_RES(true, 2, 0); }
+    else { if (z_bits) APNN_RES(true, 0, -1); else APNN_RES(true, 0, 0); }
+#undef APNN_RES
+    count_launch();
+    return cudaGetLastError();
 }
 
 // im2col + bit decomposition + packing of NHWC uint8 codes.  One CTA per output image
@@ -360,134 +464,6 @@ __global__ void __launch_bounds__(256) flatten_packed_kernel(const uint32_t* __r
     }
 }
 
-// Residual routine: one warp per (row, 32-column word), lane = column (coalesced int32
-// loads), ballot packing.  v = alpha*y + beta + rho*z in int64 (reading R24).  Each warp
-// takes kItems work items per iteration and issues all their loads before any math
-// (the kernel is latency-bound otherwise).
-constexpr int kItems = 4;
-__global__ void __launch_bounds__(256) residual_quant_pack_kernel(const int32_t* __restrict__ Y, int M, int N,
-                                                                  const void* __restrict__ Z, int z_bits,
-                                                                  const int32_t* __restrict__ rho, int Nw, Epi e,
-                                                                  uint32_t* __restrict__ out) {
-    const int total = M * Nw;  // host-checked < 2^31: 32-bit index math
-    const int lane = threadIdx.x & 31;
-    const int wstride = gridDim.x * (blockDim.x >> 5);
-    for (int idx0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); idx0 < total; idx0 += kItems * wstride) {
-        int32_t y[kItems];
-        long long z[kItems];
-        int mm[kItems], ww[kItems];
-#pragma unroll
-        for (int u = 0; u < kItems; u++) {
-            const int idx = idx0 + u * wstride;
-            mm[u] = idx / Nw;
-            ww[u] = idx - mm[u] * Nw;
-            const int n = ww[u] * 32 + lane;
-            y[u] = 0;
-            z[u] = 0;
-            if (idx < total && n < N) {
-                const long long m = mm[u];
-                y[u] = __ldg(Y + m * N + n);
-                if (z_bits == 0) {
-                    z[u] = __ldg(reinterpret_cast<const int32_t*>(Z) + m * N + n);
-                } else {
-                    const uint32_t* zp = reinterpret_cast<const uint32_t*>(Z) + m * z_bits * Nw + ww[u];
-                    uint32_t code = 0;
-#pragma unroll
-                    for (int t = 0; t < 8; t++)
-                        if (t < z_bits) code |= ((__ldg(zp + (long long)t * Nw) >> lane) & 1u) << t;
-                    z[u] = code;
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kItems; u++) {
-            const int idx = idx0 + u * wstride;
-            if (idx >= total) break;  // warp-uniform
-            const int n = ww[u] * 32 + lane;
-            uint32_t q = 0;
-            if (n < N) {
-                const long long r = rho ? __ldg(rho + n) : 1;
-                q = quantise_v(e, (long long)epi_alpha(e, n) * y[u] + epi_beta(e, n) + r * z[u]);
-            }
-            uint32_t mine = 0;
-#pragma unroll
-            for (int t = 0; t < 8; t++) {
-                if (t < e.out_bits) {
-                    const uint32_t word = __ballot_sync(0xFFFFFFFFu, (q >> t) & 1u);
-                    if (lane == t) mine = word;
-                }
-            }
-            if (lane < e.out_bits) out[((long long)mm[u] * e.out_bits + lane) * Nw + ww[u]] = mine;
-        }
-    }
-}
-
-// Vectorised residual routine (N % 4 == 0): warp = one row's 128 channels, lane = 4
-// consecutive channels (16-byte loads of Y and of an int32 shortcut; packed-code shortcut: the
-// lane's 4 bits of each plane word), nibbles OR-combined over 8 lanes into plane words.
-__global__ void __launch_bounds__(256) residual_quant_pack_v4_kernel(const int32_t* __restrict__ Y, int M, int N,
-                                                                     const void* __restrict__ Z, int z_bits,
-                                                                     const int32_t* __restrict__ rho, int Nw, Epi e,
-                                                                     uint32_t* __restrict__ out) {
-    const int Ng = Nw / 4;
-    const int total = M * Ng;  // host-checked < 2^31
-    const int lane = threadIdx.x & 31;
-    const int wstride = gridDim.x * (blockDim.x >> 5);
-    for (int idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); idx < total; idx += wstride) {
-        const int mi = idx / Ng;
-        const int grp = idx - mi * Ng;
-        const long long m = mi;
-        const int n = grp * 128 + lane * 4;
-        const int w = grp * 4 + (lane >> 3);
-        uint32_t q4 = 0;
-        if (n < N) {
-            const int4 y = __ldg(reinterpret_cast<const int4*>(Y + m * N + n));
-            int32_t z[4];
-            if (z_bits == 0) {
-                const int4 zz = __ldg(reinterpret_cast<const int4*>(reinterpret_cast<const int32_t*>(Z) + m * N + n));
-                z[0] = zz.x; z[1] = zz.y; z[2] = zz.z; z[3] = zz.w;
-            } else {
-                const uint32_t* zp = reinterpret_cast<const uint32_t*>(Z) + m * z_bits * Nw + w;
-                const int sh = (lane & 7) * 4;
-                uint32_t nib[8];
-#pragma unroll
-                for (int t = 0; t < 8; t++) nib[t] = t < z_bits ? (__ldg(zp + (long long)t * Nw) >> sh) & 0xFu : 0u;
-#pragma unroll
-                for (int c = 0; c < 4; c++) {
-                    uint32_t code = 0;
-#pragma unroll
-                    for (int t = 0; t < 8; t++) code |= ((nib[t] >> c) & 1u) << t;
-                    z[c] = (int32_t)code;
-                }
-            }
-            const int32_t yy[4] = {y.x, y.y, y.z, y.w};
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                const long long r = rho ? __ldg(rho + n + c) : 1;
-                const long long v = (long long)epi_alpha(e, n + c) * yy[c] + epi_beta(e, n + c) + r * z[c];
-                q4 |= quantise_v(e, v) << (8 * c);
-            }
-        }
-#pragma unroll
-        for (int t = 0; t < 8; t++) {
-            if (t < e.out_bits) {
-                uint32_t nb = byte_bits_to_nibble(q4, t) << (4 * (lane & 7));
-                nb |= __shfl_xor_sync(0xFFFFFFFFu, nb, 1);
-                nb |= __shfl_xor_sync(0xFFFFFFFFu, nb, 2);
-                nb |= __shfl_xor_sync(0xFFFFFFFFu, nb, 4);
-                if ((lane & 7) == 0) out[(m * e.out_bits + t) * Nw + w] = nb;
-            }
-        }
-    }
-}
-
-static int stream_grid(long long total, int sms) {
-    long long blocks = (total + 255) / 256;
-    long long cap = (long long)sms * 8;  // 8 resident 256-thread CTAs per SM, grid-stride beyond
-    if (blocks > cap) blocks = cap;
-    return (int)(blocks < 1 ? 1 : blocks);
-}
-
 cudaError_t launch_pack_bits(const uint8_t* codes, int rows, int K, int bits, uint32_t* dst,
                              int sms, cudaStream_t s) {
     const int Kw = (K + 127) / 128 * 4;
@@ -498,53 +474,6 @@ cudaError_t launch_pack_bits(const uint8_t* codes, int rows, int K, int bits, ui
         pack_bits_kernel<true><<<stream_grid(total, sms), 256, 0, s>>>(codes, rows, K, bits, Kw, dst);
     else
         pack_bits_kernel<false><<<stream_grid(total, sms), 256, 0, s>>>(codes, rows, K, bits, Kw, dst);
-    count_launch();
-    return cudaGetLastError();
-}
-
-cudaError_t launch_quant_pack(const int32_t* Y, int M, int N, const Epi& e, uint32_t* out, int sms,
-                              cudaStream_t s) {
-    const int Nw = (N + 127) / 128 * 4;
-    const long long total = (long long)M * Nw;
-    if (total == 0) return cudaSuccess;
-    const bool vec = (N % 4 == 0) && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
-    quant_pack_kernel<<<stream_grid(total, sms), 256, 0, s>>>(Y, M, N, Nw, e, out, vec);
-    count_launch();
-    return cudaGetLastError();
-}
-
-}  // namespace apnn
-
-namespace apnn {
-static bool pool_v4_enabled() {  // experiment knob APNN_POOL_V4=0: one channel per lane
-    static int v = -1;
-    if (v < 0) {
-        const char* s = getenv("APNN_POOL_V4");
-        v = s ? atoi(s) : 1;
-    }
-    return v != 0;
-}
-
-cudaError_t launch_pool_quant_pack(const int32_t* Y, int B, int H, int W, int N, const Epi& e, uint32_t* out,
-                                  int sms, cudaStream_t s) {
-    const int Hp = (H - e.pool) / e.pool_stride + 1, Wp = (W - e.pool) / e.pool_stride + 1;
-    const int Nw = (N + 127) / 128 * 4;
-    const long long total = (long long)B * Hp * Wp * Nw;
-    if (total == 0) return cudaSuccess;
-    if ((long long)B * Hp * Wp * Nw > 2147483647LL) return cudaErrorInvalidValue;
-    const int grid = stream_grid(total * 32, sms);
-    if (N % 4 == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0 && pool_v4_enabled()) {
-        const long long items = (long long)B * Hp * Wp * ((Nw + 3) / 4);
-        const int g4 = stream_grid(items * 32, sms);
-        if (e.pool == 2) pool_quant_pack_v4_kernel<2><<<g4, 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nw, e, out);
-        else if (e.pool == 3) pool_quant_pack_v4_kernel<3><<<g4, 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nw, e, out);
-        else pool_quant_pack_v4_kernel<0><<<g4, 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nw, e, out);
-        count_launch();
-        return cudaGetLastError();
-    }
-    if (e.pool == 2) pool_quant_pack_kernel<2><<<grid, 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nw, e, out);
-    else if (e.pool == 3) pool_quant_pack_kernel<3><<<grid, 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nw, e, out);
-    else pool_quant_pack_kernel<0><<<grid, 256, 0, s>>>(Y, B, H, W, N, Hp, Wp, Nw, e, out);
     count_launch();
     return cudaGetLastError();
 }
@@ -582,22 +511,3 @@ cudaError_t launch_flatten_packed(const uint32_t* src, int B, int P, int bits, i
 }
 }  // namespace apnn
 
-namespace apnn {
-cudaError_t launch_residual_quant_pack(const int32_t* Y, int M, int N, const void* Z, int z_bits,
-                                       const int32_t* rho, const Epi& e, uint32_t* out, int sms, cudaStream_t s) {
-    const int Nw = (N + 127) / 128 * 4;
-    const long long total = (long long)M * Nw;
-    if (total == 0) return cudaSuccess;
-    if (total > 2147483647LL) return cudaErrorInvalidValue;
-    if (N % 4 == 0 && ((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(Z)) & 15) == 0 &&
-        pool_v4_enabled()) {
-        residual_quant_pack_v4_kernel<<<stream_grid((long long)M * (Nw / 4) * 32, sms), 256, 0, s>>>(
-            Y, M, N, Z, z_bits, rho, Nw, e, out);
-        count_launch();
-        return cudaGetLastError();
-    }
-    residual_quant_pack_kernel<<<stream_grid(total * 32, sms), 256, 0, s>>>(Y, M, N, Z, z_bits, rho, Nw, e, out);
-    count_launch();
-    return cudaGetLastError();
-}
-}  // namespace apnn
