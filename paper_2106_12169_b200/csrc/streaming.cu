@@ -352,28 +352,34 @@ cudaError_t launch_residual_quant_pack(const int32_t* Y, int M, int N, const voi
 
 // im2col + bit decomposition + packing of NHWC uint8 codes.  One CTA per output image
 // row (b, ho): the R input rows it needs are staged in shared memory with the zero
-// padding materialised (R x (W + 2 pad) x C bytes, coalesced 4-byte loads), then each
-// thread packs (pixel wo, word w) tasks: 32 consecutive elements k = (r*S + s)*C + c
-// walked with incremental counters (no per-element division), one shared-memory byte
-// read and `bits` shift-ors each; the CTA's Wo output rows are one contiguous range,
-// so the words are staged in shared memory and written out coalesced.
-// qs > 0: X is the raw 8-bit image and every element is quantised while it is staged,
-// q = clamp(floor((x - qz) / qs), 0, 2^bits - 1) (the first layer's quantisation of the
-// 8-bit input, with the quantisation formula of PAPER.md:1283-1287);
-// out-of-frame taps stay code 0 (zero padding of the conv input).  qs = 0: X holds codes.
+// padding materialised (R x (W + 2 pad) x C bytes); qs > 0 quantises the raw 8-bit image
+// while staging, q = clamp(floor((x - qz) / qs), 0, 2^bits - 1) (the first layer's
+// quantisation of the 8-bit input, formula PAPER.md:1283-1287;
+// out-of-frame taps stay code 0).  An offset table built once per CTA maps element
+// k = (r*S + s)*C + c of a row to its staged byte for wo = 0 (k >= K -> a zero byte), so a
+// task (pixel wo, word w) is 32 table-driven byte loads, then the plane words: shift-ors
+// for <= 4 bits, 8x8 bit-matrix transposes above.  The CTA's Wo output rows are one
+// contiguous range: words are staged in shared memory and written out coalesced.
 __global__ void __launch_bounds__(256) im2col_pack_kernel(const uint8_t* __restrict__ X, int B, int H, int W,
                                                           int C, int R, int S, int stride, int pad, int Ho, int Wo,
                                                           int bits, int Kw, uint32_t* __restrict__ dst, int qz,
                                                           int qs) {
     extern __shared__ __align__(16) uint8_t sm[];
     const int Wp = W + 2 * pad, rowb = Wp * C;       // padded input row bytes
-    uint8_t* rows = sm;                              // R x rowb
-    uint32_t* outw = reinterpret_cast<uint32_t*>(sm + ((R * rowb + 15) & ~15));  // Wo x bits x Kw
-    const int K = R * S * C;
+    const int Kp = Kw * 32, K = R * S * C, SC = S * C;
+    uint8_t* rows = sm;                              // R x rowb, then one zero byte
+    const int zero_off = R * rowb;
+    int32_t* tab = reinterpret_cast<int32_t*>(sm + ((R * rowb + 1 + 15) & ~15));            // Kp offsets
+    uint32_t* outw = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(tab) + Kp * 4);   // Wo x bits x Kw
     const uint32_t keep = (1u << bits) - 1u;
+    for (int k = threadIdx.x; k < Kp; k += blockDim.x) {
+        const int r = k / SC, j = k - r * SC;
+        tab[k] = k < K ? r * rowb + j : -1;  // -1: the zero byte (wo-independent)
+    }
+    if (threadIdx.x == 0) rows[zero_off] = 0;
     for (int br = blockIdx.x; br < B * Ho; br += gridDim.x) {
         const int b = br / Ho, ho = br - b * Ho;
-        __syncthreads();  // previous row's smem readers are done
+        __syncthreads();  // previous row's smem readers are done (and the table is built)
         for (int i = threadIdx.x; i < R * Wp; i += blockDim.x) {  // one padded pixel (C bytes) per step
             const int r = i / Wp, px = i - r * Wp;
             const int hi = ho * stride - pad + r, wi = px - pad;
@@ -396,21 +402,17 @@ __global__ void __launch_bounds__(256) im2col_pack_kernel(const uint8_t* __restr
         __syncthreads();
         for (int task = threadIdx.x; task < Wo * Kw; task += blockDim.x) {
             const int wo = task / Kw, w = task - wo * Kw;
-            // for a filter row r the S*C codes of the window are one contiguous smem run:
-            // element k = r*S*C + j sits at byte r*rowb + wo*stride*C + j
-            const int SC = S * C;
-            int k = w * 32;
-            int r = k / SC, j = k - r * SC;
-            const uint8_t* base = rows + wo * stride * C;
-            int off = r * rowb + j;
+            const int base = wo * stride * C;
+            const int4* t4 = reinterpret_cast<const int4*>(tab + w * 32);
             uint32_t qb[8];  // byte i of qb[j] = code of element 4j + i (as in pack_bits_kernel)
 #pragma unroll
-            for (int q = 0; q < 8; q++) qb[q] = 0;
-#pragma unroll
-            for (int e = 0; e < 32; e++) {
-                if (k + e < K) qb[e >> 2] |= (uint32_t)base[off] << (8 * (e & 3));
-                off++;
-                if (++j == SC) { j = 0; off += rowb - SC; }
+            for (int j = 0; j < 8; j++) {
+                const int4 o = t4[j];
+                const uint32_t c0 = rows[o.x < 0 ? zero_off : o.x + base];
+                const uint32_t c1 = rows[o.y < 0 ? zero_off : o.y + base];
+                const uint32_t c2 = rows[o.z < 0 ? zero_off : o.z + base];
+                const uint32_t c3 = rows[o.w < 0 ? zero_off : o.w + base];
+                qb[j] = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
             }
             uint32_t* o = outw + wo * bits * Kw + w;
             if (bits > 4) {  // 8x8 bit-matrix transposes: byte t of group g = plane t of codes 8g..8g+7
@@ -443,8 +445,9 @@ __global__ void __launch_bounds__(256) im2col_pack_kernel(const uint8_t* __restr
             }
         }
         __syncthreads();
-        uint32_t* g = dst + (long long)br * Wo * bits * Kw;  // rows (b, ho, 0..Wo-1) are contiguous
-        for (int i = threadIdx.x; i < Wo * bits * Kw; i += blockDim.x) g[i] = outw[i];
+        uint4* g = reinterpret_cast<uint4*>(dst + (long long)br * Wo * bits * Kw);  // rows (b, ho, 0..Wo-1)
+        const uint4* sw = reinterpret_cast<const uint4*>(outw);                      // are contiguous
+        for (int i = threadIdx.x; i < Wo * bits * Kw / 4; i += blockDim.x) g[i] = sw[i];
     }
 }
 
@@ -485,7 +488,8 @@ cudaError_t launch_im2col_pack(const uint8_t* X, int B, int H, int W, int C, int
     const int Kw = (R * S * C + 127) / 128 * 4;
     const long long total = (long long)B * Ho * Wo;
     if (total == 0) return cudaSuccess;
-    const size_t smem = (((size_t)R * (W + 2 * pad) * C + 15) & ~(size_t)15) + (size_t)Wo * bits * Kw * 4;
+    const size_t smem = (((size_t)R * (W + 2 * pad) * C + 1 + 15) & ~(size_t)15) + (size_t)Kw * 32 * 4 +
+                        (size_t)Wo * bits * Kw * 4;
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(im2col_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
