@@ -274,10 +274,19 @@ apnn_status apnn_gemm_prepared_i8(const uint32_t *A, const uint8_t *Wp, int M, i
                                   apnn_stream_t stream);
 /* apnn_conv2d with prepared conv weights: Wp = apnn_prepare_weights_i8 of the packed OHWI
  * weights viewed as C_out*R*S rows of C_in (apnn_prepared_i8_bytes(C_out*R*S, C_in) bytes).
- * 2-CTA kernel only (B*Ho*Wo > 128), else APNN_ERR_UNSUPPORTED; pooling as apnn_conv2d. */
+ * Runs on the tap-reuse kernel (APConv: the input window of a 16 x 8
+ * output tile is decoded once per 128-channel chunk and every filter tap is a row offset
+ * into it) wherever apnn_conv_halo_fits says so -- any batch size, fused requantisation,
+ * 2x2/2 max pooling and the residual epilogue (0/1 activations) included -- else on the
+ * per-tap 2-CTA kernel (B*Ho*Wo > 128; pooling as apnn_conv2d), else APNN_ERR_UNSUPPORTED. */
 apnn_status apnn_conv2d_prepared_i8(const uint32_t *X, const uint8_t *Wp, const apnn_conv_shape *shape,
                                     int a_bits, int w_bits, apnn_encoding enc, const apnn_epilogue *epi,
                                     void *Y, apnn_stream_t stream);
+
+/* 1 if apnn_conv2d_prepared_i8 runs this convolution (shape, encoding, epilogue or NULL) on
+ * the tap-reuse kernel, 0 otherwise (no launch; invalid arguments give 0). */
+int apnn_conv_halo_fits(const apnn_conv_shape *shape, int a_bits, int w_bits, apnn_encoding enc,
+                        const apnn_epilogue *epi);
 
 /* Which variant APNN_VARIANT_AUTO resolves to for this problem (no launch): int32 output,
  * or the fused element-wise routine with out_bits (1..8) packed output. */

@@ -91,6 +91,8 @@ def lib() -> ctypes.CDLL:
             L.apnn_conv2d_prepared_i8.argtypes = [vp, vp, ctypes.POINTER(_Conv), ci, ci, ci, ctypes.POINTER(_Epi),
                                                   vp, vp]
             L.apnn_conv2d_prepared_i8.restype = st
+            L.apnn_conv_halo_fits.argtypes = [ctypes.POINTER(_Conv), ci, ci, ci, ctypes.POINTER(_Epi)]
+            L.apnn_conv_halo_fits.restype = ci
             L.apnn_im2col_pack.argtypes = [vp, ctypes.POINTER(_Conv), ci, vp, vp]
             L.apnn_im2col_pack.restype = st
             L.apnn_im2col_quant_pack.argtypes = [vp, ctypes.POINTER(_Conv), ci, ci, ci, vp, vp]
@@ -130,7 +132,7 @@ ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_im2col_pack", "apnn_
                "apnn_flatten_packed",
                "apnn_prepared_bytes", "apnn_prepare_weights", "apnn_gemm_prepared",
                "apnn_prepared_i8_bytes", "apnn_prepare_weights_i8", "apnn_gemm_prepared_i8",
-               "apnn_conv2d_prepared_i8", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
+               "apnn_conv2d_prepared_i8", "apnn_conv_halo_fits", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
                "apnn_conv2d", "apnn_conv2d_ex", "apnn_quant_pack_out", "apnn_pool_quant_pack_out",
                "apnn_residual_quant_pack",
                "apnn_select_variant", "apnn_select_variant_fused",
@@ -425,6 +427,12 @@ def conv2d_prepared_i8(X: torch.Tensor, Wp: PreparedWeights, shape: ConvShape, a
     _check(lib().apnn_conv2d_prepared_i8(_ptr(X), _ptr(Wp), ctypes.byref(cs), a_bits, w_bits, enc, ce, _ptr(out),
                                          _stream(X)), "apnn_conv2d_prepared_i8")
     return out
+
+
+def conv_halo_fits(shape: ConvShape, a_bits: int, w_bits: int, enc: int, epi: Optional[Epilogue] = None) -> bool:
+    """Does conv2d_prepared_i8 run this convolution on the tap-reuse kernel (apnn_conv_halo_fits)?"""
+    ce = None if epi is None else ctypes.byref(epi._c())
+    return bool(lib().apnn_conv_halo_fits(ctypes.byref(shape._c()), a_bits, w_bits, enc, ce))
 
 
 def conv2d(X: torch.Tensor, W: torch.Tensor, shape: ConvShape, a_bits: int, w_bits: int, enc: int,

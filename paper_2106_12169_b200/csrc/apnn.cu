@@ -49,6 +49,20 @@ cudaError_t launch_prepare_weights_i8(const uint32_t* W, int N, int K, int w_bit
 cudaError_t launch_tc_i8_prepared(const uint32_t* A, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
                                   int sms, cudaStream_t s);
 bool b1mma_supports(const Geom& g);
+bool conv_halo_supports(const Geom& g, const Epi& e);
+cudaError_t launch_conv_halo(const uint32_t* X, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y, int sms,
+                             cudaStream_t s);
+
+// APNN_CONV_HALO=0 (read once) keeps prepared-weight convolutions on the per-tap 2-CTA
+// kernel (A/B measurements); default: the tap-reuse kernel wherever it fits
+static bool conv_halo_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("APNN_CONV_HALO");
+        v = s ? atoi(s) : 1;
+    }
+    return v != 0;
+}
 
 // ---- device properties (cached per device ordinal)
 struct DevInfo {
@@ -452,11 +466,22 @@ static apnn_status conv_impl(const uint32_t* X, const void* Wv, bool prepared, c
     g.nchunks = g.RS * g.CB;
     g.conv = 1;
     g.H = c.H; g.W = c.W; g.Ho = Ho; g.Wo = Wo; g.S = c.S; g.stride = c.stride; g.pad = c.pad;
+    if (e.pool && (e.pool > Ho || e.pool > Wo)) return APNN_ERR_SHAPE;
+    if (prepared && !(e.res && (enc == APNN_ENC_PM1_PM1 || enc == APNN_ENC_W_01_A_PM1)) && conv_halo_enabled() &&
+        conv_halo_supports(g, e)) {
+        // tap-reuse kernel (conv_halo.cu): one decode per tile and channel chunk for all R*S taps
+        DevInfo d;
+        if ((st = device_info(&d)) != APNN_OK) return st;
+        if (g.M == 0) return APNN_OK;
+        cudaError_t err = launch_conv_halo(X, reinterpret_cast<const uint8_t*>(Wv), g, e, Y, d.sms,
+                                           (cudaStream_t)stream);
+        if (err == cudaErrorNotSupported) return APNN_ERR_UNSUPPORTED;
+        return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+    }
     if (e.res && (resolve(variant, g, &e) != APNN_VARIANT_TC_I8 || g.M <= 128 || enc == APNN_ENC_PM1_PM1 ||
                   enc == APNN_ENC_W_01_A_PM1))
         return APNN_ERR_UNSUPPORTED;
     if (e.pool) {
-        if (e.pool > Ho || e.pool > Wo) return APNN_ERR_SHAPE;
         if (resolve(variant, g) != APNN_VARIANT_TC_I8 || !tc_i8_pool_fusable(g, e)) return APNN_ERR_UNSUPPORTED;
     }
     if (prepared) {
@@ -470,6 +495,34 @@ static apnn_status conv_impl(const uint32_t* X, const void* Wv, bool prepared, c
         return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
     }
     return run(X, W, g, e, Y, variant, (cudaStream_t)stream);
+}
+
+int apnn_conv_halo_fits(const apnn_conv_shape* shp, int a_bits, int w_bits, apnn_encoding enc,
+                        const apnn_epilogue* epi) {
+    if (!shp || check_bits_enc(a_bits, w_bits, enc) != APNN_OK) return 0;
+    const apnn_conv_shape c = *shp;
+    if (c.B < 1 || c.H < 1 || c.W < 1 || c.C_in < 1 || c.C_out < 1 || c.R < 1 || c.S < 1 || c.stride < 1 ||
+        c.pad < 0 || c.H + 2 * c.pad < c.R || c.W + 2 * c.pad < c.S)
+        return 0;
+    Epi e;
+    if (make_epi(epi, &e) != APNN_OK) return 0;
+    if (e.res && (enc == APNN_ENC_PM1_PM1 || enc == APNN_ENC_W_01_A_PM1)) return 0;
+    Geom g;
+    std::memset(&g, 0, sizeof(g));
+    g.Ho = (c.H + 2 * c.pad - c.R) / c.stride + 1;
+    g.Wo = (c.W + 2 * c.pad - c.S) / c.stride + 1;
+    const long long Mll = (long long)c.B * g.Ho * g.Wo, Kll = (long long)c.R * c.S * c.C_in;
+    if (Mll > 2147483647LL || Kll > 2147483647LL) return 0;
+    g.M = (int)Mll; g.N = c.C_out; g.K = (int)Kll;
+    g.a_bits = a_bits; g.w_bits = w_bits; g.enc = enc;
+    g.Cw = (c.C_in + 127) / 128 * 4;
+    g.CB = g.Cw / 4;
+    g.C = c.C_in;
+    g.RS = c.R * c.S;
+    g.nchunks = g.RS * g.CB;
+    g.conv = 1;
+    g.H = c.H; g.W = c.W; g.S = c.S; g.stride = c.stride; g.pad = c.pad;
+    return conv_halo_enabled() && conv_halo_supports(g, e) ? 1 : 0;
 }
 
 apnn_status apnn_conv2d(const uint32_t* X, const uint32_t* W, const apnn_conv_shape* shp, int a_bits,

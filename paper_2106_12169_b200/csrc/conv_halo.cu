@@ -1,0 +1,720 @@
+// conv_halo.cu -- APConv (convolution as implicit GEMM) with filter-tap
+// reuse: the "halo" kernel behind apnn_conv2d_prepared_i8.
+//
+// The per-tap implicit GEMM of gemm_tc.cu decodes every input pixel's bit planes once PER
+// FILTER TAP (9x for a 3x3 layer) and hands a k-block to the MMA per tap.  Here a CTA owns a
+// 16 x 8 tile of output pixels and, per 128-channel chunk, decodes the tile's input window
+// (halo) ONCE from the packed planes into int8 rows in shared memory (the operand-side bit
+// combination, PAPER.md:1426-1429 applied to the operand, as in gemm_tc.cu), laid out as one
+// copy per (row phase rho = r mod stride, column tap s):
+//
+//     copy[rho][s][j][tw] = x[b][stride*hh + rho - pad][stride*(w0 + tw) + s - pad]
+//
+// where row j of the copy is "tall" row v0 + j = b*Hv + hh of the batch seen as one image of
+// Hv = Ho + (R-1)/stride rows per image (rows hh >= Ho are separators whose outputs are
+// discarded).  Filter tap (r, s) of output pixel (v0 + hv, w0 + tw) is then copy row
+// hv + r/stride of copy (r mod stride, s): the A operand of tap (r, s) is the 128-row window
+// of that copy starting (r / stride) 8-row core-matrix groups in -- a descriptor offset, no
+// data movement.  All R*S taps of the chunk run back to back on the tensor core from one
+// decode (R*S*Cc/32 MMAs per hand-off instead of Cc/32).
+//
+// Pair kernel (cta_group::2): the two CTAs of a cluster hold two 128-pixel tiles (M = 256)
+// and half of the N tile's weight rows each; prepared int8 weights (apnn_prepare_weights_i8,
+// [C_out][R*S*Cp] bytes) arrive by TMA (SWIZZLE_128B); when the whole N tile fits they are
+// loaded once and stay resident.  Warp roles per CTA:
+//   warps 0-7   decode: (pixel, 32-channel group) units -> int8 copies (K-major, no swizzle)
+//   warps 8-15  epilogue (two per TMEM lane quarter): TMEM -> int32 NHWC, or requantise + pack
+//               (PAPER.md:1296-1306), optional fused 2x2/2 max pooling (warp shuffles) or
+//               residual (reading R24)
+//   warp 16     forwards "W stage landed" to CTA 0 (the MMA issuer needs both halves)
+//   warp 17     TMA producer of the weight stages
+//   warp 18     TMEM allocator; CTA 0 lane 0 issues tcgen05.mma
+#include <cuda.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "tc_common.cuh"
+
+namespace apnn {
+namespace halo {
+
+using namespace tc;
+
+constexpr int TH = 16, TW = 8;  // CTA tile: 16 (tall) output rows x 8 columns = 128 MMA rows
+constexpr int DEC_WARPS = 8;
+constexpr int DEC_THREADS = DEC_WARPS * 32;
+constexpr int EPI0 = DEC_WARPS;
+constexpr int EPI_WARPS = 8;
+constexpr int FWD_WARP = EPI0 + EPI_WARPS;
+constexpr int TMA_WARP = FWD_WARP + 1;
+constexpr int MMA_WARP = TMA_WARP + 1;
+constexpr int THREADS = (MMA_WARP + 1) * 32;
+constexpr int MAX_WS = 40;  // weight stages (resident: all R*S*chunks of the N tile)
+constexpr int STG_WARP = 4352;  // per epilogue warp: int32 32 x 32 block; packed: 2 per quarter (32 x 68 words)
+
+struct Params {
+    Geom g;
+    Epi e;
+    void* Y;
+    const uint32_t* X;
+    int B;
+    int Hv, E;            // tall rows per image, extra copy rows (R-1)/stride
+    int nrho, ncopy;      // row phases min(stride, R); copies nrho * S
+    int crow;             // copy rows (groups of 8 pixels) = TH + E
+    int cl;               // copy row bytes: 32 / 64 / 128 (= the UMMA swizzle width; C_in <= 32 / 64 / else)
+    int cc8;              // bytes per 8-row swizzle atom = 8 * cl (the descriptor's SBO)
+    int smask;            // 16-byte chunk XOR mask of the swizzle: cl / 16 - 1
+    int G;                // 32-channel groups decoded per copy row: ceil(min(C_in, 128) / 32)
+    int nchunk;           // 128-channel chunks (= CB)
+    int ixn;              // input columns a tile touches: stride*(TW-1) + S
+    uint32_t copy_bytes, set_bytes;
+    int nbuf;             // copy sets (double buffering when it fits)
+    int ws, w_resident, nsteps;
+    int bn;               // N tile of the pair (each CTA holds bn/2 weight rows)
+    int tiles_c, cta_tiles, pair_tiles, n_tiles, num_tiles;
+    int tab_mode, pool_fused, Hp, Wp;
+    uint32_t tmem_cols;
+    int exp;              // experiment builds only (APNN_DEV): 1 skip decode, 2 skip MMAs, 4 skip epilogue
+    unsigned long long* trace;  // experiment builds only: %globaltimer stamps of CTAs 0/1 (APNN_HALO_TRACE)
+};
+#ifndef APNN_DEV
+#define APNN_DEV 0
+#endif
+constexpr bool kDev = APNN_DEV != 0;
+#ifndef APNN_HALO_SLEEP
+#define APNN_HALO_SLEEP 2
+#endif
+// barrier waits: the MMA issuer spins (its wake-up latency is on the critical path), the other
+// roles sleep in the try_wait (suspend-time hint) so they do not take the issuer's issue slots
+__device__ __forceinline__ void mma_wait(uint64_t* bar, uint32_t ph) {
+    if (APNN_HALO_SLEEP == 1) sm100::mbar_wait_sleep(bar, ph);
+    else sm100::mbar_wait(bar, ph);
+}
+__device__ __forceinline__ void role_wait(uint64_t* bar, uint32_t ph) {
+    if (APNN_HALO_SLEEP >= 1) sm100::mbar_wait_sleep(bar, ph);
+    else sm100::mbar_wait(bar, ph);
+}
+constexpr int kTrN = 512;
+enum { TR_PROD, TR_FWD, TR_MMA_W, TR_MMA_DONE, TR_DEC_GO, TR_DEC_DONE, TR_MMA_C, TR_EPI_GO, TR_EPI_DONE, TR_MMA_A,
+       TR_NEV };
+__device__ __forceinline__ void trace(const Params& p, int ev, int i) {
+    if (kDev && p.trace && blockIdx.x < 2 && i < kTrN) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));  // SM cycles (CTA 0 / CTA 1 clocks differ)
+        p.trace[((size_t)blockIdx.x * TR_NEV + ev) * kTrN + i] = t;
+    }
+}
+
+// ---------------------------------------------------------------- decode
+// One unit = (row phase rho, copy row j, input column ixo, 32-channel group gi): load the
+// pixel's NB plane words, recombine them into 32 int8 operand bytes (decode_01 / decode_pm1:
+// element order of tc_common.cuh, the prepared weights use the same), and write them into
+// every copy s that reads this input column.  Out-of-frame pixels and padded channels are
+// value 0 for every encoding (reading R16).
+template <int NB, bool PM1>
+__device__ __forceinline__ void decode_chunk(const Params& p, uint8_t* set, int v0, int w0, int ci, int tid) {
+    const Geom& g = p.g;
+    const int G = p.G, st = g.stride;
+    const int units = p.nrho * p.crow * p.ixn * G;
+    // kU units per thread per round: all their plane loads are issued before any decode, so a
+    // round costs one global-load latency instead of kU
+    constexpr int kU = NB <= 2 ? 4 : 2;
+    for (int u0 = tid; u0 < units; u0 += kU * DEC_THREADS) {
+        uint32_t pw[kU][NB];
+        uint32_t rowoff[kU], vm[kU];
+        int ixo_[kU];
+        bool in[kU];
+#pragma unroll
+        for (int k = 0; k < kU; k++) {
+            const int u = u0 + k * DEC_THREADS;
+            const int gi = u % G;
+            int rest = u / G;
+            const int ixo = rest % p.ixn;
+            rest /= p.ixn;
+            const int j = rest % p.crow;
+            const int rho = rest / p.crow;
+            const int vr = v0 + j;
+            const int b = vr / p.Hv, hh = vr - b * p.Hv;
+            const int ih = st * hh + rho - g.pad;
+            const int iw = st * w0 - g.pad + ixo;
+            const int gc = ci * 4 + gi;  // 32-channel group = word index inside a plane run
+            in[k] = u < units && b < p.B && ih >= 0 && ih < g.H && iw >= 0 && iw < g.W && gc * 32 < g.C;
+            ixo_[k] = u < units ? ixo : -1;
+            rowoff[k] = (uint32_t)rho * g.S * p.copy_bytes + (uint32_t)j * p.cc8 + (uint32_t)gi * 32;
+            vm[k] = valid_mask(g.C - gc * 32, 0);
+            const uint32_t* src = p.X + ((long long)((b * g.H + ih) * g.W + iw) * NB) * g.Cw + gc;
+#pragma unroll
+            for (int t = 0; t < NB; t++) pw[k][t] = in[k] ? __ldg(src + t * g.Cw) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < kU; k++) {
+            if (ixo_[k] < 0) continue;
+            uint32_t o[8];
+            if (PM1) {
+                decode_pm1<true>(pw[k][0], in[k] ? vm[k] : 0u, o);  // out of frame: value 0
+            } else {
+                decode_01<NB>(pw[k], o);  // zero planes decode to value 0
+            }
+            const uint4 lo = make_uint4(o[0], o[1], o[2], o[3]), hi = make_uint4(o[4], o[5], o[6], o[7]);
+            // K-major swizzled operand rows (SWIZZLE_32B/64B/128B, atoms of 8 rows x cl bytes):
+            // chunk c of a row at byte offset A lands at A ^ (((A >> 7) & smask) << 4) (sets and
+            // copies are atom-aligned)
+            for (int s = 0; s < g.S; s++) {
+                const int d = ixo_[k] - s;
+                if (d < 0) break;
+                const int tw = d / st;
+                if (tw * st != d || tw >= TW) continue;
+                const uint32_t a = rowoff[k] + (uint32_t)s * p.copy_bytes + (uint32_t)tw * p.cl;
+                const uint32_t a1 = a + 16;
+                *reinterpret_cast<uint4*>(set + (a ^ (((a >> 7) & p.smask) << 4))) = lo;
+                *reinterpret_cast<uint4*>(set + (a1 ^ (((a1 >> 7) & p.smask) << 4))) = hi;
+            }
+        }
+    }
+}
+
+template <bool PM1>
+__device__ __forceinline__ void decode_chunk_any(const Params& p, uint8_t* set, int v0, int w0, int ci, int tid) {
+    if (PM1) {
+        decode_chunk<1, true>(p, set, v0, w0, ci, tid);
+        return;
+    }
+    switch (p.g.a_bits) {
+    case 1: decode_chunk<1, false>(p, set, v0, w0, ci, tid); break;
+    case 2: decode_chunk<2, false>(p, set, v0, w0, ci, tid); break;
+    case 3: decode_chunk<3, false>(p, set, v0, w0, ci, tid); break;
+    case 4: decode_chunk<4, false>(p, set, v0, w0, ci, tid); break;
+    case 5: decode_chunk<5, false>(p, set, v0, w0, ci, tid); break;
+    case 6: decode_chunk<6, false>(p, set, v0, w0, ci, tid); break;
+    case 7: decode_chunk<7, false>(p, set, v0, w0, ci, tid); break;
+    default: decode_chunk<8, false>(p, set, v0, w0, ci, tid); break;
+    }
+}
+
+__device__ __forceinline__ void tile_origin(const Params& p, int tile, uint32_t rank, int& ct, int& v0, int& w0,
+                                            int& n0) {
+    const int pt = tile % p.pair_tiles, nt = tile / p.pair_tiles;
+    ct = 2 * pt + (int)rank;
+    const int rb = ct / p.tiles_c, cb = ct - rb * p.tiles_c;
+    v0 = rb * TH;
+    w0 = cb * TW;
+    n0 = nt * p.bn;
+}
+
+// MMA issuer (one thread of CTA 0).  Its instruction stream is the critical path (an M=256
+// N=64 K=32 MMA runs in ~32 cycles), so everything it needs is loaded into registers before the
+// tile loop: with RST = 9 (3x3 filters) the tap loop is unrolled and the taps' A offsets are
+// registers; descriptors advance by 64-bit adds; ring counters are incremental.
+template <int RST, bool A_PM1, bool W_PM1>
+__device__ __forceinline__ void mma_issuer(const Params& p, const uint32_t* sTap, uint8_t* sCopy, uint8_t* sW,
+                                        uint64_t* w_ready, uint64_t* w_empty, uint64_t* c_full, uint64_t* c_empty,
+                                        uint64_t* a_full, uint64_t* a_empty, uint32_t tmem, int my_tiles) {
+    using namespace sm100;
+    const int RS = RST ? RST : p.g.RS;
+    const int nchunk = p.nchunk, nbuf = p.nbuf, ws = p.ws, bn = p.bn, C = p.g.C;
+    const bool resident = p.w_resident != 0;
+    const bool skip_mma = kDev && (p.exp & 2);
+    const uint32_t idesc = idesc_i8(256, bn, A_PM1, W_PM1);
+    const uint64_t swz = p.cl == 128 ? 2ull : (p.cl == 64 ? 4ull : 6ull);  // descriptor layout type
+    const uint64_t ad0 = (umma_desc_sw128(smem_u32(sCopy), (uint32_t)p.cc8) & ~(7ull << 61)) | (swz << 61);
+    const uint64_t bd0 = umma_desc_sw128(smem_u32(sW), 1024);
+    const uint32_t set16 = p.set_bytes >> 4, wst16 = ((uint32_t)(bn / 2) * 128u) >> 4;
+    uint32_t toff[RST ? RST : 1];
+    if (RST) {
+#pragma unroll
+        for (int rs = 0; rs < (RST ? RST : 1); rs++) toff[rs] = sTap[rs];
+    }
+    int s = 0, cb = 0;
+    uint32_t wph = 0, cph = 0;
+    for (int k = 0; k < my_tiles; k++) {
+        const int buf = k & 1;
+        const uint32_t dtm = tmem + (uint32_t)(buf * bn);
+        mma_wait(&a_empty[buf], ((k >> 1) & 1) ^ 1);
+        trace(p, TR_MMA_A, k);
+        tc_fence_after();
+        uint32_t acc = 0;
+        for (int ci = 0; ci < nchunk; ci++) {
+            mma_wait(&c_full[cb], cph);
+            trace(p, TR_MMA_C, k * nchunk + ci);
+            tc_fence_after();
+            const int crem = C - ci * 128;
+            const int nkk = crem >= 128 ? 4 : (crem + 31) / 32;
+            const uint64_t ads = ad0 + (uint64_t)((uint32_t)cb * set16);
+            if (resident) s = ci * RS;
+#pragma unroll
+            for (int rs = 0; rs < RS; rs++) {
+                if (!resident || k == 0) {
+                    mma_wait(&w_ready[s], resident ? 0u : wph);
+                    tc_fence_after();
+                }
+                const uint64_t ad = ads + (RST ? toff[RST ? rs : 0] : sTap[rs]);
+                const uint64_t bd = bd0 + (uint64_t)((uint32_t)s * wst16);
+                if (!skip_mma) {
+                    mma2_i8_ss(dtm, ad, bd, idesc, acc);
+                    if (nkk > 1) mma2_i8_ss(dtm, ad + 2, bd + 2, idesc, 1u);
+                    if (nkk > 2) mma2_i8_ss(dtm, ad + 4, bd + 4, idesc, 1u);
+                    if (nkk > 3) mma2_i8_ss(dtm, ad + 6, bd + 6, idesc, 1u);
+                }
+                acc = 1u;
+                if (!resident) {
+                    mma2_commit_mc(&w_empty[s], 0x3);
+                    if (++s == ws) { s = 0; wph ^= 1u; }
+                } else {
+                    s++;
+                }
+            }
+            trace(p, TR_MMA_DONE, k * nchunk + ci);
+            mma2_commit_mc(&c_empty[cb], 0x3);
+            if (++cb == nbuf) { cb = 0; cph ^= 1u; }
+        }
+        mma2_commit_mc(&a_full[buf], 0x3);
+    }
+}
+
+// ================================================================ kernel
+template <bool A_PM1, bool W_PM1, bool RES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    halo_kernel(const __grid_constant__ CUtensorMap tmapW, const Params p) {
+    using namespace sm100;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const Geom& g = p.g;
+    const uint32_t WSTAGE = (uint32_t)(p.bn / 2) * 128u;
+    uint8_t* sW = smem;                                             // ws x (bn/2 rows x 128 B), SWIZZLE_128B
+    uint8_t* sCopy = sW + (size_t)p.ws * WSTAGE;                    // nbuf x set_bytes
+    uint8_t* sStg = sCopy + (size_t)p.nbuf * p.set_bytes;           // EPI_WARPS x STG_WARP
+    int32_t* sTab = reinterpret_cast<int32_t*>(sStg + EPI_WARPS * STG_WARP);  // bn x kTabStride
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sTab + p.bn * kTabStride);
+    uint64_t* w_full = bars;                  // [MAX_WS] local TMA completion
+    uint64_t* w_empty = w_full + MAX_WS;      // [MAX_WS] local, MMA commit (multicast)
+    uint64_t* w_ready = w_empty + MAX_WS;     // [MAX_WS] CTA 0: both halves landed (2 forwards)
+    uint64_t* c_full = w_ready + MAX_WS;      // [2] CTA 0: copies written (2 x DEC_WARPS)
+    uint64_t* c_empty = c_full + 2;           // [2] local, MMA commit (multicast)
+    uint64_t* a_full = c_empty + 2;           // [2] local, MMA commit (multicast)
+    uint64_t* a_empty = a_full + 2;           // [2] CTA 0: 2 x 4 epilogue warps
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(a_empty + 2);  // [4] + tap table [RS]
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_ctarank();
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+    if (warp == TMA_WARP && lane == 0) {
+        tma_prefetch(&tmapW);
+        for (int s = 0; s < p.ws; s++) {
+            mbar_init(&w_full[s], 1);
+            mbar_init(&w_empty[s], 1);
+            mbar_init(&w_ready[s], 2);
+        }
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&c_full[i], 2 * DEC_WARPS);
+            mbar_init(&c_empty[i], 1);
+            mbar_init(&a_full[i], 1);
+            mbar_init(&a_empty[i], 2 * EPI_WARPS);
+        }
+        fence_mbar_init();
+    }
+    if (warp == MMA_WARP) tmem_alloc2(tmem_holder, p.tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_holder;
+    const int my_tiles = p.num_tiles > cid ? (p.num_tiles - cid + ncl - 1) / ncl : 0;
+
+    // The single-thread roles keep their whole warp converged in the loop (every lane waits on
+    // the barriers, lane 0 issues): a lone lane spinning while its 31 siblings sit at the final
+    // __syncthreads was measured to cost ~0.4 us per loop iteration (divergent-path scheduling).
+    if (warp == TMA_WARP) {
+        // ------------------------------------------------ weight producer
+        const int nrow0 = (int)rank * (p.bn / 2);
+        if (p.w_resident) {
+            if (lane == 0) {
+                for (int s = 0; s < p.nsteps; s++) {
+                    const int ci = s / g.RS, rs = s - ci * g.RS;
+                    mbar_arrive_expect_tx(&w_full[s], WSTAGE);
+                    tma_load_2d(sW + (size_t)s * WSTAGE, &tmapW, &w_full[s], (rs * g.CB + ci) * 128, nrow0);
+                }
+            }
+            __syncwarp();
+        } else {
+            int it = 0;
+            for (int k = 0; k < my_tiles; k++) {
+                const int tile = cid + k * ncl;
+                const int n0 = (tile / p.pair_tiles) * p.bn;
+                for (int st = 0; st < p.nsteps; st++, it++) {
+                    const int ci = st / g.RS, rs = st - ci * g.RS;
+                    const int s = it % p.ws;
+                    const uint32_t ph = (uint32_t)(it / p.ws) & 1u;
+                    role_wait(&w_empty[s], ph ^ 1u);
+                    if (lane == 0) {
+                        trace(p, TR_PROD, it);
+                        mbar_arrive_expect_tx(&w_full[s], WSTAGE);
+                        tma_load_2d(sW + (size_t)s * WSTAGE, &tmapW, &w_full[s], (rs * g.CB + ci) * 128, n0 + nrow0);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else if (warp == FWD_WARP) {
+        // ------------------------------------------------ "stage landed" -> CTA 0
+        const uint32_t ready0 = mapa(smem_u32(w_ready), 0);
+        const int total = p.w_resident ? p.nsteps : my_tiles * p.nsteps;
+        for (int it = 0; it < total; it++) {
+            const int s = it % p.ws;
+            role_wait(&w_full[s], (uint32_t)(it / p.ws) & 1u);
+            if (lane == 0) {
+                trace(p, TR_FWD, it);
+                mbar_arrive_cluster(ready0 + 8u * (uint32_t)s);
+            }
+            __syncwarp();
+        }
+    } else if (warp == MMA_WARP) {
+        // ------------------------------------------------ MMA issuer (CTA 0)
+        // One thread issues every MMA, so its instruction stream is the critical path (an M=256
+        // N=64 K=32 MMA runs in ~32 cycles): all loop constants live in registers, the A offset
+        // of each tap comes from a table built once, descriptors advance by plain adds, and the
+        // ring counters are incremental (no divisions, no parameter reloads per MMA).
+        if (rank == 0) {
+            uint32_t* sTap = tmem_holder + 4;  // [RS] A-operand offsets of the taps (16-byte units)
+            for (int rs = lane; rs < g.RS; rs += 32) {
+                const int r = rs / g.S, sx = rs - r * g.S;
+                sTap[rs] = ((uint32_t)((r % g.stride) * g.S + sx) * p.copy_bytes + (uint32_t)(r / g.stride) * p.cc8) >> 4;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                if (g.RS == 9) mma_issuer<9, A_PM1, W_PM1>(p, sTap, sCopy, sW, w_ready, w_empty, c_full, c_empty,
+                                                            a_full, a_empty, tmem, my_tiles);
+                else mma_issuer<0, A_PM1, W_PM1>(p, sTap, sCopy, sW, w_ready, w_empty, c_full, c_empty, a_full,
+                                                  a_empty, tmem, my_tiles);
+            }
+        }
+    } else if (warp < DEC_WARPS) {
+        // ------------------------------------------------ decode
+        const int tid = threadIdx.x;
+        const uint32_t c_full0 = mapa(smem_u32(c_full), 0);
+        int q = 0;
+        for (int k = 0; k < my_tiles; k++) {
+            int ct, v0, w0, n0;
+            tile_origin(p, cid + k * ncl, rank, ct, v0, w0, n0);
+            for (int ci = 0; ci < p.nchunk; ci++, q++) {
+                const int cb = q % p.nbuf;
+                role_wait(&c_empty[cb], ((uint32_t)(q / p.nbuf) & 1u) ^ 1u);
+                if (threadIdx.x == 0) trace(p, TR_DEC_GO, q);
+                if (ct < p.cta_tiles && !(kDev && (p.exp & 1))) decode_chunk_any<A_PM1>(p, sCopy + (size_t)cb * p.set_bytes, v0, w0, ci, tid);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(c_full0 + 8u * (uint32_t)cb);
+                if (threadIdx.x == 0) trace(p, TR_DEC_DONE, q);
+            }
+        }
+    } else if (warp < FWD_WARP) {
+        // ------------------------------------------------ epilogue
+        // 8 warps: warp EPI0 + e reads TMEM lane quarter e & 3 (tile rows 32*(e&3)..) and takes
+        // every other 32-column chunk (half e >> 2), so each SM sub-partition runs two epilogue
+        // warps.  Packed output: both warps of a quarter stage their plane words in that
+        // quarter's [row][plane][nwt (+4 pad)] buffer, meet on a named barrier, and each thread
+        // stores whole 16-byte pieces of its own row (no shuffles, no divisions).
+        const int e8 = warp - EPI0;
+        const int qw = e8 & 3, half = e8 >> 2;
+        const int t = qw * 32 + lane;  // TMEM lane = tile row = hv * 8 + tw
+        const int et = threadIdx.x - EPI0 * 32;
+        const uint32_t tmem_lane = tmem + ((uint32_t)(qw * 32) << 16);
+        const uint32_t a_empty0 = mapa(smem_u32(a_empty), 0);
+        const int ob = p.e.out_bits;
+        const int Nw = (g.N + 127) / 128 * 4;
+        const int bn = p.bn;
+        uint8_t* stg_q = sStg + qw * (2 * STG_WARP);           // packed: the quarter's shared staging
+        uint8_t* stg_w = stg_q + half * STG_WARP;              // int32: this warp's own 32 x 32 block
+        int cur_n0 = -1;
+        for (int k = 0; k < my_tiles; k++) {
+            int ct, v0, w0, n0;
+            tile_origin(p, cid + k * ncl, rank, ct, v0, w0, n0);
+            if ((p.tab_mode == kTabQ3 || p.tab_mode == kTabHybrid) && n0 != cur_n0) {
+                named_bar_sync(1, 256);
+                for (int c = et; c < bn; c += 256) build_threshold_row(sTab + c * kTabStride, n0 + c, g.N, p.e);
+                named_bar_sync(1, 256);
+                cur_n0 = n0;
+            }
+            const int hv = t >> 3, tw = t & 7;
+            const int vr = v0 + hv;
+            const int b = vr / p.Hv, ho = vr - b * p.Hv, wo = w0 + tw;
+            const bool valid = ct < p.cta_tiles && b < p.B && ho < g.Ho && wo < g.Wo;
+            const int m = valid ? (b * g.Ho + ho) * g.Wo + wo : g.M;
+            // packed words of this tile per row: the bn columns, plus the N padding on the last tile
+            const int nwt = (n0 + bn >= g.N) ? Nw - n0 / 32 : bn / 32;
+            const int rstride = ob * nwt + 4;  // staged row stride in words (16-byte pad: conflict-free)
+            uint32_t* srow = reinterpret_cast<uint32_t*>(stg_q) + lane * rstride;
+            const int buf = k & 1;
+            role_wait(&a_full[buf], (uint32_t)(k >> 1) & 1u);
+            if (et == 0) trace(p, TR_EPI_GO, k);
+            tc_fence_after();
+            for (int cc = half * 32; cc < bn; cc += 64) {
+                if (kDev && (p.exp & 4)) break;
+                if (ob > 0 && (n0 + cc) / 32 >= Nw) break;  // past the last packed word (ragged last N tile)
+                uint32_t acc[32];
+                tmem_ld32(tmem_lane + (uint32_t)(buf * bn) + cc, acc);
+                tmem_wait_ld();
+                if (p.pool_fused) {
+                    // 2x2/2 max pooling on the codes (q is non-decreasing in v, reading R15):
+                    // the window's pixels are lanes l, l^1, l^8, l^8^1 of this warp
+                    uint32_t qb[8];
+                    requant_chunk_bytes(acc, n0 + cc, cc, g, p.e, sTab, p.tab_mode, qb);
+#pragma unroll
+                    for (int i = 0; i < 8; i++) {
+                        qb[i] = __vmaxu4(qb[i], __shfl_xor_sync(0xffffffffu, qb[i], 1));
+                        qb[i] = __vmaxu4(qb[i], __shfl_xor_sync(0xffffffffu, qb[i], 8));
+                    }
+                    if (valid && (tw & 1) == 0 && (hv & 1) == 0 && (n0 + cc) / 32 < Nw) {
+                        uint32_t w[8];
+                        bytes_to_words(qb, ob, w);
+                        const long long prow = ((long long)b * p.Hp + (ho >> 1)) * p.Wp + (wo >> 1);
+                        uint32_t* o = reinterpret_cast<uint32_t*>(p.Y) + prow * ob * Nw + (n0 + cc) / 32;
+#pragma unroll
+                        for (int tb = 0; tb < 8; tb++)
+                            if (tb < ob) o[(long long)tb * Nw] = w[tb];
+                    }
+                } else if (ob == 0) {
+                    stage_int32_chunk(acc, stg_w, lane);
+                    __syncwarp();
+                    const int j = lane & 7;
+                    const int col = n0 + cc + 4 * j;
+#pragma unroll
+                    for (int i = 0; i < 8; i++) {
+                        const int r = 4 * i + (lane >> 3);
+                        const int mr = __shfl_sync(0xffffffffu, m, r);
+                        const uint4 v = *reinterpret_cast<const uint4*>(stg_w + r * 128 + ((j ^ (r & 7)) << 4));
+                        if (mr < g.M) {
+                            int32_t* y = reinterpret_cast<int32_t*>(p.Y) + (long long)mr * g.N;
+                            if ((g.N & 3) == 0 && col + 4 <= g.N) {
+                                *reinterpret_cast<uint4*>(y + col) = v;
+                            } else {
+                                if (col < g.N) y[col] = (int32_t)v.x;
+                                if (col + 1 < g.N) y[col + 1] = (int32_t)v.y;
+                                if (col + 2 < g.N) y[col + 2] = (int32_t)v.z;
+                                if (col + 3 < g.N) y[col + 3] = (int32_t)v.w;
+                            }
+                        }
+                    }
+                    __syncwarp();
+                } else {
+                    uint32_t w[8];
+                    requant_chunk<RES>(acc, n0 + cc, cc, g, p.e, sTab, p.tab_mode, w, m);
+                    const int wi = cc >> 5;
+#pragma unroll
+                    for (int tb = 0; tb < 8; tb++)
+                        if (tb < ob) srow[tb * nwt + wi] = w[tb];
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(a_empty0 + 8u * (uint32_t)buf);
+            if (et == 0) trace(p, TR_EPI_DONE, k);
+            if (p.pool_fused) {
+                if (half == 0 && n0 + bn >= g.N && valid && (tw & 1) == 0 && (hv & 1) == 0) {  // N padding words
+                    const long long prow = ((long long)b * p.Hp + (ho >> 1)) * p.Wp + (wo >> 1);
+                    uint32_t* o = reinterpret_cast<uint32_t*>(p.Y) + prow * ob * Nw;
+                    for (int tb = 0; tb < ob; tb++)
+                        for (int wi = (n0 + bn) / 32; wi < Nw; wi++) o[(long long)tb * Nw + wi] = 0u;
+                }
+            } else if (ob > 0) {
+                // padding words past the tile's columns (last N tile) are zero
+                for (int wi = bn / 32 + half; wi < nwt; wi += 2)
+                    for (int tb = 0; tb < ob; tb++) srow[tb * nwt + wi] = 0u;
+                named_bar_sync(2 + qw, 64);  // both warps of the quarter staged their words
+                if (m < g.M) {
+                    uint32_t* orow = reinterpret_cast<uint32_t*>(p.Y) + (long long)m * ob * Nw + n0 / 32;
+                    const int pw = nwt >> 2;  // 16-byte pieces per plane
+                    for (int pc = half; pc < ob * pw; pc += 2) {
+                        const int tb = pw == 1 ? pc : pc >> 1, wq = pw == 1 ? 0 : (pc & 1) * 4;
+                        *reinterpret_cast<uint4*>(orow + tb * Nw + wq) =
+                            *reinterpret_cast<const uint4*>(srow + tb * nwt + wq);
+                    }
+                }
+                named_bar_sync(2 + qw, 64);  // staging free for the next tile
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == MMA_WARP) {
+        tc_fence_after();
+        tmem_dealloc2(tmem, p.tmem_cols);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled encode_fn() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(ptr);
+        else
+            cudaGetLastError();
+    });
+    return fn;
+}
+
+// prepared int8 conv weights [C_out][R*S*Cp] bytes; box {128 bytes = one (tap, channel block)
+// k-block, rows} landing in the UMMA K-major SWIZZLE_128B layout
+static bool make_w_map(CUtensorMap* m, const uint8_t* base, int N, int Kp, int rows) {
+    PFN_encodeTiled enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)N};
+    cuuint64_t strides[1] = {(cuuint64_t)Kp};
+    cuuint32_t box[2] = {128, (cuuint32_t)rows};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+constexpr size_t kSmemMax = 227 * 1024;
+
+// Fill the tiling / buffering plan; false when the shape does not fit this kernel.
+static bool plan(const Geom& g, const Epi& e, Params& p) {
+    std::memset(&p, 0, sizeof(p));
+    p.g = g;
+    p.e = e;
+    if (!g.conv || g.M <= 0 || g.N <= 0 || g.K <= 0 || g.RS > 60) return false;  // tap table: 60 entries
+    const int R = g.RS / g.S;
+    p.B = g.M / (g.Ho * g.Wo);
+    p.E = (R - 1) / g.stride;
+    p.Hv = g.Ho + p.E;
+    p.nrho = g.stride < R ? g.stride : R;
+    p.ncopy = p.nrho * g.S;
+    p.crow = TH + p.E;
+    p.cl = g.C > 64 ? 128 : (g.C > 32 ? 64 : 32);
+    p.cc8 = p.cl * 8;
+    p.smask = p.cl / 16 - 1;
+    p.G = ((g.C < 128 ? g.C : 128) + 31) / 32;
+    p.nchunk = g.CB;
+    p.ixn = g.stride * (TW - 1) + g.S;
+    p.copy_bytes = (uint32_t)(p.crow * p.cc8);
+    p.set_bytes = (uint32_t)p.ncopy * p.copy_bytes;
+    p.nsteps = g.RS * p.nchunk;
+    p.bn = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
+    p.n_tiles = (g.N + p.bn - 1) / p.bn;
+    p.tiles_c = (g.Wo + TW - 1) / TW;
+    const long long rows_tiles = ((long long)p.B * p.Hv + TH - 1) / TH;
+    const long long cta_tiles = rows_tiles * p.tiles_c;
+    if (cta_tiles > (1LL << 30) || (long long)p.B * p.Hv > (1LL << 30)) return false;
+    p.cta_tiles = (int)cta_tiles;
+    p.pair_tiles = (p.cta_tiles + 1) / 2;
+    p.num_tiles = p.pair_tiles * p.n_tiles;
+    // epilogue: 2x2/2 max pooling of whole windows (tile rows/cols even, images start on even rows)
+    if (e.pool) {
+        if (!(e.pool == 2 && e.pool_stride == 2 && !e.pool_avg && e.out_bits > 0 && g.Ho % 2 == 0 &&
+              g.Wo % 2 == 0 && p.Hv % 2 == 0))
+            return false;
+        p.pool_fused = 1;
+        p.Hp = g.Ho / 2;
+        p.Wp = g.Wo / 2;
+    }
+    p.tab_mode = kTabNone;
+    if (e.res) p.tab_mode = kTabResidual;
+    else if (e.out_bits > 0 && e.out_bits <= 2) p.tab_mode = kTabQ3;
+    else if (e.out_bits > 2 && (unsigned long long)e.qmax * (unsigned long long)e.S <= 0xFFFFFFFFull)
+        p.tab_mode = kTabHybrid;
+    // shared memory: weights + copies + store staging + table + barriers
+    const size_t wstage = (size_t)(p.bn / 2) * 128;
+    const size_t fixed = EPI_WARPS * (size_t)STG_WARP + (size_t)p.bn * kTabStride * 4 + (3 * MAX_WS + 8) * 8 + 16 + 4 * 64 + 1024;
+    if (fixed + p.set_bytes + 2 * wstage > kSmemMax) return false;
+    const size_t budget = kSmemMax - fixed;
+    if (p.n_tiles == 1 && p.nsteps <= MAX_WS && (size_t)p.nsteps * wstage + 2 * (size_t)p.set_bytes <= budget) {
+        p.w_resident = 1;
+        p.ws = p.nsteps;
+        p.nbuf = 2;
+    } else {
+        p.nbuf = (2 * (size_t)p.set_bytes + 4 * wstage <= budget) ? 2 : 1;
+        size_t ws = (budget - p.nbuf * (size_t)p.set_bytes) / wstage;
+        if (ws > MAX_WS) ws = MAX_WS;
+        if (ws < 2) return false;
+        p.ws = (int)ws;
+    }
+    p.tmem_cols = p.bn == 64 ? 128 : (p.bn == 128 ? 256 : 512);
+    return true;
+}
+
+static size_t smem_bytes(const Params& p) {
+    return (size_t)p.ws * (p.bn / 2) * 128 + (size_t)p.nbuf * p.set_bytes + EPI_WARPS * (size_t)STG_WARP +
+           (size_t)p.bn * kTabStride * 4 + (3 * MAX_WS + 8) * 8 + 16 + 4 * 64;
+}
+
+template <bool AP, bool WP, bool RES>
+static cudaError_t launch(const CUtensorMap& tw, const Params& p, int grid, size_t smem, cudaStream_t s) {
+    auto kfn = halo_kernel<AP, WP, RES>;
+    cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+    if (err != cudaSuccess) return err;
+    kfn<<<grid, THREADS, smem, s>>>(tw, p);
+    return cudaGetLastError();
+}
+
+}  // namespace halo
+
+// Can the tap-reuse kernel run this prepared-weight convolution?
+bool conv_halo_supports(const Geom& g, const Epi& e) {
+    halo::Params p;
+    return halo::plan(g, e, p);
+}
+
+cudaError_t launch_conv_halo(const uint32_t* X, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y, int sms,
+                             cudaStream_t s) {
+    using namespace halo;
+    Params p;
+    if (!plan(g, e, p)) return cudaErrorNotSupported;
+    p.X = X;
+    p.Y = Y;
+#if APNN_DEV
+    p.exp = getenv("APNN_HALO_EXP") ? atoi(getenv("APNN_HALO_EXP")) : 0;
+    const char* trace_path = getenv("APNN_HALO_TRACE");
+    const size_t tr_bytes = sizeof(unsigned long long) * 2 * TR_NEV * kTrN;
+    if (trace_path) {  // development only: allocates and synchronises
+        cudaMalloc(&p.trace, tr_bytes);
+        cudaMemset(p.trace, 0, tr_bytes);
+    }
+#endif
+    CUtensorMap tw;
+    if (!make_w_map(&tw, Wp, g.N, g.RS * g.Cw * 32, p.bn / 2)) return cudaErrorInvalidValue;
+    int pairs = sms / 2;
+    if (pairs > p.num_tiles) pairs = p.num_tiles;
+    if (pairs < 1) pairs = 1;
+    const size_t smem = smem_bytes(p) + 1024;
+    const bool apm = g.enc == APNN_ENC_PM1_PM1 || g.enc == APNN_ENC_W_01_A_PM1;
+    const bool wpm = g.enc == APNN_ENC_PM1_PM1 || g.enc == APNN_ENC_W_PM1_A_01;
+    cudaError_t err;
+    if (e.res) {
+        if (apm) return cudaErrorNotSupported;
+        err = wpm ? launch<false, true, true>(tw, p, 2 * pairs, smem, s) : launch<false, false, true>(tw, p, 2 * pairs, smem, s);
+    } else if (apm) {
+        err = wpm ? launch<true, true, false>(tw, p, 2 * pairs, smem, s) : launch<true, false, false>(tw, p, 2 * pairs, smem, s);
+    } else {
+        err = wpm ? launch<false, true, false>(tw, p, 2 * pairs, smem, s) : launch<false, false, false>(tw, p, 2 * pairs, smem, s);
+    }
+    count_launch();
+#if APNN_DEV
+    if (p.trace) {
+        cudaStreamSynchronize(s);
+        unsigned long long* h = (unsigned long long*)malloc(tr_bytes);
+        cudaMemcpy(h, p.trace, tr_bytes, cudaMemcpyDeviceToHost);
+        FILE* f = fopen(trace_path, "wb");
+        if (f) { fwrite(h, 1, tr_bytes, f); fclose(f); }
+        free(h);
+        cudaFree(p.trace);
+    }
+#endif
+    return err;
+}
+
+}  // namespace apnn
