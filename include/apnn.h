@@ -283,6 +283,22 @@ apnn_status apnn_conv2d_prepared_i8(const uint32_t *X, const uint8_t *Wp, const 
                                     int a_bits, int w_bits, apnn_encoding enc, const apnn_epilogue *epi,
                                     void *Y, apnn_stream_t stream);
 
+/* The first layer straight from the raw 8-bit image ("quantizes 8-bit
+ * inputs into q-bit activations"): X is the device NHWC uint8 image [B][H][W][C_in]; each pixel
+ * value is quantised to q = clamp(floor((x - zero_point) / scale), 0, 2^a_bits - 1) (reading R10/
+ * R11, as apnn_im2col_quant_pack) inside the tap-reuse conv kernel, and out-of-frame taps are
+ * code 0.  Wp = apnn_prepare_weights_i8 of the packed OHWI weights viewed as C_out*R rows of
+ * S*C_in (apnn_prepared_i8_bytes(C_out*R, S*C_in) bytes).  Needs S*C_in <= 128 and 0/1
+ * activations (enc APNN_ENC_01_01 or APNN_ENC_W_PM1_A_01); epilogue and output as apnn_conv2d
+ * (int32 NHWC, or packed with 2x2/2 max pooling fused where apnn_conv_first_fits says so);
+ * no residual.  scale in [1, 255], zero_point in [-255, 255], else APNN_ERR_INVALID_ARG. */
+apnn_status apnn_conv2d_first_prepared_i8(const uint8_t *X, const uint8_t *Wp, const apnn_conv_shape *shape,
+                                          int zero_point, int scale, int a_bits, int w_bits, apnn_encoding enc,
+                                          const apnn_epilogue *epi, void *Y, apnn_stream_t stream);
+/* 1 if apnn_conv2d_first_prepared_i8 takes this layer (shape, encoding, epilogue or NULL). */
+int apnn_conv_first_fits(const apnn_conv_shape *shape, int a_bits, int w_bits, apnn_encoding enc,
+                         const apnn_epilogue *epi);
+
 /* 1 if apnn_conv2d_prepared_i8 runs this convolution (shape, encoding, epilogue or NULL) on
  * the tap-reuse kernel, 0 otherwise (no launch; invalid arguments give 0). */
 int apnn_conv_halo_fits(const apnn_conv_shape *shape, int a_bits, int w_bits, apnn_encoding enc,

@@ -93,6 +93,11 @@ def lib() -> ctypes.CDLL:
             L.apnn_conv2d_prepared_i8.restype = st
             L.apnn_conv_halo_fits.argtypes = [ctypes.POINTER(_Conv), ci, ci, ci, ctypes.POINTER(_Epi)]
             L.apnn_conv_halo_fits.restype = ci
+            L.apnn_conv2d_first_prepared_i8.argtypes = [vp, vp, ctypes.POINTER(_Conv), ci, ci, ci, ci, ci,
+                                                        ctypes.POINTER(_Epi), vp, vp]
+            L.apnn_conv2d_first_prepared_i8.restype = st
+            L.apnn_conv_first_fits.argtypes = [ctypes.POINTER(_Conv), ci, ci, ci, ctypes.POINTER(_Epi)]
+            L.apnn_conv_first_fits.restype = ci
             L.apnn_im2col_pack.argtypes = [vp, ctypes.POINTER(_Conv), ci, vp, vp]
             L.apnn_im2col_pack.restype = st
             L.apnn_im2col_quant_pack.argtypes = [vp, ctypes.POINTER(_Conv), ci, ci, ci, vp, vp]
@@ -132,7 +137,7 @@ ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_im2col_pack", "apnn_
                "apnn_flatten_packed",
                "apnn_prepared_bytes", "apnn_prepare_weights", "apnn_gemm_prepared",
                "apnn_prepared_i8_bytes", "apnn_prepare_weights_i8", "apnn_gemm_prepared_i8",
-               "apnn_conv2d_prepared_i8", "apnn_conv_halo_fits", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
+               "apnn_conv2d_prepared_i8", "apnn_conv_halo_fits", "apnn_conv2d_first_prepared_i8", "apnn_conv_first_fits", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
                "apnn_conv2d", "apnn_conv2d_ex", "apnn_quant_pack_out", "apnn_pool_quant_pack_out",
                "apnn_residual_quant_pack",
                "apnn_select_variant", "apnn_select_variant_fused",
@@ -433,6 +438,42 @@ def conv_halo_fits(shape: ConvShape, a_bits: int, w_bits: int, enc: int, epi: Op
     """Does conv2d_prepared_i8 run this convolution on the tap-reuse kernel (apnn_conv_halo_fits)?"""
     ce = None if epi is None else ctypes.byref(epi._c())
     return bool(lib().apnn_conv_halo_fits(ctypes.byref(shape._c()), a_bits, w_bits, enc, ce))
+
+
+def conv_first_fits(shape: ConvShape, a_bits: int, w_bits: int, enc: int, epi: Optional[Epilogue] = None) -> bool:
+    """Does conv2d_first_prepared_i8 take this first layer (apnn_conv_first_fits)?"""
+    ce = None if epi is None else ctypes.byref(epi._c())
+    return bool(lib().apnn_conv_first_fits(ctypes.byref(shape._c()), a_bits, w_bits, enc, ce))
+
+
+def prepare_first_weights_i8(W: torch.Tensor, shape: ConvShape, w_bits: int, enc: int) -> "PreparedWeights":
+    """Packed first-layer weights [C_out*R, w_bits, Kw(S*C_in)] (OHWI codes viewed as C_out*R rows of
+    S*C_in) -> prepared int8 rows for conv2d_first_prepared_i8."""
+    return prepare_weights_i8(W, shape.C_out * shape.R, shape.S * shape.C_in, w_bits, enc)
+
+
+def conv2d_first_prepared_i8(X: torch.Tensor, Wp: "PreparedWeights", shape: ConvShape, zero_point: int, scale: int,
+                             a_bits: int, w_bits: int, enc: int, epi: Optional[Epilogue] = None,
+                             out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """First layer from the raw 8-bit NHWC image [B, H, W, C_in] (apnn_conv2d_first_prepared_i8): the
+    image is quantised to a_bits codes inside the conv kernel; output as conv2d."""
+    _cuda(X, "X", torch.uint8)
+    _check_out(X, (shape.B, shape.H, shape.W, shape.C_in), "X")
+    Wp = _prepared(Wp, "i8", shape.C_out * shape.R, shape.S * shape.C_in, w_bits, enc)
+    if epi is None:
+        oshape = (shape.B, shape.Ho, shape.Wo, shape.C_out)
+    else:
+        Hp, Wpp = epi.pooled(shape.Ho, shape.Wo)
+        oshape = packed_shape(shape.B * Hp * Wpp, shape.C_out, epi.out_bits)
+    if out is None:
+        out = torch.empty(oshape, dtype=torch.int32, device=X.device)
+    _cuda(out, "out", torch.int32)
+    _check_out(out, oshape)
+    ce = None if epi is None else ctypes.byref(epi._c())
+    _check(lib().apnn_conv2d_first_prepared_i8(_ptr(X), _ptr(Wp), ctypes.byref(shape._c()), zero_point, scale,
+                                               a_bits, w_bits, enc, ce, _ptr(out), _stream(X)),
+           "apnn_conv2d_first_prepared_i8")
+    return out
 
 
 def conv2d(X: torch.Tensor, W: torch.Tensor, shape: ConvShape, a_bits: int, w_bits: int, enc: int,

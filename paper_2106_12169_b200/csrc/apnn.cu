@@ -53,6 +53,10 @@ bool conv_halo_supports(const Geom& g, const Epi& e);
 cudaError_t launch_conv_halo(const uint32_t* X, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y, int sms,
                              cudaStream_t s);
 
+bool conv_first_supports(const Geom& g, const Epi& e, int S_raw, int C_raw);
+cudaError_t launch_conv_first(const uint8_t* X, const uint8_t* Wp, const Geom& g, const Epi& e, int qz, int qs,
+                              int S_raw, int C_raw, void* Y, int sms, cudaStream_t s);
+
 // APNN_CONV_HALO=0 (read once) keeps prepared-weight convolutions on the per-tap 2-CTA
 // kernel (A/B measurements); default: the tap-reuse kernel wherever it fits
 static bool conv_halo_enabled() {
@@ -523,6 +527,67 @@ int apnn_conv_halo_fits(const apnn_conv_shape* shp, int a_bits, int w_bits, apnn
     g.conv = 1;
     g.H = c.H; g.W = c.W; g.S = c.S; g.stride = c.stride; g.pad = c.pad;
     return conv_halo_enabled() && conv_halo_supports(g, e) ? 1 : 0;
+}
+
+// First layer (raw 8-bit image, quantised inside the conv kernel): geometry of the contraction
+// over taps r with K = the S x C_in window of one input row
+static apnn_status first_geom(const apnn_conv_shape* shp, int zero_point, int scale, int a_bits, int w_bits,
+                              apnn_encoding enc, const apnn_epilogue* epi, Geom* g, Epi* e) {
+    if (!shp) return APNN_ERR_INVALID_ARG;
+    const apnn_conv_shape c = *shp;
+    if (c.B < 0 || c.H < 1 || c.W < 1 || c.C_in < 1 || c.C_out < 1 || c.R < 1 || c.S < 1 || c.stride < 1 ||
+        c.pad < 0 || c.H + 2 * c.pad < c.R || c.W + 2 * c.pad < c.S)
+        return APNN_ERR_SHAPE;
+    if (scale < 1 || scale > 255 || zero_point < -255 || zero_point > 255) return APNN_ERR_INVALID_ARG;
+    apnn_status st = check_bits_enc(a_bits, w_bits, enc);
+    if (st != APNN_OK) return st;
+    if (enc == APNN_ENC_PM1_PM1 || enc == APNN_ENC_W_01_A_PM1) return APNN_ERR_ENCODING;  // codes are 0/1 values
+    if ((long long)c.S * c.C_in > 128) return APNN_ERR_UNSUPPORTED;                        // one copy row per window
+    const int Ho = (c.H + 2 * c.pad - c.R) / c.stride + 1, Wo = (c.W + 2 * c.pad - c.S) / c.stride + 1;
+    const long long Mll = (long long)c.B * Ho * Wo, Kll = (long long)c.R * c.S * c.C_in;
+    if (Mll > 2147483647LL) return APNN_ERR_SHAPE;
+    if ((st = check_overflow(Kll, a_bits, w_bits, enc)) != APNN_OK) return st;
+    if ((st = make_epi(epi, e)) != APNN_OK) return st;
+    if (e->res) return APNN_ERR_UNSUPPORTED;
+    std::memset(g, 0, sizeof(*g));
+    g->M = (int)Mll; g->N = c.C_out; g->K = (int)Kll;
+    g->a_bits = a_bits; g->w_bits = w_bits; g->enc = enc;
+    g->C = c.S * c.C_in;  // virtual channels: the window
+    g->Cw = 4;
+    g->CB = 1;
+    g->RS = c.R;          // taps: rows
+    g->nchunks = c.R;
+    g->conv = 1;
+    g->H = c.H; g->W = c.W; g->Ho = Ho; g->Wo = Wo; g->S = 1; g->stride = c.stride; g->pad = c.pad;
+    return APNN_OK;
+}
+
+int apnn_conv_first_fits(const apnn_conv_shape* shp, int a_bits, int w_bits, apnn_encoding enc,
+                         const apnn_epilogue* epi) {
+    Geom g;
+    Epi e;
+    if (first_geom(shp, 0, 1, a_bits, w_bits, enc, epi, &g, &e) != APNN_OK) return 0;
+    return conv_first_supports(g, e, shp->S, shp->C_in) ? 1 : 0;
+}
+
+apnn_status apnn_conv2d_first_prepared_i8(const uint8_t* X, const uint8_t* Wp, const apnn_conv_shape* shp,
+                                          int zero_point, int scale, int a_bits, int w_bits, apnn_encoding enc,
+                                          const apnn_epilogue* epi, void* Y, apnn_stream_t stream) {
+    Geom g;
+    Epi e;
+    apnn_status st = first_geom(shp, zero_point, scale, a_bits, w_bits, enc, epi, &g, &e);
+    if (st != APNN_OK) return st;
+    if (g.M > 0 && (!X || !Wp || !Y)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(Wp) || !aligned16(Y)) return APNN_ERR_ALIGNMENT;
+    if (e.pool && (e.pool > g.Ho || e.pool > g.Wo)) return APNN_ERR_SHAPE;
+    if (!conv_first_supports(g, e, shp->S, shp->C_in)) return APNN_ERR_UNSUPPORTED;
+    DevInfo d;
+    if ((st = device_info(&d)) != APNN_OK) return st;
+    if (g.M == 0) return APNN_OK;
+    cudaError_t err = launch_conv_first(X, Wp, g, e, zero_point, scale, shp->S, shp->C_in, Y, d.sms,
+                                        (cudaStream_t)stream);
+    if (err == cudaErrorNotSupported) return APNN_ERR_UNSUPPORTED;
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }
 
 apnn_status apnn_conv2d(const uint32_t* X, const uint32_t* W, const apnn_conv_shape* shp, int a_bits,

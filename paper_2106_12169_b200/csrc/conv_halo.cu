@@ -60,6 +60,9 @@ struct Params {
     Epi e;
     void* Y;
     const uint32_t* X;
+    const uint8_t* Xraw;  // first layer: raw 8-bit NHWC image (quantised while decoding)
+    int raw, qz, qs;      // raw mode, quantisation q = clamp(floor((x - qz) / qs), 0, 2^a_bits - 1)
+    int S_raw, C_raw;     // raw mode: the window (S_raw columns x C_raw channels) is one copy row
     int B;
     int Hv, E;            // tall rows per image, extra copy rows (R-1)/stride
     int nrho, ncopy;      // row phases min(stride, R); copies nrho * S
@@ -109,88 +112,203 @@ __device__ __forceinline__ void trace(const Params& p, int ev, int i) {
 }
 
 // ---------------------------------------------------------------- decode
-// One unit = (row phase rho, copy row j, input column ixo, 32-channel group gi): load the
-// pixel's NB plane words, recombine them into 32 int8 operand bytes (decode_01 / decode_pm1:
-// element order of tc_common.cuh, the prepared weights use the same), and write them into
-// every copy s that reads this input column.  Out-of-frame pixels and padded channels are
-// value 0 for every encoding (reading R16).
-template <int NB, bool PM1>
-__device__ __forceinline__ void decode_chunk(const Params& p, uint8_t* set, int v0, int w0, int ci, int tid) {
+// Work split of the decode warps, fixed for the kernel: thread tid owns 32-channel group gi and
+// input column ixo of every tile (units = (gi, ixo) pairs, gi fastest), and walks the copy rows
+// jr, jr + jstep, ...  The copies that read column ixo -- copy s at tile column tw where
+// stride*tw + s = ixo -- are precomputed as byte offsets, so the per-row work is one pixel
+// address, the plane loads, the recombination and the stores.
+constexpr int kMaxTg = 8;  // copies one input column feeds: ceil(S / stride) <= 8
+struct DecCtx {
+    bool active;
+    int gi, jr, jstep, iw_rel;
+    int ntg;
+    uint32_t tg[kMaxTg];  // target offsets: copy s base + tw * cl
+};
+
+__device__ __forceinline__ DecCtx make_dec_ctx(const Params& p, int tid) {
     const Geom& g = p.g;
-    const int G = p.G, st = g.stride;
-    const int units = p.nrho * p.crow * p.ixn * G;
-    // kU units per thread per round: all their plane loads are issued before any decode, so a
-    // round costs one global-load latency instead of kU
+    DecCtx d;
+    const int cols = p.G * p.ixn;
+    d.jstep = DEC_THREADS / cols;
+    d.active = tid < d.jstep * cols;
+    const int u = d.active ? tid : 0;
+    d.gi = u % p.G;
+    const int ixo = (u / p.G) % p.ixn;
+    d.jr = u / cols;
+    d.iw_rel = ixo - g.pad;
+    d.ntg = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxTg; q++) d.tg[q] = 0;
+    for (int sx = 0; sx < g.S; sx++) {
+        const int dd = ixo - sx;
+        if (dd < 0) break;
+        const int tw = dd / g.stride;
+        if (tw * g.stride != dd || tw >= TW) continue;
+        const uint32_t off = (uint32_t)sx * p.copy_bytes + (uint32_t)tw * p.cl;
+#pragma unroll
+        for (int q = 0; q < kMaxTg; q++)
+            if (q == d.ntg) d.tg[q] = off;
+        d.ntg++;
+    }
+    return d;
+}
+
+// Decode one 128-channel chunk of a tile's input window into the copies: the pixel's NB plane
+// words are recombined into 32 int8 operand bytes (decode_01 / decode_pm1: the element order of
+// tc_common.cuh, which the prepared weights share) and stored into every copy that reads the
+// pixel.  Out-of-frame pixels and padded channels are value 0 for every encoding
+// (reading R16).  kU rows per round: their loads are all issued first.
+template <int NB, bool PM1>
+__device__ __forceinline__ void decode_chunk(const Params& p, const DecCtx& d, uint8_t* set, int v0, int w0, int ci) {
+    const Geom& g = p.g;
+    const int gc = ci * 4 + d.gi;  // 32-channel group = word index inside a plane run
+    if (!d.active || gc * 32 >= g.C) return;  // groups past C_in are not read by the MMAs
     constexpr int kU = NB <= 2 ? 4 : 2;
-    for (int u0 = tid; u0 < units; u0 += kU * DEC_THREADS) {
-        uint32_t pw[kU][NB];
-        uint32_t rowoff[kU], vm[kU];
-        int ixo_[kU];
-        bool in[kU];
+    const uint32_t vm = valid_mask(g.C - gc * 32, 0);
+    const int st = g.stride, crow = p.crow, jstep = d.jstep, H = g.H, Hv = p.Hv, B = p.B, pad = g.pad;
+    const int iw = st * w0 + d.iw_rel;
+    const bool col_in = iw >= 0 && iw < g.W;
+    const long long pix_stride = (long long)NB * g.Cw;  // words per pixel record
+    const uint32_t* xcol = p.X + (long long)iw * pix_stride + gc;
+    const uint32_t smask = p.smask;
+    for (int rho = 0; rho < p.nrho; rho++) {
+        const uint32_t rbase = (uint32_t)rho * g.S * p.copy_bytes + (uint32_t)d.gi * 32;
+        for (int j0 = d.jr; j0 < crow; j0 += kU * jstep) {
+            uint32_t pw[kU][NB];
+            bool in[kU];
 #pragma unroll
-        for (int k = 0; k < kU; k++) {
-            const int u = u0 + k * DEC_THREADS;
-            const int gi = u % G;
-            int rest = u / G;
-            const int ixo = rest % p.ixn;
-            rest /= p.ixn;
-            const int j = rest % p.crow;
-            const int rho = rest / p.crow;
-            const int vr = v0 + j;
-            const int b = vr / p.Hv, hh = vr - b * p.Hv;
-            const int ih = st * hh + rho - g.pad;
-            const int iw = st * w0 - g.pad + ixo;
-            const int gc = ci * 4 + gi;  // 32-channel group = word index inside a plane run
-            in[k] = u < units && b < p.B && ih >= 0 && ih < g.H && iw >= 0 && iw < g.W && gc * 32 < g.C;
-            ixo_[k] = u < units ? ixo : -1;
-            rowoff[k] = (uint32_t)rho * g.S * p.copy_bytes + (uint32_t)j * p.cc8 + (uint32_t)gi * 32;
-            vm[k] = valid_mask(g.C - gc * 32, 0);
-            const uint32_t* src = p.X + ((long long)((b * g.H + ih) * g.W + iw) * NB) * g.Cw + gc;
+            for (int k = 0; k < kU; k++) {
+                const int j = j0 + k * jstep;
+                const int vr = v0 + j;
+                const int b = vr / Hv, hh = vr - b * Hv;
+                const int ih = st * hh + rho - pad;
+                in[k] = j < crow && col_in && b < B && ih >= 0 && ih < H;
+                const uint32_t* src = xcol + ((long long)b * H + ih) * g.W * pix_stride;
 #pragma unroll
-            for (int t = 0; t < NB; t++) pw[k][t] = in[k] ? __ldg(src + t * g.Cw) : 0u;
-        }
-#pragma unroll
-        for (int k = 0; k < kU; k++) {
-            if (ixo_[k] < 0) continue;
-            uint32_t o[8];
-            if (PM1) {
-                decode_pm1<true>(pw[k][0], in[k] ? vm[k] : 0u, o);  // out of frame: value 0
-            } else {
-                decode_01<NB>(pw[k], o);  // zero planes decode to value 0
+                for (int t = 0; t < NB; t++) pw[k][t] = in[k] ? __ldg(src + t * g.Cw) : 0u;
             }
-            const uint4 lo = make_uint4(o[0], o[1], o[2], o[3]), hi = make_uint4(o[4], o[5], o[6], o[7]);
-            // K-major swizzled operand rows (SWIZZLE_32B/64B/128B, atoms of 8 rows x cl bytes):
-            // chunk c of a row at byte offset A lands at A ^ (((A >> 7) & smask) << 4) (sets and
-            // copies are atom-aligned)
-            for (int s = 0; s < g.S; s++) {
-                const int d = ixo_[k] - s;
-                if (d < 0) break;
-                const int tw = d / st;
-                if (tw * st != d || tw >= TW) continue;
-                const uint32_t a = rowoff[k] + (uint32_t)s * p.copy_bytes + (uint32_t)tw * p.cl;
-                const uint32_t a1 = a + 16;
-                *reinterpret_cast<uint4*>(set + (a ^ (((a >> 7) & p.smask) << 4))) = lo;
-                *reinterpret_cast<uint4*>(set + (a1 ^ (((a1 >> 7) & p.smask) << 4))) = hi;
+#pragma unroll
+            for (int k = 0; k < kU; k++) {
+                const int j = j0 + k * jstep;
+                if (j >= crow) break;
+                uint32_t o[8];
+                if (PM1) decode_pm1<true>(pw[k][0], in[k] ? vm : 0u, o);  // out of frame: value 0
+                else decode_01<NB>(pw[k], o);                              // zero planes decode to 0
+                const uint4 lo = make_uint4(o[0], o[1], o[2], o[3]), hi = make_uint4(o[4], o[5], o[6], o[7]);
+                // K-major swizzled operand rows (SWIZZLE_32B/64B/128B, atoms of 8 rows x cl bytes):
+                // chunk c of a row at byte offset A lands at A ^ (((A >> 7) & smask) << 4)
+                const uint32_t row = rbase + (uint32_t)j * p.cc8;
+#pragma unroll
+                for (int q = 0; q < kMaxTg; q++) {
+                    if (q >= d.ntg) break;
+                    const uint32_t a = row + d.tg[q], a1 = a + 16;
+                    *reinterpret_cast<uint4*>(set + (a ^ (((a >> 7) & smask) << 4))) = lo;
+                    *reinterpret_cast<uint4*>(set + (a1 ^ (((a1 >> 7) & smask) << 4))) = hi;
+                }
             }
         }
     }
 }
 
 template <bool PM1>
-__device__ __forceinline__ void decode_chunk_any(const Params& p, uint8_t* set, int v0, int w0, int ci, int tid) {
+__device__ __forceinline__ void decode_chunk_any(const Params& p, const DecCtx& d, uint8_t* set, int v0, int w0,
+                                                 int ci) {
     if (PM1) {
-        decode_chunk<1, true>(p, set, v0, w0, ci, tid);
+        decode_chunk<1, true>(p, d, set, v0, w0, ci);
         return;
     }
     switch (p.g.a_bits) {
-    case 1: decode_chunk<1, false>(p, set, v0, w0, ci, tid); break;
-    case 2: decode_chunk<2, false>(p, set, v0, w0, ci, tid); break;
-    case 3: decode_chunk<3, false>(p, set, v0, w0, ci, tid); break;
-    case 4: decode_chunk<4, false>(p, set, v0, w0, ci, tid); break;
-    case 5: decode_chunk<5, false>(p, set, v0, w0, ci, tid); break;
-    case 6: decode_chunk<6, false>(p, set, v0, w0, ci, tid); break;
-    case 7: decode_chunk<7, false>(p, set, v0, w0, ci, tid); break;
-    default: decode_chunk<8, false>(p, set, v0, w0, ci, tid); break;
+    case 1: decode_chunk<1, false>(p, d, set, v0, w0, ci); break;
+    case 2: decode_chunk<2, false>(p, d, set, v0, w0, ci); break;
+    case 3: decode_chunk<3, false>(p, d, set, v0, w0, ci); break;
+    case 4: decode_chunk<4, false>(p, d, set, v0, w0, ci); break;
+    case 5: decode_chunk<5, false>(p, d, set, v0, w0, ci); break;
+    case 6: decode_chunk<6, false>(p, d, set, v0, w0, ci); break;
+    case 7: decode_chunk<7, false>(p, d, set, v0, w0, ci); break;
+    default: decode_chunk<8, false>(p, d, set, v0, w0, ci); break;
+    }
+}
+
+// ---------------------------------------------------------------- first layer
+// Raw mode (the first layer, reading R23): the layer reads the 8-bit image
+// and quantises it while decoding, q = clamp(floor((x - z) / s), 0, 2^a_bits - 1) through a
+// 256-entry table; the contraction runs over taps r (rows) with K = the S x C_in window of one
+// input row, which is contiguous in NHWC.  A unit is one copy row (rho, j, tw): its window's
+// codes land at the recombination's element positions (byte 4*(k%8) + (k%32)/8 of group k/32,
+// the order of the prepared weights, viewed as C_out*R rows of S*C_in).  Out-of-frame pixels are
+// code 0 (zero padding of the quantised activations, as the oracle's first layer).
+template <int SR, int CR>
+__device__ __forceinline__ void decode_raw_fixed(const Params& p, uint8_t* set, int v0, int w0, const uint8_t* qtab,
+                                                 int tid) {
+    constexpr int KW = SR * CR;
+    constexpr int GW = (KW + 31) / 32;  // 32-byte groups of the row
+    const Geom& g = p.g;
+    const int st = g.stride, crow = p.crow, Hv = p.Hv, H = g.H, W = g.W, pad = g.pad;
+    const int units = p.nrho * crow * TW;
+    const uint32_t smask = p.smask;
+    for (int u = tid; u < units; u += DEC_THREADS) {
+        const int tw = u & (TW - 1);
+        const int rest = u >> 3;
+        const int rho = rest / crow, j = rest - rho * crow;
+        const int vr = v0 + j;
+        const int b = vr / Hv, hh = vr - b * Hv;
+        const int ih = st * hh + rho - pad;
+        const int iw0 = st * (w0 + tw) - pad;
+        const bool rowin = b < p.B && ih >= 0 && ih < H;
+        const uint8_t* src = p.Xraw + ((long long)(b * H + ih) * W + iw0) * CR;
+        uint32_t wv[8 * GW];
+#pragma unroll
+        for (int i = 0; i < 8 * GW; i++) wv[i] = 0u;
+#pragma unroll
+        for (int sx = 0; sx < SR; sx++) {
+            const bool in = rowin && iw0 + sx >= 0 && iw0 + sx < W;
+#pragma unroll
+            for (int c = 0; c < CR; c++) {
+                const int k = sx * CR + c;
+                const uint32_t code = in ? (uint32_t)qtab[__ldg(src + k)] : 0u;
+                wv[8 * (k / 32) + (k % 8)] |= code << (8 * ((k % 32) / 8));
+            }
+        }
+        const uint32_t row = (uint32_t)rho * p.copy_bytes + (uint32_t)j * p.cc8 + (uint32_t)tw * p.cl;
+#pragma unroll
+        for (int gi = 0; gi < GW; gi++) {
+            const uint32_t a = row + (uint32_t)gi * 32, a1 = a + 16;
+            *reinterpret_cast<uint4*>(set + (a ^ (((a >> 7) & smask) << 4))) =
+                make_uint4(wv[8 * gi], wv[8 * gi + 1], wv[8 * gi + 2], wv[8 * gi + 3]);
+            *reinterpret_cast<uint4*>(set + (a1 ^ (((a1 >> 7) & smask) << 4))) =
+                make_uint4(wv[8 * gi + 4], wv[8 * gi + 5], wv[8 * gi + 6], wv[8 * gi + 7]);
+        }
+    }
+}
+
+// any window (S_raw * C_raw <= 128): codes stored byte by byte, the rest of the row's groups zeroed
+__device__ __forceinline__ void decode_raw_any(const Params& p, uint8_t* set, int v0, int w0, const uint8_t* qtab,
+                                               int tid) {
+    const Geom& g = p.g;
+    const int SR = p.S_raw, CR = p.C_raw, KW = SR * CR, GW = (KW + 31) / 32;
+    const int st = g.stride, crow = p.crow, Hv = p.Hv, H = g.H, W = g.W, pad = g.pad;
+    const int units = p.nrho * crow * TW;
+    const uint32_t smask = p.smask;
+    for (int u = tid; u < units; u += DEC_THREADS) {
+        const int tw = u & (TW - 1);
+        const int rest = u >> 3;
+        const int rho = rest / crow, j = rest - rho * crow;
+        const int vr = v0 + j;
+        const int b = vr / Hv, hh = vr - b * Hv;
+        const int ih = st * hh + rho - pad;
+        const int iw0 = st * (w0 + tw) - pad;
+        const bool rowin = b < p.B && ih >= 0 && ih < H;
+        const uint8_t* src = p.Xraw + ((long long)(b * H + ih) * W + iw0) * CR;
+        const uint32_t row = (uint32_t)rho * p.copy_bytes + (uint32_t)j * p.cc8 + (uint32_t)tw * p.cl;
+        for (int k = 0; k < GW * 32; k++) {
+            uint32_t code = 0;
+            if (k < KW) {
+                const int sx = k / CR;
+                if (rowin && iw0 + sx >= 0 && iw0 + sx < W) code = qtab[__ldg(src + k)];
+            }
+            const uint32_t a = row + (uint32_t)(k / 32) * 32 + (uint32_t)(4 * (k % 8) + (k % 32) / 8);
+            set[a ^ (((a >> 7) & smask) << 4)] = (uint8_t)code;
+        }
     }
 }
 
@@ -275,7 +393,7 @@ __device__ __forceinline__ void mma_issuer(const Params& p, const uint32_t* sTap
 }
 
 // ================================================================ kernel
-template <bool A_PM1, bool W_PM1, bool RES>
+template <bool A_PM1, bool W_PM1, bool RES, bool RAW = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     halo_kernel(const __grid_constant__ CUtensorMap tmapW, const Params p) {
     using namespace sm100;
@@ -392,8 +510,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
     } else if (warp < DEC_WARPS) {
         // ------------------------------------------------ decode
-        const int tid = threadIdx.x;
+        const DecCtx dctx = make_dec_ctx(p, threadIdx.x);
         const uint32_t c_full0 = mapa(smem_u32(c_full), 0);
+        uint8_t* qtab = reinterpret_cast<uint8_t*>(tmem_holder + 4 + 64);  // raw mode: 256-entry code table
+        if (RAW) {
+            const int x = threadIdx.x;  // DEC_THREADS == 256
+            const int v = x - p.qz;
+            const int qv = v < 0 ? 0 : v / p.qs;
+            const int qmax = (1 << g.a_bits) - 1;
+            qtab[x] = (uint8_t)(qv > qmax ? qmax : qv);
+            named_bar_sync(6, DEC_THREADS);
+        }
         int q = 0;
         for (int k = 0; k < my_tiles; k++) {
             int ct, v0, w0, n0;
@@ -402,7 +529,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 const int cb = q % p.nbuf;
                 role_wait(&c_empty[cb], ((uint32_t)(q / p.nbuf) & 1u) ^ 1u);
                 if (threadIdx.x == 0) trace(p, TR_DEC_GO, q);
-                if (ct < p.cta_tiles && !(kDev && (p.exp & 1))) decode_chunk_any<A_PM1>(p, sCopy + (size_t)cb * p.set_bytes, v0, w0, ci, tid);
+                if (ct < p.cta_tiles && !(kDev && (p.exp & 1))) {
+                    uint8_t* set = sCopy + (size_t)cb * p.set_bytes;
+                    if (RAW) {
+                        if (p.S_raw == 7 && p.C_raw == 3) decode_raw_fixed<7, 3>(p, set, v0, w0, qtab, threadIdx.x);
+                        else if (p.S_raw == 11 && p.C_raw == 3) decode_raw_fixed<11, 3>(p, set, v0, w0, qtab, threadIdx.x);
+                        else decode_raw_any(p, set, v0, w0, qtab, threadIdx.x);
+                    } else {
+                        decode_chunk_any<A_PM1>(p, dctx, set, v0, w0, ci);
+                    }
+                }
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(c_full0 + 8u * (uint32_t)cb);
@@ -431,9 +567,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int k = 0; k < my_tiles; k++) {
             int ct, v0, w0, n0;
             tile_origin(p, cid + k * ncl, rank, ct, v0, w0, n0);
-            if ((p.tab_mode == kTabQ3 || p.tab_mode == kTabHybrid) && n0 != cur_n0) {
+            if ((p.tab_mode == kTabQ3 || p.tab_mode == kTabHybrid || (RES && p.tab_mode == kTabResidual)) &&
+                n0 != cur_n0) {
                 named_bar_sync(1, 256);
-                for (int c = et; c < bn; c += 256) build_threshold_row(sTab + c * kTabStride, n0 + c, g.N, p.e);
+                for (int c = et; c < bn; c += 256) {
+                    if (RES && p.tab_mode == kTabResidual) build_residual_row(sTab + c * kTabStride, n0 + c, g.N, p.e);
+                    else build_threshold_row(sTab + c * kTabStride, n0 + c, g.N, p.e);
+                }
                 named_bar_sync(1, 256);
                 cur_n0 = n0;
             }
@@ -500,7 +640,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     __syncwarp();
                 } else {
                     uint32_t w[8];
-                    requant_chunk<RES>(acc, n0 + cc, cc, g, p.e, sTab, p.tab_mode, w, m);
+                    if (RES) {
+                        uint32_t qb[8];
+                        residual_chunk_bytes_tab(acc, m, n0 + cc, cc, g, p.e, sTab, qb);
+                        bytes_to_words(qb, ob, w);
+                    } else {
+                        requant_chunk<false>(acc, n0 + cc, cc, g, p.e, sTab, p.tab_mode, w, m);
+                    }
                     const int wi = cc >> 5;
 #pragma unroll
                     for (int tb = 0; tb < 8; tb++)
@@ -592,6 +738,7 @@ static bool plan(const Geom& g, const Epi& e, Params& p) {
     p.B = g.M / (g.Ho * g.Wo);
     p.E = (R - 1) / g.stride;
     p.Hv = g.Ho + p.E;
+    if (e.pool && (p.Hv & 1)) p.Hv++;  // pooled windows must start on even tall rows (one more separator)
     p.nrho = g.stride < R ? g.stride : R;
     p.ncopy = p.nrho * g.S;
     p.crow = TH + p.E;
@@ -601,6 +748,7 @@ static bool plan(const Geom& g, const Epi& e, Params& p) {
     p.G = ((g.C < 128 ? g.C : 128) + 31) / 32;
     p.nchunk = g.CB;
     p.ixn = g.stride * (TW - 1) + g.S;
+    if (p.G * p.ixn > DEC_THREADS || (g.S + g.stride - 1) / g.stride > kMaxTg) return false;  // decode split / targets
     p.copy_bytes = (uint32_t)(p.crow * p.cc8);
     p.set_bytes = (uint32_t)p.ncopy * p.copy_bytes;
     p.nsteps = g.RS * p.nchunk;
@@ -629,7 +777,7 @@ static bool plan(const Geom& g, const Epi& e, Params& p) {
         p.tab_mode = kTabHybrid;
     // shared memory: weights + copies + store staging + table + barriers
     const size_t wstage = (size_t)(p.bn / 2) * 128;
-    const size_t fixed = EPI_WARPS * (size_t)STG_WARP + (size_t)p.bn * kTabStride * 4 + (3 * MAX_WS + 8) * 8 + 16 + 4 * 64 + 1024;
+    const size_t fixed = EPI_WARPS * (size_t)STG_WARP + (size_t)p.bn * kTabStride * 4 + (3 * MAX_WS + 8) * 8 + 16 + 4 * 64 + 256 + 1024;
     if (fixed + p.set_bytes + 2 * wstage > kSmemMax) return false;
     const size_t budget = kSmemMax - fixed;
     if (p.n_tiles == 1 && p.nsteps <= MAX_WS && (size_t)p.nsteps * wstage + 2 * (size_t)p.set_bytes <= budget) {
@@ -649,12 +797,12 @@ static bool plan(const Geom& g, const Epi& e, Params& p) {
 
 static size_t smem_bytes(const Params& p) {
     return (size_t)p.ws * (p.bn / 2) * 128 + (size_t)p.nbuf * p.set_bytes + EPI_WARPS * (size_t)STG_WARP +
-           (size_t)p.bn * kTabStride * 4 + (3 * MAX_WS + 8) * 8 + 16 + 4 * 64;
+           (size_t)p.bn * kTabStride * 4 + (3 * MAX_WS + 8) * 8 + 16 + 4 * 64 + 256;
 }
 
-template <bool AP, bool WP, bool RES>
+template <bool AP, bool WP, bool RES, bool RAW = false>
 static cudaError_t launch(const CUtensorMap& tw, const Params& p, int grid, size_t smem, cudaStream_t s) {
-    auto kfn = halo_kernel<AP, WP, RES>;
+    auto kfn = halo_kernel<AP, WP, RES, RAW>;
     cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
     if (err != cudaSuccess) return err;
     kfn<<<grid, THREADS, smem, s>>>(tw, p);
@@ -714,6 +862,40 @@ cudaError_t launch_conv_halo(const uint32_t* X, const uint8_t* Wp, const Geom& g
         cudaFree(p.trace);
     }
 #endif
+    return err;
+}
+
+// The first layer on the tap-reuse kernel (raw mode): X is the raw 8-bit NHWC image [B][H][W][C],
+// Wp the prepared weights of W viewed as C_out*R rows of S*C_in (window order (s, c)).
+bool conv_first_supports(const Geom& g0, const Epi& e, int S_raw, int C_raw) {
+    Geom g = g0;
+    halo::Params p;
+    if (S_raw * C_raw > 128 || g.enc == APNN_ENC_PM1_PM1 || g.enc == APNN_ENC_W_01_A_PM1 || e.res) return false;
+    return halo::plan(g, e, p);
+}
+
+cudaError_t launch_conv_first(const uint8_t* X, const uint8_t* Wp, const Geom& g, const Epi& e, int qz, int qs,
+                              int S_raw, int C_raw, void* Y, int sms, cudaStream_t s) {
+    using namespace halo;
+    Params p;
+    if (!conv_first_supports(g, e, S_raw, C_raw) || !plan(g, e, p)) return cudaErrorNotSupported;
+    p.Xraw = X;
+    p.Y = Y;
+    p.raw = 1;
+    p.qz = qz;
+    p.qs = qs;
+    p.S_raw = S_raw;
+    p.C_raw = C_raw;
+    CUtensorMap tw;
+    if (!make_w_map(&tw, Wp, g.N, g.RS * 128, p.bn / 2)) return cudaErrorInvalidValue;  // rows of R x 128 B
+    int pairs = sms / 2;
+    if (pairs > p.num_tiles) pairs = p.num_tiles;
+    if (pairs < 1) pairs = 1;
+    const size_t smem = smem_bytes(p) + 1024;
+    const bool wpm = g.enc == APNN_ENC_W_PM1_A_01;
+    cudaError_t err = wpm ? launch<false, true, false, true>(tw, p, 2 * pairs, smem, s)
+                          : launch<false, false, false, true>(tw, p, 2 * pairs, smem, s);
+    count_launch();
     return err;
 }
 

@@ -434,8 +434,56 @@ __device__ __forceinline__ void requant_chunk_bytes(const uint32_t (&acc)[32], i
     }
 }
 
+// 32 byte codes (byte i of qb[j] = code 4j + i) -> 8 plane words (bit i of words[t] = bit t of
+// code i): the 32 x 8 bit matrix is four 8 x 8 blocks, each transposed with three delta swaps
+// (bit 8r + c <-> 8c + r), then byte permutes gather plane t's byte from the four blocks --
+// ~100 ops for all 8 planes instead of ~48 per plane (checked against the per-bit definition)
+__device__ __forceinline__ void bytes_to_words_t(const uint32_t (&qb)[8], uint32_t (&words)[8]) {
+    uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+        uint32_t x = qb[2 * b], y = qb[2 * b + 1], t;
+        t = (x ^ (x >> 7)) & 0x00AA00AAu;  x = x ^ t ^ (t << 7);
+        t = (y ^ (y >> 7)) & 0x00AA00AAu;  y = y ^ t ^ (t << 7);
+        t = (x ^ (x >> 14)) & 0x0000CCCCu; x = x ^ t ^ (t << 14);
+        t = (y ^ (y >> 14)) & 0x0000CCCCu; y = y ^ t ^ (t << 14);
+        t = (x ^ (y << 4)) & 0xF0F0F0F0u;  x ^= t; y ^= t >> 4;
+        lo[b] = x;
+        hi[b] = y;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; t++) {
+        const uint32_t* L = t < 4 ? lo : hi;
+        const uint32_t sel = (uint32_t)(t & 3) | ((uint32_t)((t & 3) + 4) << 4);
+        words[t] = __byte_perm(__byte_perm(L[0], L[1], sel), __byte_perm(L[2], L[3], sel), 0x5410);
+    }
+}
+
+// The inverse: 8 plane words -> 32 byte codes (byte i of qb[j] = code 4j + i).  The 8 x 8 block
+// transpose is an involution, so the byte permutes run first and the delta swaps second.
+__device__ __forceinline__ void words_to_bytes_t(const uint32_t (&words)[8], uint32_t (&qb)[8]) {
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+        const uint32_t sel = (uint32_t)b | ((uint32_t)(b + 4) << 4);  // byte b of two words -> bytes 0, 1
+        uint32_t x = __byte_perm(__byte_perm(words[0], words[1], sel), __byte_perm(words[2], words[3], sel), 0x5410);
+        uint32_t y = __byte_perm(__byte_perm(words[4], words[5], sel), __byte_perm(words[6], words[7], sel), 0x5410);
+        uint32_t t;
+        t = (x ^ (x >> 7)) & 0x00AA00AAu;  x = x ^ t ^ (t << 7);
+        t = (y ^ (y >> 7)) & 0x00AA00AAu;  y = y ^ t ^ (t << 7);
+        t = (x ^ (x >> 14)) & 0x0000CCCCu; x = x ^ t ^ (t << 14);
+        t = (y ^ (y >> 14)) & 0x0000CCCCu; y = y ^ t ^ (t << 14);
+        t = (x ^ (y << 4)) & 0xF0F0F0F0u;  x ^= t; y ^= t >> 4;
+        qb[2 * b] = x;
+        qb[2 * b + 1] = y;
+    }
+}
+
 // plane words of 32 byte codes
 __device__ __forceinline__ void bytes_to_words(const uint32_t (&qb)[8], int out_bits, uint32_t (&words)[8]) {
+    if (out_bits > 2) {
+        bytes_to_words_t(qb, words);
+        return;
+    }
 #pragma unroll
     for (int tb = 0; tb < 8; tb++) {
         uint32_t wv = 0;
@@ -496,6 +544,72 @@ __device__ __forceinline__ void residual_chunk_bytes(const uint32_t (&acc)[32], 
     }
 }
 
+// Residual table row (kTabResidual, built once per N tile like the threshold rows): [5] alpha,
+// [6] beta, [7] rho of column n; padding columns give q = 0 through alpha = beta = rho = 0.
+__device__ __forceinline__ void build_residual_row(int32_t* row, int n, int N, const Epi& e) {
+    const bool in = n < N;
+    *reinterpret_cast<int4*>(row) = make_int4(0, 0, 0, 0);
+    *reinterpret_cast<int4*>(row + 4) =
+        make_int4(0, in ? epi_alpha(e, n) : 0, in ? epi_beta(e, n) : 0, in ? (e.rho ? __ldg(e.rho + n) : 1) : 0);
+}
+
+// Residual requantisation of a 32-column chunk of row m from the residual table (reading R24):
+// v = alpha*y + beta + rho*z in 64 bits, then q = clamp(floor(v / S), 0, Q) with one float
+// estimate and one correction (v < Q*S < 2^32 in range and q <= 255, so the estimate is off by at
+// most one); packed shortcut codes come out of their planes with words_to_bytes_t.
+__device__ __forceinline__ void residual_chunk_bytes_tab(const uint32_t (&acc)[32], int m, int nb, int lc,
+                                                         const Geom& g, const Epi& e, const int32_t* tab,
+                                                         uint32_t (&qb)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) qb[i] = 0;
+    if (m >= g.M) return;
+    const int Nw = (g.N + 127) / 128 * 4;
+    uint32_t zb[8];
+    const bool packed = e.res_bits > 0;
+    if (packed) {
+        const uint32_t* zp = reinterpret_cast<const uint32_t*>(e.res) + (long long)m * e.res_bits * Nw + nb / 32;
+        uint32_t zw[8];
+#pragma unroll
+        for (int t = 0; t < 8; t++) zw[t] = t < e.res_bits ? __ldg(zp + (long long)t * Nw) : 0u;
+        words_to_bytes_t(zw, zb);
+    }
+    const int32_t* zr = reinterpret_cast<const int32_t*>(e.res) + (long long)m * g.N + nb;
+    const long long QS = (long long)e.qmax * e.S;
+    const uint32_t S = (uint32_t)e.S, Q = (uint32_t)e.qmax;
+#pragma unroll
+    for (int g8 = 0; g8 < 4; g8++) {  // 8 columns at a time (register pressure)
+        int32_t z[8];
+        if (packed) {
+#pragma unroll
+            for (int i = 0; i < 8; i++) z[i] = (int32_t)((zb[2 * g8 + (i >> 2)] >> (8 * (i & 3))) & 0xFFu);
+        } else if ((g.N & 3) == 0 && nb + 8 * g8 + 8 <= g.N) {
+            const int4 a = __ldg(reinterpret_cast<const int4*>(zr + 8 * g8));
+            const int4 b = __ldg(reinterpret_cast<const int4*>(zr + 8 * g8 + 4));
+            z[0] = a.x; z[1] = a.y; z[2] = a.z; z[3] = a.w; z[4] = b.x; z[5] = b.y; z[6] = b.z; z[7] = b.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; i++) z[i] = nb + 8 * g8 + i < g.N ? __ldg(zr + 8 * g8 + i) : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const int4 h = *reinterpret_cast<const int4*>(tab + (lc + 8 * g8 + i) * kTabStride + 4);
+            const long long v = (long long)h.y * (int32_t)acc[8 * g8 + i] + h.z + (long long)h.w * z[i];
+            uint32_t q;
+            if (v < 0) {
+                q = 0;
+            } else if (v >= QS) {
+                q = Q;
+            } else {
+                const uint32_t v32 = (uint32_t)v;
+                q = __float2uint_rz(__uint2float_rn(v32) * e.invS);
+                const int32_t r = (int32_t)(v32 - q * S);
+                q = r < 0 ? q - 1 : (r >= (int32_t)S ? q + 1 : q);
+            }
+            qb[2 * g8 + (i >> 2)] |= q << (8 * (i & 3));
+        }
+    }
+}
+
 // RES: compile the residual branch (kTabResidual) in -- only the residual kernel instances,
 // so the others keep their register allocation (the residual code cost the 2-CTA kernel
 // ~100 bytes of spills per thread when always present)
@@ -526,15 +640,7 @@ __device__ __forceinline__ void requant_chunk(const uint32_t (&acc)[32], int nb,
             qb[i >> 2] |= qv << (8 * (i & 3));
         }
     }
-#pragma unroll
-    for (int tb = 0; tb < 8; tb++) {
-        uint32_t wv = 0;
-        if (tb < e.out_bits) {
-#pragma unroll
-            for (int qq = 0; qq < 8; qq++) wv |= byte_bits_to_nibble(qb[qq], tb) << (4 * qq);
-        }
-        words[tb] = wv;
-    }
+    bytes_to_words(qb, e.out_bits, words);
 }
 
 // Direct (per-thread) stores of one 32-column chunk of row m: int32 row segment, or

@@ -24,24 +24,28 @@ from typing import Optional
 import numpy as np
 import torch
 
-from . import (ApnnError, ConvShape, Epilogue, conv2d, conv2d_prepared_i8, flatten_packed, gemm, im2col_pack,
+from . import (ApnnError, ConvShape, Epilogue, conv2d, conv2d_first_prepared_i8, conv2d_prepared_i8, conv_first_fits,
+               conv_halo_fits, flatten_packed, gemm, im2col_pack, prepare_first_weights_i8,
                pack_bits, pool_quant_pack_out, prepare_weights_i8, residual_quant_pack, synth)
 
 
 def _prep_conv(Wpacked, L, w_bits, enc):
-    """Prepared int8 conv weights (static, prepared once: apnn_prepare_weights_i8) for multi-bit
-    weights; 1-bit weights decode in 2 ops per word and measured faster unprepared (batch 256:
-    AlexNet 1.85 vs 1.92 ms, VGG-Variant 7.88 vs 8.04 ms; w2a2 VGG 8.18 -> 7.98, ResNet w2a8
-    10.8 -> 10.1 ms with prepared weights)."""
-    if w_bits < 2:
-        return None
+    """Prepared int8 conv weights (static, prepared once at load, PAPER.md:1255:
+    apnn_prepare_weights_i8): the operand the tap-reuse conv kernel loads by TMA."""
     return prepare_weights_i8(Wpacked, L["Co"] * L["R"] * L["S"], L["C"], w_bits, enc)
 
 
-def _conv(X, Wpacked, Wprep, shape, a, w, enc, epi=None, out=None):
-    """APConv on prepared weights where the 2-CTA kernel takes it, else the packed-weight path
-    (small M, or pooling the kernel cannot fuse)."""
-    if Wprep is not None and shape.B * shape.Ho * shape.Wo > 128:
+def _conv(X, Wpacked, Wprep, shape, a, w, enc, epi=None, out=None, y32=None):
+    """APConv: the tap-reuse kernel (apnn_conv2d_prepared_i8) wherever it fits -- with the
+    epilogue fused, or, for pooling it cannot fuse (3x3/2, average), as int32 into `y32` + the
+    pooling routine -- else the per-tap kernels (prepared weights for B*Ho*Wo > 128, packed
+    weights otherwise, which also run the unfused pooling pair)."""
+    if conv_halo_fits(shape, a, w, enc, epi):
+        return conv2d_prepared_i8(X, Wprep, shape, a, w, enc, epi=epi, out=out)
+    if epi is not None and epi.pool and y32 is not None and conv_halo_fits(shape, a, w, enc, None):
+        conv2d_prepared_i8(X, Wprep, shape, a, w, enc, out=y32)
+        return pool_quant_pack_out(y32, epi, out=out)
+    if shape.B * shape.Ho * shape.Wo > 128:
         try:
             return conv2d_prepared_i8(X, Wprep, shape, a, w, enc, epi=epi, out=out)
         except ApnnError as ex:
@@ -80,7 +84,17 @@ class APNNModel:
                 st["shape"] = ConvShape(batch, L["H"], L["W"], L["C"], L["Co"], L["R"], L["S"], L["stride"],
                                         L["pad"])
                 M = batch * L["Ho"] * L["Wo"]
-                st["A"] = torch.empty((M, a_bits, (L["K"] + 127) // 128 * 4), dtype=torch.int32, device=self.dev)
+                # the first layer straight from the image on the tap-reuse kernel (quantisation inside,
+                # pooling fused where it can be); else im2col + GEMM
+                st["first"] = conv_first_fits(st["shape"], a_bits, w_bits, self.enc)
+                if st["first"]:
+                    st["Wf"] = prepare_first_weights_i8(
+                        pack_bits(torch.from_numpy(Wt.reshape(L["Co"] * L["R"], -1)).to(self.dev), w_bits),
+                        st["shape"], w_bits, self.enc)
+                    st["first_epi"] = st["epi"] if conv_first_fits(st["shape"], a_bits, w_bits, self.enc,
+                                                                   st["epi"]) else None
+                st["A"] = None if st["first"] else torch.empty((M, a_bits, (L["K"] + 127) // 128 * 4),
+                                                               dtype=torch.int32, device=self.dev)
                 if L["pool"]:
                     st["Y32"] = torch.empty((batch, L["Ho"], L["Wo"], L["Co"]), dtype=torch.int32, device=self.dev)
             elif L["kind"] == "conv":
@@ -89,6 +103,10 @@ class APNNModel:
                 st["Wprep"] = _prep_conv(st["W"], L, w_bits, self.enc)
                 st["shape"] = ConvShape(batch, L["H"], L["W"], L["C"], L["Co"], L["R"], L["S"], L["stride"],
                                         L["pad"])
+                st["Y32c"] = None
+                if st["epi"] is not None and st["epi"].pool and not conv_halo_fits(
+                        st["shape"], a_bits, w_bits, self.enc, st["epi"]):
+                    st["Y32c"] = torch.empty((batch, L["Ho"], L["Wo"], L["Co"]), dtype=torch.int32, device=self.dev)
             elif L["H"] * L["W"] > 1:  # first FC: flatten the packed map, weights in [P][Cpad] order
                 st["mode"] = "flatten_fc"
                 Pn, C = L["H"] * L["W"], L["C"]
@@ -125,7 +143,15 @@ class APNNModel:
             if mark is not None and li > 0:
                 mark(li - 1)
             L, epi = st["L"], st["epi"]
-            if st["mode"] == "im2col":
+            if st["mode"] == "im2col" and st["first"]:
+                zq, sq = self.input_quant if self.input_quant is not None else (0, 1)
+                if st["first_epi"] is not None or epi is None:
+                    act = conv2d_first_prepared_i8(self.x, st["Wf"], st["shape"], zq, sq, a, w, enc, epi=epi,
+                                                   out=st["out"])
+                else:  # pooling the kernel cannot fuse (AlexNet 3x3/2): int32 + the pooling routine
+                    conv2d_first_prepared_i8(self.x, st["Wf"], st["shape"], zq, sq, a, w, enc, out=st["Y32"])
+                    act = pool_quant_pack_out(st["Y32"], epi, out=st["out"])
+            elif st["mode"] == "im2col":
                 im2col_pack(self.x, st["shape"], a, out=st["A"], quant=self.input_quant)
                 M = self.B * L["Ho"] * L["Wo"]
                 if L["pool"]:
@@ -134,7 +160,7 @@ class APNNModel:
                 else:
                     act = gemm(st["A"], st["W"], M, L["Co"], L["K"], a, w, enc, epi=epi, out=st["out"])
             elif st["mode"] == "conv":
-                act = _conv(act, st["W"], st["Wprep"], st["shape"], a, w, enc, epi=epi, out=st["out"])
+                act = _conv(act, st["W"], st["Wprep"], st["shape"], a, w, enc, epi=epi, out=st["out"], y32=st["Y32c"])
             else:
                 A = act
                 if st["mode"] == "flatten_fc":
@@ -179,10 +205,10 @@ class APNNResNet18:
     flatten GEMM with the FC weight tiled over the 7 x 7 positions (int32 logits).  Static
     buffers; capture()/run() as APNNModel."""
 
-    def __init__(self, batch: int, w_bits: int, a_bits: int, device="cuda", params=None, fuse_residual=False,
+    def __init__(self, batch: int, w_bits: int, a_bits: int, device="cuda", params=None, fuse_residual=True,
                  input_quant=None):
-        # fuse_residual: the shortcut in conv_b's epilogue.  Correct (tests) but measured slower at
-        # batch 256 (w2a8 11.5 vs 10.5 ms): the epilogue's per-row shortcut loads are uncoalesced.
+        # fuse_residual: the shortcut added in conv_b's epilogue (tap-reuse kernel); False runs
+        # conv_b to int32 + apnn_residual_quant_pack (the unfused pair, kept for A/B)
         self.B, self.w_bits, self.a_bits = batch, w_bits, a_bits
         self.input_quant = input_quant  # as APNNModel
         self.fuse_residual = fuse_residual
@@ -205,10 +231,17 @@ class APNNResNet18:
             if kind == "stem":
                 st["W"] = pack_bits(t(P["W"].reshape(L["Co"], -1)), w_bits)
                 st["shape"] = ConvShape(batch, L["H"], L["W"], L["C"], L["Co"], L["R"], L["S"], L["stride"], L["pad"])
-                st["A"] = torch.empty((batch * L["Ho"] * L["Wo"], a, (L["K"] + 127) // 128 * 4), dtype=torch.int32,
-                                      device=d)
-                st["Y32"] = torch.empty((batch, L["Ho"], L["Wo"], L["Co"]), dtype=torch.int32, device=d)
                 st["epi"] = Epilogue(a, t(P["alpha"]), t(P["beta"]), int(P["S"]), pool=2, pool_stride=2)
+                # stem straight from the image: quantisation, 7x7/2 conv, 2x2/2 max pooling and the
+                # requantisation in one tap-reuse kernel; else im2col + GEMM + pooling routine
+                st["first"] = conv_first_fits(st["shape"], a, w_bits, self.enc, st["epi"])
+                if st["first"]:
+                    st["Wf"] = prepare_first_weights_i8(pack_bits(t(P["W"].reshape(L["Co"] * L["R"], -1)), w_bits),
+                                                        st["shape"], w_bits, self.enc)
+                else:
+                    st["A"] = torch.empty((batch * L["Ho"] * L["Wo"], a, (L["K"] + 127) // 128 * 4),
+                                          dtype=torch.int32, device=d)
+                    st["Y32"] = torch.empty((batch, L["Ho"], L["Wo"], L["Co"]), dtype=torch.int32, device=d)
                 st["out"] = packed(batch * L["Hp"] * L["Wp"], L["Co"])
             elif kind == "block":
                 La, Lb, Ld = L["a"], L["b"], L["down"]
@@ -253,7 +286,11 @@ class APNNResNet18:
             if mark is not None and li > 0:
                 mark(li - 1)
             L = st["L"]
-            if st["kind"] == "stem":
+            if st["kind"] == "stem" and st["first"]:
+                zq, sq = self.input_quant if self.input_quant is not None else (0, 1)
+                act = conv2d_first_prepared_i8(self.x, st["Wf"], st["shape"], zq, sq, a, w, enc, epi=st["epi"],
+                                               out=st["out"])
+            elif st["kind"] == "stem":
                 im2col_pack(self.x, st["shape"], a, out=st["A"], quant=self.input_quant)
                 M = B * L["Ho"] * L["Wo"]
                 gemm(st["A"], st["W"], M, L["Co"], L["K"], a, w, enc, out=st["Y32"].view(M, L["Co"]))
@@ -265,9 +302,12 @@ class APNNResNet18:
                     zb = 0
                 else:
                     Z, zb = act, a
-                if self.fuse_residual:  # shortcut added in conv_b's epilogue (unfused pair if unsupported)
-                    e = st["epi"]
-                    epi_b = Epilogue(e.out_bits, e.alpha, e.beta, e.divisor, residual=Z, residual_bits=zb, rho=st["rho"])
+                e = st["epi"]
+                epi_b = Epilogue(e.out_bits, e.alpha, e.beta, e.divisor, residual=Z, residual_bits=zb, rho=st["rho"])
+                if self.fuse_residual and conv_halo_fits(st["sb"], a, w, enc, epi_b):
+                    # shortcut added in the tap-reuse kernel's epilogue (reading R24)
+                    act = conv2d_prepared_i8(qa, st["Wb_p"], st["sb"], a, w, enc, epi=epi_b, out=st["out"])
+                elif self.fuse_residual:  # per-tap kernel's fused residual (unfused pair if unsupported)
                     act = conv2d(qa, st["Wb"], st["sb"], a, w, enc, epi=epi_b, out=st["out"])
                 else:
                     _conv(qa, st["Wb"], st["Wb_p"], st["sb"], a, w, enc, out=st["Yb"])

@@ -6,6 +6,7 @@
 //   mode 3: 2-CTA  M=256 N=256 K=32, A TMEM  (TS, cta_group::2)
 //   mode 4: 1-CTA  M=128 N=256 K=64, kind::mxf4 block32 (e2m1, E8M0 scales in TMEM), SS
 //   mode 5: 2-CTA  M=256 N=256 K=64, kind::mxf4 block32, SS (cta_group::2)
+//   mode 6 / 7: 2-CTA M=256 N=64 / 128 K=32, kind::i8, A smem (SS): issue rate at small N
 // Operands are zeros (timing is value-independent).  Build:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I ../paper_2106_12169_b200/csrc mma_peak.cu -o mma_peak
 #include <cstdio>
@@ -22,8 +23,9 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(int iters, unsigned long l
     uint8_t* sB = smem + 16384;    // 256 rows x 128 B (1-CTA) / 128 rows (2-CTA)
     __shared__ uint64_t bar;
     __shared__ uint32_t holder;
-    constexpr bool two = MODE == 2 || MODE == 3 || MODE == 5;
-    constexpr bool fp4 = MODE >= 4;
+    constexpr bool two = MODE == 2 || MODE == 3 || MODE == 5 || MODE >= 6;
+    constexpr bool fp4 = MODE == 4 || MODE == 5;
+    constexpr int NN = MODE == 6 ? 64 : (MODE == 7 ? 128 : 256);
     const int warp = threadIdx.x / 32;
     for (int i = threadIdx.x; i < 49152 / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
     if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
@@ -50,7 +52,7 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(int iters, unsigned long l
     }
     unsigned long long t0 = clock64();
     if (warp == 1 && leader && (threadIdx.x % 32) == 0) {
-        const uint32_t idesc = idesc_i8(two ? 256 : 128, 256, false, false);
+        const uint32_t idesc = idesc_i8(two ? 256 : 128, NN, false, false);
         const uint32_t abase = smem_u32(sA), bbase = smem_u32(sB);
         for (int it = 0; it < iters; it++) {
 #pragma unroll
@@ -58,7 +60,7 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(int iters, unsigned long l
                 const uint64_t bd = umma_desc_sw128(bbase + kk * 32, 1024);
                 if (MODE == 0) mma_i8_ss(tmem, umma_desc_sw128(abase + kk * 32, 1024), bd, idesc, 1);
                 if (MODE == 1) mma_i8_ts(tmem, tmem + 256 + kk * 8, bd, idesc, 1);
-                if (MODE == 2) {
+                if (MODE == 2 || MODE >= 6) {
                     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
                                  "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
                                  "l"(umma_desc_sw128(abase + kk * 32, 1024)), "l"(bd), "r"(idesc) : "memory");
@@ -103,7 +105,7 @@ void run(int iters, int sms) {
     cfg.dynamicSmemBytes = 49152 + 1024;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    constexpr bool two = MODE == 2 || MODE == 3 || MODE == 5;
+    constexpr bool two = MODE == 2 || MODE == 3 || MODE == 5 || MODE >= 6;
     attr[0].val.clusterDim.x = two ? 2 : 1;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
@@ -123,13 +125,14 @@ void run(int iters, int sms) {
     unsigned long long cyc[512];
     cudaMemcpy(cyc, d, sms * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     const double M = two ? 256 : 128;
-    const double Kst = MODE >= 4 ? 64 : 32;  // K per instruction (fp4: 64 elements in 32 bytes)
+    const double Kst = (MODE == 4 || MODE == 5) ? 64 : 32;
+    const double NN = MODE == 6 ? 64 : (MODE == 7 ? 128 : 256);  // K per instruction (fp4: 64 elements in 32 bytes)
     const int units = two ? sms / 2 : sms;
-    const double ops = 2.0 * M * 256 * Kst * 4.0 * iters * units;
+    const double ops = 2.0 * M * NN * Kst * 4.0 * iters * units;
     printf("{\"mode\": %d, \"name\": \"%s\", \"err\": \"%s\", \"ms\": %.3f, \"tops\": %.1f, \"cycles_cta0\": %llu, "
            "\"mac_per_clk_per_sm\": %.0f, \"clk_ghz_cta0\": %.3f}\n",
            MODE, MODE == 0 ? "i8_1cta_SS" : MODE == 1 ? "i8_1cta_TS" : MODE == 2 ? "i8_2cta_SS" : MODE == 3 ? "i8_2cta_TS"
-                 : MODE == 4 ? "mxf4_1cta_SS" : "mxf4_2cta_SS",
+                 : MODE == 4 ? "mxf4_1cta_SS" : MODE == 5 ? "mxf4_2cta_SS" : MODE == 6 ? "i8_2cta_SS_N64" : "i8_2cta_SS_N128",
            cudaGetErrorString(err), ms, ops / (ms * 1e-3) / 1e12, cyc[0],
            (M * 256 * Kst * 4.0 * iters) / (double)cyc[0] / (two ? 2 : 1), (double)cyc[0] / (ms * 1e6));
     cudaFree(d);
@@ -144,5 +147,7 @@ int main(int argc, char** argv) {
     run<3>(iters, sms);
     run<4>(iters, sms);
     run<5>(iters, sms);
+    run<6>(iters, sms);
+    run<7>(iters, sms);
     return 0;
 }

@@ -165,3 +165,52 @@ def test_halo_fit_rules():
     assert not ap.conv_halo_fits(cs, 2, 1, 2, ap.Epilogue(2, None, None, 3, pool=2, pool_stride=2, pool_avg=True))
     odd = ap.ConvShape(2, 8, 8, 64, 64, 3, 3, 1, 0)  # Ho = 6, Hv = 8 -> fusable; pad 1 with H = 7 -> Hv odd
     assert ap.conv_halo_fits(odd, 2, 1, 2, ap.Epilogue(2, None, None, 3, pool=2, pool_stride=2))
+
+
+# ------------------------------------------------ first layer from the raw image (raw mode)
+
+FIRST_SHAPES = [  # B, H, W, C, Co, R, S, stride, pad
+    (2, 224, 224, 3, 64, 7, 7, 2, 3),     # ResNet-18 / VGG-Variant stem (7x7/2, window 21 bytes)
+    (2, 224, 224, 3, 96, 11, 11, 4, 2),   # AlexNet conv1 (11x11/4, window 33 bytes)
+    (3, 17, 23, 3, 40, 3, 3, 1, 1),       # small ragged frame, generic window path (9 bytes)
+    (1, 30, 31, 5, 70, 5, 5, 2, 2),       # C_in = 5 (generic window, 25 bytes)
+]
+
+
+@pytest.mark.parametrize("shape", FIRST_SHAPES)
+@pytest.mark.parametrize("a_bits,w_bits,enc", [(2, 1, 2), (8, 2, 0), (5, 3, 0)])
+def test_first_layer_raw_image(shape, a_bits, w_bits, enc):
+    B, H, Wd, C, Co, R, S, st, pad = shape
+    g = synth.rng(f"first:{shape}:{a_bits}")
+    x = g.integers(0, 256, size=(B, H, Wd, C)).astype(np.uint8)
+    Wt = synth.codes((Co, R, S, C), w_bits, f"first:w:{shape}")
+    zp, sc = int(g.integers(-20, 40)), int(g.integers(1, 70))
+    Xq = oracle.quantize_input(x, zp, sc, a_bits)
+    want = oracle.conv2d(Xq, Wt, st, pad, a_bits, w_bits, enc)
+    cs = ap.ConvShape(B, H, Wd, C, Co, R, S, st, pad)
+    assert ap.conv_first_fits(cs, a_bits, w_bits, enc)
+    Wq = ap.prepare_first_weights_i8(ap.pack_bits(cuda(Wt.reshape(Co * R, S * C)), w_bits), cs, w_bits, enc)
+    X = cuda(x)
+    got = ap.conv2d_first_prepared_i8(X, Wq, cs, zp, sc, a_bits, w_bits, enc)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+    alpha, beta = synth.epilogue_params(Co, tag="firstepi")
+    for ob in (2, 8):
+        wantp = oracle.pack(oracle.epilogue(want.reshape(-1, Co), alpha, beta, 37, ob), ob)
+        got = ap.conv2d_first_prepared_i8(X, Wq, cs, zp, sc, a_bits, w_bits, enc,
+                                          epi=ap.Epilogue(ob, cuda(alpha), cuda(beta), 37))
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(u32(got), wantp, err_msg=f"out_bits={ob}")
+    if cs.Ho % 2 == 0 and cs.Wo % 2 == 0:  # fused 2x2/2 max pooling (the ResNet / VGG stem)
+        epi = ap.Epilogue(a_bits, cuda(alpha), cuda(beta), 37, pool=2, pool_stride=2)
+        assert ap.conv_first_fits(cs, a_bits, w_bits, enc, epi)
+        wantq = oracle.pack(oracle.pool_epilogue(want, alpha, beta, 37, a_bits, 2, 2).reshape(-1, Co), a_bits)
+        got = ap.conv2d_first_prepared_i8(X, Wq, cs, zp, sc, a_bits, w_bits, enc, epi=epi)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(u32(got), wantq)
+
+
+def test_first_layer_rejects():
+    cs = ap.ConvShape(1, 32, 32, 3, 16, 7, 7, 2, 3)
+    assert not ap.conv_first_fits(cs, 1, 1, 1)                            # +-1 activations: codes are 0/1
+    assert not ap.conv_first_fits(ap.ConvShape(1, 32, 32, 16, 16, 3, 9, 1, 1), 2, 1, 2)  # window 144 > 128 bytes
