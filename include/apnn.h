@@ -299,6 +299,34 @@ apnn_status apnn_conv2d_first_prepared_i8(const uint8_t *X, const uint8_t *Wp, c
 int apnn_conv_first_fits(const apnn_conv_shape *shape, int a_bits, int w_bits, apnn_encoding enc,
                          const apnn_epilogue *epi);
 
+/* Tile configuration of the int8 tensor-core GEMM (row f4).  kernel 1: one CTA per 128 x bn output
+ * tile, K split over a cluster of ksplit CTAs (reduced through distributed shared memory);
+ * kernel 2: a CTA pair (cta_group::2) per 256 x bn tile.  tlp = CTAs launched, ci = the tile's
+ * compute intensity 2 bm bn / (bm + bn). */
+typedef struct {
+    int32_t kernel;   /* 1 or 2 */
+    int32_t bm, bn;   /* 128 (kernel 1) / 256 (kernel 2); bn in {64, 128, 256} */
+    int32_t ksplit;   /* 1, 2, 4 (kernel 1; > 1 needs bn <= 128 and ksplit <= ceil(K/128)) */
+    int64_t tlp;
+    double ci;
+} apnn_tile_config;
+
+/* The paper's block-tiling heuristic: candidate tiles are ordered by TLP;
+ * the highest-TLP one is taken when its TLP is below the threshold T, else the highest-CI one
+ * among those with TLP >= T.  Candidates are the int8 kernels' tiles (reading R21);
+ * out_bits: 0 for int32 output, else the packed output width (pair tiles narrower than 128
+ * columns store packed words only when N <= 64).  T = threshold, or the paper's T = 64 when
+ * threshold <= 0.  Host-only computation
+ * (no launch); apnn_gemm / apnn_gemm_fused use it for every int8 tensor-core GEMM. */
+apnn_status apnn_tune_tiles(int M, int N, int K, int out_bits, int threshold, apnn_tile_config *out);
+
+/* apnn_gemm_ex on the int8 tensor-core variant with an explicit tile configuration (measurement
+ * of the tuner's candidates, configuration-invariance tests).  APNN_ERR_UNSUPPORTED for a
+ * configuration the kernels do not implement for this shape (see apnn_tile_config). */
+apnn_status apnn_gemm_tiled(const uint32_t *A, const uint32_t *W, int M, int N, int K, int a_bits, int w_bits,
+                            apnn_encoding enc, const apnn_epilogue *epi, void *Y, const apnn_tile_config *cfg,
+                            apnn_stream_t stream);
+
 /* 1 if apnn_conv2d_prepared_i8 runs this convolution (shape, encoding, epilogue or NULL) on
  * the tap-reuse kernel, 0 otherwise (no launch; invalid arguments give 0). */
 int apnn_conv_halo_fits(const apnn_conv_shape *shape, int a_bits, int w_bits, apnn_encoding enc,

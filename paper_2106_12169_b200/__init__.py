@@ -55,6 +55,17 @@ class _Conv(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("B", "H", "W", "C_in", "C_out", "R", "S", "stride", "pad")]
 
 
+class TileConfig(ctypes.Structure):
+    """apnn_tile_config: kernel 1 = one CTA per 128 x bn tile with a split-K cluster of ksplit CTAs,
+    kernel 2 = CTA pair per 256 x bn tile; tlp = CTAs, ci = 2 bm bn / (bm + bn)."""
+    _fields_ = [("kernel", ctypes.c_int32), ("bm", ctypes.c_int32), ("bn", ctypes.c_int32),
+                ("ksplit", ctypes.c_int32), ("tlp", ctypes.c_int64), ("ci", ctypes.c_double)]
+
+    def __repr__(self):
+        return (f"TileConfig(kernel={self.kernel}, bm={self.bm}, bn={self.bn}, ksplit={self.ksplit}, "
+                f"tlp={self.tlp}, ci={self.ci:.1f})")
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -98,6 +109,11 @@ def lib() -> ctypes.CDLL:
             L.apnn_conv2d_first_prepared_i8.restype = st
             L.apnn_conv_first_fits.argtypes = [ctypes.POINTER(_Conv), ci, ci, ci, ctypes.POINTER(_Epi)]
             L.apnn_conv_first_fits.restype = ci
+            L.apnn_tune_tiles.argtypes = [ci, ci, ci, ci, ci, ctypes.POINTER(TileConfig)]
+            L.apnn_tune_tiles.restype = st
+            L.apnn_gemm_tiled.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp,
+                                          ctypes.POINTER(TileConfig), vp]
+            L.apnn_gemm_tiled.restype = st
             L.apnn_im2col_pack.argtypes = [vp, ctypes.POINTER(_Conv), ci, vp, vp]
             L.apnn_im2col_pack.restype = st
             L.apnn_im2col_quant_pack.argtypes = [vp, ctypes.POINTER(_Conv), ci, ci, ci, vp, vp]
@@ -137,7 +153,7 @@ ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_im2col_pack", "apnn_
                "apnn_flatten_packed",
                "apnn_prepared_bytes", "apnn_prepare_weights", "apnn_gemm_prepared",
                "apnn_prepared_i8_bytes", "apnn_prepare_weights_i8", "apnn_gemm_prepared_i8",
-               "apnn_conv2d_prepared_i8", "apnn_conv_halo_fits", "apnn_conv2d_first_prepared_i8", "apnn_conv_first_fits", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
+               "apnn_conv2d_prepared_i8", "apnn_conv_halo_fits", "apnn_conv2d_first_prepared_i8", "apnn_conv_first_fits", "apnn_tune_tiles", "apnn_gemm_tiled", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
                "apnn_conv2d", "apnn_conv2d_ex", "apnn_quant_pack_out", "apnn_pool_quant_pack_out",
                "apnn_residual_quant_pack",
                "apnn_select_variant", "apnn_select_variant_fused",
@@ -438,6 +454,29 @@ def conv_halo_fits(shape: ConvShape, a_bits: int, w_bits: int, enc: int, epi: Op
     """Does conv2d_prepared_i8 run this convolution on the tap-reuse kernel (apnn_conv_halo_fits)?"""
     ce = None if epi is None else ctypes.byref(epi._c())
     return bool(lib().apnn_conv_halo_fits(ctypes.byref(shape._c()), a_bits, w_bits, enc, ce))
+
+
+def tune_tiles(M: int, N: int, K: int, threshold: int = 0, out_bits: int = 0) -> TileConfig:
+    """The paper's TLP/CI tiling heuristic for the int8 GEMM (apnn_tune_tiles; threshold <= 0: the
+    paper's T = 64).  Host computation only."""
+    c = TileConfig()
+    _check(lib().apnn_tune_tiles(M, N, K, out_bits, threshold, ctypes.byref(c)), "apnn_tune_tiles")
+    return c
+
+
+def gemm_tiled(A: torch.Tensor, W: torch.Tensor, M: int, N: int, K: int, a_bits: int, w_bits: int, enc: int,
+               cfg: TileConfig, epi: Optional[Epilogue] = None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """APMM on the int8 tensor-core kernels with an explicit tile configuration (apnn_gemm_tiled)."""
+    _cuda(A, "A", torch.int32)
+    _cuda(W, "W", torch.int32)
+    oshape = (M, N) if epi is None else packed_shape(M, N, epi.out_bits)
+    if out is None:
+        out = torch.empty(oshape, dtype=torch.int32, device=A.device)
+    _check_out(out, oshape)
+    ce = None if epi is None else ctypes.byref(epi._c())
+    _check(lib().apnn_gemm_tiled(_ptr(A), _ptr(W), M, N, K, a_bits, w_bits, enc, ce, _ptr(out), ctypes.byref(cfg),
+                                 _stream(A)), "apnn_gemm_tiled")
+    return out
 
 
 def conv_first_fits(shape: ConvShape, a_bits: int, w_bits: int, enc: int, epi: Optional[Epilogue] = None) -> bool:

@@ -53,6 +53,8 @@ bool conv_halo_supports(const Geom& g, const Epi& e);
 cudaError_t launch_conv_halo(const uint32_t* X, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y, int sms,
                              cudaStream_t s);
 
+cudaError_t launch_tc_i8_tiled(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
+                               const TileCfg& cfg, int sms, cudaStream_t s);
 bool conv_first_supports(const Geom& g, const Epi& e, int S_raw, int C_raw);
 cudaError_t launch_conv_first(const uint8_t* X, const uint8_t* Wp, const Geom& g, const Epi& e, int qz, int qs,
                               int S_raw, int C_raw, void* Y, int sms, cudaStream_t s);
@@ -404,6 +406,45 @@ apnn_status apnn_gemm_prepared_i8(const uint32_t* A, const uint8_t* Wp, int M, i
     if ((st = device_info(&d)) != APNN_OK) return st;
     if (N == 0) return APNN_OK;
     cudaError_t err = launch_tc_i8_prepared(A, Wp, g, e, Y, d.sms, (cudaStream_t)stream);
+    if (err == cudaErrorNotSupported) return APNN_ERR_UNSUPPORTED;
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_status apnn_tune_tiles(int M, int N, int K, int out_bits, int threshold, apnn_tile_config* out) {
+    if (M < 1 || N < 1 || K < 1) return APNN_ERR_SHAPE;
+    if (!out) return APNN_ERR_INVALID_ARG;
+    const int T = threshold > 0 ? threshold : 64;  // the paper's T
+    const TileCfg c = tune_tiles(M, N, K, T, out_bits > 0);
+    out->kernel = c.kernel;
+    out->bm = c.bm;
+    out->bn = c.bn;
+    out->ksplit = c.z;
+    out->tlp = c.tlp;
+    out->ci = c.ci;
+    return APNN_OK;
+}
+
+apnn_status apnn_gemm_tiled(const uint32_t* A, const uint32_t* W, int M, int N, int K, int a_bits, int w_bits,
+                            apnn_encoding enc, const apnn_epilogue* epi, void* Y, const apnn_tile_config* cfg,
+                            apnn_stream_t stream) {
+    if (M < 0 || N < 0 || K < 0) return APNN_ERR_SHAPE;
+    if (!cfg) return APNN_ERR_INVALID_ARG;
+    apnn_status st = check_bits_enc(a_bits, w_bits, enc);
+    if (st != APNN_OK) return st;
+    if ((M > 0 && K > 0 && !A) || (N > 0 && K > 0 && !W) || (M > 0 && N > 0 && !Y)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(A) || !aligned16(W) || !aligned16(Y)) return APNN_ERR_ALIGNMENT;
+    if ((st = check_overflow(K, a_bits, w_bits, enc)) != APNN_OK) return st;
+    Epi e;
+    if ((st = make_epi(epi, &e)) != APNN_OK) return st;
+    if (e.pool || e.res) return APNN_ERR_INVALID_ARG;
+    const TileCfg c{cfg->kernel, cfg->bm, cfg->bn, cfg->ksplit, 0, 0.0};
+    if (K == 0 || !tile_cfg_valid(c, M, N, K, e.out_bits > 0)) return APNN_ERR_UNSUPPORTED;
+    Geom g;
+    gemm_geom(&g, M, N, K, a_bits, w_bits, enc);
+    DevInfo d;
+    if ((st = device_info(&d)) != APNN_OK) return st;
+    if (M == 0 || N == 0) return APNN_OK;
+    cudaError_t err = launch_tc_i8_tiled(A, W, g, e, Y, c, d.sms, (cudaStream_t)stream);
     if (err == cudaErrorNotSupported) return APNN_ERR_UNSUPPORTED;
     return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }

@@ -35,6 +35,16 @@ struct Geom {
     int H, W, Ho, Wo, S, stride, pad;
 };
 
+// Tile configuration of the int8 tensor-core kernels (row f4, tuner.cu): kernel 1 = one-CTA
+// 128 x bn tile with a split-K cluster of z CTAs, kernel 2 = CTA pair 256 x bn.
+struct TileCfg {
+    int kernel, bm, bn, z;
+    long long tlp;  // CTAs launched (the paper's TLP, Eq. TLP adapted)
+    double ci;      // Eq. CI of the tile
+};
+TileCfg tune_tiles(int M, int N, int K, int T, bool packed);
+bool tile_cfg_valid(const TileCfg& c, int M, int N, int K, bool packed);
+
 // Per-row context for gathering A chunks (computed once per row per tile).
 struct RowCtx {
     long long pix;  // GEMM: m; conv: b*H*W (base pixel index of image b)

@@ -52,6 +52,7 @@ constexpr int kStgWarpBytes = 8192;  // store staging per epilogue warp (1024-al
 #define APNN_PROD_LANES 4
 #endif
 constexpr int kProdLanes = APNN_PROD_LANES;  // TMA-issuing lanes of the producer warp (2-CTA kernel)
+constexpr int kTunerT = 64;  // TLP threshold of the tiling heuristic (the paper's T, tuner.cu)
 // Development-only knobs (pipeline trace, skipped stores / B work -- the latter two give wrong
 // results by design) exist only in experiment builds: build.py --variant NAME -DAPNN_DEV=1.
 #ifndef APNN_DEV
@@ -1214,7 +1215,7 @@ static int halves_knob() {
 }
 
 static cudaError_t launch_tc_i8_impl(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
-                                     int sms, cudaStream_t s, const uint8_t* Wprep) {
+                                     int sms, cudaStream_t s, const uint8_t* Wprep, const TileCfg* force = nullptr) {
     using namespace tc;
     Params p;
     p.prep = Wprep ? 1 : 0;
@@ -1256,19 +1257,23 @@ static cudaError_t launch_tc_i8_impl(const uint32_t* A, const uint32_t* W, const
     const int ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
     bool two = (g.M > 128) && tc_kernel_override() != 1 && (!g.conv || conv2_fits(g));
     if (e.res && !two) return cudaErrorNotSupported;  // residual epilogue: 2-CTA kernel only (ABI checks first)
-    // small GEMMs (row f4): when the 2-CTA grid would occupy <= 1/4 of the SMs, run the
-    // 1-CTA kernel with split-K clusters instead (latency: more CTAs, fewer k-blocks each)
     if (Wprep && !two) return cudaErrorNotSupported;  // prepared W: 2-CTA kernel only
-    if (two && !g.conv && !e.res && !Wprep && g.M <= 1024 && g.nchunks >= 4 && tc_kernel_override() != 2) {
-        const int BNP = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
-        const long long pair_tiles = (long long)((g.M + 255) / 256) * ((g.N + BNP - 1) / BNP);
-        if (pair_tiles * 2 * 4 <= sms) two = false;
+    // plain GEMMs (row f4): the tile -- CTA pair 256 x bn, or one CTA 128 x bn with a split-K
+    // cluster of z CTAs -- comes from the paper's TLP/CI heuristic (tuner.cu), or the caller
+    TileCfg cfg{0, 0, 0, 1, 0, 0.0};
+    const bool tunable = !g.conv && !e.res && !Wprep && tc_kernel_override() == 0;
+    if (force) {
+        if (!tunable || !tile_cfg_valid(*force, g.M, g.N, g.K, e.out_bits > 0)) return cudaErrorNotSupported;
+        cfg = *force;
+    } else if (tunable) {
+        cfg = tune_tiles(g.M, g.N, g.K, kTunerT, e.out_bits > 0);
     }
+    if (cfg.kernel) two = cfg.kernel == 2;
     CUtensorMap ta, tb, ty;
     std::memset(&ty, 0, sizeof(ty));
     cudaError_t err;
     if (two) {
-        const int BNP = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);   // pair tile width
+        const int BNP = cfg.kernel ? cfg.bn : (g.N > 128 ? 256 : (g.N > 64 ? 128 : 64));   // pair tile width
         const int brows = BNP / 2;
         p.b_bytes = p.prep ? 0u : 16u * brows * g.w_bits;
         p.conv_box_stride = 0;
@@ -1381,7 +1386,10 @@ static cudaError_t launch_tc_i8_impl(const uint32_t* A, const uint32_t* W, const
         int BN = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
         // split-K over a cluster of Z CTAs when the output tiles alone leave SMs idle
         p.ksplit = 1;
-        if (tc_kernel_override() != 3) {
+        if (cfg.kernel) {
+            BN = cfg.bn;
+            p.ksplit = cfg.z;
+        } else if (tc_kernel_override() != 3) {
             const int BNs = g.N > 1024 ? 128 : 64;
             const long long tiles = (long long)((g.M + BM - 1) / BM) * ((ncols + BNs - 1) / BNs);
             int Z = 1;
@@ -1454,6 +1462,11 @@ static cudaError_t launch_tc_i8_impl(const uint32_t* A, const uint32_t* W, const
 cudaError_t launch_tc_i8(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y, int sms,
                          cudaStream_t s) {
     return launch_tc_i8_impl(A, W, g, e, Y, sms, s, nullptr);
+}
+
+cudaError_t launch_tc_i8_tiled(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
+                               const TileCfg& cfg, int sms, cudaStream_t s) {
+    return launch_tc_i8_impl(A, W, g, e, Y, sms, s, nullptr, &cfg);
 }
 
 cudaError_t launch_tc_i8_prepared(const uint32_t* A, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
