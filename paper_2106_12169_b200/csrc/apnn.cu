@@ -183,6 +183,12 @@ static apnn_variant resolve(apnn_variant v, const Geom& g, const Epi* e = nullpt
     if (fp4_enabled() && tc_fp4_supports(g) && fp4_tiles >= 64 && !(e && (e->res || e->pool)) &&
         (fused || g.N >= 256))
         return APNN_VARIANT_TC_FP4;
+    // latency-scale +-1 x +-1 GEMMs (Case II, the XNOR networks' FC layers): the warp-level
+    // popc/shuffle kernel beats every tensor-core launch below ~2^28 MACs (profiles/r02_popc_time.json:
+    // M = 64, N = K = 1024 in 3.6 us vs 7.8 us)
+    if (!g.conv && g.enc == APNN_ENC_PM1_PM1 && (long long)g.M * g.N * g.K <= (1LL << 28) && g.M <= 256 &&
+        !(e && (e->res || e->pool)))
+        return APNN_VARIANT_POPC;
     if (tc_i8_supports(g)) return APNN_VARIANT_TC_I8;
     return APNN_VARIANT_POPC;
 }

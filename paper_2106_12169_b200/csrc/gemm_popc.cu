@@ -17,12 +17,24 @@
 // plane index is just a shared-memory dimension = virtual batching,
 // PAPER.md:1528-1533).  The fused epilogue requantises into shared memory and
 // packs 32 columns per word.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace apnn {
 
 namespace {
 constexpr int BM = 64, BN = 64, NT = 256;
+}
+
+// APNN_POPC_WARP=0 (read once) keeps GEMMs on the tiled popc kernel (A/B measurements)
+static bool popc_warp_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("APNN_POPC_WARP");
+        v = s ? atoi(s) : 1;
+    }
+    return v != 0;
 }
 
 template <int ENC>
@@ -214,8 +226,162 @@ __global__ void __launch_bounds__(NT) popc_gemm_kernel(const uint32_t* __restric
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Warp-level variant for GEMMs (the north star's "warp-level popc/shuffle reductions"): a warp
+// owns MR rows x 32 columns of Y; lane l takes K words l, l+32, ... of every plane (coalesced
+// 128-byte loads of A and W rows), accumulates the bit-plane products of all MR x 32 outputs, and
+// a butterfly reduce-scatter over the warp (31 __shfl_xor per row, no shared memory) leaves
+// column n0 + l of each row in lane l.  The fused epilogue then packs each plane of the 32
+// requantised columns with one __ballot_sync (the paper's packing).
+// Latency-scale problems (the paper's FC layers, M <= 64) need one k-word per lane per plane.
+template <int ENC, int MR>
+__global__ void __launch_bounds__(128) popc_warp_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict__ Wt,
+                                                        Geom g, Epi e, void* __restrict__ Yout) {
+    const int lane = threadIdx.x & 31;
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int ntn = (g.N + 31) / 32;
+    const int m0 = (wid / ntn) * MR, n0 = (wid % ntn) * 32;
+    if (m0 >= g.M) return;  // whole warp
+    const int ab = g.a_bits, wb = g.w_bits, Kw = g.Cw;
+    int acc[MR][32], aux[MR][32];
+#pragma unroll
+    for (int r = 0; r < MR; r++)
+#pragma unroll
+        for (int j = 0; j < 32; j++) acc[r][j] = aux[r][j] = 0;
+    int rowpop[MR];  // Case III: sum_t 2^t popc(a_t) of the row (the J.X term)
+#pragma unroll
+    for (int r = 0; r < MR; r++) rowpop[r] = 0;
+    for (int kw = lane; kw < Kw; kw += 32) {
+        uint32_t a[MR][8];
+#pragma unroll
+        for (int r = 0; r < MR; r++) {
+            const bool in = m0 + r < g.M;
+#pragma unroll
+            for (int t = 0; t < 8; t++)
+                a[r][t] = (t < ab && in) ? __ldg(A + ((long long)(m0 + r) * ab + t) * Kw + kw) : 0u;
+        }
+        if (ENC == APNN_ENC_W_PM1_A_01) {
+#pragma unroll
+            for (int r = 0; r < MR; r++)
+#pragma unroll
+                for (int t = 0; t < 8; t++)
+                    if (t < ab) rowpop[r] += __popc(a[r][t]) << t;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; j++) {
+            const int n = n0 + j;
+            const bool nin = n < g.N;  // uniform (columns past N accumulate zeros)
+            const uint32_t* wp = Wt + (long long)(nin ? n : 0) * wb * Kw + kw;
+            if (ENC == APNN_ENC_01_01) {
+                for (int sp = 0; sp < wb; sp++) {
+                    const uint32_t w = nin ? __ldg(wp + (long long)sp * Kw) : 0u;
+#pragma unroll
+                    for (int r = 0; r < MR; r++) {
+                        int y = 0;
+#pragma unroll
+                        for (int t = 0; t < 8; t++)
+                            if (t < ab) y += __popc(a[r][t] & w) << t;
+                        acc[r][j] += y << sp;
+                    }
+                }
+            } else if (ENC == APNN_ENC_PM1_PM1) {
+                const uint32_t w = nin ? __ldg(wp) : 0u;
+#pragma unroll
+                for (int r = 0; r < MR; r++) acc[r][j] += __popc(a[r][0] ^ w);
+            } else if (ENC == APNN_ENC_W_PM1_A_01) {
+                const uint32_t w = nin ? __ldg(wp) : 0u;
+#pragma unroll
+                for (int r = 0; r < MR; r++) {
+                    int y = 0;
+#pragma unroll
+                    for (int t = 0; t < 8; t++)
+                        if (t < ab) y += __popc(a[r][t] & w) << t;
+                    acc[r][j] += y;
+                }
+            } else {  // APNN_ENC_W_01_A_PM1
+                for (int sp = 0; sp < wb; sp++) {
+                    const uint32_t w = nin ? __ldg(wp + (long long)sp * Kw) : 0u;
+                    const int pw = __popc(w) << sp;
+#pragma unroll
+                    for (int r = 0; r < MR; r++) {
+                        acc[r][j] += __popc(a[r][0] & w) << sp;
+                        aux[r][j] += pw;
+                    }
+                }
+            }
+        }
+    }
+    // encoding corrections, per lane partial sums over its k-words
+#pragma unroll
+    for (int r = 0; r < MR; r++)
+#pragma unroll
+        for (int j = 0; j < 32; j++) {
+            if (ENC == APNN_ENC_PM1_PM1) acc[r][j] = -2 * acc[r][j];  // K_valid added after the reduction
+            else if (ENC == APNN_ENC_W_PM1_A_01) acc[r][j] = 2 * acc[r][j] - rowpop[r];
+            else if (ENC == APNN_ENC_W_01_A_PM1) acc[r][j] = 2 * acc[r][j] - aux[r][j];
+        }
+    // butterfly reduce-scatter: after the step with distance d a lane keeps the half of its
+    // values whose index has bit d equal to its own lane bit, summed with its partner's
+    const int Nw = (g.N + 127) / 128 * 4;
+#pragma unroll
+    for (int r = 0; r < MR; r++) {
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) {
+            const bool up = (lane & d) != 0;
+#pragma unroll
+            for (int i = 0; i < d; i++) {
+                const int send = up ? acc[r][i] : acc[r][i + d];
+                const int keep = up ? acc[r][i + d] : acc[r][i];
+                acc[r][i] = keep + __shfl_xor_sync(0xffffffffu, send, d);
+            }
+        }
+        const int m = m0 + r, n = n0 + lane;
+        int y = acc[r][0];
+        if (ENC == APNN_ENC_PM1_PM1) y += g.K;  // K_valid - 2 popc(a XOR w) (padding bits agree)
+        if (m >= g.M) continue;  // uniform per row
+        if (e.out_bits == 0) {
+            if (n < g.N) reinterpret_cast<int32_t*>(Yout)[(long long)m * g.N + n] = y;
+        } else {
+            const uint32_t q = n < g.N ? requant(e, y, epi_alpha(e, n), epi_beta(e, n)) : 0u;
+            uint32_t* o = reinterpret_cast<uint32_t*>(Yout) + (long long)m * e.out_bits * Nw;
+            for (int t = 0; t < e.out_bits; t++) {
+                const uint32_t wv = __ballot_sync(0xffffffffu, (q >> t) & 1u);
+                if (lane == 0) o[(long long)t * Nw + n0 / 32] = wv;
+            }
+            if (n0 + 32 >= g.N && lane < Nw - (n0 / 32 + 1)) {  // N padding words of the row
+                for (int t = 0; t < e.out_bits; t++) o[(long long)t * Nw + n0 / 32 + 1 + lane] = 0u;
+            }
+        }
+    }
+}
+
+template <int MR>
+static void launch_popc_warp_mr(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
+                                cudaStream_t s) {
+    const long long warps = (long long)((g.M + MR - 1) / MR) * ((g.N + 31) / 32);
+    const int blocks = (int)((warps * 32 + 127) / 128);
+    switch (g.enc) {
+    case APNN_ENC_01_01: popc_warp_kernel<APNN_ENC_01_01, MR><<<blocks, 128, 0, s>>>(A, W, g, e, Y); break;
+    case APNN_ENC_PM1_PM1: popc_warp_kernel<APNN_ENC_PM1_PM1, MR><<<blocks, 128, 0, s>>>(A, W, g, e, Y); break;
+    case APNN_ENC_W_PM1_A_01: popc_warp_kernel<APNN_ENC_W_PM1_A_01, MR><<<blocks, 128, 0, s>>>(A, W, g, e, Y); break;
+    default: popc_warp_kernel<APNN_ENC_W_01_A_PM1, MR><<<blocks, 128, 0, s>>>(A, W, g, e, Y); break;
+    }
+}
+
+// GEMM rows per warp: MR = 1 for M <= 32, else 2
+static cudaError_t launch_popc_warp(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
+                                   cudaStream_t s) {
+    if (g.M <= 32) launch_popc_warp_mr<1>(A, W, g, e, Y, s);
+    else launch_popc_warp_mr<2>(A, W, g, e, Y, s);
+    count_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_popc(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
                         cudaStream_t s) {
+    // measured (profiles/r02_popc_time.json): the warp kernel wins for M <= 256, the tiled kernel
+    // (rows share the staged W chunk) above
+    if (!g.conv && g.M <= 256 && popc_warp_enabled()) return launch_popc_warp(A, W, g, e, Y, s);
     const int ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;  // packed: cover the padding words
     dim3 grid((ncols + BN - 1) / BN, (g.M + BM - 1) / BM);
     if (grid.x == 0 || grid.y == 0) return cudaSuccess;
