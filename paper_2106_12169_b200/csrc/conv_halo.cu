@@ -729,7 +729,7 @@ static bool make_w_map(CUtensorMap* m, const uint8_t* base, int N, int Kp, int r
 constexpr size_t kSmemMax = 227 * 1024;
 
 // Fill the tiling / buffering plan; false when the shape does not fit this kernel.
-static bool plan(const Geom& g, const Epi& e, Params& p) {
+static bool plan(const Geom& g, const Epi& e, Params& p, int sms = 148) {
     std::memset(&p, 0, sizeof(p));
     p.g = g;
     p.e = e;
@@ -753,13 +753,24 @@ static bool plan(const Geom& g, const Epi& e, Params& p) {
     p.set_bytes = (uint32_t)p.ncopy * p.copy_bytes;
     p.nsteps = g.RS * p.nchunk;
     p.bn = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
-    p.n_tiles = (g.N + p.bn - 1) / p.bn;
     p.tiles_c = (g.Wo + TW - 1) / TW;
     const long long rows_tiles = ((long long)p.B * p.Hv + TH - 1) / TH;
     const long long cta_tiles = rows_tiles * p.tiles_c;
     if (cta_tiles > (1LL << 30) || (long long)p.B * p.Hv > (1LL << 30)) return false;
     p.cta_tiles = (int)cta_tiles;
     p.pair_tiles = (p.cta_tiles + 1) / 2;
+    // narrower N tiles while fewer than half the CTA pairs would get a tile (measured on the C3
+    // layers at batch 64: 7x7 and 14x14 stride-2 maps run 10 % faster at bn = 128)
+    // (packed outputs keep whole 128-column words groups per tile: bn >= 128 unless N <= 64)
+    const int bn_min = (e.out_bits > 0 && g.N > 64) ? 128 : 64;
+    while (p.bn > bn_min && (long long)p.pair_tiles * ((g.N + p.bn - 1) / p.bn) < sms / 4) p.bn /= 2;
+#if APNN_DEV
+    {
+        const char* b = getenv("APNN_HALO_BN");
+        if (b && atoi(b) >= 64 && atoi(b) <= 256) p.bn = atoi(b);
+    }
+#endif
+    p.n_tiles = (g.N + p.bn - 1) / p.bn;
     p.num_tiles = p.pair_tiles * p.n_tiles;
     // epilogue: 2x2/2 max pooling of whole windows (tile rows/cols even, images start on even rows)
     if (e.pool) {
@@ -821,7 +832,7 @@ cudaError_t launch_conv_halo(const uint32_t* X, const uint8_t* Wp, const Geom& g
                              cudaStream_t s) {
     using namespace halo;
     Params p;
-    if (!plan(g, e, p)) return cudaErrorNotSupported;
+    if (!plan(g, e, p, sms)) return cudaErrorNotSupported;
     p.X = X;
     p.Y = Y;
 #if APNN_DEV
@@ -878,7 +889,7 @@ cudaError_t launch_conv_first(const uint8_t* X, const uint8_t* Wp, const Geom& g
                               int S_raw, int C_raw, void* Y, int sms, cudaStream_t s) {
     using namespace halo;
     Params p;
-    if (!conv_first_supports(g, e, S_raw, C_raw) || !plan(g, e, p)) return cudaErrorNotSupported;
+    if (!conv_first_supports(g, e, S_raw, C_raw) || !plan(g, e, p, sms)) return cudaErrorNotSupported;
     p.Xraw = X;
     p.Y = Y;
     p.raw = 1;
