@@ -362,8 +362,9 @@ __device__ __forceinline__ void mma_issuer(const Params& p, const uint32_t* sTap
             const int nkk = crem >= 128 ? 4 : (crem + 31) / 32;
             const uint64_t ads = ad0 + (uint64_t)((uint32_t)cb * set16);
             if (resident) s = ci * RS;
+            const int rs_end = (kDev && (p.exp & 32) && k > 0) ? 0 : RS;
 #pragma unroll
-            for (int rs = 0; rs < RS; rs++) {
+            for (int rs = 0; rs < rs_end; rs++) {
                 if (!resident || k == 0) {
                     mma_wait(&w_ready[s], resident ? 0u : wph);
                     tc_fence_after();
@@ -897,6 +898,15 @@ cudaError_t launch_conv_first(const uint8_t* X, const uint8_t* Wp, const Geom& g
     p.qs = qs;
     p.S_raw = S_raw;
     p.C_raw = C_raw;
+#if APNN_DEV
+    p.exp = getenv("APNN_HALO_EXP") ? atoi(getenv("APNN_HALO_EXP")) : 0;
+    const char* trace_path = getenv("APNN_HALO_TRACE");
+    const size_t tr_bytes = sizeof(unsigned long long) * 2 * TR_NEV * kTrN;
+    if (trace_path) {
+        cudaMalloc(&p.trace, tr_bytes);
+        cudaMemset(p.trace, 0, tr_bytes);
+    }
+#endif
     CUtensorMap tw;
     if (!make_w_map(&tw, Wp, g.N, g.RS * 128, p.bn / 2)) return cudaErrorInvalidValue;  // rows of R x 128 B
     int pairs = sms / 2;
@@ -907,6 +917,17 @@ cudaError_t launch_conv_first(const uint8_t* X, const uint8_t* Wp, const Geom& g
     cudaError_t err = wpm ? launch<false, true, false, true>(tw, p, 2 * pairs, smem, s)
                           : launch<false, false, false, true>(tw, p, 2 * pairs, smem, s);
     count_launch();
+#if APNN_DEV
+    if (p.trace) {
+        cudaStreamSynchronize(s);
+        unsigned long long* h = (unsigned long long*)malloc(tr_bytes);
+        cudaMemcpy(h, p.trace, tr_bytes, cudaMemcpyDeviceToHost);
+        FILE* f = fopen(trace_path, "wb");
+        if (f) { fwrite(h, 1, tr_bytes, f); fclose(f); }
+        free(h);
+        cudaFree(p.trace);
+    }
+#endif
     return err;
 }
 
