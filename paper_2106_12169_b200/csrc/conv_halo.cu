@@ -53,7 +53,9 @@ constexpr int TMA_WARP = FWD_WARP + 1;
 constexpr int MMA_WARP = TMA_WARP + 1;
 constexpr int THREADS = (MMA_WARP + 1) * 32;
 constexpr int MAX_WS = 40;  // weight stages (resident: all R*S*chunks of the N tile)
-constexpr int STG_WARP = 4352;  // per epilogue warp: int32 32 x 32 block; packed: 2 per quarter (32 x 68 words)
+// epilogue staging per warp: int32 32 x 32 block (4 KB); packed: mt = 1 two warps share 32 x 68 words
+// per quarter (2 x 4352 B), mt = 2 one warp owns 32 x 36 words (4608 B)
+constexpr int STG1 = 4352, STG2 = 4608;
 
 struct Params {
     Geom g;
@@ -80,6 +82,8 @@ struct Params {
     int tiles_c, cta_tiles, pair_tiles, n_tiles, num_tiles;
     int tab_mode, pool_fused, Hp, Wp;
     uint32_t tmem_cols;
+    int mt, th;           // 128-row sub-tiles per CTA tile (1 or 2) and the tile's tall rows (16 * mt)
+    int stg;              // epilogue staging bytes per warp (STG1 / STG2)
     int exp;              // experiment builds only (APNN_DEV): 1 skip decode, 2 skip MMAs, 4 skip epilogue
     unsigned long long* trace;  // experiment builds only: %globaltimer stamps of CTAs 0/1 (APNN_HALO_TRACE)
 };
@@ -317,7 +321,7 @@ __device__ __forceinline__ void tile_origin(const Params& p, int tile, uint32_t 
     const int pt = tile % p.pair_tiles, nt = tile / p.pair_tiles;
     ct = 2 * pt + (int)rank;
     const int rb = ct / p.tiles_c, cb = ct - rb * p.tiles_c;
-    v0 = rb * TH;
+    v0 = rb * p.th;
     w0 = cb * TW;
     n0 = nt * p.bn;
 }
@@ -326,7 +330,7 @@ __device__ __forceinline__ void tile_origin(const Params& p, int tile, uint32_t 
 // N=64 K=32 MMA runs in ~32 cycles), so everything it needs is loaded into registers before the
 // tile loop: with RST = 9 (3x3 filters) the tap loop is unrolled and the taps' A offsets are
 // registers; descriptors advance by 64-bit adds; ring counters are incremental.
-template <int RST, bool A_PM1, bool W_PM1>
+template <int RST, int MT, bool A_PM1, bool W_PM1>
 __device__ __forceinline__ void mma_issuer(const Params& p, const uint32_t* sTap, uint8_t* sCopy, uint8_t* sW,
                                         uint64_t* w_ready, uint64_t* w_empty, uint64_t* c_full, uint64_t* c_empty,
                                         uint64_t* a_full, uint64_t* a_empty, uint32_t tmem, int my_tiles) {
@@ -340,6 +344,8 @@ __device__ __forceinline__ void mma_issuer(const Params& p, const uint32_t* sTap
     const uint64_t ad0 = (umma_desc_sw128(smem_u32(sCopy), (uint32_t)p.cc8) & ~(7ull << 61)) | (swz << 61);
     const uint64_t bd0 = umma_desc_sw128(smem_u32(sW), 1024);
     const uint32_t set16 = p.set_bytes >> 4, wst16 = ((uint32_t)(bn / 2) * 128u) >> 4;
+    constexpr int mt = MT;
+    const uint32_t sub16 = (uint32_t)p.cc8;  // 16 copy rows (one 8-row swizzle atom each) = 16 * cc8 bytes, in 16-B units
     uint32_t toff[RST ? RST : 1];
     if (RST) {
 #pragma unroll
@@ -349,7 +355,7 @@ __device__ __forceinline__ void mma_issuer(const Params& p, const uint32_t* sTap
     uint32_t wph = 0, cph = 0;
     for (int k = 0; k < my_tiles; k++) {
         const int buf = k & 1;
-        const uint32_t dtm = tmem + (uint32_t)(buf * bn);
+        const uint32_t dtm = tmem + (uint32_t)(buf * mt * bn);
         mma_wait(&a_empty[buf], ((k >> 1) & 1) ^ 1);
         trace(p, TR_MMA_A, k);
         tc_fence_after();
@@ -376,6 +382,14 @@ __device__ __forceinline__ void mma_issuer(const Params& p, const uint32_t* sTap
                     if (nkk > 1) mma2_i8_ss(dtm, ad + 2, bd + 2, idesc, 1u);
                     if (nkk > 2) mma2_i8_ss(dtm, ad + 4, bd + 4, idesc, 1u);
                     if (nkk > 3) mma2_i8_ss(dtm, ad + 6, bd + 6, idesc, 1u);
+                    if (mt > 1) {  // second 128-row sub-tile: the A window 16 copy rows further, its own accumulator
+                        const uint64_t ad1 = ad + sub16;
+                        const uint32_t d1 = dtm + (uint32_t)bn;
+                        mma2_i8_ss(d1, ad1, bd, idesc, acc);
+                        if (nkk > 1) mma2_i8_ss(d1, ad1 + 2, bd + 2, idesc, 1u);
+                        if (nkk > 2) mma2_i8_ss(d1, ad1 + 4, bd + 4, idesc, 1u);
+                        if (nkk > 3) mma2_i8_ss(d1, ad1 + 6, bd + 6, idesc, 1u);
+                    }
                 }
                 acc = 1u;
                 if (!resident) {
@@ -403,8 +417,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint32_t WSTAGE = (uint32_t)(p.bn / 2) * 128u;
     uint8_t* sW = smem;                                             // ws x (bn/2 rows x 128 B), SWIZZLE_128B
     uint8_t* sCopy = sW + (size_t)p.ws * WSTAGE;                    // nbuf x set_bytes
-    uint8_t* sStg = sCopy + (size_t)p.nbuf * p.set_bytes;           // EPI_WARPS x STG_WARP
-    int32_t* sTab = reinterpret_cast<int32_t*>(sStg + EPI_WARPS * STG_WARP);  // bn x kTabStride
+    uint8_t* sStg = sCopy + (size_t)p.nbuf * p.set_bytes;           // EPI_WARPS x p.stg
+    int32_t* sTab = reinterpret_cast<int32_t*>(sStg + EPI_WARPS * p.stg);  // bn x kTabStride
     uint64_t* bars = reinterpret_cast<uint64_t*>(sTab + p.bn * kTabStride);
     uint64_t* w_full = bars;                  // [MAX_WS] local TMA completion
     uint64_t* w_empty = w_full + MAX_WS;      // [MAX_WS] local, MMA commit (multicast)
@@ -503,10 +517,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             }
             __syncwarp();
             if (lane == 0) {
-                if (g.RS == 9) mma_issuer<9, A_PM1, W_PM1>(p, sTap, sCopy, sW, w_ready, w_empty, c_full, c_empty,
-                                                            a_full, a_empty, tmem, my_tiles);
-                else mma_issuer<0, A_PM1, W_PM1>(p, sTap, sCopy, sW, w_ready, w_empty, c_full, c_empty, a_full,
-                                                  a_empty, tmem, my_tiles);
+                // one instantiation per (3x3 or not, sub-tiles): the single issuing thread runs
+                // straight-line code without branches for the other shapes
+                if (g.RS == 9 && p.mt == 2)
+                    mma_issuer<9, 2, A_PM1, W_PM1>(p, sTap, sCopy, sW, w_ready, w_empty, c_full, c_empty, a_full,
+                                                   a_empty, tmem, my_tiles);
+                else if (g.RS == 9)
+                    mma_issuer<9, 1, A_PM1, W_PM1>(p, sTap, sCopy, sW, w_ready, w_empty, c_full, c_empty, a_full,
+                                                   a_empty, tmem, my_tiles);
+                else if (p.mt == 2)
+                    mma_issuer<0, 2, A_PM1, W_PM1>(p, sTap, sCopy, sW, w_ready, w_empty, c_full, c_empty, a_full,
+                                                   a_empty, tmem, my_tiles);
+                else
+                    mma_issuer<0, 1, A_PM1, W_PM1>(p, sTap, sCopy, sW, w_ready, w_empty, c_full, c_empty, a_full,
+                                                   a_empty, tmem, my_tiles);
             }
         }
     } else if (warp < DEC_WARPS) {
@@ -555,15 +579,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         // stores whole 16-byte pieces of its own row (no shuffles, no divisions).
         const int e8 = warp - EPI0;
         const int qw = e8 & 3, half = e8 >> 2;
-        const int t = qw * 32 + lane;  // TMEM lane = tile row = hv * 8 + tw
+        // mt = 1: the two warps of a quarter split the columns (half); mt = 2: warp half takes
+        // sub-tile `half` (tile rows 128 * half + ...) with all the columns, its own staging
+        const int mt = p.mt, sub = mt > 1 ? half : 0, cstep = mt > 1 ? 32 : 64, c0 = mt > 1 ? 0 : half * 32;
+        const int t = sub * 128 + qw * 32 + lane;  // tile row = hv * 8 + tw (TMEM lane qw * 32 + lane)
         const int et = threadIdx.x - EPI0 * 32;
         const uint32_t tmem_lane = tmem + ((uint32_t)(qw * 32) << 16);
         const uint32_t a_empty0 = mapa(smem_u32(a_empty), 0);
         const int ob = p.e.out_bits;
         const int Nw = (g.N + 127) / 128 * 4;
         const int bn = p.bn;
-        uint8_t* stg_q = sStg + qw * (2 * STG_WARP);           // packed: the quarter's shared staging
-        uint8_t* stg_w = stg_q + half * STG_WARP;              // int32: this warp's own 32 x 32 block
+        uint8_t* stg_q = sStg + qw * (2 * p.stg) + (mt > 1 ? half * p.stg : 0);  // packed staging
+        uint8_t* stg_w = sStg + qw * (2 * p.stg) + half * p.stg;  // int32: this warp's own 32 x 32 block
         int cur_n0 = -1;
         for (int k = 0; k < my_tiles; k++) {
             int ct, v0, w0, n0;
@@ -591,11 +618,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             role_wait(&a_full[buf], (uint32_t)(k >> 1) & 1u);
             if (et == 0) trace(p, TR_EPI_GO, k);
             tc_fence_after();
-            for (int cc = half * 32; cc < bn; cc += 64) {
+            for (int cc = c0; cc < bn; cc += cstep) {
                 if (kDev && (p.exp & 4)) break;
                 if (ob > 0 && (n0 + cc) / 32 >= Nw) break;  // past the last packed word (ragged last N tile)
                 uint32_t acc[32];
-                tmem_ld32(tmem_lane + (uint32_t)(buf * bn) + cc, acc);
+                tmem_ld32(tmem_lane + (uint32_t)((buf * mt + sub) * bn) + cc, acc);
                 tmem_wait_ld();
                 if (p.pool_fused) {
                     // 2x2/2 max pooling on the codes (q is non-decreasing in v, reading R15):
@@ -659,7 +686,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             if (lane == 0) mbar_arrive_cluster(a_empty0 + 8u * (uint32_t)buf);
             if (et == 0) trace(p, TR_EPI_DONE, k);
             if (p.pool_fused) {
-                if (half == 0 && n0 + bn >= g.N && valid && (tw & 1) == 0 && (hv & 1) == 0) {  // N padding words
+                if ((mt > 1 || half == 0) && n0 + bn >= g.N && valid && (tw & 1) == 0 && (hv & 1) == 0) {  // N padding
                     const long long prow = ((long long)b * p.Hp + (ho >> 1)) * p.Wp + (wo >> 1);
                     uint32_t* o = reinterpret_cast<uint32_t*>(p.Y) + prow * ob * Nw;
                     for (int tb = 0; tb < ob; tb++)
@@ -667,19 +694,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 }
             } else if (ob > 0) {
                 // padding words past the tile's columns (last N tile) are zero
-                for (int wi = bn / 32 + half; wi < nwt; wi += 2)
+                for (int wi = bn / 32 + (mt > 1 ? 0 : half); wi < nwt; wi += (mt > 1 ? 1 : 2))
                     for (int tb = 0; tb < ob; tb++) srow[tb * nwt + wi] = 0u;
-                named_bar_sync(2 + qw, 64);  // both warps of the quarter staged their words
+                if (mt > 1) __syncwarp();
+                else named_bar_sync(2 + qw, 64);  // both warps of the quarter staged their words
                 if (m < g.M) {
                     uint32_t* orow = reinterpret_cast<uint32_t*>(p.Y) + (long long)m * ob * Nw + n0 / 32;
                     const int pw = nwt >> 2;  // 16-byte pieces per plane
-                    for (int pc = half; pc < ob * pw; pc += 2) {
+                    for (int pc = (mt > 1 ? 0 : half); pc < ob * pw; pc += (mt > 1 ? 1 : 2)) {
                         const int tb = pw == 1 ? pc : pc >> 1, wq = pw == 1 ? 0 : (pc & 1) * 4;
                         *reinterpret_cast<uint4*>(orow + tb * Nw + wq) =
                             *reinterpret_cast<const uint4*>(srow + tb * nwt + wq);
                     }
                 }
-                named_bar_sync(2 + qw, 64);  // staging free for the next tile
+                if (mt > 1) __syncwarp();
+                else named_bar_sync(2 + qw, 64);  // staging free for the next tile
             }
         }
     }
@@ -742,6 +771,9 @@ static bool plan(const Geom& g, const Epi& e, Params& p, int sms = 148) {
     if (e.pool && (p.Hv & 1)) p.Hv++;  // pooled windows must start on even tall rows (one more separator)
     p.nrho = g.stride < R ? g.stride : R;
     p.ncopy = p.nrho * g.S;
+    p.mt = 1;
+    p.th = TH;
+    p.stg = STG1;
     p.crow = TH + p.E;
     p.cl = g.C > 64 ? 128 : (g.C > 32 ? 64 : 32);
     p.cc8 = p.cl * 8;
@@ -773,6 +805,33 @@ static bool plan(const Geom& g, const Epi& e, Params& p, int sms = 148) {
 #endif
     p.n_tiles = (g.N + p.bn - 1) / p.bn;
     p.num_tiles = p.pair_tiles * p.n_tiles;
+    // two 128-row sub-tiles per CTA tile (32 tall rows) when the N tile leaves TMEM room for two
+    // double-buffered accumulators and every pair still gets >= 2 tiles: the per-tile hand-offs
+    // and the MMA issuer's per-tap work are paid once per 256 rows
+    {
+        const long long rt2 = ((long long)p.B * p.Hv + 2 * TH - 1) / (2 * TH);
+        const long long pt2 = (rt2 * p.tiles_c + 1) / 2;
+        const size_t set2 = (size_t)p.ncopy * (2 * TH + p.E) * p.cc8;
+        const size_t fixed2 = EPI_WARPS * (size_t)STG2 + (size_t)p.bn * kTabStride * 4 + (3 * MAX_WS + 8) * 8 +
+                              16 + 4 * 64 + 256 + 1024;
+        bool two = p.bn <= 128 && pt2 * p.n_tiles >= 2LL * (sms / 2) &&
+                   fixed2 + 2 * set2 + 4 * (size_t)(p.bn / 2) * 128 <= kSmemMax;
+#if APNN_DEV
+        if (getenv("APNN_HALO_MT"))
+            two = atoi(getenv("APNN_HALO_MT")) == 2 && p.bn <= 128 && fixed2 + 2 * set2 + 4 * (size_t)(p.bn / 2) * 128 <= kSmemMax;
+#endif
+        if (two) {
+            p.mt = 2;
+            p.stg = STG2;
+            p.th = 2 * TH;
+            p.crow = p.th + p.E;
+            p.copy_bytes = (uint32_t)(p.crow * p.cc8);
+            p.set_bytes = (uint32_t)p.ncopy * p.copy_bytes;
+            p.cta_tiles = (int)(rt2 * p.tiles_c);
+            p.pair_tiles = (p.cta_tiles + 1) / 2;
+            p.num_tiles = p.pair_tiles * p.n_tiles;
+        }
+    }
     // epilogue: 2x2/2 max pooling of whole windows (tile rows/cols even, images start on even rows)
     if (e.pool) {
         if (!(e.pool == 2 && e.pool_stride == 2 && !e.pool_avg && e.out_bits > 0 && g.Ho % 2 == 0 &&
@@ -789,7 +848,7 @@ static bool plan(const Geom& g, const Epi& e, Params& p, int sms = 148) {
         p.tab_mode = kTabHybrid;
     // shared memory: weights + copies + store staging + table + barriers
     const size_t wstage = (size_t)(p.bn / 2) * 128;
-    const size_t fixed = EPI_WARPS * (size_t)STG_WARP + (size_t)p.bn * kTabStride * 4 + (3 * MAX_WS + 8) * 8 + 16 + 4 * 64 + 256 + 1024;
+    const size_t fixed = EPI_WARPS * (size_t)p.stg + (size_t)p.bn * kTabStride * 4 + (3 * MAX_WS + 8) * 8 + 16 + 4 * 64 + 256 + 1024;
     if (fixed + p.set_bytes + 2 * wstage > kSmemMax) return false;
     const size_t budget = kSmemMax - fixed;
     if (p.n_tiles == 1 && p.nsteps <= MAX_WS && (size_t)p.nsteps * wstage + 2 * (size_t)p.set_bytes <= budget) {
@@ -803,12 +862,16 @@ static bool plan(const Geom& g, const Epi& e, Params& p, int sms = 148) {
         if (ws < 2) return false;
         p.ws = (int)ws;
     }
-    p.tmem_cols = p.bn == 64 ? 128 : (p.bn == 128 ? 256 : 512);
+    {
+        uint32_t cols = 32;
+        while (cols < (uint32_t)(2 * p.mt * p.bn)) cols <<= 1;
+        p.tmem_cols = cols;
+    }
     return true;
 }
 
 static size_t smem_bytes(const Params& p) {
-    return (size_t)p.ws * (p.bn / 2) * 128 + (size_t)p.nbuf * p.set_bytes + EPI_WARPS * (size_t)STG_WARP +
+    return (size_t)p.ws * (p.bn / 2) * 128 + (size_t)p.nbuf * p.set_bytes + EPI_WARPS * (size_t)p.stg +
            (size_t)p.bn * kTabStride * 4 + (3 * MAX_WS + 8) * 8 + 16 + 4 * 64 + 256;
 }
 

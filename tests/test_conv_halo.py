@@ -214,3 +214,67 @@ def test_first_layer_rejects():
     cs = ap.ConvShape(1, 32, 32, 3, 16, 7, 7, 2, 3)
     assert not ap.conv_first_fits(cs, 1, 1, 1)                            # +-1 activations: codes are 0/1
     assert not ap.conv_first_fits(ap.ConvShape(1, 32, 32, 16, 16, 3, 9, 1, 1), 2, 1, 2)  # window 144 > 128 bytes
+
+
+# ------------------------------------------------ two 128-row sub-tiles per CTA tile (mt = 2)
+
+MT2_SHAPES = [  # enough tiles that the plan takes 32-row CTA tiles (>= 2 pair tiles per pair, copies fit)
+    (32, 56, 56, 64, 64, 3, 3, 1, 1),      # ResNet L1: W resident, bn = 64
+    (32, 56, 56, 64, 128, 3, 3, 1, 1),     # bn = 128
+    (48, 30, 30, 32, 96, 3, 3, 1, 1),      # C_in = 32 (32-byte copy rows), N = 96, 30 = 3 x 8 + 6 columns
+    (24, 28, 28, 128, 128, 3, 3, 1, 1),    # copies too large for two sub-tiles: one sub-tile
+]
+
+
+@pytest.mark.parametrize("shape", MT2_SHAPES)
+@pytest.mark.parametrize("a_bits,w_bits,enc", [(2, 1, 2), (8, 2, 0)])
+def test_halo_conv_two_subtiles(shape, a_bits, w_bits, enc):
+    B, H, Wd, C, Co, R, S, st, pad = shape
+    X, Wt, Xp, cs = _setup(shape, a_bits, w_bits, "halomt2")
+    Wprep = _prep(Wt, shape, w_bits, enc)
+    got = ap.conv2d_prepared_i8(Xp, Wprep, cs, a_bits, w_bits, enc)
+    alpha, beta = synth.epilogue_params(Co, tag="halomt2")
+    epi = ap.Epilogue(a_bits, cuda(alpha), cuda(beta), 37)
+    gotp = ap.conv2d_prepared_i8(Xp, Wprep, cs, a_bits, w_bits, enc, epi=epi)
+    torch.cuda.synchronize()
+    want = oracle.conv2d(X, Wt, st, pad, a_bits, w_bits, enc)
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+    np.testing.assert_array_equal(u32(gotp), oracle.pack(oracle.epilogue(want.reshape(-1, Co), alpha, beta, 37,
+                                                                          a_bits), a_bits))
+    if cs.Ho % 2 == 0 and cs.Wo % 2 == 0 and st == 1:
+        epip = ap.Epilogue(a_bits, cuda(alpha), cuda(beta), 37, pool=2, pool_stride=2)
+        gotq = ap.conv2d_prepared_i8(Xp, Wprep, cs, a_bits, w_bits, enc, epi=epip)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(u32(gotq), oracle.pack(
+            oracle.pool_epilogue(want, alpha, beta, 37, a_bits, 2, 2).reshape(-1, Co), a_bits))
+    if enc == 0 and st == 1 and C == Co:  # residual with the block input's packed codes as shortcut
+        M = want.reshape(-1, Co).shape[0]
+        rho = synth.rng("mt2rho").integers(-2, 3, size=Co).astype(np.int32)
+        epir = ap.Epilogue(a_bits, cuda(alpha), cuda(beta), 37, residual=Xp, residual_bits=a_bits, rho=cuda(rho))
+        gotr = ap.conv2d_prepared_i8(Xp, Wprep, cs, a_bits, w_bits, enc, epi=epir)
+        torch.cuda.synchronize()
+        wantr = oracle.residual_epilogue(want.reshape(-1, Co), X.reshape(-1, C), alpha, beta, rho, 37, a_bits)
+        np.testing.assert_array_equal(u32(gotr), oracle.pack(wantr, a_bits))
+
+
+def test_first_layer_two_subtiles_stem():
+    # the ResNet / VGG stem at batch 16: 32-row CTA tiles, fused 2x2 pooling + 8-bit requantisation
+    shape = (16, 224, 224, 3, 64, 7, 7, 2, 3)
+    B, H, Wd, C, Co, R, S, st, pad = shape
+    a_bits, w_bits, enc = 8, 2, 0
+    g = synth.rng("first:mt2")
+    x = g.integers(0, 256, size=(B, H, Wd, C)).astype(np.uint8)
+    Wt = synth.codes((Co, R, S, C), w_bits, "first:mt2:w")
+    Xq = oracle.quantize_input(x, 5, 3, a_bits)
+    want = oracle.conv2d(Xq, Wt, st, pad, a_bits, w_bits, enc)
+    cs = ap.ConvShape(*shape)
+    Wq = ap.prepare_first_weights_i8(ap.pack_bits(cuda(Wt.reshape(Co * R, S * C)), w_bits), cs, w_bits, enc)
+    alpha, beta = synth.epilogue_params(Co, tag="firstmt2")
+    epi = ap.Epilogue(a_bits, cuda(alpha), cuda(beta), 37, pool=2, pool_stride=2)
+    X = cuda(x)
+    got = ap.conv2d_first_prepared_i8(X, Wq, cs, 5, 3, a_bits, w_bits, enc)
+    gotq = ap.conv2d_first_prepared_i8(X, Wq, cs, 5, 3, a_bits, w_bits, enc, epi=epi)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+    np.testing.assert_array_equal(u32(gotq), oracle.pack(
+        oracle.pool_epilogue(want, alpha, beta, 37, a_bits, 2, 2).reshape(-1, Co), a_bits))
