@@ -5,9 +5,11 @@ Workload (BASELINE.json configs[1], the GEMM sweep the metric is quoted on;
 its largest point): M = N = K = 8192, w1a2, 0/1 activations x +-1 weights
 (Case III).  One step = the whole hot path over one batch:
     apnn_pack_bits(A codes)                      row a1 (bit decomposition)
-    apnn_gemm_fused(A planes, W planes, epi)     rows a2-a5 + a7 (contraction,
-                                                 combination, requant + repack)
-W is packed once at init (weights are quantised before inference).
+    apnn_prepare_activations(A planes)           row a4 on A's side (planes -> e2m1 operand
+                                                 rows, once per step instead of per N tile)
+    apnn_gemm_prepared_ab(A op, W op, epi)       rows a2-a5 + a7 (contraction on the fp4 pipe,
+                                                 exact; requant + repack fused)
+W is packed and prepared once at init (weights are static).
 metric: effective TOPS = 2 M N K / step time (logical integer MACs x 2).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -60,6 +62,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-models", action="store_true")
     ap.add_argument("--no-prepared", action="store_true", help="FP4 kernel with per-tile W recombination")
+    ap.add_argument("--no-prepared-a", action="store_true",
+                    help="A planes decoded inside the GEMM (apnn_gemm_prepared) instead of once per step")
     ap.add_argument("--model-batch", type=int, default=256, help="global batch of AlexNet / VGG-Variant")
     ap.add_argument("--resnet-batch", type=int, default=1024, help="global batch of ResNet-18 w2a8")
     return ap.parse_args()
@@ -297,6 +301,10 @@ def run_ours(args):
     if variant in (0, ap.VARIANT_TC_FP4) and ap.select_variant(M, N, K, a, w, enc, out_bits) == ap.VARIANT_TC_FP4 \
             and not args.no_prepared:
         W_prep = ap.prepare_weights(W_planes, N, K, w, enc)
+    # the activations' operand rows are decoded once per step (apnn_prepare_activations, inside
+    # the timed step) instead of once per N tile inside the GEMM
+    prep_a = W_prep is not None and a <= 2 and not args.no_prepared_a
+    A_prep = None
     epi = ap.Epilogue(out_bits, torch.from_numpy(alpha_np).to(dev), torch.from_numpy(beta_np).to(dev), S)
     A_planes = torch.empty(ap.packed_shape(M, K, a), dtype=torch.int32, device=dev)
     Y_packed = torch.empty(ap.packed_shape(M, N, out_bits), dtype=torch.int32, device=dev)
@@ -308,11 +316,18 @@ def run_ours(args):
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
+    if prep_a:
+        A_prep = ap.prepare_activations(A_planes, M, K, a, enc)
+
     def step(ev_g0=None, ev_g1=None):
         ap.pack_bits(A_codes, a, out=A_planes)
+        if prep_a:
+            ap.prepare_activations(A_planes, M, K, a, enc, out=A_prep.data)
         if ev_g0 is not None:
             ev_g0.record(stream)
-        if W_prep is not None:
+        if prep_a:
+            ap.gemm_prepared_ab(A_prep, W_prep, M, N, K, a, w, enc, epi=epi, out=Y_packed)
+        elif W_prep is not None:
             ap.gemm_prepared(A_planes, W_prep, M, N, K, a, w, enc, epi=epi, out=Y_packed)
         else:
             ap.gemm(A_planes, W_planes, M, N, K, a, w, enc, epi=epi, variant=variant, out=Y_packed)
@@ -389,6 +404,7 @@ def run_ours(args):
         Y_host = [torch.empty(tuple(Y_packed.shape), dtype=torch.int32).pin_memory() for _ in range(2)]
         A_dev = [torch.empty_like(A_codes) for _ in range(2)]
         P_dev = [torch.empty_like(A_planes) for _ in range(2)]
+        Q_dev = [ap.prepare_activations(A_planes, M, K, a, enc) for _ in range(2)] if prep_a else None
         Y_dev = [torch.empty_like(Y_packed) for _ in range(2)]
         s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         ev = lambda: torch.cuda.Event()
@@ -405,9 +421,13 @@ def run_ours(args):
                 stream.wait_event(up)
                 ap.pack_bits(A_dev[b], a, out=P_dev[b])
                 packed_ev[b] = ev(); packed_ev[b].record(stream)
+                if prep_a:
+                    ap.prepare_activations(P_dev[b], M, K, a, enc, out=Q_dev[b].data)
                 if d2h_ev[b] is not None:
                     stream.wait_event(d2h_ev[b])              # Y_dev[b] downloaded
-                if W_prep is not None:
+                if prep_a:
+                    ap.gemm_prepared_ab(Q_dev[b], W_prep, M, N, K, a, w, enc, epi=epi, out=Y_dev[b])
+                elif W_prep is not None:
                     ap.gemm_prepared(P_dev[b], W_prep, M, N, K, a, w, enc, epi=epi, out=Y_dev[b])
                 else:
                     ap.gemm(P_dev[b], W_planes, M, N, K, a, w, enc, epi=epi, variant=variant, out=Y_dev[b])
@@ -451,12 +471,12 @@ def run_ours(args):
     peak, peak_src = int8_peak_tops(peaks, fp4=fp4)
     achieved = ops / (gemm_avg_ms * 1e-3) / 1e12
     # which kernel ran (the library's dispatch: prepared W with M > 128 -> the CTA-pair kernel)
-    kname = (("fp4_pair_kernel" if M > 128 else "fp4_kernel") if W_prep is not None
+    kname = ("fp4_pp_kernel" if prep_a else ("fp4_pair_kernel" if M > 128 else "fp4_kernel") if W_prep is not None
              else ap.variant_name(resolved))
     traffic = None
     try:
         summ = json.load(open(NCU_SUMMARY))
-        key = f"{M}x{N}x{K}_w{w}a{a}_enc{enc}_{kname}" + ("_prepared" if W_prep is not None else "")
+        key = f"{M}x{N}x{K}_w{w}a{a}_enc{enc}_{kname}" + ("_prepared" if W_prep is not None and not prep_a else "")
         traffic = summ.get("traffic_bytes_per_launch", {}).get(key)
     except Exception:
         pass
@@ -476,16 +496,18 @@ def run_ours(args):
         "config": {"workload": f"apmm_w{w}a{a}_{M if args.scaling == 'weak' else M_global}x{N}x{K}_fused_pack",
                    "M": M_global, "M_per_rank": M, "N": N, "K": K, "a_bits": a,
                    "w_bits": w, "encoding": ENC_NAME[enc], "out": f"packed {out_bits}-bit (fused requant)",
-                   "step": "apnn_pack_bits(A) + " + ("apnn_gemm_prepared (W prepared at init)" if W_prep is not None
-                                                      else "apnn_gemm_fused"),
-                   "variant": ap.variant_name(resolved) + ("_prepared" if W_prep is not None else ""),
+                   "step": "apnn_pack_bits(A) + " + (
+                       "apnn_prepare_activations(A planes) + apnn_gemm_prepared_ab (W prepared at init)" if prep_a
+                       else "apnn_gemm_prepared (W prepared at init)" if W_prep is not None else "apnn_gemm_fused"),
+                   "variant": ap.variant_name(resolved) + ("_prepared_ab" if prep_a else "_prepared" if W_prep is not None
+                                                           else ""),
                    "parallelism": f"dp{world} (" + ("M-row batch per GPU" if args.scaling == "weak"
                                                     else "global M sharded by rows") + ", W replicated)",
                    "l2": "flushed (512 MB write) between timed steps", "allgather": bool(gathered is not None)},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": f"{kname} (apnn {ap.variant_name(resolved)} GEMM, fused epilogue"
-                               + (", prepared W)" if W_prep is not None else ")"),
+                               + (", prepared A and W)" if prep_a else ", prepared W)" if W_prep is not None else ")"),
                      "kernel_ms": gemm_avg_ms, "kernel_share_of_step": gemm_avg_ms / ms_per_step,
                      "peak_source": peak_src,
                      "peak_mma_microbench": micro,

@@ -260,6 +260,25 @@ apnn_status apnn_gemm_prepared(const uint32_t *A, const uint8_t *Wp, int M, int 
                                int w_bits, apnn_encoding enc, const apnn_epilogue *epi, void *Y,
                                apnn_stream_t stream);
 
+/* Prepared activations (both operands prepared; the bench GEMM).  An activation matrix is used
+ * by every N tile of a GEMM, so decoding its bit-planes inside the GEMM repeats the decode
+ * ceil(N / 256) times; apnn_prepare_activations decodes them once (the operand-side bit
+ * combination of PAPER.md:1426-1429, +-1 codes per Case II / III) into the
+ * e2m1 operand rows of apnn_prepare_weights:
+ *   A:  device, packed activation planes [M][a_bits][Kw] (apnn_pack_bits layout), a_bits <= 2
+ *       (+-1 activations, enc APNN_ENC_PM1_PM1 / APNN_ENC_W_01_A_PM1: a_bits == 1);
+ *   Ap: device, apnn_prepared_bytes(M, K) bytes, caller-owned; elements >= K are value 0.
+ * apnn_gemm_prepared_ab: Y = A W^T from Ap and Wp (apnn_prepare_weights) on the persistent
+ * CTA-pair exact-FP4 kernel (both operands land by TMA; no CUDA-core decode in the main loop);
+ * int32 when epi == NULL, else the fused requantise + pack routine (no pooling / residual).
+ * Same results as apnn_gemm_ex.  APNN_ERR_UNSUPPORTED where apnn_gemm_prepared is. Asynchronous
+ * on `stream`; no allocation. */
+apnn_status apnn_prepare_activations(const uint32_t *A, int M, int K, int a_bits, apnn_encoding enc,
+                                     uint8_t *Ap, apnn_stream_t stream);
+apnn_status apnn_gemm_prepared_ab(const uint8_t *Ap, const uint8_t *Wp, int M, int N, int K, int a_bits,
+                                  int w_bits, apnn_encoding enc, const apnn_epilogue *epi, void *Y,
+                                  apnn_stream_t stream);
+
 /* Prepared int8 weights for the int8 tensor-core kernel (any w_bits; the B decode that grows
  * with w_bits is done once at load time):
  *   Wp: device, apnn_prepared_i8_bytes(N, K) bytes: int8 operand rows [N][roundup(K,128)] in

@@ -42,6 +42,8 @@ cudaError_t launch_tc_fp4_prepared(const uint32_t* A, const uint8_t* Wp, const G
                                    cudaStream_t s);
 cudaError_t launch_prepare_weights(const uint32_t* W, int N, int K, int w_bits, int enc, uint8_t* out, int sms,
                                    cudaStream_t s);
+cudaError_t launch_tc_fp4_pair_prepared_ab(const uint8_t* Ap, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
+                                           int sms, cudaStream_t s);
 cudaError_t launch_tc_fp4_pair_prepared(const uint32_t* A, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
                                         int sms, cudaStream_t s);
 cudaError_t launch_prepare_weights_i8(const uint32_t* W, int N, int K, int w_bits, int enc, uint8_t* out, int sms,
@@ -183,11 +185,13 @@ static apnn_variant resolve(apnn_variant v, const Geom& g, const Epi* e = nullpt
     if (fp4_enabled() && tc_fp4_supports(g) && fp4_tiles >= 64 && !(e && (e->res || e->pool)) &&
         (fused || g.N >= 256))
         return APNN_VARIANT_TC_FP4;
-    // latency-scale +-1 x +-1 GEMMs (Case II, the XNOR networks' FC layers): the warp-level
-    // popc/shuffle kernel beats every tensor-core launch below ~2^28 MACs (profiles/r02_popc_time.json:
-    // M = 64, N = K = 1024 in 3.6 us vs 7.8 us)
-    if (!g.conv && g.enc == APNN_ENC_PM1_PM1 && (long long)g.M * g.N * g.K <= (1LL << 28) && g.M <= 256 &&
-        !(e && (e->res || e->pool)))
+    // latency-scale GEMMs with 1-bit weights and <= 2-bit activations (the paper's FC layers):
+    // the warp-level popc/shuffle kernel beats every tensor-core launch up to ~2^28 plane-bit
+    // MACs (profiles/r02_popc_time.json: M = 64, N = K = 1024 w1a2 4.1 us vs 8.1 us, w1a1 3.4 vs
+    // 7.8; 128^3 w1a2 3.2 vs 5.1; M = 1, N = K = 4096 w1a2 5.8 vs 15.2); wider weights loop over
+    // their planes and lose
+    if (!g.conv && g.w_bits == 1 && g.a_bits <= 2 && g.M <= 256 &&
+        (long long)g.M * g.N * g.K * g.a_bits <= (1LL << 28) && !(e && (e->res || e->pool)))
         return APNN_VARIANT_POPC;
     if (tc_i8_supports(g)) return APNN_VARIANT_TC_I8;
     return APNN_VARIANT_POPC;
@@ -371,6 +375,45 @@ apnn_status apnn_gemm_prepared(const uint32_t* A, const uint8_t* Wp, int M, int 
     cudaError_t err = (M > 128 && fp4_kernel_choice() != 1)
                           ? launch_tc_fp4_pair_prepared(A, Wp, g, e, Y, d.sms, (cudaStream_t)stream)
                           : launch_tc_fp4_prepared(A, Wp, g, e, Y, (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_status apnn_prepare_activations(const uint32_t* A, int M, int K, int a_bits, apnn_encoding enc, uint8_t* Ap,
+                                     apnn_stream_t stream) {
+    if (M < 0 || K < 0) return APNN_ERR_SHAPE;
+    apnn_status st = APNN_OK;
+    if (a_bits < 1 || a_bits > 8) return APNN_ERR_BITS;
+    if (enc < 0 || enc > 3) return APNN_ERR_ENCODING;
+    const bool apm = enc == APNN_ENC_PM1_PM1 || enc == APNN_ENC_W_01_A_PM1;
+    if (apm && a_bits != 1) return APNN_ERR_ENCODING;
+    if (a_bits > 2) return APNN_ERR_UNSUPPORTED;
+    if (M > 0 && K > 0 && (!A || !Ap)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(A) || !aligned16(Ap)) return APNN_ERR_ALIGNMENT;
+    DevInfo d;
+    if ((st = device_info(&d)) != APNN_OK) return st;
+    // the operand rows of apnn_prepare_weights, with the +-1 decision taken on A's side
+    cudaError_t err = launch_prepare_weights(A, M, K, a_bits, apm ? APNN_ENC_PM1_PM1 : APNN_ENC_01_01, Ap, d.sms,
+                                             (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_status apnn_gemm_prepared_ab(const uint8_t* Ap, const uint8_t* Wp, int M, int N, int K, int a_bits, int w_bits,
+                                  apnn_encoding enc, const apnn_epilogue* epi, void* Y, apnn_stream_t stream) {
+    if (M < 0 || N < 0 || K < 0) return APNN_ERR_SHAPE;
+    apnn_status st = check_bits_enc(a_bits, w_bits, enc);
+    if (st != APNN_OK) return st;
+    if ((M > 0 && K > 0 && !Ap) || (N > 0 && K > 0 && !Wp) || (M > 0 && N > 0 && !Y)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(Ap) || !aligned16(Wp) || !aligned16(Y)) return APNN_ERR_ALIGNMENT;
+    Epi e;
+    if ((st = make_epi(epi, &e)) != APNN_OK) return st;
+    if (e.pool || e.res) return APNN_ERR_INVALID_ARG;
+    Geom g;
+    gemm_geom(&g, M, N, K, a_bits, w_bits, enc);
+    if (!tc_fp4_supports(g)) return APNN_ERR_UNSUPPORTED;
+    DevInfo d;
+    if ((st = device_info(&d)) != APNN_OK) return st;
+    if (M == 0 || N == 0) return APNN_OK;
+    cudaError_t err = launch_tc_fp4_pair_prepared_ab(Ap, Wp, g, e, Y, d.sms, (cudaStream_t)stream);
     return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }
 

@@ -130,23 +130,36 @@ __device__ __forceinline__ void recomb_row(const uint8_t* planes, int rows, int 
 template <int NB, bool PM1>
 __global__ void __launch_bounds__(256) prepare_kernel(const uint32_t* __restrict__ W, int N, int K, int Kw,
                                                       uint8_t* __restrict__ out) {
-    const long long total = (long long)N * Kw;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const long long n = idx / Kw;
-        const int gidx = (int)(idx - n * Kw);
-        uint32_t pw[2] = {0u, 0u};
+    // a thread takes 4 consecutive groups (one 16-byte word of each plane, Kw is a multiple of 4):
+    // 32-bit index math only (the 64-bit division of a flat index was the kernel's cost)
+    const int Kq = Kw / 4;
+    for (int n = blockIdx.y * blockDim.y + threadIdx.y; n < N; n += gridDim.y * blockDim.y) {
+        const uint32_t* wrow = W + (long long)n * NB * Kw;
+        uint8_t* orow = out + (long long)n * Kw * 16;
+        for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Kq; q += gridDim.x * blockDim.x) {
+            uint4 pv[2];
 #pragma unroll
-        for (int pl = 0; pl < NB; pl++) pw[pl] = __ldg(W + (n * NB + pl) * Kw + gidx);
-        const int nv = K - gidx * 32;
-        const uint32_t vm = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
-        uint32_t o[4];
-        decode_group_fp4<NB, PM1>(pw, vm, true, o);
-        if (!PM1) {  // 0/1 codes: padding bits are zero already; mask anyway (robust to dirty padding)
+            for (int pl = 0; pl < NB; pl++) pv[pl] = __ldg(reinterpret_cast<const uint4*>(wrow + (long long)pl * Kw) + q);
+            uint4 o4[4];
 #pragma unroll
-            for (int j = 0; j < 4; j++) o[j] &= ((vm >> j) & 0x11111111u) * 0xFu;
+            for (int gi = 0; gi < 4; gi++) {
+                const int gidx = q * 4 + gi;
+                uint32_t pw[2] = {0u, 0u};
+#pragma unroll
+                for (int pl = 0; pl < NB; pl++) pw[pl] = tc::sel4(pv[pl], gi);
+                const int nv = K - gidx * 32;
+                const uint32_t vm = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
+                uint32_t o[4];
+                decode_group_fp4<NB, PM1>(pw, vm, true, o);
+                if (!PM1) {  // 0/1 codes: padding bits are zero already; mask anyway (robust to dirty padding)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) o[j] &= ((vm >> j) & 0x11111111u) * 0xFu;
+                }
+                o4[gi] = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+#pragma unroll
+            for (int gi = 0; gi < 4; gi++) reinterpret_cast<uint4*>(orow)[q * 4 + gi] = o4[gi];
         }
-        *reinterpret_cast<uint4*>(out + n * (long long)Kw * 16 + gidx * 16) = make_uint4(o[0], o[1], o[2], o[3]);
     }
 }
 
@@ -522,14 +535,20 @@ cudaError_t launch_prepare_weights(const uint32_t* W, int N, int K, int w_bits, 
                                    cudaStream_t s) {
     using namespace fp4;
     const int Kw = (K + 127) / 128 * 4;
-    const long long total = (long long)N * Kw;
-    if (total == 0) return cudaSuccess;
-    long long blocks = (total + 255) / 256;
-    if (blocks > (long long)sms * 8) blocks = (long long)sms * 8;
+    if ((long long)N * Kw == 0) return cudaSuccess;
+    const int Kq = Kw / 4;
+    // 256-thread CTAs: x over a row's 16-byte plane words, y over rows; ~8 CTAs per SM
+    dim3 threads(Kq >= 256 ? 256 : (Kq + 31) / 32 * 32, 1);
+    threads.y = 256 / threads.x;
+    dim3 blocks((Kq + threads.x - 1) / threads.x, 1);
+    long long ry = ((long long)sms * 8 + blocks.x - 1) / blocks.x;
+    long long need = ((long long)N + threads.y - 1) / threads.y;
+    blocks.y = (unsigned)(ry < need ? ry : need);
+    if (blocks.y > 65535) blocks.y = 65535;
     const bool pm1 = enc == APNN_ENC_PM1_PM1 || enc == APNN_ENC_W_PM1_A_01;
-    if (pm1) prepare_kernel<1, true><<<(int)blocks, 256, 0, s>>>(W, N, K, Kw, out);
-    else if (w_bits == 1) prepare_kernel<1, false><<<(int)blocks, 256, 0, s>>>(W, N, K, Kw, out);
-    else prepare_kernel<2, false><<<(int)blocks, 256, 0, s>>>(W, N, K, Kw, out);
+    if (pm1) prepare_kernel<1, true><<<blocks, threads, 0, s>>>(W, N, K, Kw, out);
+    else if (w_bits == 1) prepare_kernel<1, false><<<blocks, threads, 0, s>>>(W, N, K, Kw, out);
+    else prepare_kernel<2, false><<<blocks, threads, 0, s>>>(W, N, K, Kw, out);
     count_launch();
     return cudaGetLastError();
 }

@@ -486,6 +486,285 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Both operands prepared (apnn_gemm_prepared_ab): A's e2m1 rows come from apnn_prepare_activations
+// (the planes decoded ONCE per GEMM instead of once per N tile), so the main loop has no CUDA-core
+// hand-off at all -- TMA lands A and W straight in the operand layout, and the MMA issuer waits on
+// one barrier per stage in CTA 0 that both CTAs' TMA loads complete (.cta_group::2 TMA).
+// Both operands are at full scale: the accumulator holds Y itself.
+//
+// Warp roles per CTA: warps 0..PP_EPI-1 epilogue (PP_EPI / 4 warps per TMEM lane quarter, each
+// a slice of the columns); warp PP_EPI TMA producer (one lane); warp PP_EPI+1 TMEM allocator and,
+// in CTA 0, the single-thread MMA issuer.
+//
+// Experiment builds only (build.py --variant NAME -DAPNN_EXP_PP=n; wrong results by design):
+//   1 the epilogue releases the accumulator without reading it (no output)
+//   2 the MMA issuer commits without issuing MMAs
+//   3 the producer arrives without loading (no operand traffic); 4 = 1 + 3
+//   5 = 4 + the issuer neither waits on the stage barriers nor fences; 6 = 4 + no fence;
+//   7 = 5 + no producer and no threshold tables (the issuer and the accumulator hand-off alone)
+#ifndef APNN_EXP_PP
+#define APNN_EXP_PP 0
+#endif
+// APNN_EXP_PP_TRACE=1 (experiment builds): CTA 0's issuer stamps clock64 / %globaltimer around
+// each stage (wait start, wait done, MMAs + commit issued) and epilogue warp 0 around each tile;
+// read back with apnn_exp_pp_trace()
+#ifndef APNN_EXP_PP_TRACE
+#define APNN_EXP_PP_TRACE 0
+#endif
+constexpr int kPpTrN = 1024;
+#if APNN_EXP_PP_TRACE
+__device__ unsigned long long g_pp_trace[8 * kPpTrN];
+#endif
+__device__ __forceinline__ void pp_tr(int ev, int i) {
+#if APNN_EXP_PP_TRACE
+    if (blockIdx.x == 0 && i < kPpTrN) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_pp_trace[(2 * ev) * kPpTrN + i] = clock64();
+        g_pp_trace[(2 * ev + 1) * kPpTrN + i] = t;
+    }
+#endif
+}
+constexpr int PP_EPI = 16;
+constexpr int PP_TMA = PP_EPI;
+constexpr int PP_MMA = PP_EPI + 1;
+constexpr int PP_THREADS = (PP_MMA + 1) * 32;
+constexpr int PP_MAXS = 8;
+
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, uint32_t bar_cluster, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(tmap), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+template <int BNP, bool I32>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
+    fp4_pp_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
+                  const Params p) {
+    constexpr int BROWS = BNP / 2;
+    constexpr uint32_t BOP = BROWS * 128;
+    // a stage is K = 512: two 128-byte TMA boxes of each operand, 8 MMAs per barrier hand-off (the
+    // issuer pays ~590 cycles per hand-off whatever its MMA work, scripts/pp_trace.py: with 4 MMAs
+    // of 448-512 cycles per stage it, not the tensor pipe, set the pace)
+    constexpr uint32_t AST = 2 * AOP, BST = 2 * BOP;
+    // two accumulators when they leave room for the scale-factor columns (32 + 32)
+    constexpr int NACC = (2 * BNP + 64 <= 512) ? 2 : 1;
+    constexpr uint32_t SFA = (uint32_t)(NACC * BNP + 31) / 32 * 32, SFB = SFA + 32;
+    static_assert(SFB + 32 <= 512, "TMEM budget");
+    constexpr int NCK = BNP / 32;
+    constexpr int QW = PP_EPI / 4;  // epilogue warps per lane quarter
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int S = p.S;
+    uint8_t* sAop = smem;                                   // S x AST
+    uint8_t* sBop = sAop + (size_t)S * AST;                 // S x BST
+    uint8_t* sStg = sBop + (size_t)S * BST;                 // PP_EPI x stg_warp
+    int32_t* sTab = reinterpret_cast<int32_t*>(sStg + (size_t)PP_EPI * p.stg_warp);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sTab + (I32 ? 0 : BNP * tc::kTabStride));
+    uint64_t* full = bars;                   // [PP_MAXS] (CTA 0: both CTAs' A + W bytes)
+    uint64_t* empty = bars + PP_MAXS;        // [PP_MAXS] (multicast MMA commit)
+    uint64_t* accum_full = empty + PP_MAXS;  // [2]
+    uint64_t* accum_empty = accum_full + 2;  // [2] (CTA 0: both CTAs' epilogue warps)
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accum_empty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_ctarank();
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const Geom& g = p.g;
+    const int nst = p.nst;
+
+    if (warp == PP_TMA && lane == 0) {
+        tma_prefetch(&tmapA);
+        tma_prefetch(&tmapB);
+        for (int s = 0; s < S; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&accum_full[i], 1);
+            mbar_init(&accum_empty[i], 2 * PP_EPI);
+        }
+        fence_mbar_init();
+    }
+    if (warp == PP_MMA) tmem_alloc2(tmem_holder, 512);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_holder;
+    if (warp < 4) {  // every scale-factor byte = E8M0 127 (2^0), all lanes, both CTAs
+        const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
+        const uint32_t ones[8] = {0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu,
+                                  0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu};
+#pragma unroll
+        for (uint32_t c = 0; c < 64; c += 8) tmem_st8(lb + SFA + c, ones);
+        tmem_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+
+    if (warp == PP_TMA) {
+        // ------------------------------------------------------------ TMA producer (A + W)
+        const int my_tiles = p.num_tiles > cid ? (p.num_tiles - cid + ncl - 1) / ncl : 0;
+        const int total = APNN_EXP_PP == 7 ? 0 : my_tiles * nst;
+        const uint32_t full0 = mapa(smem_u32(full), 0);
+        if (lane == 0) {
+            int ti = 0, st = 0, s = 0;
+            uint32_t ph = 0;
+            for (int it = 0; it < total; it++) {
+                const int tile = cid + ti * ncl;
+                const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+                sm100::mbar_wait_sleep(&empty[s], ph ^ 1);  // parked, not spinning: the issuer needs the slots
+#if APNN_EXP_PP >= 3
+                if (rank == 0) mbar_arrive(&full[s]);
+#else
+                if (rank == 0) mbar_arrive_expect_tx(&full[s], 2u * (AST + BST));
+                const uint32_t fb = full0 + (uint32_t)s * 8u;
+                const int arow = (tm * 2 + (int)rank) * 128, brow = tn * BNP + (int)rank * BROWS;
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    tma_load_2d_pair(sAop + (size_t)s * AST + h * AOP, &tmapA, fb, st * 256 + h * 128, arow);
+                    tma_load_2d_pair(sBop + (size_t)s * BST + h * BOP, &tmapB, fb, st * 256 + h * 128, brow);
+                }
+#endif
+                if (++st == nst) { st = 0; ti++; }
+                if (++s == S) { s = 0; ph ^= 1; }
+            }
+        }
+        __syncwarp();
+    } else if (warp == PP_MMA) {
+        // ------------------------------------------------------------ MMA issuer (CTA 0)
+        if (rank == 0 && lane == 0) {
+            const uint32_t idesc = idesc_mxf4(256, BNP);
+            const uint32_t a0 = smem_u32(sAop), b0 = smem_u32(sBop), full_a = smem_u32(full);
+            int s = 0, tc = 0, itr = 0;
+            uint32_t ph = 0;
+            for (int tile = cid; tile < p.num_tiles; tile += ncl, tc++) {
+                const int buf = NACC == 2 ? (tc & 1) : 0;
+                mbar_wait_cluster(&accum_empty[buf], ((tc / NACC) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(buf * BNP);
+                // the next stage's barrier is probed (test_wait, non-blocking) BEFORE this stage's MMAs
+                // are issued, so the probe's latency overlaps them; the blocking wait only runs when
+                // the probe said "not yet" (a blocking try_wait cost ~200 cycles per stage)
+                bool ready = mbar_test_wait(full_a + (uint32_t)s * 8u, ph);
+                for (int st = 0; st < nst; st++, itr++) {
+                    pp_tr(0, itr);
+                    if (!ready && APNN_EXP_PP < 5) mbar_wait_cluster(&full[s], ph);
+                    pp_tr(1, itr);
+                    if (APNN_EXP_PP < 5) tc_fence_after();
+                    const int s_next = s + 1 == S ? 0 : s + 1;
+                    const uint32_t ph_next = s + 1 == S ? ph ^ 1 : ph;
+                    ready = st + 1 < nst && mbar_test_wait(full_a + (uint32_t)s_next * 8u, ph_next);
+                    const uint32_t ab = a0 + (uint32_t)s * AST, bb = b0 + (uint32_t)s * BST;
+#pragma unroll
+                    for (int kk = 0; kk < 8; kk++)  // K = 64 e2m1 per MMA; boxes of 256 at AOP / BOP
+                        if (APNN_EXP_PP != 2)
+                            mma2_mxf4(d, tc::b_desc(ab + (kk >> 2) * AOP, kk & 3), tc::b_desc(bb + (kk >> 2) * BOP, kk & 3),
+                                      idesc, tmem + SFA, tmem + SFB, (st | kk) != 0);
+                    mma2_commit_mc(&empty[s], 0x3);
+                    pp_tr(2, itr);
+                    s = s_next;
+                    ph = ph_next;
+                }
+                mma2_commit_mc(&accum_full[buf], 0x3);
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int q = warp & 3;       // TMEM lane quarter
+        const int slice = warp >> 2;  // column slice
+        const int c_begin = slice * NCK / QW, c_end = (slice + 1) * NCK / QW;
+        const int nwb = c_end - c_begin;
+        const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
+        const uint32_t accum_empty0 = mapa(smem_u32(accum_empty), 0);
+        const int ob = p.e.out_bits;
+        const int Nw = (g.N + 127) / 128 * 4;
+        uint8_t* stg = sStg + (size_t)warp * p.stg_warp;
+        int tc = 0;
+        for (int tile = cid; tile < p.num_tiles; tile += ncl, tc++) {
+            const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+            const int row0 = (tm * 2 + (int)rank) * 128 + q * 32;
+            const int n0 = tn * BNP;
+            if (!I32 && (p.tab_mode == tc::kTabQ3 || p.tab_mode == tc::kTabHybrid) && APNN_EXP_PP != 7) {
+                named_bar_sync(1, PP_EPI * 32);  // the previous tile's table readers are done
+                for (int c = threadIdx.x; c < BNP; c += PP_EPI * 32)
+                    tc::build_threshold_row(sTab + c * tc::kTabStride, n0 + c, g.N, p.e);
+                named_bar_sync(1, PP_EPI * 32);
+            }
+            const int buf = NACC == 2 ? (tc & 1) : 0;
+            sm100::mbar_wait_sleep(&accum_full[buf], (uint32_t)(tc / NACC) & 1u);
+            if (warp == 0 && lane == 0) pp_tr(3, tc);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = c_begin; c < c_end && APNN_EXP_PP != 1 && APNN_EXP_PP < 4; c++) {
+                uint32_t acc[32];
+                tmem_ld32(tmem_lane + (uint32_t)(buf * BNP + c * 32), acc);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; i++) acc[i] = (uint32_t)__float2int_rn(__uint_as_float(acc[i]));
+                if (I32) {
+                    if (row0 < g.M) {
+                        if ((g.N & 3) == 0) {
+                            tc::stage_int32_chunk(acc, stg, lane);
+                            __syncwarp();
+                            tc::writeback_int32_block(stg, lane, reinterpret_cast<int32_t*>(p.Y), row0, g.M,
+                                                      n0 + c * 32, g.N);
+                            __syncwarp();
+                        } else {
+                            tc::epilogue_chunk(acc, row0 + lane, n0 + c * 32, c * 32, g, p.e, p.Y, nullptr,
+                                               tc::kTabNone);
+                        }
+                    }
+                } else {
+                    uint32_t w[8];
+                    if (p.tab_mode == tc::kTabQ3) {
+                        tc::requant_chunk_words_q3(acc, sTab, c * 32, w[0], w[1]);
+                    } else {
+                        tc::requant_chunk(acc, n0 + c * 32, c * 32, g, p.e, sTab, p.tab_mode, w);
+                    }
+                    uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * ob * nwb + (c - c_begin);
+#pragma unroll
+                    for (int tb = 0; tb < 8; tb++)
+                        if (tb < ob) srow[tb * nwb] = w[tb];
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(accum_empty0 + 8u * (uint32_t)buf);
+            if (warp == 0 && lane == 0) pp_tr(3, 512 + tc);
+            if (!I32 && row0 < g.M && APNN_EXP_PP != 1 && APNN_EXP_PP < 4) {
+                __syncwarp();
+                writeback_words(reinterpret_cast<const uint32_t*>(stg), lane, reinterpret_cast<uint32_t*>(p.Y), row0,
+                                g.M, n0 / 32 + c_begin, Nw, ob, nwb);
+            }
+            __syncwarp();
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == PP_MMA) {
+        tc_fence_after();
+        tmem_dealloc2(tmem, 512);
+    }
+}
+
+template <int BNP>
+static cudaError_t launch_pp(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid, size_t smem,
+                             cudaStream_t s) {
+    auto kfn = p.e.out_bits == 0 ? fp4_pp_kernel<BNP, true> : fp4_pp_kernel<BNP, false>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kfn<<<grid, PP_THREADS, smem, s>>>(ta, tb, p);
+    return cudaGetLastError();
+}
+
 template <int BNP, bool AP, bool WP>
 static cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid, size_t smem,
                           cudaStream_t s) {
@@ -509,6 +788,15 @@ static cudaError_t launch_enc(int enc, const CUtensorMap& ta, const CUtensorMap&
 
 }  // namespace pair
 }  // namespace fp4
+
+#if APNN_EXP_PP_TRACE
+extern "C" int apnn_exp_pp_trace(unsigned long long* host, int n) {
+    const int total = 8 * fp4::pair::kPpTrN;
+    if (n < total) return -1;
+    return cudaMemcpyFromSymbol(host, fp4::pair::g_pp_trace, total * sizeof(unsigned long long)) == cudaSuccess
+               ? total : -2;
+}
+#endif
 
 #if APNN_EXP_PAIR_TRACE
 extern "C" int apnn_exp_pair_trace(unsigned long long* host, int n) {
@@ -599,6 +887,62 @@ cudaError_t launch_tc_fp4_pair_prepared(const uint32_t* A, const uint8_t* Wp, co
     const int grid = 2 * pairs;
     cudaError_t err = BNP == 224 ? launch_enc<224>(g.enc, ta, tb, p, grid, smem, s)
                                  : launch_enc<256>(g.enc, ta, tb, p, grid, smem, s);
+    count_launch();
+    return err;
+}
+
+
+// both operands prepared (apnn_gemm_prepared_ab): the persistent pair kernel without decode warps.
+// Tile width: 224 (two accumulators, the epilogue overlapped with the next tile's MMAs; 8192^3
+// w1a2 fused 6100 TOPS) unless APNN_FP4_PP_BN=256 (read once; one accumulator, 16 epilogue warps
+// drain it between tiles: 5477 TOPS, scripts/fp4_pp_time.py)
+static int fp4_pp_bn_override() {
+    static int v = -1;
+    if (v < 0) {
+        const char* s = getenv("APNN_FP4_PP_BN");
+        v = s ? atoi(s) : 0;
+    }
+    return v;
+}
+
+cudaError_t launch_tc_fp4_pair_prepared_ab(const uint8_t* Ap, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
+                                           int sms, cudaStream_t s) {
+    using namespace fp4::pair;
+    Params p;
+    std::memset(&p, 0, sizeof(p));
+    p.g = g;
+    p.e = e;
+    p.Y = Y;
+    const int Kw = (g.K + 127) / 128 * 4;
+    p.nst = (Kw + 15) / 16;  // K = 512 stages
+    p.tab_mode = tc::kTabNone;
+    if (e.out_bits > 0 && e.out_bits <= 2) p.tab_mode = tc::kTabQ3;
+    else if (e.out_bits > 2 && (unsigned long long)e.qmax * (unsigned long long)e.S <= 0xFFFFFFFFull)
+        p.tab_mode = tc::kTabHybrid;
+    p.ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
+    const int BNP = fp4_pp_bn_override() == 256 ? 256 : 224;
+    p.tiles_m = (g.M + 255) / 256;
+    p.tiles_n = (p.ncols + BNP - 1) / BNP;
+    p.num_tiles = p.tiles_m * p.tiles_n;
+    const int nck = BNP / 32, nwb_max = (nck + PP_EPI / 4 - 1) / (PP_EPI / 4);
+    p.stg_warp = e.out_bits == 0 ? 4096 : (32 * e.out_bits * nwb_max * 4 + 127) / 128 * 128;
+    const size_t bop = (size_t)(BNP / 2) * 128;
+    const size_t fixed = (size_t)PP_EPI * p.stg_warp + (e.out_bits ? (size_t)BNP * tc::kTabStride * 4 : 0) +
+                         (2 * PP_MAXS + 4) * 8 + 8;
+    int S = (int)((227 * 1024 - fixed) / (2 * (AOP + bop)));
+    if (S > PP_MAXS) S = PP_MAXS;
+    static const int s_override = [] { const char* v = getenv("APNN_FP4_PP_STAGES"); return v ? atoi(v) : 0; }();
+    if (s_override >= 2 && s_override < S) S = s_override;  // experiments: shallower rings
+    if (S < 2) return cudaErrorInvalidConfiguration;
+    p.S = S;
+    const size_t smem = (size_t)S * 2 * (AOP + bop) + fixed;
+    CUtensorMap ta, tb;
+    if (!fp4::make_map_prep(&ta, Ap, g.M, Kw, 128)) return cudaErrorInvalidValue;
+    if (!fp4::make_map_prep(&tb, Wp, g.N, Kw, BNP / 2)) return cudaErrorInvalidValue;
+    int pairs = sms / 2;
+    if (pairs > p.num_tiles) pairs = p.num_tiles;
+    const int grid = 2 * pairs;
+    cudaError_t err = BNP == 224 ? launch_pp<224>(ta, tb, p, grid, smem, s) : launch_pp<256>(ta, tb, p, grid, smem, s);
     count_launch();
     return err;
 }

@@ -234,7 +234,9 @@ __global__ void __launch_bounds__(NT) popc_gemm_kernel(const uint32_t* __restric
 // column n0 + l of each row in lane l.  The fused epilogue then packs each plane of the 32
 // requantised columns with one __ballot_sync (the paper's packing).
 // Latency-scale problems (the paper's FC layers, M <= 64) need one k-word per lane per plane.
-template <int ENC, int MR>
+// AB = a_bits as a compile-time constant: with a runtime plane count the unrolled plane loops
+// issue all 8 (predicated-off) popc steps per column (w1a2 FC 9.1 us vs 3.6 us for w1a1)
+template <int ENC, int MR, int AB>
 __global__ void __launch_bounds__(128) popc_warp_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict__ Wt,
                                                         Geom g, Epi e, void* __restrict__ Yout) {
     const int lane = threadIdx.x & 31;
@@ -242,7 +244,8 @@ __global__ void __launch_bounds__(128) popc_warp_kernel(const uint32_t* __restri
     const int ntn = (g.N + 31) / 32;
     const int m0 = (wid / ntn) * MR, n0 = (wid % ntn) * 32;
     if (m0 >= g.M) return;  // whole warp
-    const int ab = g.a_bits, wb = g.w_bits, Kw = g.Cw;
+    constexpr int ab = AB;
+    const int wb = g.w_bits, Kw = g.Cw;
     int acc[MR][32], aux[MR][32];
 #pragma unroll
     for (int r = 0; r < MR; r++)
@@ -267,40 +270,39 @@ __global__ void __launch_bounds__(128) popc_warp_kernel(const uint32_t* __restri
                 for (int t = 0; t < 8; t++)
                     if (t < ab) rowpop[r] += __popc(a[r][t]) << t;
         }
+        // one plane of the 32 columns' k-word, all 32 loads issued before any use (columns past N
+        // read row N-1: valid memory, and their sums are never stored)
+        const uint32_t* wcol = Wt + kw;
+        for (int sp = 0; sp < ((ENC == APNN_ENC_PM1_PM1 || ENC == APNN_ENC_W_PM1_A_01) ? 1 : wb); sp++) {
+            uint32_t wv[32];
 #pragma unroll
-        for (int j = 0; j < 32; j++) {
-            const int n = n0 + j;
-            const bool nin = n < g.N;  // uniform (columns past N accumulate zeros)
-            const uint32_t* wp = Wt + (long long)(nin ? n : 0) * wb * Kw + kw;
-            if (ENC == APNN_ENC_01_01) {
-                for (int sp = 0; sp < wb; sp++) {
-                    const uint32_t w = nin ? __ldg(wp + (long long)sp * Kw) : 0u;
+            for (int j = 0; j < 32; j++) {
+                const int n = min(n0 + j, g.N - 1);
+                wv[j] = __ldg(wcol + ((long long)n * wb + sp) * Kw);
+            }
+#pragma unroll
+            for (int j = 0; j < 32; j++) {
+                const uint32_t w = wv[j];
+                if (ENC == APNN_ENC_01_01) {
 #pragma unroll
                     for (int r = 0; r < MR; r++) {
                         int y = 0;
 #pragma unroll
-                        for (int t = 0; t < 8; t++)
-                            if (t < ab) y += __popc(a[r][t] & w) << t;
+                        for (int t = 0; t < ab; t++) y += __popc(a[r][t] & w) << t;
                         acc[r][j] += y << sp;
                     }
-                }
-            } else if (ENC == APNN_ENC_PM1_PM1) {
-                const uint32_t w = nin ? __ldg(wp) : 0u;
+                } else if (ENC == APNN_ENC_PM1_PM1) {
 #pragma unroll
-                for (int r = 0; r < MR; r++) acc[r][j] += __popc(a[r][0] ^ w);
-            } else if (ENC == APNN_ENC_W_PM1_A_01) {
-                const uint32_t w = nin ? __ldg(wp) : 0u;
+                    for (int r = 0; r < MR; r++) acc[r][j] += __popc(a[r][0] ^ w);
+                } else if (ENC == APNN_ENC_W_PM1_A_01) {
 #pragma unroll
-                for (int r = 0; r < MR; r++) {
-                    int y = 0;
+                    for (int r = 0; r < MR; r++) {
+                        int y = 0;
 #pragma unroll
-                    for (int t = 0; t < 8; t++)
-                        if (t < ab) y += __popc(a[r][t] & w) << t;
-                    acc[r][j] += y;
-                }
-            } else {  // APNN_ENC_W_01_A_PM1
-                for (int sp = 0; sp < wb; sp++) {
-                    const uint32_t w = nin ? __ldg(wp + (long long)sp * Kw) : 0u;
+                        for (int t = 0; t < ab; t++) y += __popc(a[r][t] & w) << t;
+                        acc[r][j] += y;
+                    }
+                } else {  // APNN_ENC_W_01_A_PM1
                     const int pw = __popc(w) << sp;
 #pragma unroll
                     for (int r = 0; r < MR; r++) {
@@ -355,16 +357,36 @@ __global__ void __launch_bounds__(128) popc_warp_kernel(const uint32_t* __restri
     }
 }
 
+template <int MR, int AB>
+static void launch_popc_warp_ab(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
+                                int blocks, cudaStream_t s) {
+    if (g.enc == APNN_ENC_01_01) popc_warp_kernel<APNN_ENC_01_01, MR, AB><<<blocks, 128, 0, s>>>(A, W, g, e, Y);
+    else popc_warp_kernel<APNN_ENC_W_PM1_A_01, MR, AB><<<blocks, 128, 0, s>>>(A, W, g, e, Y);
+}
+
+// +-1 activations have one plane (Case II, Case III swapped)
 template <int MR>
 static void launch_popc_warp_mr(const uint32_t* A, const uint32_t* W, const Geom& g, const Epi& e, void* Y,
                                 cudaStream_t s) {
     const long long warps = (long long)((g.M + MR - 1) / MR) * ((g.N + 31) / 32);
     const int blocks = (int)((warps * 32 + 127) / 128);
-    switch (g.enc) {
-    case APNN_ENC_01_01: popc_warp_kernel<APNN_ENC_01_01, MR><<<blocks, 128, 0, s>>>(A, W, g, e, Y); break;
-    case APNN_ENC_PM1_PM1: popc_warp_kernel<APNN_ENC_PM1_PM1, MR><<<blocks, 128, 0, s>>>(A, W, g, e, Y); break;
-    case APNN_ENC_W_PM1_A_01: popc_warp_kernel<APNN_ENC_W_PM1_A_01, MR><<<blocks, 128, 0, s>>>(A, W, g, e, Y); break;
-    default: popc_warp_kernel<APNN_ENC_W_01_A_PM1, MR><<<blocks, 128, 0, s>>>(A, W, g, e, Y); break;
+    if (g.enc == APNN_ENC_PM1_PM1) {
+        popc_warp_kernel<APNN_ENC_PM1_PM1, MR, 1><<<blocks, 128, 0, s>>>(A, W, g, e, Y);
+        return;
+    }
+    if (g.enc == APNN_ENC_W_01_A_PM1) {
+        popc_warp_kernel<APNN_ENC_W_01_A_PM1, MR, 1><<<blocks, 128, 0, s>>>(A, W, g, e, Y);
+        return;
+    }
+    switch (g.a_bits) {
+    case 1: launch_popc_warp_ab<MR, 1>(A, W, g, e, Y, blocks, s); break;
+    case 2: launch_popc_warp_ab<MR, 2>(A, W, g, e, Y, blocks, s); break;
+    case 3: launch_popc_warp_ab<MR, 3>(A, W, g, e, Y, blocks, s); break;
+    case 4: launch_popc_warp_ab<MR, 4>(A, W, g, e, Y, blocks, s); break;
+    case 5: launch_popc_warp_ab<MR, 5>(A, W, g, e, Y, blocks, s); break;
+    case 6: launch_popc_warp_ab<MR, 6>(A, W, g, e, Y, blocks, s); break;
+    case 7: launch_popc_warp_ab<MR, 7>(A, W, g, e, Y, blocks, s); break;
+    default: launch_popc_warp_ab<MR, 8>(A, W, g, e, Y, blocks, s); break;
     }
 }
 

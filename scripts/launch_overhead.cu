@@ -45,6 +45,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(704, 1) k_cluster(in
     if (out == nullptr) smem[threadIdx.x] = 1;
 }
 
+
+// PDL: setup (TMEM alloc, barriers) before griddepcontrol.wait; dependents released at entry
+template <int MODE>
+__global__ void __launch_bounds__(704, 1) k_pdl(int* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint32_t holder;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (MODE >= 1 && threadIdx.x / 32 == 0) tmem_alloc_dyn(&holder, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (MODE == 2 && threadIdx.x < 128) {
+        int4* o = reinterpret_cast<int4*>(out) + (size_t)blockIdx.x * 128 * 64 + threadIdx.x * 64;
+        for (int i = 0; i < 64; i++) o[i] = make_int4(i, i, i, i);
+    }
+    if (MODE >= 1) {
+        tc_fence_before();
+        __syncthreads();
+        if (threadIdx.x / 32 == 0) { tc_fence_after(); tmem_dealloc(holder, 512); }
+    }
+    if (out == nullptr) smem[threadIdx.x] = 1;
+}
+
+template <int MODE>
+static void launch_pdl(int grid, int smem, cudaStream_t s, int* out) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(704);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_pdl<MODE>, out);
+}
+
 template <typename F>
 static float graph_us(F launch) {
     cudaStream_t s;
@@ -87,6 +126,8 @@ int main() {
     cudaFuncSetAttribute(k_plain<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
     cudaFuncSetAttribute(k_plain<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
     cudaFuncSetAttribute(k_cluster<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
+    cudaFuncSetAttribute(k_pdl<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
+    cudaFuncSetAttribute(k_pdl<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
     for (int grid : {4, 32, 148}) {
         printf("grid %3d  plain 0smem %.2f us | plain 227K %.2f | +tmem %.2f | +tmem+strided 128KB stores %.2f | cluster2+tmem2 %.2f\n",
                grid, graph_us([&](cudaStream_t s) { k_plain<0><<<grid, 704, 0, s>>>(out); }),
@@ -94,6 +135,12 @@ int main() {
                graph_us([&](cudaStream_t s) { k_plain<1><<<grid, 704, SM, s>>>(out); }),
                graph_us([&](cudaStream_t s) { k_plain<2><<<grid, 704, SM, s>>>(out); }),
                graph_us([&](cudaStream_t s) { k_cluster<0><<<grid, 704, SM, s>>>(out); }));
+    }
+    for (int grid : {4, 32, 148}) {
+        printf("grid %3d  PDL: +tmem %.2f us | +tmem+stores %.2f | (no PDL, 8KB smem: %.2f)\n", grid,
+               graph_us([&](cudaStream_t s) { launch_pdl<1>(grid, SM, s, out); }),
+               graph_us([&](cudaStream_t s) { launch_pdl<2>(grid, SM, s, out); }),
+               graph_us([&](cudaStream_t s) { k_plain<1><<<grid, 704, 8192, s>>>(out); }));
     }
     printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;

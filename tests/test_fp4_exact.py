@@ -59,7 +59,7 @@ def w_pm1(enc):
 
 
 def run_fp4_both(A, W, a, w, enc, epi=None):
-    """(per-tile W decode result, prepared-W result) on the FP4 kernel."""
+    """(per-tile W decode result, prepared-W result, both-prepared result) on the FP4 kernels."""
     M, K = A.shape
     N = W.shape[0]
     Ap = ap.pack_bits(cuda(A), a)
@@ -67,15 +67,17 @@ def run_fp4_both(A, W, a, w, enc, epi=None):
     y1 = ap.gemm(Ap, Wpl, M, N, K, a, w, enc, epi=epi, variant=ap.VARIANT_TC_FP4)
     Wprep = ap.prepare_weights(Wpl, N, K, w, enc)
     y2 = ap.gemm_prepared(Ap, Wprep, M, N, K, a, w, enc, epi=epi)
+    y3 = ap.gemm_prepared_ab(ap.prepare_activations(Ap, M, K, a, enc), Wprep, M, N, K, a, w, enc, epi=epi)
     torch.cuda.synchronize()
-    return y1, y2
+    return y1, y2, y3
 
 
 def check(A, W, a, w, enc, what):
     want = oracle.gemm(A, W, a, w, enc)
-    y1, y2 = run_fp4_both(A, W, a, w, enc)
+    y1, y2, y3 = run_fp4_both(A, W, a, w, enc)
     np.testing.assert_array_equal(y1.cpu().numpy(), want, err_msg=f"{what}: tc_fp4")
     np.testing.assert_array_equal(y2.cpu().numpy(), want, err_msg=f"{what}: tc_fp4 prepared")
+    np.testing.assert_array_equal(y3.cpu().numpy(), want, err_msg=f"{what}: tc_fp4 both prepared")
     return want
 
 
@@ -199,6 +201,7 @@ def test_fp4_full_size_w2a2_auto_sampled_rows(fused):
     Y = ap.gemm(Ap, Wpl, M, N, K, a, w, enc, epi=epi)
     Wprep = ap.prepare_weights(Wpl, N, K, w, enc)
     Y2 = ap.gemm_prepared(Ap, Wprep, M, N, K, a, w, enc, epi=epi)
+    Y3 = ap.gemm_prepared_ab(ap.prepare_activations(Ap, M, K, a, enc), Wprep, M, N, K, a, w, enc, epi=epi)
     torch.cuda.synchronize()
     g = synth.rng("fp4-w2a2-full-rows")
     rows = np.array(sorted(set([0, 1, 127, 128, M - 1] + g.integers(0, M, size=24).tolist())))
@@ -207,10 +210,12 @@ def test_fp4_full_size_w2a2_auto_sampled_rows(fused):
         want = oracle.pack(oracle.epilogue(want, alpha, beta, S, a), a)
         np.testing.assert_array_equal(u32(Y)[rows], want)
         np.testing.assert_array_equal(u32(Y2)[rows], want)
+        np.testing.assert_array_equal(u32(Y3)[rows], want)
     else:
         assert np.abs(want).mean() > 1.5e4
         np.testing.assert_array_equal(Y.cpu().numpy()[rows], want)
         np.testing.assert_array_equal(Y2.cpu().numpy()[rows], want)
+        np.testing.assert_array_equal(Y3.cpu().numpy()[rows], want)
 
 
 @pytest.mark.parametrize("a,w,enc", [(2, 1, 2), (2, 2, 0), (1, 1, 1), (1, 2, 3)])
@@ -235,3 +240,50 @@ def test_fp4_pair_kernel_persistent_tiles(a, w, enc, out_bits):
         got = ap.gemm_prepared(Ap, Wprep, M, N, K, a, w, enc, epi=ap.Epilogue(out_bits, cuda(alpha), cuda(beta), S))
         torch.cuda.synchronize()
         np.testing.assert_array_equal(u32(got), want)
+
+
+@pytest.mark.parametrize("bn", [256, 224])
+@pytest.mark.parametrize("a,w,enc", FP4_COMBOS)
+@pytest.mark.parametrize("out_bits", [0, 2, 5])
+@pytest.mark.parametrize("M,N,K", [(4096, 1200, 1000), (300, 520, 2048), (1, 33, 64), (1000, 8192, 256)])
+def test_fp4_both_prepared_tiles(bn, a, w, enc, out_bits, M, N, K):
+    # apnn_gemm_prepared_ab: ragged M / N / K, several tiles per CTA pair (4096 x 1200: 96 tiles
+    # at 256, 112 at 224), a single row, the widest N.  The tile width is read once per process
+    # (APNN_FP4_PP_BN): the default run covers its width, an APNN_FP4_PP_BN=256 run the other.
+    if _pp_bn() != bn:
+        pytest.skip(f"this process runs APNN_FP4_PP_BN={_pp_bn()} (the other width runs in its own process)")
+    A, W = synth.gemm_inputs(M, N, K, a, w, tag=f"fp4-pp-{M}")
+    Y = oracle.gemm(A, W, a, w, enc)
+    Apl = ap.pack_bits(cuda(A), a)
+    Aprep = ap.prepare_activations(Apl, M, K, a, enc)
+    Wprep = ap.prepare_weights(ap.pack_bits(cuda(W), w), N, K, w, enc)
+    if out_bits == 0:
+        got = ap.gemm_prepared_ab(Aprep, Wprep, M, N, K, a, w, enc)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(got.cpu().numpy(), Y)
+    else:
+        alpha, beta = synth.epilogue_params(N, tag="fp4-pp")
+        S = 53
+        want = oracle.pack(oracle.epilogue(Y, alpha, beta, S, out_bits), out_bits)
+        got = ap.gemm_prepared_ab(Aprep, Wprep, M, N, K, a, w, enc,
+                                  epi=ap.Epilogue(out_bits, cuda(alpha), cuda(beta), S))
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(u32(got), want)
+
+
+def _pp_bn():
+    import os
+    return 256 if os.environ.get("APNN_FP4_PP_BN") == "256" else 224
+
+
+def test_fp4_both_prepared_rejects_mismatched_tags():
+    M, N, K = 256, 256, 256
+    A, W = synth.gemm_inputs(M, N, K, 2, 1, tag="fp4-pp-tag")
+    Apl = ap.pack_bits(cuda(A), 2)
+    Wpl = ap.pack_bits(cuda(W), 1)
+    Aprep = ap.prepare_activations(Apl, M, K, 2, 2)
+    Wprep = ap.prepare_weights(Wpl, N, K, 1, 2)
+    with pytest.raises(ValueError):
+        ap.gemm_prepared_ab(Wprep, Wprep, M, N, K, 2, 1, 2)  # weights passed as activations
+    with pytest.raises(ValueError):
+        ap.gemm_prepared_ab(Aprep, Wprep, M, N, K, 2, 1, 0)  # other encoding
