@@ -291,6 +291,17 @@ apnn_status apnn_prepare_weights_i8(const uint32_t *W, int N, int K, int w_bits,
 apnn_status apnn_gemm_prepared_i8(const uint32_t *A, const uint8_t *Wp, int M, int N, int K, int a_bits,
                                   int w_bits, apnn_encoding enc, const apnn_epilogue *epi, void *Y,
                                   apnn_stream_t stream);
+/* Both operands prepared, int8 (any a_bits / w_bits): apnn_prepare_activations_i8 decodes the
+ * activation planes once into the int8 operand rows of apnn_prepare_weights_i8 (u8 codes, or s8 +-1
+ * with value-0 padding; Ap: apnn_prepared_i8_bytes(M, K) bytes, caller-owned), and
+ * apnn_gemm_prepared_ab_i8 runs the persistent CTA-pair kind::i8 kernel on Ap and Wp (both by TMA,
+ * two int32 TMEM accumulators); int32 when epi == NULL, else the fused routine without pooling /
+ * residual.  Same results as apnn_gemm_ex; APNN_ERR_OVERFLOW where that is. */
+apnn_status apnn_prepare_activations_i8(const uint32_t *A, int M, int K, int a_bits, apnn_encoding enc,
+                                        uint8_t *Ap, apnn_stream_t stream);
+apnn_status apnn_gemm_prepared_ab_i8(const uint8_t *Ap, const uint8_t *Wp, int M, int N, int K, int a_bits,
+                                     int w_bits, apnn_encoding enc, const apnn_epilogue *epi, void *Y,
+                                     apnn_stream_t stream);
 /* apnn_conv2d with prepared conv weights: Wp = apnn_prepare_weights_i8 of the packed OHWI
  * weights viewed as C_out*R*S rows of C_in (apnn_prepared_i8_bytes(C_out*R*S, C_in) bytes).
  * Runs on the tap-reuse kernel (APConv: the input window of a 16 x 8

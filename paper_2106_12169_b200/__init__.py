@@ -97,6 +97,10 @@ def lib() -> ctypes.CDLL:
             L.apnn_prepare_activations.restype = st
             L.apnn_gemm_prepared_ab.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp, vp]
             L.apnn_gemm_prepared_ab.restype = st
+            L.apnn_prepare_activations_i8.argtypes = [vp, ci, ci, ci, ci, vp, vp]
+            L.apnn_prepare_activations_i8.restype = st
+            L.apnn_gemm_prepared_ab_i8.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp, vp]
+            L.apnn_gemm_prepared_ab_i8.restype = st
             L.apnn_prepared_i8_bytes.argtypes = [ci, ci]
             L.apnn_prepared_i8_bytes.restype = ctypes.c_size_t
             L.apnn_prepare_weights_i8.argtypes = [vp, ci, ci, ci, ci, vp, vp]
@@ -157,6 +161,7 @@ ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_im2col_pack", "apnn_
                "apnn_flatten_packed",
                "apnn_prepared_bytes", "apnn_prepare_weights", "apnn_gemm_prepared",
                "apnn_prepare_activations", "apnn_gemm_prepared_ab",
+               "apnn_prepare_activations_i8", "apnn_gemm_prepared_ab_i8",
                "apnn_prepared_i8_bytes", "apnn_prepare_weights_i8", "apnn_gemm_prepared_i8",
                "apnn_conv2d_prepared_i8", "apnn_conv_halo_fits", "apnn_conv2d_first_prepared_i8", "apnn_conv_first_fits", "apnn_tune_tiles", "apnn_gemm_tiled", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
                "apnn_conv2d", "apnn_conv2d_ex", "apnn_quant_pack_out", "apnn_pool_quant_pack_out",
@@ -216,7 +221,7 @@ class PreparedWeights:
     only meaningful to the kernel kind and (N, K, w_bits, encoding) it was built for; the
     prepared-weight calls reject a mismatch instead of computing with the wrong operand."""
     data: torch.Tensor  # uint8, device
-    kind: str           # "fp4" (e2m1 operand rows), "fp4a" (e2m1 activation rows) or "i8" (int8 operand rows)
+    kind: str           # "fp4" / "fp4a" (e2m1 weight / activation rows), "i8" / "i8a" (int8 weight / activation rows)
     N: int
     K: int
     w_bits: int
@@ -431,6 +436,41 @@ def gemm_prepared_ab(Ap: PreparedWeights, Wp: PreparedWeights, M: int, N: int, K
     ce = None if epi is None else ctypes.byref(epi._c())
     _check(lib().apnn_gemm_prepared_ab(_ptr(At), _ptr(Wt), M, N, K, a_bits, w_bits, enc, ce, _ptr(out), _stream(At)),
            "apnn_gemm_prepared_ab")
+    return out
+
+
+def prepare_activations_i8(A: torch.Tensor, M: int, K: int, a_bits: int, enc: int,
+                           out: Optional[torch.Tensor] = None) -> PreparedWeights:
+    """Packed activation planes -> int8 operand rows, decoded once per GEMM (apnn_prepare_activations_i8;
+    tagged kind "i8a" with (M, K, a_bits, enc))."""
+    _cuda(A, "A", torch.int32)
+    _check_out(A, packed_shape(M, K, a_bits), "A")
+    nbytes = int(lib().apnn_prepared_i8_bytes(M, K))
+    if out is None:
+        out = torch.empty(nbytes, dtype=torch.uint8, device=A.device)
+    _cuda(out, "out", torch.uint8)
+    _check_out(out, (nbytes,))
+    _check(lib().apnn_prepare_activations_i8(_ptr(A), M, K, a_bits, enc, _ptr(out), _stream(A)),
+           "apnn_prepare_activations_i8")
+    return PreparedWeights(out, "i8a", M, K, a_bits, enc)
+
+
+def gemm_prepared_ab_i8(Ap: PreparedWeights, Wp: PreparedWeights, M: int, N: int, K: int, a_bits: int, w_bits: int,
+                        enc: int, epi: Optional[Epilogue] = None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """APMM with both operands prepared as int8 rows on the kind::i8 pair kernel (apnn_gemm_prepared_ab_i8)."""
+    if not isinstance(Ap, PreparedWeights):
+        raise TypeError("gemm_prepared_ab_i8 takes the PreparedWeights returned by prepare_activations_i8")
+    At = Ap.check("i8a", M, K, a_bits, enc)
+    _cuda(At, "Ap", torch.uint8)
+    Wt = _prepared(Wp, "i8", N, K, w_bits, enc)
+    shape = (M, N) if epi is None else packed_shape(M, N, epi.out_bits)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.int32, device=At.device)
+    _cuda(out, "out", torch.int32)
+    _check_out(out, shape)
+    ce = None if epi is None else ctypes.byref(epi._c())
+    _check(lib().apnn_gemm_prepared_ab_i8(_ptr(At), _ptr(Wt), M, N, K, a_bits, w_bits, enc, ce, _ptr(out),
+                                          _stream(At)), "apnn_gemm_prepared_ab_i8")
     return out
 
 

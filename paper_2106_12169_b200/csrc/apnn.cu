@@ -44,6 +44,8 @@ cudaError_t launch_prepare_weights(const uint32_t* W, int N, int K, int w_bits, 
                                    cudaStream_t s);
 cudaError_t launch_tc_fp4_pair_prepared_ab(const uint8_t* Ap, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
                                            int sms, cudaStream_t s);
+cudaError_t launch_tc_i8_prepared_ab(const uint8_t* Ap, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
+                                     int sms, cudaStream_t s);
 cudaError_t launch_tc_fp4_pair_prepared(const uint32_t* A, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
                                         int sms, cudaStream_t s);
 cudaError_t launch_prepare_weights_i8(const uint32_t* W, int N, int K, int w_bits, int enc, uint8_t* out, int sms,
@@ -414,6 +416,44 @@ apnn_status apnn_gemm_prepared_ab(const uint8_t* Ap, const uint8_t* Wp, int M, i
     if ((st = device_info(&d)) != APNN_OK) return st;
     if (M == 0 || N == 0) return APNN_OK;
     cudaError_t err = launch_tc_fp4_pair_prepared_ab(Ap, Wp, g, e, Y, d.sms, (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_status apnn_prepare_activations_i8(const uint32_t* A, int M, int K, int a_bits, apnn_encoding enc, uint8_t* Ap,
+                                        apnn_stream_t stream) {
+    if (M < 0 || K < 0) return APNN_ERR_SHAPE;
+    apnn_status st = APNN_OK;
+    if (a_bits < 1 || a_bits > 8) return APNN_ERR_BITS;
+    if (enc < 0 || enc > 3) return APNN_ERR_ENCODING;
+    const bool apm = enc == APNN_ENC_PM1_PM1 || enc == APNN_ENC_W_01_A_PM1;
+    if (apm && a_bits != 1) return APNN_ERR_ENCODING;
+    if (M > 0 && K > 0 && (!A || !Ap)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(A) || !aligned16(Ap)) return APNN_ERR_ALIGNMENT;
+    DevInfo d;
+    if ((st = device_info(&d)) != APNN_OK) return st;
+    // the int8 operand rows of apnn_prepare_weights_i8, with the +-1 decision taken on A's side
+    cudaError_t err = launch_prepare_weights_i8(A, M, K, a_bits, apm ? APNN_ENC_PM1_PM1 : APNN_ENC_01_01, Ap, d.sms,
+                                                (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_status apnn_gemm_prepared_ab_i8(const uint8_t* Ap, const uint8_t* Wp, int M, int N, int K, int a_bits,
+                                     int w_bits, apnn_encoding enc, const apnn_epilogue* epi, void* Y,
+                                     apnn_stream_t stream) {
+    if (M < 0 || N < 0 || K < 0) return APNN_ERR_SHAPE;
+    apnn_status st = check_bits_enc(a_bits, w_bits, enc);
+    if (st != APNN_OK) return st;
+    if ((M > 0 && K > 0 && !Ap) || (N > 0 && K > 0 && !Wp) || (M > 0 && N > 0 && !Y)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(Ap) || !aligned16(Wp) || !aligned16(Y)) return APNN_ERR_ALIGNMENT;
+    Epi e;
+    if ((st = make_epi(epi, &e)) != APNN_OK) return st;
+    if (e.pool || e.res) return APNN_ERR_INVALID_ARG;
+    Geom g;
+    gemm_geom(&g, M, N, K, a_bits, w_bits, enc);
+    DevInfo d;
+    if ((st = device_info(&d)) != APNN_OK) return st;
+    if (M == 0 || N == 0) return APNN_OK;
+    cudaError_t err = launch_tc_i8_prepared_ab(Ap, Wp, g, e, Y, d.sms, (cudaStream_t)stream);
     return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }
 

@@ -413,6 +413,19 @@ bool make_map_prep(CUtensorMap* m, const uint8_t* base, int N, int Kw, int box_r
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// operand rows of row_bytes bytes (prepared e2m1 or int8); box {128 bytes, box_rows}, SWIZZLE_128B
+bool make_map_rows(CUtensorMap* m, const uint8_t* base, int rows, int row_bytes, int box_rows) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+    cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int BN, bool AP, bool WP, bool PREP>
 static cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, dim3 grid, size_t smem,
                           cudaStream_t s) {

@@ -42,6 +42,7 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 bool make_map(CUtensorMap* m, const uint32_t* base, int rows, int bits, int Kw, int box_rows);
 bool make_map_prep(CUtensorMap* m, const uint8_t* base, int N, int Kw, int box_rows);
+bool make_map_rows(CUtensorMap* m, const uint8_t* base, int rows, int row_bytes, int box_rows);
 
 namespace pair {
 
@@ -108,6 +109,7 @@ struct Params {
     int tab_mode;
     int stg_warp;     // epilogue staging bytes per warp
     int ncols;        // columns the tiles cover (int32: N; packed: Nw * 32)
+    uint32_t idesc;   // pp kernel, kind::i8: the instruction descriptor (operand signedness)
 };
 
 __host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
@@ -540,7 +542,10 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, ui
         : "memory");
 }
 
-template <int BNP, bool I32>
+// I8: the same kernel on kind::i8 (int8 operand rows from apnn_prepare_weights_i8 /
+// apnn_prepare_activations_i8, int32 accumulators, no scale factors): a 128-byte box is 128 K
+// elements instead of 256, the descriptors and the stage walk are the same
+template <int BNP, bool I32, bool I8>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
     fp4_pp_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
                   const Params p) {
@@ -550,10 +555,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
     // issuer pays ~590 cycles per hand-off whatever its MMA work, scripts/pp_trace.py: with 4 MMAs
     // of 448-512 cycles per stage it, not the tensor pipe, set the pace)
     constexpr uint32_t AST = 2 * AOP, BST = 2 * BOP;
-    // two accumulators when they leave room for the scale-factor columns (32 + 32)
-    constexpr int NACC = (2 * BNP + 64 <= 512) ? 2 : 1;
+    // two accumulators when they leave room for the scale-factor columns (32 + 32; kind::i8: none)
+    constexpr int NACC = (2 * BNP + (I8 ? 0 : 64) <= 512) ? 2 : 1;
     constexpr uint32_t SFA = (uint32_t)(NACC * BNP + 31) / 32 * 32, SFB = SFA + 32;
-    static_assert(SFB + 32 <= 512, "TMEM budget");
+    static_assert(I8 || SFB + 32 <= 512, "TMEM budget");
     constexpr int NCK = BNP / 32;
     constexpr int QW = PP_EPI / 4;  // epilogue warps per lane quarter
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -594,7 +599,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem = *tmem_holder;
-    if (warp < 4) {  // every scale-factor byte = E8M0 127 (2^0), all lanes, both CTAs
+    if (!I8 && warp < 4) {  // every scale-factor byte = E8M0 127 (2^0), all lanes, both CTAs
         const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
         const uint32_t ones[8] = {0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu,
                                   0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu};
@@ -639,7 +644,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
     } else if (warp == PP_MMA) {
         // ------------------------------------------------------------ MMA issuer (CTA 0)
         if (rank == 0 && lane == 0) {
-            const uint32_t idesc = idesc_mxf4(256, BNP);
+            const uint32_t idesc = I8 ? p.idesc : idesc_mxf4(256, BNP);
             const uint32_t a0 = smem_u32(sAop), b0 = smem_u32(sBop), full_a = smem_u32(full);
             int s = 0, tc = 0, itr = 0;
             uint32_t ph = 0;
@@ -662,10 +667,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
                     ready = st + 1 < nst && mbar_test_wait(full_a + (uint32_t)s_next * 8u, ph_next);
                     const uint32_t ab = a0 + (uint32_t)s * AST, bb = b0 + (uint32_t)s * BST;
 #pragma unroll
-                    for (int kk = 0; kk < 8; kk++)  // K = 64 e2m1 per MMA; boxes of 256 at AOP / BOP
-                        if (APNN_EXP_PP != 2)
-                            mma2_mxf4(d, tc::b_desc(ab + (kk >> 2) * AOP, kk & 3), tc::b_desc(bb + (kk >> 2) * BOP, kk & 3),
-                                      idesc, tmem + SFA, tmem + SFB, (st | kk) != 0);
+                    for (int kk = 0; kk < 8; kk++) {  // 32 bytes of K per MMA (64 e2m1 / 32 int8); boxes at AOP / BOP
+                        const uint64_t da = tc::b_desc(ab + (kk >> 2) * AOP, kk & 3);
+                        const uint64_t db = tc::b_desc(bb + (kk >> 2) * BOP, kk & 3);
+                        if (APNN_EXP_PP == 2) continue;
+                        if (I8) mma2_i8_ss(d, da, db, idesc, (st | kk) != 0);
+                        else mma2_mxf4(d, da, db, idesc, tmem + SFA, tmem + SFB, (st | kk) != 0);
+                    }
                     mma2_commit_mc(&empty[s], 0x3);
                     pp_tr(2, itr);
                     s = s_next;
@@ -705,8 +713,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
                 uint32_t acc[32];
                 tmem_ld32(tmem_lane + (uint32_t)(buf * BNP + c * 32), acc);
                 tmem_wait_ld();
+                if (!I8) {  // fp32 accumulator holding an exact integer
 #pragma unroll
-                for (int i = 0; i < 32; i++) acc[i] = (uint32_t)__float2int_rn(__uint_as_float(acc[i]));
+                    for (int i = 0; i < 32; i++) acc[i] = (uint32_t)__float2int_rn(__uint_as_float(acc[i]));
+                }
                 if (I32) {
                     if (row0 < g.M) {
                         if ((g.N & 3) == 0) {
@@ -755,10 +765,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
     }
 }
 
-template <int BNP>
+template <int BNP, bool I8>
 static cudaError_t launch_pp(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid, size_t smem,
                              cudaStream_t s) {
-    auto kfn = p.e.out_bits == 0 ? fp4_pp_kernel<BNP, true> : fp4_pp_kernel<BNP, false>;
+    auto kfn = p.e.out_bits == 0 ? fp4_pp_kernel<BNP, true, I8> : fp4_pp_kernel<BNP, false, I8>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kfn<<<grid, PP_THREADS, smem, s>>>(ta, tb, p);
@@ -905,8 +915,10 @@ static int fp4_pp_bn_override() {
     return v;
 }
 
-cudaError_t launch_tc_fp4_pair_prepared_ab(const uint8_t* Ap, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
-                                           int sms, cudaStream_t s) {
+// both operands prepared, e2m1 (I8 = false: apnn_prepare_weights / apnn_prepare_activations rows of
+// Kw * 16 bytes) or int8 (I8 = true: the _i8 preparations, rows of roundup(K, 128) bytes)
+static cudaError_t launch_pp_any(const uint8_t* Ap, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y, int sms,
+                                 cudaStream_t s, bool i8) {
     using namespace fp4::pair;
     Params p;
     std::memset(&p, 0, sizeof(p));
@@ -914,16 +926,22 @@ cudaError_t launch_tc_fp4_pair_prepared_ab(const uint8_t* Ap, const uint8_t* Wp,
     p.e = e;
     p.Y = Y;
     const int Kw = (g.K + 127) / 128 * 4;
-    p.nst = (Kw + 15) / 16;  // K = 512 stages
+    const int row_bytes = i8 ? Kw * 32 : Kw * 16;
+    p.nst = (row_bytes + 255) / 256;  // a stage: two 128-byte boxes of K (512 e2m1 / 256 int8 elements)
     p.tab_mode = tc::kTabNone;
     if (e.out_bits > 0 && e.out_bits <= 2) p.tab_mode = tc::kTabQ3;
     else if (e.out_bits > 2 && (unsigned long long)e.qmax * (unsigned long long)e.S <= 0xFFFFFFFFull)
         p.tab_mode = tc::kTabHybrid;
     p.ncols = e.out_bits ? (g.N + 127) / 128 * 128 : g.N;
-    const int BNP = fp4_pp_bn_override() == 256 ? 256 : 224;
+    // e2m1: 224 (two accumulators beside the scale factors) unless APNN_FP4_PP_BN=256; int8: 256 with
+    // two accumulators (no scale-factor columns)
+    const int BNP = i8 ? 256 : (fp4_pp_bn_override() == 256 ? 256 : 224);
     p.tiles_m = (g.M + 255) / 256;
     p.tiles_n = (p.ncols + BNP - 1) / BNP;
     p.num_tiles = p.tiles_m * p.tiles_n;
+    const bool a_pm1 = g.enc == APNN_ENC_PM1_PM1 || g.enc == APNN_ENC_W_01_A_PM1;
+    const bool w_pm1 = g.enc == APNN_ENC_PM1_PM1 || g.enc == APNN_ENC_W_PM1_A_01;
+    p.idesc = sm100::idesc_i8(256, BNP, a_pm1, w_pm1);
     const int nck = BNP / 32, nwb_max = (nck + PP_EPI / 4 - 1) / (PP_EPI / 4);
     p.stg_warp = e.out_bits == 0 ? 4096 : (32 * e.out_bits * nwb_max * 4 + 127) / 128 * 128;
     const size_t bop = (size_t)(BNP / 2) * 128;
@@ -937,14 +955,26 @@ cudaError_t launch_tc_fp4_pair_prepared_ab(const uint8_t* Ap, const uint8_t* Wp,
     p.S = S;
     const size_t smem = (size_t)S * 2 * (AOP + bop) + fixed;
     CUtensorMap ta, tb;
-    if (!fp4::make_map_prep(&ta, Ap, g.M, Kw, 128)) return cudaErrorInvalidValue;
-    if (!fp4::make_map_prep(&tb, Wp, g.N, Kw, BNP / 2)) return cudaErrorInvalidValue;
+    if (!fp4::make_map_rows(&ta, Ap, g.M, row_bytes, 128)) return cudaErrorInvalidValue;
+    if (!fp4::make_map_rows(&tb, Wp, g.N, row_bytes, BNP / 2)) return cudaErrorInvalidValue;
     int pairs = sms / 2;
     if (pairs > p.num_tiles) pairs = p.num_tiles;
     const int grid = 2 * pairs;
-    cudaError_t err = BNP == 224 ? launch_pp<224>(ta, tb, p, grid, smem, s) : launch_pp<256>(ta, tb, p, grid, smem, s);
+    cudaError_t err = i8 ? launch_pp<256, true>(ta, tb, p, grid, smem, s)
+                         : (BNP == 224 ? launch_pp<224, false>(ta, tb, p, grid, smem, s)
+                                       : launch_pp<256, false>(ta, tb, p, grid, smem, s));
     count_launch();
     return err;
+}
+
+cudaError_t launch_tc_fp4_pair_prepared_ab(const uint8_t* Ap, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
+                                           int sms, cudaStream_t s) {
+    return launch_pp_any(Ap, Wp, g, e, Y, sms, s, false);
+}
+
+cudaError_t launch_tc_i8_prepared_ab(const uint8_t* Ap, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y,
+                                     int sms, cudaStream_t s) {
+    return launch_pp_any(Ap, Wp, g, e, Y, sms, s, true);
 }
 
 }  // namespace apnn

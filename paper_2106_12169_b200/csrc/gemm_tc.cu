@@ -1092,22 +1092,23 @@ namespace tc {
 template <int NB, bool PM1>
 __global__ void __launch_bounds__(256) prepare_i8_kernel(const uint32_t* __restrict__ W, int N, int K, int Kw,
                                                          uint8_t* __restrict__ out) {
-    const long long total = (long long)N * Kw;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const long long n = idx / Kw;
-        const int gidx = (int)(idx - n * Kw);
-        uint32_t pw[NB];
+    // x over a row's 32-element groups, y over rows, 32-bit index math (it also decodes the
+    // activations of every both-prepared GEMM step: a flat 64-bit index division was its cost)
+    for (int n = blockIdx.y * blockDim.y + threadIdx.y; n < N; n += gridDim.y * blockDim.y) {
+        const uint32_t* wrow = W + (long long)n * NB * Kw;
+        uint4* orow = reinterpret_cast<uint4*>(out + (long long)n * Kw * 32);
+        for (int gidx = blockIdx.x * blockDim.x + threadIdx.x; gidx < Kw; gidx += gridDim.x * blockDim.x) {
+            uint32_t pw[NB];
 #pragma unroll
-        for (int pl = 0; pl < NB; pl++) pw[pl] = __ldg(W + (n * NB + pl) * Kw + gidx);
-        uint32_t o[8];
-        const int nv = K - gidx * 32;  // valid elements of this 32-element group
-        const uint32_t vm = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
-        if (PM1) decode_pm1<true>(pw[0], vm, o);  // padding -> value 0
-        else decode_01<NB>(pw, o);
-        uint4* dst = reinterpret_cast<uint4*>(out + n * (long long)Kw * 32 + gidx * 32);
-        dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-        dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+            for (int pl = 0; pl < NB; pl++) pw[pl] = __ldg(wrow + pl * Kw + gidx);
+            uint32_t o[8];
+            const int nv = K - gidx * 32;  // valid elements of this 32-element group
+            const uint32_t vm = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
+            if (PM1) decode_pm1<true>(pw[0], vm, o);  // padding -> value 0
+            else decode_01<NB>(pw, o);
+            orow[gidx * 2] = make_uint4(o[0], o[1], o[2], o[3]);
+            orow[gidx * 2 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+        }
     }
 }
 }  // namespace tc
@@ -1116,23 +1117,25 @@ cudaError_t launch_prepare_weights_i8(const uint32_t* W, int N, int K, int w_bit
                                       cudaStream_t s) {
     using namespace tc;
     const int Kw = (K + 127) / 128 * 4;
-    const long long total = (long long)N * Kw;
-    if (total == 0) return cudaSuccess;
-    long long blocks = (total + 255) / 256;
-    if (blocks > (long long)sms * 8) blocks = (long long)sms * 8;
-    const int gb = (int)blocks;
+    if ((long long)N * Kw == 0) return cudaSuccess;
+    dim3 threads(Kw >= 256 ? 256 : (Kw + 31) / 32 * 32, 1);
+    threads.y = 256 / threads.x;
+    dim3 gb((Kw + threads.x - 1) / threads.x, 1);
+    const long long ry = ((long long)sms * 8 + gb.x - 1) / gb.x, need = ((long long)N + threads.y - 1) / threads.y;
+    gb.y = (unsigned)(ry < need ? ry : need);
+    if (gb.y > 65535) gb.y = 65535;
     const bool pm1 = enc == APNN_ENC_PM1_PM1 || enc == APNN_ENC_W_PM1_A_01;
-    if (pm1) { prepare_i8_kernel<1, true><<<gb, 256, 0, s>>>(W, N, K, Kw, out); }
+    if (pm1) { prepare_i8_kernel<1, true><<<gb, threads, 0, s>>>(W, N, K, Kw, out); }
     else {
         switch (w_bits) {
-        case 1: prepare_i8_kernel<1, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
-        case 2: prepare_i8_kernel<2, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
-        case 3: prepare_i8_kernel<3, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
-        case 4: prepare_i8_kernel<4, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
-        case 5: prepare_i8_kernel<5, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
-        case 6: prepare_i8_kernel<6, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
-        case 7: prepare_i8_kernel<7, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
-        default: prepare_i8_kernel<8, false><<<gb, 256, 0, s>>>(W, N, K, Kw, out); break;
+        case 1: prepare_i8_kernel<1, false><<<gb, threads, 0, s>>>(W, N, K, Kw, out); break;
+        case 2: prepare_i8_kernel<2, false><<<gb, threads, 0, s>>>(W, N, K, Kw, out); break;
+        case 3: prepare_i8_kernel<3, false><<<gb, threads, 0, s>>>(W, N, K, Kw, out); break;
+        case 4: prepare_i8_kernel<4, false><<<gb, threads, 0, s>>>(W, N, K, Kw, out); break;
+        case 5: prepare_i8_kernel<5, false><<<gb, threads, 0, s>>>(W, N, K, Kw, out); break;
+        case 6: prepare_i8_kernel<6, false><<<gb, threads, 0, s>>>(W, N, K, Kw, out); break;
+        case 7: prepare_i8_kernel<7, false><<<gb, threads, 0, s>>>(W, N, K, Kw, out); break;
+        default: prepare_i8_kernel<8, false><<<gb, threads, 0, s>>>(W, N, K, Kw, out); break;
         }
     }
     count_launch();

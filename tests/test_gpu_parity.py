@@ -483,6 +483,42 @@ def test_fp4_prepared_full_size_sampled_rows():
 
 
 
+@pytest.mark.parametrize("M,N,K", [(300, 270, 300), (257, 520, 2048), (1000, 64, 640), (4096, 1200, 1000), (1, 33, 64)])
+@pytest.mark.parametrize("a_bits,w_bits,enc", [(2, 1, 2), (8, 8, 0), (4, 4, 0), (1, 1, 1), (1, 3, 3), (3, 5, 0),
+                                               (1, 4, 3), (4, 1, 2)])
+def test_i8_both_prepared_exact(M, N, K, a_bits, w_bits, enc):
+    # apnn_gemm_prepared_ab_i8: int8 activation rows (apnn_prepare_activations_i8) x prepared int8
+    # weights on the persistent kind::i8 pair kernel; ragged M / N / K, several tiles per pair
+    # (4096 x 1200: 80 tiles of 256 x 256 on 74 pairs), a single row; int32 and fused output
+    A, W = synth.gemm_inputs(M, N, K, a_bits, w_bits, tag="i8pp")
+    Y = oracle.gemm(A, W, a_bits, w_bits, enc)
+    Aq = ap.prepare_activations_i8(ap.pack_bits(cuda(A), a_bits), M, K, a_bits, enc)
+    Wprep = ap.prepare_weights_i8(ap.pack_bits(cuda(W), w_bits), N, K, w_bits, enc)
+    got = ap.gemm_prepared_ab_i8(Aq, Wprep, M, N, K, a_bits, w_bits, enc)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy(), Y)
+    for ob in (2, 5):
+        alpha, beta, S = epi_case(N, ob, "i8pp")
+        want = oracle.pack(oracle.epilogue(Y, alpha, beta, S, ob), ob)
+        got = ap.gemm_prepared_ab_i8(Aq, Wprep, M, N, K, a_bits, w_bits, enc,
+                                     epi=ap.Epilogue(ob, cuda(alpha), cuda(beta), S))
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(u32(got), want)
+
+
+def test_i8_both_prepared_full_size_sampled_rows():
+    # w8a8 at the sweep's largest point: |Y| up to K * 255^2 ~ 5.3e8 (int32, no FP4 bound)
+    M = N = K = 8192
+    a, w, enc = 8, 8, 0
+    A, W = synth.gemm_inputs(M, N, K, a, w, tag="i8pp-full")
+    Aq = ap.prepare_activations_i8(ap.pack_bits(cuda(A), a), M, K, a, enc)
+    Wprep = ap.prepare_weights_i8(ap.pack_bits(cuda(W), w), N, K, w, enc)
+    Y = ap.gemm_prepared_ab_i8(Aq, Wprep, M, N, K, a, w, enc)
+    torch.cuda.synchronize()
+    rows = _sample_rows(M, 12, "i8pp-full")
+    np.testing.assert_array_equal(Y.cpu().numpy()[rows], oracle.gemm(A[rows], W, a, w, enc))
+
+
 @pytest.mark.parametrize("M,N,K", [(300, 270, 300), (257, 520, 2048), (1000, 64, 640), (600, 100, 1152)])
 @pytest.mark.parametrize("a_bits,w_bits,enc", [(2, 1, 2), (8, 8, 0), (4, 4, 0), (1, 1, 1), (1, 3, 3), (3, 5, 0)])
 def test_i8_prepared_weights_exact(M, N, K, a_bits, w_bits, enc):
