@@ -242,16 +242,17 @@ def test_fp4_pair_kernel_persistent_tiles(a, w, enc, out_bits):
         np.testing.assert_array_equal(u32(got), want)
 
 
-@pytest.mark.parametrize("bn", [256, 224])
 @pytest.mark.parametrize("a,w,enc", FP4_COMBOS)
 @pytest.mark.parametrize("out_bits", [0, 2, 5])
 @pytest.mark.parametrize("M,N,K", [(4096, 1200, 1000), (300, 520, 2048), (1, 33, 64), (1000, 8192, 256)])
-def test_fp4_both_prepared_tiles(bn, a, w, enc, out_bits, M, N, K):
+def test_fp4_both_prepared_tiles(a, w, enc, out_bits, M, N, K):
     # apnn_gemm_prepared_ab: ragged M / N / K, several tiles per CTA pair (4096 x 1200: 96 tiles
-    # at 256, 112 at 224), a single row, the widest N.  The tile width is read once per process
-    # (APNN_FP4_PP_BN): the default run covers its width, an APNN_FP4_PP_BN=256 run the other.
-    if _pp_bn() != bn:
-        pytest.skip(f"this process runs APNN_FP4_PP_BN={_pp_bn()} (the other width runs in its own process)")
+    # at 256, 112 at 224), a single row, the widest N (the process's tile width; the other width
+    # runs in test_fp4_both_prepared_other_width)
+    check_both_prepared(a, w, enc, out_bits, M, N, K)
+
+
+def check_both_prepared(a, w, enc, out_bits, M, N, K):
     A, W = synth.gemm_inputs(M, N, K, a, w, tag=f"fp4-pp-{M}")
     Y = oracle.gemm(A, W, a, w, enc)
     Apl = ap.pack_bits(cuda(A), a)
@@ -271,9 +272,22 @@ def test_fp4_both_prepared_tiles(bn, a, w, enc, out_bits, M, N, K):
         np.testing.assert_array_equal(u32(got), want)
 
 
-def _pp_bn():
+def test_fp4_both_prepared_other_width():
+    # the tile width is read once per process (APNN_FP4_PP_BN): run the 256-wide, one-accumulator
+    # variant in a child process over a subset of the cases above
     import os
-    return 256 if os.environ.get("APNN_FP4_PP_BN") == "256" else 224
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_fp4_exact as t\n"
+            "for (a, w, enc) in t.FP4_COMBOS:\n"
+            "    for ob in (0, 2):\n"
+            "        for (M, N, K) in ((4096, 1200, 1000), (1, 33, 64)):\n"
+            "            t.check_both_prepared(a, w, enc, ob, M, N, K)\n"
+            "print('ok')\n")
+    env = dict(os.environ, APNN_FP4_PP_BN="256")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
 
 
 def test_fp4_both_prepared_rejects_mismatched_tags():
