@@ -229,6 +229,16 @@ apnn_status apnn_quant_pack_out(const int32_t *Y, int M, int N, const apnn_epilo
 apnn_status apnn_pool_quant_pack_out(const int32_t *Y, int B, int H, int W, int N,
                                      const apnn_epilogue *epi, uint32_t *out, apnn_stream_t stream);
 
+/* k x k / stride max pooling over packed codes ("maximum" pooling; reading R15:
+ * the requantisation is non-decreasing in v, so max-pooling the codes equals quantising the
+ * max-pooled v -- a conv with the fused requant + pack followed by this call is the pooled layer,
+ * for any window, without an int32 map in HBM):
+ *   X: device packed codes [B*H*W][bits][roundup(C,128)/32] (NHWC pixel rows)
+ *   Y: device packed codes [B*Hp*Wp][bits][roundup(C,128)/32], Hp = (H - k)/stride + 1, Wp likewise
+ *   (no padding; padding words of X come out as zeros).  Asynchronous on `stream`; no allocation. */
+apnn_status apnn_maxpool_packed(const uint32_t *X, int B, int H, int W, int C, int bits, int k, int stride,
+                                uint32_t *Y, apnn_stream_t stream);
+
 /* Residual element-wise routine (ResNet basic block; reading R24 -- the paper does not
  * describe residual connections): the shortcut is added to the folded-BN value before
  * the quantisation,

@@ -169,6 +169,22 @@ def pool_epilogue(Y, alpha, beta, S, out_bits, k, stride=None, avg=False):
     return q
 
 
+def maxpool_codes(Q, k, stride=None):
+    """k x k / stride max pooling of codes Q [B,H,W,N] (no padding), the definition written out:
+    out[b,i,j,n] = max over dy, dx < k of Q[b, stride*i + dy, stride*j + dx, n] (PAPER.md:1293,
+    "maximum" pooling over k x k grids; applied to codes per reading R15)."""
+    Q = np.asarray(Q)
+    stride = k if stride is None else stride
+    B, H, Wd, N = Q.shape
+    Hp, Wp = (H - k) // stride + 1, (Wd - k) // stride + 1
+    out = np.zeros((B, Hp, Wp, N), dtype=Q.dtype)
+    for dy in range(k):
+        for dx in range(k):
+            win = Q[:, dy:dy + stride * (Hp - 1) + 1:stride, dx:dx + stride * (Wp - 1) + 1:stride, :]
+            out = np.maximum(out, win)
+    return out
+
+
 def residual_epilogue(Y, Z, alpha, beta, rho, S, out_bits):
     """Residual requantisation (reading R24; ResNet blocks are not described in the paper):
     v = alpha[n]*Y + beta[n] + rho[n]*Z in int64, q = clamp(floor(v / S), 0, 2^out_bits - 1).

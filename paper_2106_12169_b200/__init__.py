@@ -139,6 +139,8 @@ def lib() -> ctypes.CDLL:
             L.apnn_conv2d_ex.restype = st
             L.apnn_quant_pack_out.argtypes = [vp, ci, ci, ctypes.POINTER(_Epi), vp, vp]
             L.apnn_quant_pack_out.restype = st
+            L.apnn_maxpool_packed.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, vp, vp]
+            L.apnn_maxpool_packed.restype = st
             L.apnn_pool_quant_pack_out.argtypes = [vp, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp, vp]
             L.apnn_pool_quant_pack_out.restype = st
             L.apnn_select_variant.argtypes = [ci, ci, ci, ci, ci, ci]
@@ -164,7 +166,7 @@ ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_im2col_pack", "apnn_
                "apnn_prepare_activations_i8", "apnn_gemm_prepared_ab_i8",
                "apnn_prepared_i8_bytes", "apnn_prepare_weights_i8", "apnn_gemm_prepared_i8",
                "apnn_conv2d_prepared_i8", "apnn_conv_halo_fits", "apnn_conv2d_first_prepared_i8", "apnn_conv_first_fits", "apnn_tune_tiles", "apnn_gemm_tiled", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
-               "apnn_conv2d", "apnn_conv2d_ex", "apnn_quant_pack_out", "apnn_pool_quant_pack_out",
+               "apnn_conv2d", "apnn_conv2d_ex", "apnn_quant_pack_out", "apnn_pool_quant_pack_out", "apnn_maxpool_packed",
                "apnn_residual_quant_pack",
                "apnn_select_variant", "apnn_select_variant_fused",
                "apnn_status_string", "apnn_variant_name", "apnn_launch_count", "apnn_version")
@@ -654,6 +656,24 @@ def pool_quant_pack_out(Y: torch.Tensor, epi: Epilogue, out: Optional[torch.Tens
     _check_out(out, packed_shape(B * Hp * Wp, N, epi.out_bits))
     _check(lib().apnn_pool_quant_pack_out(_ptr(Y), B, H, Wd, N, ctypes.byref(epi._c()), _ptr(out), _stream(Y)),
            "apnn_pool_quant_pack_out")
+    return out
+
+
+def maxpool_packed(X: torch.Tensor, B: int, H: int, W: int, C: int, bits: int, k: int, stride: int = 0,
+                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """k x k / stride max pooling of packed codes [B*H*W, bits, Kw(C)] -> [B*Hp*Wp, bits, Kw(C)]
+    (apnn_maxpool_packed)."""
+    stride = stride or k
+    _cuda(X, "X", torch.int32)
+    _check_out(X, packed_shape(B * H * W, C, bits), "X")
+    Hp, Wp = (H - k) // stride + 1, (W - k) // stride + 1
+    shape = packed_shape(B * Hp * Wp, C, bits)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.int32, device=X.device)
+    _cuda(out, "out", torch.int32)
+    _check_out(out, shape)
+    _check(lib().apnn_maxpool_packed(_ptr(X), B, H, W, C, bits, k, stride, _ptr(out), _stream(X)),
+           "apnn_maxpool_packed")
     return out
 
 

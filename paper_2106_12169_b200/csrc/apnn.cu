@@ -18,6 +18,8 @@ cudaError_t launch_pack_bits(const uint8_t* codes, int rows, int K, int bits, ui
                              cudaStream_t s);
 cudaError_t launch_quant_pack(const int32_t* Y, int M, int N, const Epi& e, uint32_t* out, int sms,
                               cudaStream_t s);
+cudaError_t launch_maxpool_packed(const uint32_t* X, int B, int H, int W, int C, int bits, int k, int stride,
+                                  uint32_t* Y, int sms, cudaStream_t s);
 cudaError_t launch_pool_quant_pack(const int32_t* Y, int B, int H, int W, int N, const Epi& e, uint32_t* out,
                                   int sms, cudaStream_t s);
 bool tc_i8_pool_fusable(const Geom& g, const Epi& e);
@@ -759,6 +761,24 @@ apnn_status apnn_pool_quant_pack_out(const int32_t* Y, int B, int H, int W, int 
     DevInfo d;
     if ((st = device_info(&d)) != APNN_OK) return st;
     cudaError_t err = launch_pool_quant_pack(Y, B, H, W, N, e, out, d.sms, (cudaStream_t)stream);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_status apnn_maxpool_packed(const uint32_t* X, int B, int H, int W, int C, int bits, int k, int stride,
+                                uint32_t* Y, apnn_stream_t stream) {
+    if (B < 0 || H < 1 || W < 1 || C < 0) return APNN_ERR_SHAPE;
+    if (bits < 1 || bits > 8) return APNN_ERR_BITS;
+    if (k < 1 || stride < 1) return APNN_ERR_INVALID_ARG;
+    if (k > H || k > W) return APNN_ERR_SHAPE;
+    const int Hp = (H - k) / stride + 1, Wp = (W - k) / stride + 1;
+    if ((long long)B * H * W > 2147483647LL || (long long)B * Hp * Wp > 2147483647LL) return APNN_ERR_SHAPE;
+    if (B > 0 && C > 0 && (!X || !Y)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(X) || !aligned16(Y)) return APNN_ERR_ALIGNMENT;
+    DevInfo d;
+    apnn_status st;
+    if ((st = device_info(&d)) != APNN_OK) return st;
+    if (B == 0 || C == 0) return APNN_OK;
+    cudaError_t err = launch_maxpool_packed(X, B, H, W, C, bits, k, stride, Y, d.sms, (cudaStream_t)stream);
     return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }
 

@@ -513,5 +513,75 @@ cudaError_t launch_flatten_packed(const uint32_t* src, int B, int P, int bits, i
     count_launch();
     return cudaGetLastError();
 }
+
+// ---------------------------------------------------------------------------------------------
+// k x k / stride max pooling over PACKED codes (apnn_maxpool_packed).  The requantisation
+// q = clamp(floor(v / S), 0, Q) is non-decreasing in v, so max-pooling the codes equals
+// quantising the max-pooled v (reading R15): a conv with the fused
+// requant + pack followed by this pass does max pooling of any window without the int32 map
+// ever reaching HBM.  Bit-sliced: one thread owns one 32-channel word of one output pixel and
+// keeps the running maximum of its window as `bits` plane words; max(x, y) per lane walks the
+// planes from the MSB (x > y at the first differing plane where x has the 1).
+template <int BITS>
+__global__ void __launch_bounds__(256) maxpool_packed_kernel(const uint32_t* __restrict__ X, int B, int H, int W,
+                                                             int Cw, int k, int stride, int Hp, int Wp,
+                                                             uint32_t* __restrict__ Y) {
+    const long long total = (long long)B * Hp * Wp * Cw;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int wd = (int)(idx % Cw);
+        const long long pix = idx / Cw;
+        const int px = (int)(pix % Wp);
+        const long long t = pix / Wp;
+        const int py = (int)(t % Hp);
+        const int b = (int)(t / Hp);
+        uint32_t m[BITS];
+        const uint32_t* src = X + (((long long)b * H + (long long)py * stride) * W + (long long)px * stride) * BITS * Cw + wd;
+#pragma unroll
+        for (int pl = 0; pl < BITS; pl++) m[pl] = __ldg(src + pl * Cw);
+        for (int dy = 0; dy < k; dy++)
+            for (int dx = 0; dx < k; dx++) {
+                if ((dy | dx) == 0) continue;
+                const uint32_t* q = src + ((long long)dy * W + dx) * BITS * Cw;
+                uint32_t x[BITS];
+#pragma unroll
+                for (int pl = 0; pl < BITS; pl++) x[pl] = __ldg(q + pl * Cw);
+                uint32_t gt = 0u, eq = 0xFFFFFFFFu;  // lanes where x > m so far / still equal
+#pragma unroll
+                for (int pl = BITS - 1; pl >= 0; pl--) {
+                    gt |= eq & x[pl] & ~m[pl];
+                    eq &= ~(x[pl] ^ m[pl]);
+                }
+#pragma unroll
+                for (int pl = 0; pl < BITS; pl++) m[pl] = (gt & x[pl]) | (~gt & m[pl]);
+            }
+        uint32_t* dst = Y + pix * BITS * Cw + wd;
+#pragma unroll
+        for (int pl = 0; pl < BITS; pl++) dst[pl * Cw] = m[pl];
+    }
+}
+
+cudaError_t launch_maxpool_packed(const uint32_t* X, int B, int H, int W, int C, int bits, int k, int stride,
+                                  uint32_t* Y, int sms, cudaStream_t s) {
+    const int Cw = (C + 127) / 128 * 4;
+    const int Hp = (H - k) / stride + 1, Wp = (W - k) / stride + 1;
+    const long long total = (long long)B * Hp * Wp * Cw;
+    if (total <= 0) return cudaSuccess;
+    long long blocks = (total + 255) / 256;
+    if (blocks > (long long)sms * 16) blocks = (long long)sms * 16;
+    const int gb = (int)blocks;
+    switch (bits) {
+    case 1: maxpool_packed_kernel<1><<<gb, 256, 0, s>>>(X, B, H, W, Cw, k, stride, Hp, Wp, Y); break;
+    case 2: maxpool_packed_kernel<2><<<gb, 256, 0, s>>>(X, B, H, W, Cw, k, stride, Hp, Wp, Y); break;
+    case 3: maxpool_packed_kernel<3><<<gb, 256, 0, s>>>(X, B, H, W, Cw, k, stride, Hp, Wp, Y); break;
+    case 4: maxpool_packed_kernel<4><<<gb, 256, 0, s>>>(X, B, H, W, Cw, k, stride, Hp, Wp, Y); break;
+    case 5: maxpool_packed_kernel<5><<<gb, 256, 0, s>>>(X, B, H, W, Cw, k, stride, Hp, Wp, Y); break;
+    case 6: maxpool_packed_kernel<6><<<gb, 256, 0, s>>>(X, B, H, W, Cw, k, stride, Hp, Wp, Y); break;
+    case 7: maxpool_packed_kernel<7><<<gb, 256, 0, s>>>(X, B, H, W, Cw, k, stride, Hp, Wp, Y); break;
+    default: maxpool_packed_kernel<8><<<gb, 256, 0, s>>>(X, B, H, W, Cw, k, stride, Hp, Wp, Y); break;
+    }
+    count_launch();
+    return cudaGetLastError();
+}
 }  // namespace apnn
 

@@ -5,11 +5,12 @@ straight to the next layer (minimal-traffic dataflow).
 
 This module only sequences calls of the C ABI (every step runs in libapnn's kernels):
 
-  first conv   apnn_im2col_pack (NHWC uint8 image codes -> packed im2col rows, K = R*S*3)
-               + apnn_gemm_fused, or int32 apnn_gemm + apnn_pool_quant_pack_out when the
-               layer is followed by pooling
-  conv         apnn_conv2d with the fused epilogue (2x2 max pooling fused when the library
-               can; otherwise the unfused pair conv + apnn_pool_quant_pack_out)
+  first conv   apnn_conv2d_first_prepared_i8 straight from the raw image (or apnn_im2col_pack
+               + apnn_gemm_fused), pooling fused where the kernel can
+  conv         apnn_conv2d[_prepared_i8] with the fused epilogue (2x2/2 max pooling fused)
+  pooling the conv kernels cannot fuse: max pooling (AlexNet's 3x3/2) = the conv with the fused
+               requant + pack, then apnn_maxpool_packed over the packed codes (reading R15);
+               average pooling = int32 conv + apnn_pool_quant_pack_out
   first FC     apnn_flatten_packed + apnn_gemm_fused (split-K clusters at small batch)
   FC           apnn_gemm_fused; the classifier returns int32 logits.
 
@@ -19,6 +20,7 @@ folded-BN parameters come from `synth` (they are the oracle's inputs too).
 """
 from __future__ import annotations
 
+import dataclasses
 from typing import Optional
 
 import numpy as np
@@ -26,7 +28,7 @@ import torch
 
 from . import (ApnnError, ConvShape, Epilogue, conv2d, conv2d_first_prepared_i8, conv2d_prepared_i8, conv_first_fits,
                conv_halo_fits, flatten_packed, gemm, im2col_pack, prepare_first_weights_i8,
-               pack_bits, pool_quant_pack_out, prepare_weights_i8, residual_quant_pack, synth)
+               maxpool_packed, pack_bits, pool_quant_pack_out, prepare_weights_i8, residual_quant_pack, synth)
 
 
 def _prep_conv(Wpacked, L, w_bits, enc):
@@ -35,13 +37,24 @@ def _prep_conv(Wpacked, L, w_bits, enc):
     return prepare_weights_i8(Wpacked, L["Co"] * L["R"] * L["S"], L["C"], w_bits, enc)
 
 
-def _conv(X, Wpacked, Wprep, shape, a, w, enc, epi=None, out=None, y32=None):
+def _no_pool(epi):
+    return None if epi is None else dataclasses.replace(epi, pool=0, pool_stride=0, pool_avg=False)
+
+
+def _conv(X, Wpacked, Wprep, shape, a, w, enc, epi=None, out=None, y32=None, qfull=None):
     """APConv: the tap-reuse kernel (apnn_conv2d_prepared_i8) wherever it fits -- with the
-    epilogue fused, or, for pooling it cannot fuse (3x3/2, average), as int32 into `y32` + the
-    pooling routine -- else the per-tap kernels (prepared weights for B*Ho*Wo > 128, packed
+    epilogue fused; for max pooling it cannot fuse (AlexNet's 3x3/2) with the requantisation
+    fused into the conv (packed codes into `qfull`) + apnn_maxpool_packed over the codes (R15:
+    max-pooling codes = quantising the max-pooled v); for average pooling as int32 into `y32` +
+    the pooling routine -- else the per-tap kernels (prepared weights for B*Ho*Wo > 128, packed
     weights otherwise, which also run the unfused pooling pair)."""
     if conv_halo_fits(shape, a, w, enc, epi):
         return conv2d_prepared_i8(X, Wprep, shape, a, w, enc, epi=epi, out=out)
+    if (epi is not None and epi.pool and not epi.pool_avg and qfull is not None
+            and conv_halo_fits(shape, a, w, enc, _no_pool(epi))):
+        conv2d_prepared_i8(X, Wprep, shape, a, w, enc, epi=_no_pool(epi), out=qfull)
+        return maxpool_packed(qfull, shape.B, shape.Ho, shape.Wo, shape.C_out, epi.out_bits, epi.pool,
+                              epi.pool_stride or epi.pool, out=out)
     if epi is not None and epi.pool and y32 is not None and conv_halo_fits(shape, a, w, enc, None):
         conv2d_prepared_i8(X, Wprep, shape, a, w, enc, out=y32)
         return pool_quant_pack_out(y32, epi, out=out)
@@ -97,16 +110,21 @@ class APNNModel:
                                                                dtype=torch.int32, device=self.dev)
                 if L["pool"]:
                     st["Y32"] = torch.empty((batch, L["Ho"], L["Wo"], L["Co"]), dtype=torch.int32, device=self.dev)
+                    # max pooling the kernel cannot fuse: requantise in the conv, pool the codes
+                    st["Qf"] = torch.empty((M, a_bits, (L["Co"] + 127) // 128 * 4), dtype=torch.int32,
+                                           device=self.dev)
             elif L["kind"] == "conv":
                 st["mode"] = "conv"
                 st["W"] = pack_bits(torch.from_numpy(Wt.reshape(-1, L["C"])).to(self.dev), w_bits)
                 st["Wprep"] = _prep_conv(st["W"], L, w_bits, self.enc)
                 st["shape"] = ConvShape(batch, L["H"], L["W"], L["C"], L["Co"], L["R"], L["S"], L["stride"],
                                         L["pad"])
-                st["Y32c"] = None
+                st["Y32c"] = st["Qc"] = None
                 if st["epi"] is not None and st["epi"].pool and not conv_halo_fits(
                         st["shape"], a_bits, w_bits, self.enc, st["epi"]):
                     st["Y32c"] = torch.empty((batch, L["Ho"], L["Wo"], L["Co"]), dtype=torch.int32, device=self.dev)
+                    st["Qc"] = torch.empty((batch * L["Ho"] * L["Wo"], a_bits, (L["Co"] + 127) // 128 * 4),
+                                           dtype=torch.int32, device=self.dev)
             elif L["H"] * L["W"] > 1:  # first FC: flatten the packed map, weights in [P][Cpad] order
                 st["mode"] = "flatten_fc"
                 Pn, C = L["H"] * L["W"], L["C"]
@@ -148,19 +166,30 @@ class APNNModel:
                 if st["first_epi"] is not None or epi is None:
                     act = conv2d_first_prepared_i8(self.x, st["Wf"], st["shape"], zq, sq, a, w, enc, epi=epi,
                                                    out=st["out"])
-                else:  # pooling the kernel cannot fuse (AlexNet 3x3/2): int32 + the pooling routine
+                elif not epi.pool_avg:  # max pooling the kernel cannot fuse (AlexNet 3x3/2):
+                    # requantise in the conv, then max-pool the packed codes (reading R15)
+                    conv2d_first_prepared_i8(self.x, st["Wf"], st["shape"], zq, sq, a, w, enc, epi=_no_pool(epi),
+                                             out=st["Qf"])
+                    act = maxpool_packed(st["Qf"], self.B, L["Ho"], L["Wo"], L["Co"], epi.out_bits, epi.pool,
+                                         epi.pool_stride or epi.pool, out=st["out"])
+                else:  # average pooling: int32 + the pooling routine
                     conv2d_first_prepared_i8(self.x, st["Wf"], st["shape"], zq, sq, a, w, enc, out=st["Y32"])
                     act = pool_quant_pack_out(st["Y32"], epi, out=st["out"])
             elif st["mode"] == "im2col":
                 im2col_pack(self.x, st["shape"], a, out=st["A"], quant=self.input_quant)
                 M = self.B * L["Ho"] * L["Wo"]
-                if L["pool"]:
+                if L["pool"] and not epi.pool_avg:  # fused requant, then max-pool the codes (R15)
+                    gemm(st["A"], st["W"], M, L["Co"], L["K"], a, w, enc, epi=_no_pool(epi), out=st["Qf"])
+                    act = maxpool_packed(st["Qf"], self.B, L["Ho"], L["Wo"], L["Co"], epi.out_bits, epi.pool,
+                                         epi.pool_stride or epi.pool, out=st["out"])
+                elif L["pool"]:
                     Y = gemm(st["A"], st["W"], M, L["Co"], L["K"], a, w, enc, out=st["Y32"].view(M, L["Co"]))
                     act = pool_quant_pack_out(st["Y32"], epi, out=st["out"])
                 else:
                     act = gemm(st["A"], st["W"], M, L["Co"], L["K"], a, w, enc, epi=epi, out=st["out"])
             elif st["mode"] == "conv":
-                act = _conv(act, st["W"], st["Wprep"], st["shape"], a, w, enc, epi=epi, out=st["out"], y32=st["Y32c"])
+                act = _conv(act, st["W"], st["Wprep"], st["shape"], a, w, enc, epi=epi, out=st["out"], y32=st["Y32c"],
+                            qfull=st["Qc"])
             else:
                 A = act
                 if st["mode"] == "flatten_fc":

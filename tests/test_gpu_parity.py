@@ -353,6 +353,39 @@ POOL_CASES = [  # (B, H, W, C, Co, stride, pool, pool_stride, avg, fused expecte
 ]
 
 
+@pytest.mark.parametrize("B,H,W,C,k,st", [(2, 55, 55, 96, 3, 2), (3, 27, 27, 256, 3, 2), (1, 13, 13, 384, 3, 2),
+                                         (2, 14, 15, 64, 2, 2), (1, 9, 7, 130, 3, 1), (4, 8, 8, 33, 3, 3),
+                                         (1, 5, 5, 1, 5, 1)])
+@pytest.mark.parametrize("bits", [1, 2, 3, 8])
+def test_maxpool_packed(B, H, W, C, k, st, bits):
+    # apnn_maxpool_packed (bit-sliced max over packed codes) against oracle.maxpool_codes; ragged
+    # C (channel-padding words must come out zero), overlapping 3x3/2 windows of AlexNet's maps
+    Q = synth.codes((B, H, W, C), bits, f"mp{H}{C}{k}{st}")
+    X = ap.pack_bits(cuda(Q.reshape(-1, C)), bits)
+    got = ap.maxpool_packed(X, B, H, W, C, bits, k, st)
+    torch.cuda.synchronize()
+    want = oracle.maxpool_codes(Q, k, st)
+    np.testing.assert_array_equal(u32(got), oracle.pack(want.reshape(-1, C), bits))
+
+
+def test_conv_fused_requant_then_maxpool_equals_pool_epilogue():
+    # the models' path for AlexNet's 3x3/2: conv with the fused requant + pack on the tap-reuse
+    # kernel, then the packed max pool == the oracle's conv -> BN -> 3x3/2 max pool -> quant
+    B, H, C, Co = 2, 27, 96, 256
+    a, w, enc, ob = 2, 1, 2, 2
+    X, Wt = synth.conv_inputs(B, H, H, C, Co, 5, 5, a, w, tag="c3pool")
+    alpha, beta, S = epi_case(Co, ob, "c3pool")
+    shape = ap.ConvShape(B, H, H, C, Co, 5, 5, 1, 2)
+    Xp = ap.pack_bits(cuda(X.reshape(-1, C)), a)
+    Wprep = ap.prepare_weights_i8(ap.pack_bits(cuda(Wt.reshape(-1, C)), w), Co * 25, C, w, enc)
+    q = ap.conv2d_prepared_i8(Xp, Wprep, shape, a, w, enc, epi=ap.Epilogue(ob, cuda(alpha), cuda(beta), S))
+    got = ap.maxpool_packed(q, B, H, H, Co, ob, 3, 2)
+    torch.cuda.synchronize()
+    Y = oracle.conv2d(X, Wt, 1, 2, a, w, enc)
+    want = oracle.pool_epilogue(Y, alpha, beta, S, ob, 3, 2)
+    np.testing.assert_array_equal(u32(got), oracle.pack(want.reshape(-1, Co), ob))
+
+
 @pytest.mark.parametrize("case", POOL_CASES)
 @pytest.mark.parametrize("a_bits,w_bits,enc,out_bits", [(2, 1, 2, 2), (2, 2, 0, 1), (1, 1, 1, 5)])
 def test_conv_pool_fused_and_unfused(case, a_bits, w_bits, enc, out_bits):

@@ -234,6 +234,22 @@ def test_pool_max_commutes_with_requant():
             np.testing.assert_array_equal(q, m)
 
 
+@pytest.mark.parametrize("k,st", [(2, 2), (3, 2), (2, 1), (3, 3), (3, 1)])
+def test_maxpool_codes_vs_torch_and_commutation(k, st):
+    """oracle.maxpool_codes (max pooling of codes, used after a conv with the fused requant)
+    against torch max_pool2d in float64, and the R15 identity against the C oracle's
+    pool_epilogue: quantise-then-max-pool == max-pool-then-quantise for any alpha sign."""
+    import torch
+    g = synth.rng(f"mpc{k}{st}")
+    Q = g.integers(0, 8, size=(2, 11, 9, 13)).astype(np.uint8)
+    want = torch.nn.functional.max_pool2d(torch.from_numpy(Q.astype(np.float64)).permute(0, 3, 1, 2), k, st)
+    np.testing.assert_array_equal(oracle.maxpool_codes(Q, k, st), want.permute(0, 2, 3, 1).numpy().astype(np.uint8))
+    Y, alpha, beta = _pool_case(f"mpc-commute{k}{st}", B=2, H=11, W=9, N=13)
+    for S, b in ((1, 1), (61, 2), (2**16, 8)):
+        u = oracle.epilogue(Y.reshape(-1, 13), alpha, beta, S, b).reshape(Y.shape)
+        np.testing.assert_array_equal(oracle.maxpool_codes(u, k, st), oracle.pool_epilogue(Y, alpha, beta, S, b, k, st))
+
+
 def test_pool_identity_window_and_hand_example():
     Y, alpha, beta = _pool_case("id")
     q1 = oracle.pool_epilogue(Y, alpha, beta, 7, 5, 1, 1)
