@@ -4,9 +4,10 @@
 Workload (BASELINE.json configs[1], the GEMM sweep the metric is quoted on;
 its largest point): M = N = K = 8192, w1a2, 0/1 activations x +-1 weights
 (Case III).  One step = the whole hot path over one batch:
-    apnn_pack_bits(A codes)                      row a1 (bit decomposition)
-    apnn_prepare_activations(A planes)           row a4 on A's side (planes -> e2m1 operand
-                                                 rows, once per step instead of per N tile)
+    apnn_pack_bits_prepared(A codes)             row a1 (bit decomposition into the packed
+                                                 planes) fused with row a4 on A's side (the
+                                                 e2m1 operand rows, once per step instead of
+                                                 once per N tile inside the GEMM)
     apnn_gemm_prepared_ab(A op, W op, epi)       rows a2-a5 + a7 (contraction on the fp4 pipe,
                                                  exact; requant + repack fused)
 W is packed and prepared once at init (weights are static).
@@ -64,6 +65,8 @@ def parse():
     ap.add_argument("--no-prepared", action="store_true", help="FP4 kernel with per-tile W recombination")
     ap.add_argument("--no-prepared-a", action="store_true",
                     help="A planes decoded inside the GEMM (apnn_gemm_prepared) instead of once per step")
+    ap.add_argument("--no-fused-pack", action="store_true",
+                    help="apnn_pack_bits + apnn_prepare_activations as two passes instead of apnn_pack_bits_prepared")
     ap.add_argument("--model-batch", type=int, default=256, help="global batch of AlexNet / VGG-Variant")
     ap.add_argument("--resnet-batch", type=int, default=1024, help="global batch of ResNet-18 w2a8")
     return ap.parse_args()
@@ -319,9 +322,14 @@ def run_ours(args):
     if prep_a:
         A_prep = ap.prepare_activations(A_planes, M, K, a, enc)
 
+    fused_pack = prep_a and not args.no_fused_pack
+
     def step(ev_g0=None, ev_g1=None):
-        ap.pack_bits(A_codes, a, out=A_planes)
-        if prep_a:
+        if fused_pack:  # one pass: planes (the bit decomposition) + the e2m1 operand rows
+            ap.pack_bits_prepared(A_codes, a, enc, out=A_planes, prep=A_prep)
+        else:
+            ap.pack_bits(A_codes, a, out=A_planes)
+        if prep_a and not fused_pack:
             ap.prepare_activations(A_planes, M, K, a, enc, out=A_prep.data)
         if ev_g0 is not None:
             ev_g0.record(stream)
@@ -419,9 +427,12 @@ def run_ours(args):
                     A_dev[b].copy_(A_host, non_blocking=True)
                     up = ev(); up.record(s_h2d)
                 stream.wait_event(up)
-                ap.pack_bits(A_dev[b], a, out=P_dev[b])
+                if fused_pack:
+                    ap.pack_bits_prepared(A_dev[b], a, enc, out=P_dev[b], prep=Q_dev[b])
+                else:
+                    ap.pack_bits(A_dev[b], a, out=P_dev[b])
                 packed_ev[b] = ev(); packed_ev[b].record(stream)
-                if prep_a:
+                if prep_a and not fused_pack:
                     ap.prepare_activations(P_dev[b], M, K, a, enc, out=Q_dev[b].data)
                 if d2h_ev[b] is not None:
                     stream.wait_event(d2h_ev[b])              # Y_dev[b] downloaded
@@ -496,7 +507,8 @@ def run_ours(args):
         "config": {"workload": f"apmm_w{w}a{a}_{M if args.scaling == 'weak' else M_global}x{N}x{K}_fused_pack",
                    "M": M_global, "M_per_rank": M, "N": N, "K": K, "a_bits": a,
                    "w_bits": w, "encoding": ENC_NAME[enc], "out": f"packed {out_bits}-bit (fused requant)",
-                   "step": "apnn_pack_bits(A) + " + (
+                   "step": ("apnn_pack_bits_prepared(A codes -> planes + e2m1 rows) + apnn_gemm_prepared_ab "
+                            "(W prepared at init)") if fused_pack else "apnn_pack_bits(A) + " + (
                        "apnn_prepare_activations(A planes) + apnn_gemm_prepared_ab (W prepared at init)" if prep_a
                        else "apnn_gemm_prepared (W prepared at init)" if W_prep is not None else "apnn_gemm_fused"),
                    "variant": ap.variant_name(resolved) + ("_prepared_ab" if prep_a else "_prepared" if W_prep is not None

@@ -289,6 +289,14 @@ apnn_status apnn_gemm_prepared_ab(const uint8_t *Ap, const uint8_t *Wp, int M, i
                                   int w_bits, apnn_encoding enc, const apnn_epilogue *epi, void *Y,
                                   apnn_stream_t stream);
 
+/* apnn_pack_bits fused with apnn_prepare_activations (<= 2-bit codes): one pass over the codes
+ * writes the packed planes to dst (exactly as apnn_pack_bits) AND the e2m1 operand rows to Ap
+ * (exactly as apnn_prepare_activations of those planes; apnn_prepared_bytes(rows, K) bytes).
+ * enc decides whether the codes are +-1 activations (APNN_ENC_PM1_PM1 / APNN_ENC_W_01_A_PM1,
+ * bits == 1).  bits > 2: APNN_ERR_UNSUPPORTED. */
+apnn_status apnn_pack_bits_prepared(const uint8_t *codes, int rows, int K, int bits, apnn_encoding enc,
+                                    uint32_t *dst, uint8_t *Ap, apnn_stream_t stream);
+
 /* Prepared int8 weights for the int8 tensor-core kernel (any w_bits; the B decode that grows
  * with w_bits is done once at load time):
  *   Wp: device, apnn_prepared_i8_bytes(N, K) bytes: int8 operand rows [N][roundup(K,128)] in

@@ -93,6 +93,8 @@ def lib() -> ctypes.CDLL:
             L.apnn_prepare_weights.restype = st
             L.apnn_gemm_prepared.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp, vp]
             L.apnn_gemm_prepared.restype = st
+            L.apnn_pack_bits_prepared.argtypes = [vp, ci, ci, ci, ci, vp, vp, vp]
+            L.apnn_pack_bits_prepared.restype = st
             L.apnn_prepare_activations.argtypes = [vp, ci, ci, ci, ci, vp, vp]
             L.apnn_prepare_activations.restype = st
             L.apnn_gemm_prepared_ab.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp, vp]
@@ -162,7 +164,7 @@ def lib() -> ctypes.CDLL:
 ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_im2col_pack", "apnn_im2col_quant_pack",
                "apnn_flatten_packed",
                "apnn_prepared_bytes", "apnn_prepare_weights", "apnn_gemm_prepared",
-               "apnn_prepare_activations", "apnn_gemm_prepared_ab",
+               "apnn_prepare_activations", "apnn_gemm_prepared_ab", "apnn_pack_bits_prepared",
                "apnn_prepare_activations_i8", "apnn_gemm_prepared_ab_i8",
                "apnn_prepared_i8_bytes", "apnn_prepare_weights_i8", "apnn_gemm_prepared_i8",
                "apnn_conv2d_prepared_i8", "apnn_conv_halo_fits", "apnn_conv2d_first_prepared_i8", "apnn_conv_first_fits", "apnn_tune_tiles", "apnn_gemm_tiled", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
@@ -420,6 +422,27 @@ def prepare_activations(A: torch.Tensor, M: int, K: int, a_bits: int, enc: int,
     _check(lib().apnn_prepare_activations(_ptr(A), M, K, a_bits, enc, _ptr(out), _stream(A)),
            "apnn_prepare_activations")
     return PreparedWeights(out, "fp4a", M, K, a_bits, enc)
+
+
+def pack_bits_prepared(codes: torch.Tensor, bits: int, enc: int, out: Optional[torch.Tensor] = None,
+                       prep: Optional[PreparedWeights] = None):
+    """Codes [rows, K] -> (packed planes [rows, bits, Kw], e2m1 activation rows tagged "fp4a") in one
+    pass (apnn_pack_bits_prepared; bits <= 2)."""
+    _cuda(codes, "codes", torch.uint8)
+    rows, K = codes.shape
+    if out is None:
+        out = torch.empty(packed_shape(rows, K, bits), dtype=torch.int32, device=codes.device)
+    _cuda(out, "out", torch.int32)
+    _check_out(out, packed_shape(rows, K, bits))
+    nbytes = int(lib().apnn_prepared_bytes(rows, K))
+    if prep is None:
+        prep = PreparedWeights(torch.empty(nbytes, dtype=torch.uint8, device=codes.device), "fp4a", rows, K, bits, enc)
+    t = prep.check("fp4a", rows, K, bits, enc)
+    _cuda(t, "prep", torch.uint8)
+    _check_out(t, (nbytes,))
+    _check(lib().apnn_pack_bits_prepared(_ptr(codes), rows, K, bits, enc, _ptr(out), _ptr(t), _stream(codes)),
+           "apnn_pack_bits_prepared")
+    return out, prep
 
 
 def gemm_prepared_ab(Ap: PreparedWeights, Wp: PreparedWeights, M: int, N: int, K: int, a_bits: int, w_bits: int,

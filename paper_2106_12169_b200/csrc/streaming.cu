@@ -17,53 +17,73 @@
 
 namespace apnn {
 
-// codes [rows][K] -> dst [rows][bits][Kw]
-template <bool kVec>
+// codes [rows][K] -> dst [rows][bits][Kw].  PREP (apnn_pack_bits_prepared, <= 2-bit codes): the
+// same thread also writes the 32 codes' e2m1 operand bytes (the rows of apnn_prepare_activations:
+// word j of a 32-element group holds elements j, j+4, ..., j+28; 0/1 codes v -> value v, +-1
+// codes (PM1) -> +-1.0 with elements >= K value 0), so the GEMM's A operand comes out of the bit
+// decomposition without a second pass over the planes.  x over a row's words, y over rows,
+// 32-bit index math.
+template <bool kVec, bool PREP, bool PM1>
 __global__ void __launch_bounds__(256) pack_bits_kernel(const uint8_t* __restrict__ codes, int rows,
                                                         int K, int bits, int Kw,
-                                                        uint32_t* __restrict__ dst) {
-    const long long total = (long long)rows * Kw;
+                                                        uint32_t* __restrict__ dst, uint8_t* __restrict__ prep) {
     const uint32_t keep = (bits >= 8) ? 0xFFFFFFFFu : (0x01010101u * ((1u << bits) - 1u));
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(idx / Kw);
-        const int w = (int)(idx - (long long)r * Kw);
-        const int k0 = w * 32;
-        uint32_t u[8];
-        if (k0 + 32 <= K) {
-            const uint8_t* src = codes + (long long)r * K + k0;
-            if (kVec) {
-                uint4 v0 = __ldg(reinterpret_cast<const uint4*>(src));
-                uint4 v1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
-                u[0] = v0.x; u[1] = v0.y; u[2] = v0.z; u[3] = v0.w;
-                u[4] = v1.x; u[5] = v1.y; u[6] = v1.z; u[7] = v1.w;
-            } else {
+    for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < rows; r += gridDim.y * blockDim.y) {
+        const uint8_t* crow = codes + (long long)r * K;
+        uint32_t* out = dst + (long long)r * bits * Kw;
+        for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < Kw; w += gridDim.x * blockDim.x) {
+            const int k0 = w * 32;
+            uint32_t u[8];
+            if (k0 + 32 <= K) {
+                const uint8_t* src = crow + k0;
+                if (kVec) {
+                    uint4 v0 = __ldg(reinterpret_cast<const uint4*>(src));
+                    uint4 v1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+                    u[0] = v0.x; u[1] = v0.y; u[2] = v0.z; u[3] = v0.w;
+                    u[4] = v1.x; u[5] = v1.y; u[6] = v1.z; u[7] = v1.w;
+                } else {
 #pragma unroll
-                for (int q = 0; q < 8; q++)
-                    u[q] = (uint32_t)src[4 * q] | ((uint32_t)src[4 * q + 1] << 8) |
-                           ((uint32_t)src[4 * q + 2] << 16) | ((uint32_t)src[4 * q + 3] << 24);
-            }
-        } else {
-            // ragged tail / padding run: codes beyond K are zero
-#pragma unroll
-            for (int q = 0; q < 8; q++) {
-                uint32_t x = 0;
-#pragma unroll
-                for (int b = 0; b < 4; b++) {
-                    int k = k0 + 4 * q + b;
-                    if (k < K) x |= (uint32_t)codes[(long long)r * K + k] << (8 * b);
+                    for (int q = 0; q < 8; q++)
+                        u[q] = (uint32_t)src[4 * q] | ((uint32_t)src[4 * q + 1] << 8) |
+                               ((uint32_t)src[4 * q + 2] << 16) | ((uint32_t)src[4 * q + 3] << 24);
                 }
-                u[q] = x;
+            } else {
+                // ragged tail / padding run: codes beyond K are zero
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    uint32_t x = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; b++) {
+                        int k = k0 + 4 * q + b;
+                        if (k < K) x |= (uint32_t)crow[k] << (8 * b);
+                    }
+                    u[q] = x;
+                }
             }
-        }
 #pragma unroll
-        for (int q = 0; q < 8; q++) u[q] &= keep;  // codes are masked to their low `bits` bits
-        uint32_t* out = dst + (long long)r * bits * Kw + w;
-        for (int t = 0; t < bits; t++) {
-            uint32_t word = 0;
+            for (int q = 0; q < 8; q++) u[q] &= keep;  // codes are masked to their low `bits` bits
+            uint32_t pw[2] = {0u, 0u};
+            for (int t = 0; t < bits; t++) {
+                uint32_t word = 0;
 #pragma unroll
-            for (int q = 0; q < 8; q++) word |= byte_bits_to_nibble(u[q], t) << (4 * q);
-            out[(long long)t * Kw] = word;
+                for (int q = 0; q < 8; q++) word |= byte_bits_to_nibble(u[q], t) << (4 * q);
+                out[(long long)t * Kw + w] = word;
+                if (PREP && t < 2) pw[t] = word;
+            }
+            if (PREP) {
+                const int nv = K - k0;
+                const uint32_t vm = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
+                uint32_t o[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const uint32_t b0 = (pw[0] >> j) & 0x11111111u, b1 = (pw[1] >> j) & 0x11111111u;
+                    uint32_t v;
+                    if (PM1) v = 0x22222222u | ((b0 ^ 0x11111111u) << 3);  // +1 -> 0x2, -1 -> 0xA
+                    else v = (b1 << 2) | ((b0 & ~b1) << 1) | (b0 & b1);    // 0..3 -> 0x0, 0x2, 0x4, 0x5
+                    o[j] = v & (((vm >> j) & 0x11111111u) * 0xFu);         // elements >= K: value 0
+                }
+                *reinterpret_cast<uint4*>(prep + ((long long)r * Kw + w) * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+            }
         }
     }
 }
@@ -467,16 +487,28 @@ __global__ void __launch_bounds__(256) flatten_packed_kernel(const uint32_t* __r
     }
 }
 
+template <bool PREP, bool PM1>
+static void pack_launch(bool vec, dim3 grid, dim3 threads, cudaStream_t s, const uint8_t* codes, int rows, int K,
+                        int bits, int Kw, uint32_t* dst, uint8_t* prep) {
+    if (vec) pack_bits_kernel<true, PREP, PM1><<<grid, threads, 0, s>>>(codes, rows, K, bits, Kw, dst, prep);
+    else pack_bits_kernel<false, PREP, PM1><<<grid, threads, 0, s>>>(codes, rows, K, bits, Kw, dst, prep);
+}
+
+// prep != nullptr: also the e2m1 operand rows (bits <= 2; pm1: +-1 codes)
 cudaError_t launch_pack_bits(const uint8_t* codes, int rows, int K, int bits, uint32_t* dst,
-                             int sms, cudaStream_t s) {
+                             int sms, cudaStream_t s, uint8_t* prep, bool pm1) {
     const int Kw = (K + 127) / 128 * 4;
-    const long long total = (long long)rows * Kw;
-    if (total == 0) return cudaSuccess;
+    if ((long long)rows * Kw == 0) return cudaSuccess;
     const bool vec = (K % 16 == 0) && ((reinterpret_cast<uintptr_t>(codes) & 15) == 0);
-    if (vec)
-        pack_bits_kernel<true><<<stream_grid(total, sms), 256, 0, s>>>(codes, rows, K, bits, Kw, dst);
-    else
-        pack_bits_kernel<false><<<stream_grid(total, sms), 256, 0, s>>>(codes, rows, K, bits, Kw, dst);
+    dim3 threads(Kw >= 256 ? 256 : (Kw + 31) / 32 * 32, 1);
+    threads.y = 256 / threads.x;
+    dim3 grid((Kw + threads.x - 1) / threads.x, 1);
+    const long long ry = ((long long)sms * 8 + grid.x - 1) / grid.x, need = ((long long)rows + threads.y - 1) / threads.y;
+    grid.y = (unsigned)(ry < need ? ry : need);
+    if (grid.y > 65535) grid.y = 65535;
+    if (!prep) pack_launch<false, false>(vec, grid, threads, s, codes, rows, K, bits, Kw, dst, prep);
+    else if (pm1) pack_launch<true, true>(vec, grid, threads, s, codes, rows, K, bits, Kw, dst, prep);
+    else pack_launch<true, false>(vec, grid, threads, s, codes, rows, K, bits, Kw, dst, prep);
     count_launch();
     return cudaGetLastError();
 }

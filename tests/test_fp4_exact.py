@@ -301,3 +301,35 @@ def test_fp4_both_prepared_rejects_mismatched_tags():
         ap.gemm_prepared_ab(Wprep, Wprep, M, N, K, 2, 1, 2)  # weights passed as activations
     with pytest.raises(ValueError):
         ap.gemm_prepared_ab(Aprep, Wprep, M, N, K, 2, 1, 0)  # other encoding
+
+
+@pytest.mark.parametrize("a,enc", [(1, 0), (2, 0), (1, 1), (2, 2), (1, 3)])
+@pytest.mark.parametrize("rows,K", [(300, 1000), (7, 8192), (129, 33), (1, 4096)])
+def test_pack_bits_prepared_matches_two_pass(a, enc, rows, K):
+    # the fused decomposition + operand preparation writes exactly the planes of apnn_pack_bits
+    # and the rows of apnn_prepare_activations (ragged K: the +-1 padding must be value 0)
+    codes = synth.codes((rows, K), a, f"pbp{rows}{K}")
+    planes, prep = ap.pack_bits_prepared(cuda(codes), a, enc)
+    ref_planes = ap.pack_bits(cuda(codes), a)
+    ref_prep = ap.prepare_activations(ref_planes, rows, K, a, enc)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(u32(planes), oracle.pack(codes, a))
+    assert torch.equal(planes, ref_planes)
+    assert torch.equal(prep.data, ref_prep.data)
+
+
+def test_pack_bits_prepared_bench_step_sampled_rows():
+    # the bench step end to end at full size: codes -> (planes, operand rows) -> both-prepared GEMM
+    M = N = K = 8192
+    a, w, enc = 2, 1, 2
+    A, W = synth.gemm_inputs(M, N, K, a, w, tag="bench")
+    alpha, beta = synth.epilogue_params(N, tag="bench")
+    S = 1 << 10
+    _, Aq = ap.pack_bits_prepared(cuda(A), a, enc)
+    Wq = ap.prepare_weights(ap.pack_bits(cuda(W), w), N, K, w, enc)
+    Y = ap.gemm_prepared_ab(Aq, Wq, M, N, K, a, w, enc, epi=ap.Epilogue(a, cuda(alpha), cuda(beta), S))
+    torch.cuda.synchronize()
+    g = synth.rng("pbp-bench-rows")
+    rows = np.array(sorted(set([0, 255, 256, M - 1] + g.integers(0, M, size=12).tolist())))
+    want = oracle.pack(oracle.epilogue(oracle.gemm(A[rows], W, a, w, enc), alpha, beta, S, a), a)
+    np.testing.assert_array_equal(u32(Y)[rows], want)
