@@ -26,6 +26,12 @@ def gemm_case(M, N, K, a, w, enc, variant, ob=0, prepared=None):
         got = ap.gemm_prepared(Ap, ap.prepare_weights(Wp, N, K, w, enc), M, N, K, a, w, enc, epi=epi)
     elif prepared == "i8":
         got = ap.gemm_prepared_i8(Ap, ap.prepare_weights_i8(Wp, N, K, w, enc), M, N, K, a, w, enc, epi=epi)
+    elif prepared == "fp4ab":  # fused pack + operand rows, both-prepared FP4 pair kernel
+        _, Aq = ap.pack_bits_prepared(cuda(A), a, enc)
+        got = ap.gemm_prepared_ab(Aq, ap.prepare_weights(Wp, N, K, w, enc), M, N, K, a, w, enc, epi=epi)
+    elif prepared == "i8ab":
+        got = ap.gemm_prepared_ab_i8(ap.prepare_activations_i8(Ap, M, K, a, enc), ap.prepare_weights_i8(Wp, N, K, w, enc),
+                                     M, N, K, a, w, enc, epi=epi)
     else:
         got = ap.gemm(Ap, Wp, M, N, K, a, w, enc, epi=epi, variant=variant)
     torch.cuda.synchronize()
@@ -62,11 +68,20 @@ gemm_case(300, 270, 300, 2, 1, 2, ap.VARIANT_TC_FP4)           # one-CTA fp4
 gemm_case(100, 270, 300, 2, 1, 2, ap.VARIANT_TC_FP4, prepared="fp4")      # one-CTA fp4 prepared
 gemm_case(600, 520, 700, 2, 1, 2, ap.VARIANT_TC_FP4, ob=2, prepared="fp4")  # fp4 pair kernel
 gemm_case(600, 520, 700, 2, 2, 0, ap.VARIANT_TC_FP4, prepared="fp4")        # fp4 pair kernel int32
+gemm_case(600, 520, 1100, 2, 1, 2, ap.VARIANT_TC_FP4, ob=2, prepared="fp4ab")  # both prepared, fused
+gemm_case(300, 260, 700, 1, 1, 1, ap.VARIANT_TC_FP4, prepared="fp4ab")        # both prepared, int32
+gemm_case(600, 300, 700, 4, 4, 0, ap.VARIANT_TC_I8, ob=4, prepared="i8ab")    # int8 both prepared
+gemm_case(64, 1024, 1024, 2, 1, 2, ap.VARIANT_POPC, ob=2)                     # warp popc kernel
 gemm_case(70, 90, 300, 3, 2, 0, ap.VARIANT_POPC)
 gemm_case(70, 90, 300, 2, 1, 2, ap.VARIANT_B1MMA)
 conv_case((2, 14, 14, 64, 64, 3, 3, 1, 1), 2, 1, 2)
 conv_case((2, 16, 16, 64, 64, 3, 3, 1, 1), 2, 1, 2, ob=2, pool=2)
 conv_case((1, 9, 9, 70, 40, 3, 3, 2, 1), 2, 2, 0, ob=2)
+# max pooling over packed codes (AlexNet 3x3/2)
+Q = synth.codes((2, 13, 13, 100), 2, "san-mp")
+got = ap.maxpool_packed(ap.pack_bits(cuda(Q.reshape(-1, 100)), 2), 2, 13, 13, 100, 2, 3, 2)
+torch.cuda.synchronize()
+checks.append(("maxpool_packed 2x13x13x100 3x3/2", np.array_equal(u32(got), oracle.pack(oracle.maxpool_codes(Q, 3, 2).reshape(-1, 100), 2))))
 bad = [n for n, ok in checks if not ok]
 for n, ok in checks:
     print(("ok  " if ok else "BAD ") + n)
