@@ -545,8 +545,22 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, ui
 // I8: the same kernel on kind::i8 (int8 operand rows from apnn_prepare_weights_i8 /
 // apnn_prepare_activations_i8, int32 accumulators, no scale factors): a 128-byte box is 128 K
 // elements instead of 256, the descriptors and the stage walk are the same
-template <int BNP, bool I32, bool I8>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
+//
+// MC: clusters of two CTA pairs that work on vertically adjacent tiles (tm, tm + 1) of the same
+// N tile; the W operand is loaded once per cluster and multicast to both pairs (CTA r of pair 0
+// issues W half r into CTA r and CTA r + 2), halving W's L2 -> SM traffic; a stage slot is freed
+// only when both pairs' MMAs are done with it (the empty barriers count both pairs' commits).
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const void* tmap, uint32_t bar_cluster, int c0, int c1,
+                                                    uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster.cta_group::2 "
+        "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(tmap), "r"(bar_cluster), "r"(c0), "r"(c1), "h"(mask)
+        : "memory");
+}
+
+template <int BNP, bool I32, bool I8, bool MC>
+__global__ void __launch_bounds__(PP_THREADS, 1)
     fp4_pp_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
                   const Params p) {
     constexpr int BROWS = BNP / 2;
@@ -575,8 +589,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accum_empty + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const uint32_t rank = cluster_ctarank();
-    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    constexpr int CL = MC ? 4 : 2;                     // CTAs per cluster
+    const uint32_t crank = cluster_ctarank();
+    const uint32_t rank = crank & 1u;                  // rank within the CTA pair
+    const uint32_t lead = crank & ~1u;                 // the pair's leader (barriers, MMA issue)
+    const int pic = MC ? (int)(crank >> 1) : 0;        // pair within the cluster
+    const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+    const int units_m = MC ? p.tiles_m / 2 : p.tiles_m;
+    const int num_units = units_m * p.tiles_n;
     const Geom& g = p.g;
     const int nst = p.nst;
 
@@ -585,7 +605,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
         tma_prefetch(&tmapB);
         for (int s = 0; s < S; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], MC ? 2 : 1);  // both pairs' commits
         }
         for (int i = 0; i < 2; i++) {
             mbar_init(&accum_full[i], 1);
@@ -614,15 +634,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
 
     if (warp == PP_TMA) {
         // ------------------------------------------------------------ TMA producer (A + W)
-        const int my_tiles = p.num_tiles > cid ? (p.num_tiles - cid + ncl - 1) / ncl : 0;
+        const int my_tiles = num_units > cid ? (num_units - cid + ncl - 1) / ncl : 0;
         const int total = APNN_EXP_PP == 7 ? 0 : my_tiles * nst;
-        const uint32_t full0 = mapa(smem_u32(full), 0);
+        const uint32_t full0 = mapa(smem_u32(full), lead);
         if (lane == 0) {
             int ti = 0, st = 0, s = 0;
             uint32_t ph = 0;
             for (int it = 0; it < total; it++) {
-                const int tile = cid + ti * ncl;
-                const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+                const int u = cid + ti * ncl;
+                const int tm = (u % units_m) * (MC ? 2 : 1) + pic, tn = u / units_m;
                 sm100::mbar_wait_sleep(&empty[s], ph ^ 1);  // parked, not spinning: the issuer needs the slots
 #if APNN_EXP_PP >= 3
                 if (rank == 0) mbar_arrive(&full[s]);
@@ -633,7 +653,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
 #pragma unroll
                 for (int h = 0; h < 2; h++) {
                     tma_load_2d_pair(sAop + (size_t)s * AST + h * AOP, &tmapA, fb, st * 256 + h * 128, arow);
-                    tma_load_2d_pair(sBop + (size_t)s * BST + h * BOP, &tmapB, fb, st * 256 + h * 128, brow);
+                    if (!MC)
+                        tma_load_2d_pair(sBop + (size_t)s * BST + h * BOP, &tmapB, fb, st * 256 + h * 128, brow);
+                    else if (pic == 0)  // W half `rank` into this CTA and its counterpart in pair 1
+                        tma_load_2d_pair_mc(sBop + (size_t)s * BST + h * BOP, &tmapB, fb, st * 256 + h * 128, brow,
+                                            (uint16_t)((1u << rank) | (1u << (rank + 2))));
                 }
 #endif
                 if (++st == nst) { st = 0; ti++; }
@@ -644,11 +668,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
     } else if (warp == PP_MMA) {
         // ------------------------------------------------------------ MMA issuer (CTA 0)
         if (rank == 0 && lane == 0) {
+            const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pic));
+            const uint16_t empty_mask = MC ? (uint16_t)0xF : (uint16_t)0x3;
             const uint32_t idesc = I8 ? p.idesc : idesc_mxf4(256, BNP);
             const uint32_t a0 = smem_u32(sAop), b0 = smem_u32(sBop), full_a = smem_u32(full);
             int s = 0, tc = 0, itr = 0;
             uint32_t ph = 0;
-            for (int tile = cid; tile < p.num_tiles; tile += ncl, tc++) {
+            for (int u = cid; u < num_units; u += ncl, tc++) {
                 const int buf = NACC == 2 ? (tc & 1) : 0;
                 mbar_wait_cluster(&accum_empty[buf], ((tc / NACC) & 1) ^ 1);
                 tc_fence_after();
@@ -674,12 +700,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
                         if (I8) mma2_i8_ss(d, da, db, idesc, (st | kk) != 0);
                         else mma2_mxf4(d, da, db, idesc, tmem + SFA, tmem + SFB, (st | kk) != 0);
                     }
-                    mma2_commit_mc(&empty[s], 0x3);
+                    mma2_commit_mc(&empty[s], empty_mask);
                     pp_tr(2, itr);
                     s = s_next;
                     ph = ph_next;
                 }
-                mma2_commit_mc(&accum_full[buf], 0x3);
+                mma2_commit_mc(&accum_full[buf], pair_mask);
             }
         }
     } else {
@@ -689,13 +715,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
         const int c_begin = slice * NCK / QW, c_end = (slice + 1) * NCK / QW;
         const int nwb = c_end - c_begin;
         const uint32_t tmem_lane = tmem + ((uint32_t)(q * 32) << 16);
-        const uint32_t accum_empty0 = mapa(smem_u32(accum_empty), 0);
+        const uint32_t accum_empty0 = mapa(smem_u32(accum_empty), lead);
         const int ob = p.e.out_bits;
         const int Nw = (g.N + 127) / 128 * 4;
         uint8_t* stg = sStg + (size_t)warp * p.stg_warp;
         int tc = 0;
-        for (int tile = cid; tile < p.num_tiles; tile += ncl, tc++) {
-            const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+        for (int u = cid; u < num_units; u += ncl, tc++) {
+            const int tm = (u % units_m) * (MC ? 2 : 1) + pic, tn = u / units_m;
             const int row0 = (tm * 2 + (int)rank) * 128 + q * 32;
             const int n0 = tn * BNP;
             if (!I32 && (p.tab_mode == tc::kTabQ3 || p.tab_mode == tc::kTabHybrid) && APNN_EXP_PP != 7) {
@@ -767,11 +793,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
 
 template <int BNP, bool I8>
 static cudaError_t launch_pp(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid, size_t smem,
-                             cudaStream_t s) {
-    auto kfn = p.e.out_bits == 0 ? fp4_pp_kernel<BNP, true, I8> : fp4_pp_kernel<BNP, false, I8>;
+                             cudaStream_t s, bool mc) {
+    auto kfn = mc ? (p.e.out_bits == 0 ? fp4_pp_kernel<BNP, true, I8, true> : fp4_pp_kernel<BNP, false, I8, true>)
+                  : (p.e.out_bits == 0 ? fp4_pp_kernel<BNP, true, I8, false> : fp4_pp_kernel<BNP, false, I8, false>);
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kfn<<<grid, PP_THREADS, smem, s>>>(ta, tb, p);
+    if (mc) e = cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(PP_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = mc ? 4 : 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kfn, ta, tb, p);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -915,6 +956,44 @@ static int fp4_pp_bn_override() {
     return v;
 }
 
+template <int BNP, bool I32, bool I8>
+static int max_clusters4(size_t smem) {
+    using namespace fp4::pair;
+    auto kfn = fp4_pp_kernel<BNP, I32, I8, true>;
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(4);
+    cfg.blockDim = dim3(PP_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 4;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kfn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+static int max_active_clusters_pp(bool i8, int bnp, bool i32, size_t smem) {
+    static int cache[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+    static size_t cache_smem[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int key = (i8 ? 4 : 0) + (bnp == 224 ? 2 : 0) + (i32 ? 1 : 0);
+    if (cache[key] >= 0 && cache_smem[key] == smem) return cache[key];
+    int n;
+    if (i8) n = i32 ? max_clusters4<256, true, true>(smem) : max_clusters4<256, false, true>(smem);
+    else if (bnp == 224) n = i32 ? max_clusters4<224, true, false>(smem) : max_clusters4<224, false, false>(smem);
+    else n = i32 ? max_clusters4<256, true, false>(smem) : max_clusters4<256, false, false>(smem);
+    cache[key] = n;
+    cache_smem[key] = smem;
+    return n;
+}
+
 // both operands prepared, e2m1 (I8 = false: apnn_prepare_weights / apnn_prepare_activations rows of
 // Kw * 16 bytes) or int8 (I8 = true: the _i8 preparations, rows of roundup(K, 128) bytes)
 static cudaError_t launch_pp_any(const uint8_t* Ap, const uint8_t* Wp, const Geom& g, const Epi& e, void* Y, int sms,
@@ -957,12 +1036,28 @@ static cudaError_t launch_pp_any(const uint8_t* Ap, const uint8_t* Wp, const Geo
     CUtensorMap ta, tb;
     if (!fp4::make_map_rows(&ta, Ap, g.M, row_bytes, 128)) return cudaErrorInvalidValue;
     if (!fp4::make_map_rows(&tb, Wp, g.N, row_bytes, BNP / 2)) return cudaErrorInvalidValue;
-    int pairs = sms / 2;
-    if (pairs > p.num_tiles) pairs = p.num_tiles;
-    const int grid = 2 * pairs;
-    cudaError_t err = i8 ? launch_pp<256, true>(ta, tb, p, grid, smem, s)
-                         : (BNP == 224 ? launch_pp<224, false>(ta, tb, p, grid, smem, s)
-                                       : launch_pp<256, false>(ta, tb, p, grid, smem, s));
+    // W multicast across the two pairs of a 4-CTA cluster (APNN_FP4_PP_MC=1, read once; off by
+    // default): bit-exact and halves W's L2 -> SM bytes, but measured slower on the bench GEMM
+    // (8192^3 w1a2 fused 0.203 vs 0.182 ms: fewer SMs hold whole 4-CTA clusters than CTA pairs,
+    // and the two pairs advance in lockstep through the shared stage slots)
+    static const int mc_env = [] { const char* v = getenv("APNN_FP4_PP_MC"); return v ? atoi(v) : 0; }();
+    const bool mc = mc_env != 0 && p.tiles_m % 2 == 0 && (long long)(p.tiles_m / 2) * p.tiles_n >= sms / 4;
+    int grid;
+    if (mc) {
+        // persistent: as many 4-CTA clusters as can be co-resident (GPC sizes need not be
+        // multiples of 4), never more than the cluster units
+        int clusters = max_active_clusters_pp(i8, BNP, e.out_bits == 0, smem);
+        if (clusters < 1) clusters = sms / 4;
+        if (clusters > (p.tiles_m / 2) * p.tiles_n) clusters = (p.tiles_m / 2) * p.tiles_n;
+        grid = 4 * clusters;
+    } else {
+        int pairs = sms / 2;
+        if (pairs > p.num_tiles) pairs = p.num_tiles;
+        grid = 2 * pairs;
+    }
+    cudaError_t err = i8 ? launch_pp<256, true>(ta, tb, p, grid, smem, s, mc)
+                         : (BNP == 224 ? launch_pp<224, false>(ta, tb, p, grid, smem, s, mc)
+                                       : launch_pp<256, false>(ta, tb, p, grid, smem, s, mc));
     count_launch();
     return err;
 }

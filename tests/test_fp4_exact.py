@@ -272,9 +272,10 @@ def check_both_prepared(a, w, enc, out_bits, M, N, K):
         np.testing.assert_array_equal(u32(got), want)
 
 
-def test_fp4_both_prepared_other_width():
-    # the tile width is read once per process (APNN_FP4_PP_BN): run the 256-wide, one-accumulator
-    # variant in a child process over a subset of the cases above
+@pytest.mark.parametrize("env", [{"APNN_FP4_PP_BN": "256"}, {"APNN_FP4_PP_MC": "1"}])
+def test_fp4_both_prepared_other_width(env):
+    # knobs read once per process: the 256-wide one-accumulator variant and the W-multicast
+    # 4-CTA-cluster variant, each in a child process over a subset of the cases above
     import os
     import subprocess
     import sys
@@ -282,10 +283,10 @@ def test_fp4_both_prepared_other_width():
     code = ("import sys; sys.path.insert(0, 'tests'); import test_fp4_exact as t\n"
             "for (a, w, enc) in t.FP4_COMBOS:\n"
             "    for ob in (0, 2):\n"
-            "        for (M, N, K) in ((4096, 1200, 1000), (1, 33, 64)):\n"
+            "        for (M, N, K) in ((4096, 1200, 1000), (1, 33, 64), (2048, 4100, 700)):\n"
             "            t.check_both_prepared(a, w, enc, ob, M, N, K)\n"
             "print('ok')\n")
-    env = dict(os.environ, APNN_FP4_PP_BN="256")
+    env = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
 
