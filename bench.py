@@ -4,10 +4,12 @@
 Workload (BASELINE.json configs[1], the GEMM sweep the metric is quoted on;
 its largest point): M = N = K = 8192, w1a2, 0/1 activations x +-1 weights
 (Case III).  One step = the whole hot path over one batch:
-    apnn_pack_bits_prepared(A codes)             row a1 (bit decomposition into the packed
+    apnn_pack_bits_dense(A codes, a bits each)   row a1 (bit decomposition into the packed
                                                  planes) fused with row a4 on A's side (the
                                                  e2m1 operand rows, once per step instead of
                                                  once per N tile inside the GEMM)
+The activations arrive as dense a-bit codes (the compact format of low-bit data: 16.8 MB for
+8192^2 w1a2); --byte-codes takes one byte per code (apnn_pack_bits_prepared, 67 MB).
     apnn_gemm_prepared_ab(A op, W op, epi)       rows a2-a5 + a7 (contraction on the fp4 pipe,
                                                  exact; requant + repack fused)
 W is packed and prepared once at init (weights are static).
@@ -65,6 +67,8 @@ def parse():
     ap.add_argument("--no-prepared", action="store_true", help="FP4 kernel with per-tile W recombination")
     ap.add_argument("--no-prepared-a", action="store_true",
                     help="A planes decoded inside the GEMM (apnn_gemm_prepared) instead of once per step")
+    ap.add_argument("--byte-codes", action="store_true",
+                    help="activations as one byte per code (apnn_pack_bits_prepared) instead of dense a-bit codes")
     ap.add_argument("--no-fused-pack", action="store_true",
                     help="apnn_pack_bits + apnn_prepare_activations as two passes instead of apnn_pack_bits_prepared")
     ap.add_argument("--model-batch", type=int, default=256, help="global batch of AlexNet / VGG-Variant")
@@ -323,9 +327,15 @@ def run_ours(args):
         A_prep = ap.prepare_activations(A_planes, M, K, a, enc)
 
     fused_pack = prep_a and not args.no_fused_pack
+    # the fused path takes the activations in their compact host format: a-bit codes stored densely
+    # (a bits per element, LSB first; 16.8 MB for 8192^2 w1a2 instead of 67 MB of one-byte codes)
+    dense = fused_pack and a <= 2 and not args.byte_codes
+    A_dense = torch.from_numpy(synth.dense_codes(A_np, a)).to(dev) if dense else None
 
     def step(ev_g0=None, ev_g1=None):
-        if fused_pack:  # one pass: planes (the bit decomposition) + the e2m1 operand rows
+        if dense:  # one pass from the dense codes: planes (the bit decomposition) + e2m1 operand rows
+            ap.pack_bits_dense(A_dense, M, K, a, enc, out=A_planes, prep=A_prep)
+        elif fused_pack:  # one pass: planes (the bit decomposition) + the e2m1 operand rows
             ap.pack_bits_prepared(A_codes, a, enc, out=A_planes, prep=A_prep)
         else:
             ap.pack_bits(A_codes, a, out=A_planes)
@@ -408,9 +418,9 @@ def run_ours(args):
     # unchanged).
     e2e = None
     if not args.no_e2e:
-        A_host = torch.from_numpy(A_np).pin_memory()
+        A_host = torch.from_numpy(synth.dense_codes(A_np, a) if dense else A_np).pin_memory()
         Y_host = [torch.empty(tuple(Y_packed.shape), dtype=torch.int32).pin_memory() for _ in range(2)]
-        A_dev = [torch.empty_like(A_codes) for _ in range(2)]
+        A_dev = [torch.empty(tuple(A_host.shape), dtype=torch.uint8, device=dev) for _ in range(2)]
         P_dev = [torch.empty_like(A_planes) for _ in range(2)]
         Q_dev = [ap.prepare_activations(A_planes, M, K, a, enc) for _ in range(2)] if prep_a else None
         Y_dev = [torch.empty_like(Y_packed) for _ in range(2)]
@@ -427,7 +437,9 @@ def run_ours(args):
                     A_dev[b].copy_(A_host, non_blocking=True)
                     up = ev(); up.record(s_h2d)
                 stream.wait_event(up)
-                if fused_pack:
+                if dense:
+                    ap.pack_bits_dense(A_dev[b], M, K, a, enc, out=P_dev[b], prep=Q_dev[b])
+                elif fused_pack:
                     ap.pack_bits_prepared(A_dev[b], a, enc, out=P_dev[b], prep=Q_dev[b])
                 else:
                     ap.pack_bits(A_dev[b], a, out=P_dev[b])
@@ -507,7 +519,9 @@ def run_ours(args):
         "config": {"workload": f"apmm_w{w}a{a}_{M if args.scaling == 'weak' else M_global}x{N}x{K}_fused_pack",
                    "M": M_global, "M_per_rank": M, "N": N, "K": K, "a_bits": a,
                    "w_bits": w, "encoding": ENC_NAME[enc], "out": f"packed {out_bits}-bit (fused requant)",
-                   "step": ("apnn_pack_bits_prepared(A codes -> planes + e2m1 rows) + apnn_gemm_prepared_ab "
+                   "step": ("apnn_pack_bits_dense(dense a-bit A codes -> planes + e2m1 rows) + apnn_gemm_prepared_ab "
+                            "(W prepared at init)") if dense else
+                           ("apnn_pack_bits_prepared(A codes -> planes + e2m1 rows) + apnn_gemm_prepared_ab "
                             "(W prepared at init)") if fused_pack else "apnn_pack_bits(A) + " + (
                        "apnn_prepare_activations(A planes) + apnn_gemm_prepared_ab (W prepared at init)" if prep_a
                        else "apnn_gemm_prepared (W prepared at init)" if W_prep is not None else "apnn_gemm_fused"),
@@ -515,6 +529,8 @@ def run_ours(args):
                                                            else ""),
                    "parallelism": f"dp{world} (" + ("M-row batch per GPU" if args.scaling == "weak"
                                                     else "global M sharded by rows") + ", W replicated)",
+                   "a_input": (f"dense {a}-bit codes, {A_dense.numel()} bytes" if dense
+                               else f"one byte per code, {A_codes.numel()} bytes"),
                    "l2": "flushed (512 MB write) between timed steps", "allgather": bool(gathered is not None)},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
                      "frac": achieved / peak, "traffic": traffic,

@@ -297,6 +297,16 @@ apnn_status apnn_gemm_prepared_ab(const uint8_t *Ap, const uint8_t *Wp, int M, i
 apnn_status apnn_pack_bits_prepared(const uint8_t *codes, int rows, int K, int bits, apnn_encoding enc,
                                     uint32_t *dst, uint8_t *Ap, apnn_stream_t stream);
 
+/* The bit decomposition from DENSE codes (the compact host format of low-bit data, bits <= 2):
+ *   dcodes: device; row r starts at byte r * ceil(K*bits/8); element k of a row is the `bits`-bit
+ *           field at bit k*bits of the row's little-endian bit stream (LSB first)
+ *   dst:    device packed planes [rows][bits][Kw], exactly as apnn_pack_bits of the same codes
+ *   Ap:     NULL, or device apnn_prepared_bytes(rows, K) bytes: also the e2m1 operand rows, exactly
+ *           as apnn_prepare_activations (enc decides +-1 activations, bits == 1)
+ * bits > 2: APNN_ERR_UNSUPPORTED. */
+apnn_status apnn_pack_bits_dense(const uint8_t *dcodes, int rows, int K, int bits, apnn_encoding enc,
+                                 uint32_t *dst, uint8_t *Ap, apnn_stream_t stream);
+
 /* Prepared int8 weights for the int8 tensor-core kernel (any w_bits; the B decode that grows
  * with w_bits is done once at load time):
  *   Wp: device, apnn_prepared_i8_bytes(N, K) bytes: int8 operand rows [N][roundup(K,128)] in

@@ -93,6 +93,8 @@ def lib() -> ctypes.CDLL:
             L.apnn_prepare_weights.restype = st
             L.apnn_gemm_prepared.argtypes = [vp, vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(_Epi), vp, vp]
             L.apnn_gemm_prepared.restype = st
+            L.apnn_pack_bits_dense.argtypes = [vp, ci, ci, ci, ci, vp, vp, vp]
+            L.apnn_pack_bits_dense.restype = st
             L.apnn_pack_bits_prepared.argtypes = [vp, ci, ci, ci, ci, vp, vp, vp]
             L.apnn_pack_bits_prepared.restype = st
             L.apnn_prepare_activations.argtypes = [vp, ci, ci, ci, ci, vp, vp]
@@ -164,7 +166,7 @@ def lib() -> ctypes.CDLL:
 ABI_SYMBOLS = ("apnn_packed_bytes", "apnn_pack_bits", "apnn_im2col_pack", "apnn_im2col_quant_pack",
                "apnn_flatten_packed",
                "apnn_prepared_bytes", "apnn_prepare_weights", "apnn_gemm_prepared",
-               "apnn_prepare_activations", "apnn_gemm_prepared_ab", "apnn_pack_bits_prepared",
+               "apnn_prepare_activations", "apnn_gemm_prepared_ab", "apnn_pack_bits_prepared", "apnn_pack_bits_dense",
                "apnn_prepare_activations_i8", "apnn_gemm_prepared_ab_i8",
                "apnn_prepared_i8_bytes", "apnn_prepare_weights_i8", "apnn_gemm_prepared_i8",
                "apnn_conv2d_prepared_i8", "apnn_conv_halo_fits", "apnn_conv2d_first_prepared_i8", "apnn_conv_first_fits", "apnn_tune_tiles", "apnn_gemm_tiled", "apnn_gemm", "apnn_gemm_fused", "apnn_gemm_ex",
@@ -442,6 +444,30 @@ def pack_bits_prepared(codes: torch.Tensor, bits: int, enc: int, out: Optional[t
     _check_out(t, (nbytes,))
     _check(lib().apnn_pack_bits_prepared(_ptr(codes), rows, K, bits, enc, _ptr(out), _ptr(t), _stream(codes)),
            "apnn_pack_bits_prepared")
+    return out, prep
+
+
+def pack_bits_dense(dcodes: torch.Tensor, rows: int, K: int, bits: int, enc: int = 0,
+                    out: Optional[torch.Tensor] = None, prep: Optional[PreparedWeights] = None, with_prep: bool = True):
+    """Dense bits-per-element codes (uint8 [rows, ceil(K*bits/8)], LSB first) -> packed planes
+    [rows, bits, Kw] and, with_prep, the e2m1 activation rows tagged "fp4a" (apnn_pack_bits_dense)."""
+    _cuda(dcodes, "dcodes", torch.uint8)
+    _check_out(dcodes, (rows, (K * bits + 7) // 8), "dcodes")
+    if out is None:
+        out = torch.empty(packed_shape(rows, K, bits), dtype=torch.int32, device=dcodes.device)
+    _cuda(out, "out", torch.int32)
+    _check_out(out, packed_shape(rows, K, bits))
+    t = None
+    if with_prep:
+        nbytes = int(lib().apnn_prepared_bytes(rows, K))
+        if prep is None:
+            prep = PreparedWeights(torch.empty(nbytes, dtype=torch.uint8, device=dcodes.device), "fp4a", rows, K,
+                                   bits, enc)
+        t = prep.check("fp4a", rows, K, bits, enc)
+        _cuda(t, "prep", torch.uint8)
+        _check_out(t, (nbytes,))
+    _check(lib().apnn_pack_bits_dense(_ptr(dcodes), rows, K, bits, enc, _ptr(out), None if t is None else _ptr(t),
+                                      _stream(dcodes)), "apnn_pack_bits_dense")
     return out, prep
 
 

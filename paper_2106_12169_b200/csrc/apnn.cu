@@ -16,6 +16,8 @@ void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_r
 
 cudaError_t launch_pack_bits(const uint8_t* codes, int rows, int K, int bits, uint32_t* dst, int sms,
                              cudaStream_t s, uint8_t* prep = nullptr, bool pm1 = false);
+cudaError_t launch_pack_dense(const uint8_t* codes, int rows, int K, int bits, uint32_t* dst, int sms,
+                              cudaStream_t s, uint8_t* prep, bool pm1);
 cudaError_t launch_quant_pack(const int32_t* Y, int M, int N, const Epi& e, uint32_t* out, int sms,
                               cudaStream_t s);
 cudaError_t launch_maxpool_packed(const uint32_t* X, int B, int H, int W, int C, int bits, int k, int stride,
@@ -278,6 +280,24 @@ apnn_status apnn_pack_bits_prepared(const uint8_t* codes, int rows, int K, int b
     apnn_status st = device_info(&d);
     if (st != APNN_OK) return st;
     cudaError_t err = launch_pack_bits(codes, rows, K, bits, dst, d.sms, (cudaStream_t)stream, Ap, apm);
+    return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
+}
+
+apnn_status apnn_pack_bits_dense(const uint8_t* dcodes, int rows, int K, int bits, apnn_encoding enc,
+                                 uint32_t* dst, uint8_t* Ap, apnn_stream_t stream) {
+    if (rows < 0 || K < 0) return APNN_ERR_SHAPE;
+    if (bits < 1 || bits > 8) return APNN_ERR_BITS;
+    if (enc < 0 || enc > 3) return APNN_ERR_ENCODING;
+    const bool apm = enc == APNN_ENC_PM1_PM1 || enc == APNN_ENC_W_01_A_PM1;
+    if (apm && bits != 1) return APNN_ERR_ENCODING;
+    if (bits > 2) return APNN_ERR_UNSUPPORTED;
+    if ((long long)K * bits > 2147483647LL) return APNN_ERR_SHAPE;
+    if ((rows > 0 && K > 0 && !dcodes) || (rows > 0 && !dst)) return APNN_ERR_INVALID_ARG;
+    if (!aligned16(dst) || !aligned16(Ap)) return APNN_ERR_ALIGNMENT;
+    DevInfo d;
+    apnn_status st = device_info(&d);
+    if (st != APNN_OK) return st;
+    cudaError_t err = launch_pack_dense(dcodes, rows, K, bits, dst, d.sms, (cudaStream_t)stream, Ap, apm);
     return err == cudaSuccess ? APNN_OK : APNN_ERR_CUDA;
 }
 

@@ -487,6 +487,103 @@ __global__ void __launch_bounds__(256) flatten_packed_kernel(const uint32_t* __r
     }
 }
 
+// Dense codes (apnn_pack_bits_dense): `BITS`-bit codes stored back to back, LSB first, each row
+// starting on a byte boundary (ceil(K * BITS / 8) bytes) -- the compact host format of low-bit
+// activations.  A thread takes the 32 * BITS bits of one 32-element group; for BITS = 2 plane t is
+// bit t of every 2-bit field, gathered by a 64 -> 32-bit compress; PREP writes the e2m1 rows too.
+__device__ __forceinline__ uint32_t compress_even_bits(unsigned long long x) {
+    x &= 0x5555555555555555ull;
+    x = (x | (x >> 1)) & 0x3333333333333333ull;
+    x = (x | (x >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+    x = (x | (x >> 4)) & 0x00FF00FF00FF00FFull;
+    x = (x | (x >> 8)) & 0x0000FFFF0000FFFFull;
+    x = (x | (x >> 16)) & 0x00000000FFFFFFFFull;
+    return (uint32_t)x;
+}
+
+template <int BITS, bool ALIGNED, bool PREP, bool PM1>
+__global__ void __launch_bounds__(256) pack_dense_kernel(const uint8_t* __restrict__ codes, int rows, int K,
+                                                         int row_bytes, int Kw, uint32_t* __restrict__ dst,
+                                                         uint8_t* __restrict__ prep) {
+    for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < rows; r += gridDim.y * blockDim.y) {
+        const uint8_t* crow = codes + (long long)r * row_bytes;
+        uint32_t* out = dst + (long long)r * BITS * Kw;
+        for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < Kw; w += gridDim.x * blockDim.x) {
+            const int k0 = w * 32;
+            const int nv = K - k0;  // valid elements of this group
+            unsigned long long x = 0;
+            if (nv > 0) {
+                const int b0 = k0 * BITS / 8, nb = BITS * 4;  // bytes of a full group
+                if (ALIGNED && nv >= 32) {
+                    x = BITS == 2 ? __ldg(reinterpret_cast<const unsigned long long*>(crow + b0))
+                                  : (unsigned long long)__ldg(reinterpret_cast<const uint32_t*>(crow + b0));
+                } else {
+                    const int have = (nv * BITS + 7) / 8 < nb ? (nv * BITS + 7) / 8 : nb;
+                    for (int i = 0; i < have; i++) x |= (unsigned long long)crow[b0 + i] << (8 * i);
+                }
+                if (nv < 32) x &= (BITS * nv >= 64) ? ~0ull : ((1ull << (BITS * nv)) - 1ull);
+            }
+            uint32_t pw[2];
+            if (BITS == 1) {
+                pw[0] = (uint32_t)x;
+                pw[1] = 0u;
+            } else {
+                pw[0] = compress_even_bits(x);
+                pw[1] = compress_even_bits(x >> 1);
+            }
+#pragma unroll
+            for (int t = 0; t < BITS; t++) out[(long long)t * Kw + w] = pw[t];
+            if (PREP) {
+                const uint32_t vm = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
+                uint32_t o[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const uint32_t e0 = (pw[0] >> j) & 0x11111111u, e1 = (pw[1] >> j) & 0x11111111u;
+                    uint32_t v;
+                    if (PM1) v = 0x22222222u | ((e0 ^ 0x11111111u) << 3);  // +1 -> 0x2, -1 -> 0xA
+                    else v = (e1 << 2) | ((e0 & ~e1) << 1) | (e0 & e1);    // 0..3 -> 0x0, 0x2, 0x4, 0x5
+                    o[j] = v & (((vm >> j) & 0x11111111u) * 0xFu);
+                }
+                *reinterpret_cast<uint4*>(prep + ((long long)r * Kw + w) * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+        }
+    }
+}
+
+template <int BITS, bool PREP, bool PM1>
+static void dense_launch(bool aligned, dim3 grid, dim3 threads, cudaStream_t s, const uint8_t* codes, int rows,
+                         int K, int row_bytes, int Kw, uint32_t* dst, uint8_t* prep) {
+    if (aligned)
+        pack_dense_kernel<BITS, true, PREP, PM1><<<grid, threads, 0, s>>>(codes, rows, K, row_bytes, Kw, dst, prep);
+    else
+        pack_dense_kernel<BITS, false, PREP, PM1><<<grid, threads, 0, s>>>(codes, rows, K, row_bytes, Kw, dst, prep);
+}
+
+// dense bits-per-element codes (bits 1 or 2) -> planes (+ e2m1 rows when prep != nullptr)
+cudaError_t launch_pack_dense(const uint8_t* codes, int rows, int K, int bits, uint32_t* dst, int sms,
+                              cudaStream_t s, uint8_t* prep, bool pm1) {
+    const int Kw = (K + 127) / 128 * 4;
+    if ((long long)rows * Kw == 0) return cudaSuccess;
+    const int row_bytes = (K * bits + 7) / 8;
+    const bool aligned = (row_bytes % (bits * 4) == 0) && ((reinterpret_cast<uintptr_t>(codes) & 7) == 0);
+    dim3 threads(Kw >= 256 ? 256 : (Kw + 31) / 32 * 32, 1);
+    threads.y = 256 / threads.x;
+    dim3 grid((Kw + threads.x - 1) / threads.x, 1);
+    const long long ry = ((long long)sms * 8 + grid.x - 1) / grid.x, need = ((long long)rows + threads.y - 1) / threads.y;
+    grid.y = (unsigned)(ry < need ? ry : need);
+    if (grid.y > 65535) grid.y = 65535;
+    if (bits == 1) {
+        if (!prep) dense_launch<1, false, false>(aligned, grid, threads, s, codes, rows, K, row_bytes, Kw, dst, prep);
+        else if (pm1) dense_launch<1, true, true>(aligned, grid, threads, s, codes, rows, K, row_bytes, Kw, dst, prep);
+        else dense_launch<1, true, false>(aligned, grid, threads, s, codes, rows, K, row_bytes, Kw, dst, prep);
+    } else {
+        if (!prep) dense_launch<2, false, false>(aligned, grid, threads, s, codes, rows, K, row_bytes, Kw, dst, prep);
+        else dense_launch<2, true, false>(aligned, grid, threads, s, codes, rows, K, row_bytes, Kw, dst, prep);
+    }
+    count_launch();
+    return cudaGetLastError();
+}
+
 template <bool PREP, bool PM1>
 static void pack_launch(bool vec, dim3 grid, dim3 threads, cudaStream_t s, const uint8_t* codes, int rows, int K,
                         int bits, int Kw, uint32_t* dst, uint8_t* prep) {

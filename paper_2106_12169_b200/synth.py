@@ -234,3 +234,13 @@ def resnet18_params(w_bits: int, a_bits: int, tag: str = "resnet18"):
         else:
             out.append(dict(W=weights(op, i), alpha=None, beta=None, S=None))
     return out
+
+
+def dense_codes(codes: np.ndarray, bits: int) -> np.ndarray:
+    """Storage format only: codes [rows, K] (< 2^bits) as a dense bit stream per row, `bits` bits per
+    element, LSB first, rows padded to whole bytes -> uint8 [rows, ceil(K*bits/8)] (the input of
+    apnn_pack_bits_dense).  numpy.packbits on the code bits; no arithmetic of the method."""
+    codes = np.asarray(codes, dtype=np.uint8)
+    rows, K = codes.shape
+    fields = ((codes[:, :, None] >> np.arange(bits, dtype=np.uint8)) & 1).reshape(rows, K * bits)
+    return np.packbits(fields, axis=1, bitorder="little")

@@ -334,3 +334,19 @@ def test_pack_bits_prepared_bench_step_sampled_rows():
     rows = np.array(sorted(set([0, 255, 256, M - 1] + g.integers(0, M, size=12).tolist())))
     want = oracle.pack(oracle.epilogue(oracle.gemm(A[rows], W, a, w, enc), alpha, beta, S, a), a)
     np.testing.assert_array_equal(u32(Y)[rows], want)
+
+
+@pytest.mark.parametrize("a,enc", [(1, 0), (2, 0), (1, 1), (2, 2), (1, 3)])
+@pytest.mark.parametrize("rows,K", [(300, 1000), (7, 8192), (129, 33), (5, 31), (64, 4096)])
+def test_pack_bits_dense(a, enc, rows, K):
+    # the decomposition from dense a-bit codes: the planes of apnn_pack_bits (== oracle.pack) and the
+    # rows of apnn_prepare_activations; unaligned row strides (K = 33, 31) take the byte-gather path
+    codes = synth.codes((rows, K), a, f"dense{rows}{K}")
+    d = cuda(synth.dense_codes(codes, a))
+    planes, prep = ap.pack_bits_dense(d, rows, K, a, enc)
+    planes_only, none = ap.pack_bits_dense(d, rows, K, a, enc, with_prep=False)
+    ref_prep = ap.prepare_activations(ap.pack_bits(cuda(codes), a), rows, K, a, enc)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(u32(planes), oracle.pack(codes, a))
+    assert torch.equal(planes_only, planes) and none is None
+    assert torch.equal(prep.data, ref_prep.data)
