@@ -502,49 +502,68 @@ __device__ __forceinline__ uint32_t compress_even_bits(unsigned long long x) {
 }
 
 template <int BITS, bool ALIGNED, bool PREP, bool PM1>
+__device__ __forceinline__ unsigned long long dense_group(const uint8_t* crow, int k0, int K) {
+    const int nv = K - k0;  // valid elements of this group
+    unsigned long long x = 0;
+    if (nv > 0) {
+        const int b0 = k0 * BITS / 8, nb = BITS * 4;  // bytes of a full group
+        if (ALIGNED && nv >= 32) {
+            x = BITS == 2 ? __ldg(reinterpret_cast<const unsigned long long*>(crow + b0))
+                          : (unsigned long long)__ldg(reinterpret_cast<const uint32_t*>(crow + b0));
+        } else {
+            const int have = (nv * BITS + 7) / 8 < nb ? (nv * BITS + 7) / 8 : nb;
+            for (int i = 0; i < have; i++) x |= (unsigned long long)crow[b0 + i] << (8 * i);
+        }
+        if (nv < 32) x &= (BITS * nv >= 64) ? ~0ull : ((1ull << (BITS * nv)) - 1ull);
+    }
+    return x;
+}
+
+template <int BITS, bool ALIGNED, bool PREP, bool PM1>
 __global__ void __launch_bounds__(256) pack_dense_kernel(const uint8_t* __restrict__ codes, int rows, int K,
                                                          int row_bytes, int Kw, uint32_t* __restrict__ dst,
                                                          uint8_t* __restrict__ prep) {
-    for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < rows; r += gridDim.y * blockDim.y) {
-        const uint8_t* crow = codes + (long long)r * row_bytes;
-        uint32_t* out = dst + (long long)r * BITS * Kw;
+    constexpr int RU = 4;  // rows per pass: their loads are all in flight before any store
+    const int rstep = gridDim.y * blockDim.y;
+    for (int r0 = blockIdx.y * blockDim.y + threadIdx.y; r0 < rows; r0 += RU * rstep) {
         for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < Kw; w += gridDim.x * blockDim.x) {
             const int k0 = w * 32;
-            const int nv = K - k0;  // valid elements of this group
-            unsigned long long x = 0;
-            if (nv > 0) {
-                const int b0 = k0 * BITS / 8, nb = BITS * 4;  // bytes of a full group
-                if (ALIGNED && nv >= 32) {
-                    x = BITS == 2 ? __ldg(reinterpret_cast<const unsigned long long*>(crow + b0))
-                                  : (unsigned long long)__ldg(reinterpret_cast<const uint32_t*>(crow + b0));
+            unsigned long long x[RU];
+#pragma unroll
+            for (int u = 0; u < RU; u++) {
+                const int r = r0 + u * rstep;
+                x[u] = r < rows ? dense_group<BITS, ALIGNED, PREP, PM1>(codes + (long long)r * row_bytes, k0, K) : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < RU; u++) {
+                const int r = r0 + u * rstep;
+                if (r >= rows) break;
+                uint32_t pw[2];
+                if (BITS == 1) {
+                    pw[0] = (uint32_t)x[u];
+                    pw[1] = 0u;
                 } else {
-                    const int have = (nv * BITS + 7) / 8 < nb ? (nv * BITS + 7) / 8 : nb;
-                    for (int i = 0; i < have; i++) x |= (unsigned long long)crow[b0 + i] << (8 * i);
+                    pw[0] = compress_even_bits(x[u]);
+                    pw[1] = compress_even_bits(x[u] >> 1);
                 }
-                if (nv < 32) x &= (BITS * nv >= 64) ? ~0ull : ((1ull << (BITS * nv)) - 1ull);
-            }
-            uint32_t pw[2];
-            if (BITS == 1) {
-                pw[0] = (uint32_t)x;
-                pw[1] = 0u;
-            } else {
-                pw[0] = compress_even_bits(x);
-                pw[1] = compress_even_bits(x >> 1);
-            }
+                uint32_t* out = dst + (long long)r * BITS * Kw;
 #pragma unroll
-            for (int t = 0; t < BITS; t++) out[(long long)t * Kw + w] = pw[t];
-            if (PREP) {
-                const uint32_t vm = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
-                uint32_t o[4];
+                for (int t = 0; t < BITS; t++) out[(long long)t * Kw + w] = pw[t];
+                if (PREP) {
+                    const int nv = K - k0;
+                    const uint32_t vm = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
+                    uint32_t o[4];
 #pragma unroll
-                for (int j = 0; j < 4; j++) {
-                    const uint32_t e0 = (pw[0] >> j) & 0x11111111u, e1 = (pw[1] >> j) & 0x11111111u;
-                    uint32_t v;
-                    if (PM1) v = 0x22222222u | ((e0 ^ 0x11111111u) << 3);  // +1 -> 0x2, -1 -> 0xA
-                    else v = (e1 << 2) | ((e0 & ~e1) << 1) | (e0 & e1);    // 0..3 -> 0x0, 0x2, 0x4, 0x5
-                    o[j] = v & (((vm >> j) & 0x11111111u) * 0xFu);
+                    for (int j = 0; j < 4; j++) {
+                        const uint32_t e0 = (pw[0] >> j) & 0x11111111u, e1 = (pw[1] >> j) & 0x11111111u;
+                        uint32_t v;
+                        if (PM1) v = 0x22222222u | ((e0 ^ 0x11111111u) << 3);  // +1 -> 0x2, -1 -> 0xA
+                        else v = (e1 << 2) | ((e0 & ~e1) << 1) | (e0 & e1);    // 0..3 -> 0x0, 0x2, 0x4, 0x5
+                        o[j] = v & (((vm >> j) & 0x11111111u) * 0xFu);
+                    }
+                    *reinterpret_cast<uint4*>(prep + ((long long)r * Kw + w) * 16) =
+                        make_uint4(o[0], o[1], o[2], o[3]);
                 }
-                *reinterpret_cast<uint4*>(prep + ((long long)r * Kw + w) * 16) = make_uint4(o[0], o[1], o[2], o[3]);
             }
         }
     }
