@@ -455,6 +455,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_holder;
     const int my_tiles = p.num_tiles > cid ? (p.num_tiles - cid + ncl - 1) / ncl : 0;
+    // Programmatic dependent launch (the host launches with programmatic stream serialization):
+    // the prologue above -- barrier init, TMEM allocation, tensor-map prefetch -- overlaps the
+    // previous kernel's tail; activations, weights and outputs are touched only after the previous
+    // grid has completed and its memory is visible.  The next kernel may be scheduled as soon as
+    // every CTA of this one is past this point (its CTAs start on SMs this grid has left).
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     // The single-thread roles keep their whole warp converged in the loop (every lane waits on
     // the barriers, lane 0 issues): a lone lane spinning while its 31 siblings sit at the final
@@ -880,7 +887,18 @@ static cudaError_t launch(const CUtensorMap& tw, const Params& p, int grid, size
     auto kfn = halo_kernel<AP, WP, RES, RAW>;
     cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
     if (err != cudaSuccess) return err;
-    kfn<<<grid, THREADS, smem, s>>>(tw, p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // the kernel waits (griddepcontrol)
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    err = cudaLaunchKernelEx(&cfg, kfn, tw, p);
+    if (err != cudaSuccess) return err;
     return cudaGetLastError();
 }
 
