@@ -482,6 +482,7 @@ apnn_status apnn_gemm_prepared_ab_i8(const uint8_t* Ap, const uint8_t* Wp, int M
     if (M < 0 || N < 0 || K < 0) return APNN_ERR_SHAPE;
     apnn_status st = check_bits_enc(a_bits, w_bits, enc);
     if (st != APNN_OK) return st;
+    if ((st = check_overflow(K, a_bits, w_bits, enc)) != APNN_OK) return st;  // int32 accumulators (R8)
     if ((M > 0 && K > 0 && !Ap) || (N > 0 && K > 0 && !Wp) || (M > 0 && N > 0 && !Y)) return APNN_ERR_INVALID_ARG;
     if (!aligned16(Ap) || !aligned16(Wp) || !aligned16(Y)) return APNN_ERR_ALIGNMENT;
     Epi e;

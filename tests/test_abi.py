@@ -95,3 +95,31 @@ def test_no_device_fails_loudly():
     # valid arguments, no CUDA device: must be APNN_ERR_CUDA, never a CPU result
     assert gemm_ex() == 8
     assert ap.lib().apnn_pack_bits(FAKE, 4, 4, 2, FAKE, None) == 8
+
+
+def test_round2_entry_points_validate_before_the_device():
+    # the both-prepared GEMMs, operand preparation, fused / dense decomposition and packed max pool
+    # reject bad arguments on the host (status codes of include/apnn.h), without a device
+    L = ap.lib()
+    U = 7  # APNN_ERR_UNSUPPORTED
+    assert L.apnn_prepare_activations(FAKE, 4, 64, 3, 0, FAKE, None) == U           # > 2-bit codes
+    assert L.apnn_prepare_activations(FAKE, 4, 64, 2, 1, FAKE, None) == 3           # +-1 needs 1 bit
+    assert L.apnn_prepare_activations(FAKE, -1, 64, 2, 0, FAKE, None) == 4
+    assert L.apnn_prepare_activations_i8(FAKE, 4, 64, 9, 0, FAKE, None) == 2
+    assert L.apnn_gemm_prepared_ab(None, FAKE, 4, 4, 64, 2, 1, 2, None, FAKE, None) == 1
+    assert L.apnn_gemm_prepared_ab(FAKE, FAKE, 4, 4, 64, 2, 2, 1, None, FAKE, None) == 3
+    assert L.apnn_gemm_prepared_ab(FAKE, FAKE, 4, 4, 64, 4, 1, 2, None, FAKE, None) == U  # FP4: <= 2 bits
+    assert L.apnn_gemm_prepared_ab(FAKE, FAKE, 4, 4, 1 << 23, 2, 2, 0, None, FAKE, None) == U  # past 2^24
+    assert L.apnn_gemm_prepared_ab_i8(FAKE, FAKE, 4, 4, 33026, 8, 8, 0, None, FAKE, None) == 6  # int32 overflow
+    pooled = ap._Epi(2, None, None, 1, 2, 0, 0, None, 0, None)
+    assert L.apnn_gemm_prepared_ab(FAKE, FAKE, 4, 4, 64, 2, 1, 2, ctypes.byref(pooled), FAKE, None) == 1
+    assert L.apnn_gemm_prepared_ab_i8(FAKE, FAKE, 4, 4, 64, 4, 4, 0, ctypes.byref(pooled), FAKE, None) == 1
+    assert L.apnn_pack_bits_prepared(FAKE, 4, 64, 3, 0, FAKE, FAKE, None) == U
+    assert L.apnn_pack_bits_prepared(FAKE, 4, 64, 2, 3, FAKE, FAKE, None) == 3
+    assert L.apnn_pack_bits_dense(FAKE, 4, 64, 4, 0, FAKE, None, None) == U
+    assert L.apnn_pack_bits_dense(FAKE, 4, 64, 0, 0, FAKE, None, None) == 2
+    assert L.apnn_pack_bits_dense(FAKE, 4, 64, 2, 9, FAKE, None, None) == 3
+    assert L.apnn_maxpool_packed(FAKE, 1, 4, 4, 8, 2, 5, 1, FAKE, None) == 4       # window > map
+    assert L.apnn_maxpool_packed(FAKE, 1, 4, 4, 8, 9, 2, 2, FAKE, None) == 2
+    assert L.apnn_maxpool_packed(FAKE, 1, 4, 4, 8, 2, 0, 2, FAKE, None) == 1
+    assert L.apnn_maxpool_packed(ctypes.c_void_p((1 << 20) + 4), 1, 4, 4, 8, 2, 2, 2, FAKE, None) == 5
