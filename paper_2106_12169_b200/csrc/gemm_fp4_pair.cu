@@ -744,16 +744,18 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
                     for (int i = 0; i < 32; i++) acc[i] = (uint32_t)__float2int_rn(__uint_as_float(acc[i]));
                 }
                 if (I32) {
-                    if (row0 < g.M) {
-                        if ((g.N & 3) == 0) {
-                            tc::stage_int32_chunk(acc, stg, lane);
-                            __syncwarp();
-                            tc::writeback_int32_block(stg, lane, reinterpret_cast<int32_t*>(p.Y), row0, g.M,
-                                                      n0 + c * 32, g.N);
-                            __syncwarp();
+                    // each lane writes its row's 128-byte segment (whole lines, no staging: the
+                    // shared memory goes to the operand ring)
+                    const int m = row0 + lane, col0 = n0 + c * 32;
+                    if (m < g.M) {
+                        if ((g.N & 3) == 0 && col0 + 32 <= g.N) {
+                            int4* y = reinterpret_cast<int4*>(reinterpret_cast<int32_t*>(p.Y) + (long long)m * g.N + col0);
+#pragma unroll
+                            for (int q4 = 0; q4 < 8; q4++)
+                                y[q4] = make_int4((int)acc[4 * q4], (int)acc[4 * q4 + 1], (int)acc[4 * q4 + 2],
+                                                  (int)acc[4 * q4 + 3]);
                         } else {
-                            tc::epilogue_chunk(acc, row0 + lane, n0 + c * 32, c * 32, g, p.e, p.Y, nullptr,
-                                               tc::kTabNone);
+                            tc::epilogue_chunk(acc, m, col0, c * 32, g, p.e, p.Y, nullptr, tc::kTabNone);
                         }
                     }
                 } else {
@@ -1022,7 +1024,7 @@ static cudaError_t launch_pp_any(const uint8_t* Ap, const uint8_t* Wp, const Geo
     const bool w_pm1 = g.enc == APNN_ENC_PM1_PM1 || g.enc == APNN_ENC_W_PM1_A_01;
     p.idesc = sm100::idesc_i8(256, BNP, a_pm1, w_pm1);
     const int nck = BNP / 32, nwb_max = (nck + PP_EPI / 4 - 1) / (PP_EPI / 4);
-    p.stg_warp = e.out_bits == 0 ? 4096 : (32 * e.out_bits * nwb_max * 4 + 127) / 128 * 128;
+    p.stg_warp = e.out_bits == 0 ? 0 : (32 * e.out_bits * nwb_max * 4 + 127) / 128 * 128;  // int32: direct row stores
     const size_t bop = (size_t)(BNP / 2) * 128;
     const size_t fixed = (size_t)PP_EPI * p.stg_warp + (e.out_bits ? (size_t)BNP * tc::kTabStride * 4 : 0) +
                          (2 * PP_MAXS + 4) * 8 + 8;
