@@ -648,3 +648,27 @@ def test_prepared_weights_tags_checked():
     got = ap.gemm_prepared(Ap, Wfp4, M, N, K, 2, 1, 2)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(got.cpu().numpy(), oracle.gemm(A, W, 2, 1, 2))
+
+
+def test_bench_contract_line_small():
+    # bench.py end to end at a small size: one JSON line with the contract's keys, the step's
+    # kernels counted (dense pack + both-prepared GEMM per step), e2e bytes from the tensors copied
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--M", "2048", "--N", "2048", "--K", "2048",
+                        "--steps", "4", "--warmup", "3", "--no-models", "--no-cpu"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [x for x in r.stdout.splitlines() if x.startswith("{")][-1]
+    d = json.loads(line)
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "dtype", "data", "config", "roofline", "clocks", "e2e", "gpu_launches"):
+        assert key in d, key
+    assert d["value"] > 0 and d["steps"] == 4 and d["n_gpus"] == 1
+    assert d["gpu_launches"] == 2 * 4
+    assert d["roofline"]["kernel"].startswith("fp4_pp_kernel") and 0 < d["roofline"]["frac"] < 1.5
+    assert d["e2e"]["h2d_bytes_per_step"] == 2048 * 2048 * 2 // 8  # dense 2-bit codes
+    assert d["e2e"]["d2h_bytes_per_step"] == 2048 * 2 * (2048 // 32) * 4  # packed 2-bit output
