@@ -882,6 +882,6 @@ const char* apnn_variant_name(apnn_variant v) {
 
 uint64_t apnn_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
-int apnn_version(void) { return 200; }
+int apnn_version(void) { return 300; }  // 0.3.0: both-prepared GEMMs, fused / dense decomposition, packed max pool
 
 }  // extern "C"
