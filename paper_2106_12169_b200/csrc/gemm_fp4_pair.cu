@@ -528,7 +528,10 @@ __device__ __forceinline__ void pp_tr(int ev, int i) {
     }
 #endif
 }
-constexpr int PP_EPI = 16;
+// 8 epilogue warps (two per TMEM lane quarter): with the accumulator double-buffered their drain
+// hides behind the next tile's MMAs, and 16 took issue slots from the lone MMA-issuing thread on
+// its sub-partition (8192^3 w4a4 int8 fused 0.332 -> 0.319 ms with 8)
+constexpr int PP_EPI = 8;
 constexpr int PP_TMA = PP_EPI;
 constexpr int PP_MMA = PP_EPI + 1;
 constexpr int PP_THREADS = (PP_MMA + 1) * 32;
@@ -947,7 +950,7 @@ cudaError_t launch_tc_fp4_pair_prepared(const uint32_t* A, const uint8_t* Wp, co
 
 // both operands prepared (apnn_gemm_prepared_ab): the persistent pair kernel without decode warps.
 // Tile width: 224 (two accumulators, the epilogue overlapped with the next tile's MMAs; 8192^3
-// w1a2 fused 6100 TOPS) unless APNN_FP4_PP_BN=256 (read once; one accumulator, 16 epilogue warps
+// w1a2 fused 6100 TOPS) unless APNN_FP4_PP_BN=256 (read once; one accumulator, the epilogue warps
 // drain it between tiles: 5477 TOPS, scripts/fp4_pp_time.py)
 static int fp4_pp_bn_override() {
     static int v = -1;
