@@ -551,7 +551,7 @@ def run_ours(args):
         line["comm"] = comm
     if allgather is not None:
         line["allgather"] = allgather
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:  # the oracle beside the bench: rank 0 at N = 1 only (contract)
         line["cpu_baseline"] = oracle_sample(A_np, W_np, args, args.cpu_seconds, out_bits, alpha_np, beta_np, S)
     print(json.dumps(line), flush=True)
     if dist is not None:
